@@ -1,0 +1,31 @@
+# Builds libspecmesh_b200.so (sm_100a) in-tree and the oracle's C++ helpers.
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+SRC_DIR := paper_1810_02719_b200/csrc
+OBJ_DIR := build/obj
+LIB := paper_1810_02719_b200/lib/libspecmesh_b200.so
+SRCS := $(wildcard $(SRC_DIR)/*.cu)
+OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
+HDRS := $(wildcard $(SRC_DIR)/*.h) $(wildcard $(SRC_DIR)/*.cuh) include/specmesh_gpu.h
+
+all: $(LIB) oracle
+
+$(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(OBJ_DIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.log || (cat $@.log; false)
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $(LIB))
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static -lcuda
+
+oracle: oracle/_ref/rng_ref
+
+oracle/_ref/rng_ref: oracle/rng_ref.cpp
+	@mkdir -p oracle/_ref
+	g++ -O2 -std=c++17 -o $@ $<
+
+clean:
+	rm -rf build $(LIB) oracle/_ref
+
+.PHONY: all clean oracle

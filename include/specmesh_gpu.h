@@ -1,0 +1,214 @@
+/*
+ * specmesh_gpu.h -- C ABI of the B200-native OI spectral path (libspecmesh_b200.so).
+ *
+ * Drop-in boundary for the reference's per-submesh spectral chain
+ * (/root/reference/proj/include/specmesh; header-only C++ over Eigen, no FFI of
+ * its own -- SURVEY.md §8(b)).  Each entry point below names the reference
+ * interface it replaces.  Plain pointers and sizes only; exceptions never cross
+ * the boundary: every call returns a status and smg_last_error() holds the
+ * reference's message text ("orthonormalize: block is rank deficient at column 14").
+ *
+ * Conventions
+ *   - Status codes follow the SPEC CLI exit codes: 0 ok,
+ *     2 InvalidArgument (core.hpp:24-28, `require` preconditions), 3 Error
+ *     (numerical failures, core.hpp:18-22).
+ *   - Dense matrices cross the ABI column-major (Eigen's default storage of
+ *     MatrixXd / MatrixX3d): an n x c basis is c contiguous columns of n doubles,
+ *     Points (n x 3) are x[0..n) | y[0..n) | z[0..n).
+ *   - The Laplacian crosses as CSR with int32 indices; for the symmetric L these
+ *     are exactly Eigen's compressed-column arrays (spectral.hpp:63-66).
+ *   - `on_device` = 0: host pointers (copied in/out inside the call);
+ *     1: device pointers on the context's device (no host copies).
+ *   - A context owns one CUDA device and one stream; it is thread-compatible
+ *     (one context per host thread).
+ *   - There is no CPU fallback: every compute call runs sm_100a kernels and
+ *     fails with status 3 if the device cannot run them.
+ */
+#ifndef SPECMESH_GPU_H
+#define SPECMESH_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMG_ABI_VERSION 1
+
+typedef enum { SMG_OK = 0, SMG_INVALID_ARGUMENT = 2, SMG_ERROR = 3 } smg_status;
+
+/* spectral.hpp:22 Weighting */
+typedef enum { SMG_WEIGHTING_BINARY = 0, SMG_WEIGHTING_DISTANCE = 1 } smg_weighting;
+/* pipeline.hpp:12 BasisMode (SVD is the non-OI comparison baseline: out of scope) */
+typedef enum { SMG_BASIS_OI = 0, SMG_BASIS_DOI = 1 } smg_basis_mode;
+
+typedef struct smg_context smg_context;
+typedef struct smg_operator smg_operator;
+
+/* Mesh (mesh.hpp:18-37) + EdgeSet (mesh.hpp:40-50, neighbour lists sorted ascending). */
+typedef struct {
+    int64_t vertex_count;
+    const double* x;            /* vertex_count */
+    const double* y;
+    const double* z;
+    const int32_t* adj_offsets; /* vertex_count + 1 */
+    const int32_t* adj_cols;    /* adj_offsets[vertex_count] */
+    int32_t on_device;
+} smg_mesh;
+
+/* Segmentation (pipeline.hpp:125-129) reduced to what the path reads: the
+ * submeshes' member lists (partition.hpp:34-47; sorted ascending = local order)
+ * and the SubmeshOrder sequence (partition.hpp:49-51). */
+typedef struct {
+    int32_t submesh_count;
+    const int32_t* member_offsets; /* submesh_count + 1 */
+    const int32_t* members;
+    int32_t sequence_length;
+    const int32_t* sequence;       /* permutation of submesh ids */
+    int32_t on_device;
+} smg_segmentation;
+
+/* PipelineConfig (pipeline.hpp:41-68), path fields only, field for field. */
+typedef struct {
+    int32_t weighting;          /* smg_weighting; reference default distance */
+    int32_t basis_mode;         /* smg_basis_mode */
+    int32_t subspace_size;      /* fixed c; initial c in DOI mode (16) */
+    double eps_low;             /* DOI band, relative to bbox diagonal (0.004) */
+    double eps_high;            /* (0.04) */
+    int32_t c_min;              /* (2) */
+    int32_t c_max;              /* 0: derived, resolve_c_max (pipeline.hpp:60-63) */
+    int32_t power;              /* z (2) */
+    int32_t iterations;         /* t_max per OI update (2) */
+    int32_t initial_iterations; /* cold-start OI when n_d > dense_limit (60) */
+    int32_t doi_iterations;     /* 0: derived, resolve_doi_iterations (pipeline.hpp:64-67) */
+    uint64_t seed;              /* (1) */
+    int32_t dense_limit;        /* (4096) */
+    double shift_scale;         /* delta = shift_scale * trace(L)/n_d (1e-8) */
+} smg_pipeline_config;
+
+/* Results of a chain: BlockBases.stats (pipeline.hpp:70-92) plus the optional
+ * coefficient / reconstruction / basis outputs.  Arrays are indexed by submesh
+ * id.  Optional pointers may be NULL. */
+typedef struct {
+    int32_t* subspace_size;   /* [submesh_count] */
+    double* residual_rms;     /* [submesh_count] projection_residual_rms */
+    double* doi_residual;     /* [submesh_count] */
+    int32_t* converged;       /* [submesh_count] */
+    int32_t* oi_iterations;   /* [submesh_count] */
+    /* coarse_reconstruct_points (pipeline.hpp:300-305), Weighted mode: vertex_count x 3 */
+    double* reconstruction;
+    /* gft coefficients C = U^T X (spectral.hpp:290-293), c_id x 3 column-major per
+     * submesh id, packed at coefficient_offsets[id] (offsets written by the call) */
+    double* coefficients;
+    int64_t coefficients_capacity;  /* doubles available in `coefficients` */
+    int64_t* coefficient_offsets;   /* [submesh_count + 1] */
+    /* tracked bases n_d x c_id column-major at basis_offsets[id] */
+    double* bases;
+    int64_t bases_capacity;         /* doubles available in `bases` */
+    int64_t* basis_offsets;         /* [submesh_count + 1] */
+    int32_t on_device;              /* applies to reconstruction/coefficients/bases */
+    /* StageTimings (core.hpp:41-68), device-event seconds:
+     * [0] laplacian [1] factorize [2] basis (first submesh) [3] basis_total
+     * [4] project (gft+igft+stitch) [5] total */
+    double timings[6];
+} smg_chain_output;
+
+int smg_abi_version(void);
+const char* smg_last_error(const smg_context* ctx);
+
+/* Context on CUDA device `device`.  Fails (status 3) without a usable sm_100 device. */
+smg_status smg_create(int device, smg_context** out);
+void smg_destroy(smg_context* ctx);
+
+/* PipelineConfig defaults (pipeline.hpp:41-58). */
+void smg_default_config(smg_pipeline_config* cfg);
+
+/* ---------------------------------------------------------------- L4 chain */
+
+/* compute_block_bases_fixed_sizes (pipeline.hpp:144-194) followed, when the
+ * output requests it, by project_blocks + coarse_reconstruct_points
+ * (pipeline.hpp:290-305).  sizes_in_order: one c per order position (host). */
+smg_status smg_compute_block_bases_fixed_sizes(smg_context* ctx, const smg_mesh* mesh,
+                                               const smg_segmentation* seg,
+                                               const smg_pipeline_config* cfg,
+                                               const int32_t* sizes_in_order,
+                                               smg_chain_output* out);
+
+/* compute_block_bases (pipeline.hpp:198-287) for basis_mode OI or DOI, over an
+ * EXTERNAL segmentation (the reference segments internally at :201; the
+ * configs supply their own tiles). */
+smg_status smg_compute_block_bases(smg_context* ctx, const smg_mesh* mesh,
+                                   const smg_segmentation* seg,
+                                   const smg_pipeline_config* cfg, smg_chain_output* out);
+
+/* n_chains independent fixed-size chains (one per mesh) processed in lockstep
+ * on this context's device; all submeshes of all chains must share n_d and c.
+ * meshes/segs/outs are arrays of n_chains.  This is config 5's per-GPU shard. */
+smg_status smg_run_chains(smg_context* ctx, int32_t n_chains, const smg_mesh* meshes,
+                          const smg_segmentation* segs, const smg_pipeline_config* cfg,
+                          const int32_t* sizes_in_order, smg_chain_output* outs);
+
+/* ------------------------------------------------------------ L3 primitives
+ * Host pointers, column-major.  They run the same kernels as the chain. */
+
+/* detail::build_submesh adjacency (partition.hpp:169-184) + build_laplacian
+ * (spectral.hpp:39-68) for one submesh.  Writes CSR (rowptr n+1, cols/vals nnz);
+ * nnz_capacity bounds cols/vals; *nnz_out gets the count; *trace_out = trace(L)
+ * (spectral.hpp:32-36).  Coincident connected vertices under distance weighting
+ * -> status 3 with the reference message. */
+smg_status smg_build_laplacian(smg_context* ctx, const smg_mesh* mesh, const int32_t* members,
+                               int32_t n, int32_t weighting, int32_t* rowptr, int32_t* cols,
+                               double* vals, int64_t nnz_capacity, int64_t* nnz_out,
+                               double* trace_out);
+
+/* default_shift (spectral.hpp:193-196). */
+double smg_default_shift(double trace, int32_t n, double scale);
+
+/* ShiftedInverseOperator (spectral.hpp:145-190): factor L + delta I (host CSR). */
+smg_status smg_operator_create(smg_context* ctx, int32_t n, const int32_t* rowptr,
+                               const int32_t* cols, const double* vals, double delta, int32_t z,
+                               smg_operator** out);
+void smg_operator_destroy(smg_operator* op);
+/* apply (z solves, spectral.hpp:172-176) or apply_once (:166-169). */
+smg_status smg_operator_apply(smg_context* ctx, const smg_operator* op, int32_t c,
+                              const double* block, double* out, int32_t once);
+/* (L + delta I) X  -- CSR SpMM (no reference symbol; residual / verification). */
+smg_status smg_operator_spmm(smg_context* ctx, const smg_operator* op, int32_t c,
+                             const double* block, double* out);
+
+/* orthonormalize (spectral.hpp:120-132): thin Q with the reference rank test and
+ * sign convention.  Status 3 "orthonormalize: block is rank deficient at column k". */
+smg_status smg_orthonormalize(smg_context* ctx, int32_t rows, int32_t cols, const double* block,
+                              double* q);
+
+/* orthogonal_iteration (spectral.hpp:204-211). */
+smg_status smg_orthogonal_iteration(smg_context* ctx, const smg_operator* op, int32_t c,
+                                    const double* init, int32_t t_max, double* out);
+
+/* dynamic_oi (spectral.hpp:244-287).  basis_out holds n x c_max doubles; the
+ * final c is written to *c_out. coords: n x 3 column-major. */
+smg_status smg_dynamic_oi(smg_context* ctx, const smg_operator* op, int32_t c,
+                          const double* init, const double* coords, double eps_low,
+                          double eps_high, int32_t c_min, int32_t c_max, int32_t t_max,
+                          double* basis_out, int32_t* c_out, int32_t* converged,
+                          double* residual, int32_t* iterations);
+
+/* bottom_subspace(dense_eigendecomposition(L), c) (spectral.hpp:92-117): the
+ * first-submesh basis, produced on the GPU by shift-invert subspace iteration +
+ * Rayleigh-Ritz on the operator's factor (K9).  eigenvalues_out
+ * (optional, c doubles) gets the ascending Ritz values. */
+smg_status smg_bottom_subspace(smg_context* ctx, const smg_operator* op, int32_t c,
+                               double* basis_out, double* eigenvalues_out);
+
+/* gft / igft (spectral.hpp:290-298). */
+smg_status smg_gft(smg_context* ctx, int32_t rows, int32_t c, const double* basis,
+                   const double* coords, double* coeffs);
+smg_status smg_igft(smg_context* ctx, int32_t rows, int32_t c, const double* basis,
+                    const double* coeffs, double* coords);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPECMESH_GPU_H */

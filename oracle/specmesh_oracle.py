@@ -1,0 +1,741 @@
+"""CPU oracle: a numpy/scipy restatement of the reference's hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+module, and only as the checker or the timed CPU baseline -- never as the thing
+measured or shipped.  The product path (``paper_1810_02719_b200``) never imports
+it and fails loudly without its CUDA library.
+
+What it restates (reference = /root/reference/proj/include/specmesh, cited file:line):
+  * build_submesh             partition.hpp:169-197  (local order = ascending id)
+  * build_laplacian           spectral.hpp:39-68     (L = D - C, D_ii = |N(i)|)
+  * Laplacian.trace / default_shift   spectral.hpp:32-36, :193-196
+  * ShiftedInverseOperator    spectral.hpp:145-190   (R^z by z factor solves)
+  * apply_sign_convention     spectral.hpp:72-85
+  * dense_eigendecomposition / bottom_subspace   spectral.hpp:92-117
+  * orthonormalize            spectral.hpp:120-132   (Householder QR, rank test)
+  * random_orthonormal_basis  spectral.hpp:134-141
+  * orthogonal_iteration      spectral.hpp:204-211
+  * projection_residual(_rms), bounding_box_diagonal   spectral.hpp:216-231
+  * dynamic_oi                spectral.hpp:244-287
+  * gft / igft                spectral.hpp:290-298
+  * max_principal_angle       spectral.hpp:303-309
+  * write_basis / read_basis  spectral.hpp:312-365  (SMBASIS1)
+  * PipelineConfig            pipeline.hpp:41-68
+  * resize_basis              pipeline.hpp:97-109
+  * initial_block_basis       pipeline.hpp:113-120
+  * compute_block_bases_fixed_sizes   pipeline.hpp:144-194
+  * compute_block_bases (DOI branch)  pipeline.hpp:245-285, with an external
+    Segmentation (the reference segments internally, :201)
+  * project_blocks / coarse_reconstruct_points   pipeline.hpp:290-305
+  * reconstruct_weighted      partition.hpp:311-355
+
+Third-party dependency: the reference's arithmetic comes from Eigen (version
+unpinned; absent from this image, so the reference cannot be compiled here or on
+the GPU box -- SURVEY.md §8(c)).  Its published algorithms are restated with
+LAPACK through scipy: SimplicialLDLT (AMD order, no pivoting) -> banded Cholesky
+(LAPACK dpbtrf/dpbtrs) in natural or RCM order, with a no-pivot banded LDL^T for
+indefinite matrices (what Eigen's LDL^T tolerates); HouseholderQR ->
+LAPACK dgeqrf/dorgqr; SelfAdjointEigenSolver -> LAPACK dsyevd.  They differ from
+Eigen only in rounding.
+
+Parity pin: the reference ships no tests, fixtures or golden vectors.  This
+oracle is pinned to the SPEC.md known-answer examples in
+tests/test_oracle_known_answers.py, and its RNG to libstdc++'s own
+std::mt19937_64 / std::normal_distribution (oracle/rng_ref.cpp).  Against the
+reference's code itself parity is UNPINNED (Eigen absent).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+import struct
+import time
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+from scipy.sparse.csgraph import reverse_cuthill_mckee
+
+
+class Error(RuntimeError):
+    """core.hpp:18-22"""
+
+
+class InvalidArgument(Error):
+    """core.hpp:24-28"""
+
+
+class ParseError(Error):
+    """core.hpp:30-34"""
+
+
+def require(cond: bool, message: str) -> None:
+    """core.hpp:36-38"""
+    if not cond:
+        raise InvalidArgument(message)
+
+
+BINARY = "binary"
+DISTANCE = "distance"
+
+# --------------------------------------------------------------------------
+# RNG: libstdc++ std::mt19937_64 + std::normal_distribution (polar method)
+
+_MASK = (1 << 64) - 1
+
+
+class MT19937_64:
+    """std::mt19937_64 (Matsumoto-Nishimura 64-bit parameters)."""
+
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & _MASK
+        for i in range(1, 312):
+            prev = self.mt[i - 1]
+            self.mt[i] = (6364136223846793005 * (prev ^ (prev >> 62)) + i) & _MASK
+        self.idx = 312
+
+    def _twist(self):
+        mt = self.mt
+        for i in range(312):
+            x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + 156) % 312] ^ xa
+        self.idx = 0
+
+    def __call__(self) -> int:
+        if self.idx >= 312:
+            self._twist()
+        y = self.mt[self.idx]
+        self.idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & _MASK
+
+
+class NormalDistribution:
+    """libstdc++ normal_distribution<double>(0,1): Marsaglia polar method,
+    second deviate cached; uniforms via generate_canonical<double,53>."""
+
+    def __init__(self):
+        self.saved = None
+
+    @staticmethod
+    def _canonical(rng: MT19937_64) -> float:
+        r = float(rng()) / 18446744073709551616.0
+        if r >= 1.0:
+            r = math.nextafter(1.0, 0.0)
+        return r
+
+    def __call__(self, rng: MT19937_64) -> float:
+        if self.saved is not None:
+            v, self.saved = self.saved, None
+            return v
+        while True:
+            x = 2.0 * self._canonical(rng) - 1.0
+            y = 2.0 * self._canonical(rng) - 1.0
+            r2 = x * x + y * y
+            if not (r2 > 1.0 or r2 == 0.0):
+                break
+        mult = math.sqrt(-2.0 * math.log(r2) / r2)
+        self.saved = x * mult
+        return y * mult
+
+
+def gaussian_block(rows: int, cols: int, seed: int) -> np.ndarray:
+    """Column-major fill order of spectral.hpp:138-139 / pipeline.hpp:106-107."""
+    rng = MT19937_64(seed)
+    g = NormalDistribution()
+    out = np.empty((rows, cols))
+    for j in range(cols):
+        for i in range(rows):
+            out[i, j] = g(rng)
+    return out
+
+
+# --------------------------------------------------------------------------
+# submesh + Laplacian
+
+@dataclasses.dataclass
+class Submesh:
+    """partition.hpp:34-47 (local faces omitted: not read by the path)."""
+
+    global_indices: np.ndarray
+    local_adjacency: List[np.ndarray]
+    local_degrees: np.ndarray
+
+    def size(self) -> int:
+        return int(self.global_indices.size)
+
+    def local_coords(self, vertices: np.ndarray) -> np.ndarray:
+        return vertices[self.global_indices]
+
+
+def build_submesh(adj_offsets: np.ndarray, adj_cols: np.ndarray, members) -> Submesh:
+    """partition.hpp:169-184: sort members, induced adjacency in neighbour-list order."""
+    g = np.sort(np.asarray(members, dtype=np.int64))
+    adj = []
+    for gi in g:
+        nb = adj_cols[adj_offsets[gi]:adj_offsets[gi + 1]]
+        pos = np.searchsorted(g, nb)
+        pos = np.minimum(pos, g.size - 1)
+        inside = g[pos] == nb
+        adj.append(pos[inside].astype(np.int64))
+    deg = np.array([a.size for a in adj], dtype=np.int64)
+    return Submesh(g, adj, deg)
+
+
+@dataclasses.dataclass
+class Laplacian:
+    """spectral.hpp:27-37; CSR of the symmetric matrix (== Eigen's CSC arrays)."""
+
+    rowptr: np.ndarray
+    cols: np.ndarray
+    vals: np.ndarray
+    weighting: str
+
+    def size(self) -> int:
+        return int(self.rowptr.size - 1)
+
+    def trace(self) -> float:
+        n = self.size()
+        t = 0.0
+        for i in range(n):
+            s, e = self.rowptr[i], self.rowptr[i + 1]
+            k = np.nonzero(self.cols[s:e] == i)[0]
+            t += float(self.vals[s + k[0]]) if k.size else 0.0
+        return t
+
+    def to_scipy(self) -> sp.csr_matrix:
+        n = self.size()
+        return sp.csr_matrix((self.vals, self.cols, self.rowptr), shape=(n, n))
+
+    def dense(self) -> np.ndarray:
+        return self.to_scipy().toarray()
+
+
+def build_laplacian(sub: Submesh, vertices: np.ndarray, weighting: str) -> Laplacian:
+    """spectral.hpp:39-68.  setFromTriplets sorts each column by row; for the
+    symmetric L those are our CSR rows sorted by column."""
+    n = sub.size()
+    require(n >= 2, "submesh must have at least 2 vertices")
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    cols_l, vals_l = [], []
+    for i in range(n):
+        nb = sub.local_adjacency[i]
+        w = np.ones(nb.size)
+        if weighting == DISTANCE:
+            gi = sub.global_indices[i]
+            for t, j in enumerate(nb):
+                gj = sub.global_indices[j]
+                dx = vertices[gi, 0] - vertices[gj, 0]
+                dy = vertices[gi, 1] - vertices[gj, 1]
+                dz = vertices[gi, 2] - vertices[gj, 2]
+                d2 = (dx * dx + dy * dy) + dz * dz
+                with np.errstate(divide="ignore"):
+                    inv = 1.0 / d2 if d2 != 0.0 else math.inf
+                if not (d2 > 0.0) or not math.isfinite(inv):
+                    raise Error(f"coincident connected vertices {gi} and {gj} make the "
+                                "distance weight singular")
+                w[t] = inv
+        c = np.concatenate([[i], nb])
+        v = np.concatenate([[float(sub.local_degrees[i])], -w])
+        order = np.argsort(c, kind="stable")
+        cols_l.append(c[order])
+        vals_l.append(v[order])
+        rowptr[i + 1] = rowptr[i] + c.size
+    return Laplacian(rowptr, np.concatenate(cols_l), np.concatenate(vals_l), weighting)
+
+
+def default_shift(lap: Laplacian, scale: float = 1e-8) -> float:
+    """spectral.hpp:193-196 -- operation order scale * (trace / n) kept."""
+    mean_diag = lap.trace() / float(lap.size())
+    return max(scale * mean_diag, 1e-300)
+
+
+# --------------------------------------------------------------------------
+# shifted-inverse operator
+
+class ShiftedInverseOperator:
+    """spectral.hpp:145-190.  Factor of L + delta*I in natural order (grid
+    tiles are banded there) or RCM order, banded Cholesky via LAPACK; a no-pivot
+    banded LDL^T takes over when the matrix is not positive definite."""
+
+    def __init__(self, lap: Laplacian, delta: float, z: int):
+        require(delta > 0.0, "shift delta must be positive")
+        require(z >= 1, "power z must be at least 1")
+        self.shift_, self.power_, self.size_ = delta, z, lap.size()
+        a = lap.to_scipy().tocsr().copy()
+        a = a + delta * sp.identity(self.size_, format="csr")
+        a = a.tocsr()
+        a.sort_indices()
+        perm = np.arange(self.size_)
+        bw = self._bandwidth(a)
+        if bw > 96:
+            p = reverse_cuthill_mckee(a, symmetric_mode=True)
+            ap = a[p][:, p].tocsr()
+            if self._bandwidth(ap) < bw:
+                perm, a, bw = p, ap, self._bandwidth(ap)
+        self.perm = perm
+        self.bw = bw
+        n = self.size_
+        ab = np.zeros((bw + 1, n))
+        coo = a.tocoo()
+        lower = coo.row >= coo.col
+        ab[coo.row[lower] - coo.col[lower], coo.col[lower]] = coo.data[lower]
+        self.ldl = None
+        try:
+            self.cb = sla.cholesky_banded(ab, lower=True)
+        except np.linalg.LinAlgError:
+            self.cb = None
+            self.ldl = self._banded_ldlt(a.toarray(), bw)
+
+    @staticmethod
+    def _bandwidth(a) -> int:
+        coo = a.tocoo()
+        return int(np.abs(coo.row - coo.col).max()) if coo.nnz else 0
+
+    @staticmethod
+    def _banded_ldlt(A: np.ndarray, bw: int):
+        n = A.shape[0]
+        L = np.eye(n)
+        d = np.zeros(n)
+        for j in range(n):
+            lo = max(0, j - bw)
+            dj = A[j, j] - np.dot(L[j, lo:j] ** 2, d[lo:j])
+            if dj == 0.0 or not math.isfinite(dj):
+                raise Error("sparse factorization of the shifted Laplacian failed")
+            d[j] = dj
+            hi = min(n, j + bw + 1)
+            L[j + 1:hi, j] = (A[j + 1:hi, j] - L[j + 1:hi, lo:j] @ (d[lo:j] * L[j, lo:j])) / dj
+        return L, d
+
+    def size(self) -> int:
+        return self.size_
+
+    def shift(self) -> float:
+        return self.shift_
+
+    def power(self) -> int:
+        return self.power_
+
+    def _solve(self, b: np.ndarray) -> np.ndarray:
+        bp = b[self.perm]
+        if self.cb is not None:
+            xp = sla.cho_solve_banded((self.cb, True), bp, check_finite=False)
+        else:
+            L, d = self.ldl
+            y = sla.solve_triangular(L, bp, lower=True, unit_diagonal=True)
+            y = y / (d[:, None] if y.ndim == 2 else d)
+            xp = sla.solve_triangular(L.T, y, lower=False, unit_diagonal=True)
+        x = np.empty_like(xp)
+        x[self.perm] = xp
+        return x
+
+    def apply_once(self, block: np.ndarray) -> np.ndarray:
+        require(block.shape[0] == self.size_, "operator/block dimension mismatch")
+        return self._solve(block)
+
+    def apply(self, block: np.ndarray) -> np.ndarray:
+        out = self.apply_once(block)
+        for _ in range(1, self.power_):
+            out = self._solve(out)
+        return out
+
+
+# --------------------------------------------------------------------------
+# dense linear algebra
+
+def apply_sign_convention(cols: np.ndarray) -> np.ndarray:
+    """spectral.hpp:72-85: per column argmax |.| (strict >, first index wins),
+    flip if that entry is negative.  In place; returns the array."""
+    if cols.shape[0] == 0:
+        return cols
+    at = np.argmax(np.abs(cols), axis=0)  # first occurrence of the maximum
+    neg = cols[at, np.arange(cols.shape[1])] < 0.0
+    cols[:, neg] *= -1.0
+    return cols
+
+
+def dense_eigendecomposition(lap: Laplacian, dense_limit: int = 4096):
+    """spectral.hpp:92-104 -> (ascending eigenvalues, sign-fixed eigenvectors)."""
+    require(lap.size() <= dense_limit, "submesh size exceeds the dense eigendecomposition limit")
+    w, v = np.linalg.eigh(lap.dense())
+    if not np.all(np.isfinite(w)):
+        raise Error("dense eigendecomposition failed to converge")
+    return w, apply_sign_convention(np.ascontiguousarray(v))
+
+
+def bottom_subspace(spectrum, c: int) -> np.ndarray:
+    """spectral.hpp:114-117"""
+    require(1 <= c <= spectrum[1].shape[1], "subspace size out of range")
+    return spectrum[1][:, :c].copy()
+
+
+def orthonormalize(block: np.ndarray) -> np.ndarray:
+    """spectral.hpp:120-132"""
+    rows, cols = block.shape
+    require(cols >= 1 and rows >= cols, "block must be tall (rows >= cols >= 1)")
+    scale = float(np.linalg.norm(block))
+    if scale == 0.0:
+        raise Error("orthonormalize: block is rank deficient (all zero)")
+    q, r = sla.qr(block, mode="economic", check_finite=False)
+    d = np.abs(np.diag(r))
+    bad = np.nonzero(d < 1e-13 * scale)[0]
+    if bad.size:
+        raise Error(f"orthonormalize: block is rank deficient at column {int(bad[0])}")
+    return apply_sign_convention(np.ascontiguousarray(q))
+
+
+def random_orthonormal_basis(rows: int, c: int, seed: int) -> np.ndarray:
+    """spectral.hpp:134-141"""
+    return orthonormalize(gaussian_block(rows, c, seed))
+
+
+def orthogonal_iteration(op: ShiftedInverseOperator, init: np.ndarray, t_max: int) -> np.ndarray:
+    """spectral.hpp:204-211"""
+    require(init.shape[0] == op.size(), "initial basis does not match the operator size")
+    require(t_max >= 0, "t_max must be nonnegative")
+    u = init
+    for _ in range(t_max):
+        u = orthonormalize(op.apply(u))
+    return u
+
+
+def projection_residual(basis: np.ndarray, coords: np.ndarray) -> np.ndarray:
+    """spectral.hpp:216-220: e = s - U (U^T s), s = x + y + z."""
+    require(coords.shape[0] == basis.shape[0], "coordinate/basis dimension mismatch")
+    summed = coords.sum(axis=1)
+    return summed - basis @ (basis.T @ summed)
+
+
+def projection_residual_rms(basis: np.ndarray, coords: np.ndarray) -> float:
+    """spectral.hpp:223-226"""
+    residual = coords - basis @ (basis.T @ coords)
+    return math.sqrt(float(np.sum(residual * residual)) / float(coords.size))
+
+
+def bounding_box_diagonal(coords: np.ndarray) -> float:
+    """spectral.hpp:228-231"""
+    if coords.shape[0] == 0:
+        return 0.0
+    return float(np.linalg.norm(coords.max(axis=0) - coords.min(axis=0)))
+
+
+@dataclasses.dataclass
+class DoiResult:
+    """spectral.hpp:233-238"""
+
+    basis: np.ndarray
+    converged: bool = False
+    residual: float = 0.0
+    iterations: int = 0
+
+
+def dynamic_oi(op, init, coords, eps_low, eps_high, c_min, c_max, t_max) -> DoiResult:
+    """spectral.hpp:244-287"""
+    require(eps_low > 0.0 and eps_low < eps_high, "need 0 < eps_low < eps_high")
+    require(c_min >= 1 and c_min <= init.shape[1] and init.shape[1] <= c_max,
+            "need c_min <= init subspace size <= c_max")
+    require(c_max <= op.size(), "c_max cannot exceed the submesh size")
+    require(coords.shape[0] == op.size(), "coordinate/operator dimension mismatch")
+    scale = bounding_box_diagonal(coords)
+    if scale == 0.0:
+        scale = 1.0
+    u = init
+    appended_raw = False
+    res = DoiResult(basis=init)
+    for t in range(1, t_max + 1):
+        u = orthonormalize(op.apply(u))
+        appended_raw = False
+        res.iterations = t
+        e = projection_residual(u, coords)
+        en = float(np.linalg.norm(e))
+        res.residual = en / scale
+        if res.residual > eps_high:
+            if u.shape[1] >= c_max:
+                break
+            u = np.concatenate([u, (e / en)[:, None]], axis=1)
+            appended_raw = True
+        elif res.residual < eps_low:
+            if u.shape[1] <= c_min:
+                res.converged = True
+                break
+            u = u[:, :-1].copy()
+        else:
+            res.converged = True
+            break
+    if appended_raw:
+        u = orthonormalize(u)
+    res.basis = u
+    return res
+
+
+def gft(basis: np.ndarray, coords: np.ndarray) -> np.ndarray:
+    """spectral.hpp:290-293"""
+    require(coords.shape[0] == basis.shape[0], "coordinate/basis dimension mismatch")
+    return basis.T @ coords
+
+
+def igft(basis: np.ndarray, coeffs: np.ndarray) -> np.ndarray:
+    """spectral.hpp:295-298"""
+    require(coeffs.shape[0] == basis.shape[1], "coefficient/basis dimension mismatch")
+    return basis @ coeffs
+
+
+def max_principal_angle(a: np.ndarray, b: np.ndarray) -> float:
+    """spectral.hpp:303-309"""
+    require(a.shape == b.shape, "principal angles need equally shaped bases")
+    residual = a - b @ (b.T @ a)
+    s = float(np.linalg.svd(residual, compute_uv=False)[0]) if residual.size else 0.0
+    return math.asin(min(max(s, 0.0), 1.0))
+
+
+BASIS_MAGIC = b"SMBASIS1"
+
+
+def write_basis(basis: np.ndarray, path: str) -> None:
+    """spectral.hpp:337-347: magic, u64 rows, u64 cols, row-major f64 LE."""
+    with open(path, "wb") as f:
+        f.write(BASIS_MAGIC)
+        f.write(struct.pack("<QQ", basis.shape[0], basis.shape[1]))
+        f.write(np.ascontiguousarray(basis, dtype="<f8").tobytes())
+
+
+def read_basis(path: str) -> np.ndarray:
+    """spectral.hpp:349-365"""
+    with open(path, "rb") as f:
+        data = f.read()
+    if data[:8] != BASIS_MAGIC:
+        raise ParseError(f"{path}: not a basis dump")
+    if len(data) < 24:
+        raise ParseError(f"{path}: bad basis header")
+    rows, cols = struct.unpack("<QQ", data[8:24])
+    if rows < 1 or cols < 1 or cols > rows:
+        raise ParseError(f"{path}: bad basis header")
+    body = data[24:]
+    if len(body) < rows * cols * 8:
+        raise ParseError(f"{path}: truncated basis dump")
+    return np.frombuffer(body[:rows * cols * 8], dtype="<f8").reshape(rows, cols).copy()
+
+
+# --------------------------------------------------------------------------
+# pipeline
+
+@dataclasses.dataclass
+class PipelineConfig:
+    """pipeline.hpp:41-68 (segmentation fields unused: Segmentation is an input)."""
+
+    weighting: str = DISTANCE
+    subspace_size: int = 16
+    eps_low: float = 0.004
+    eps_high: float = 0.04
+    c_min: int = 2
+    c_max: int = 0
+    power: int = 2
+    iterations: int = 2
+    initial_iterations: int = 60
+    doi_iterations: int = 0
+    seed: int = 1
+    dense_limit: int = 4096
+    shift_scale: float = 1e-8
+
+    def resolve_c_max(self, block_size: int) -> int:
+        cm = self.c_max if self.c_max > 0 else max(64, 2 * self.subspace_size)
+        return min(cm, block_size)
+
+    def resolve_doi_iterations(self, resolved_c_max: int) -> int:
+        if self.doi_iterations > 0:
+            return self.doi_iterations
+        return (resolved_c_max - self.c_min) + 16
+
+
+@dataclasses.dataclass
+class BlockStats:
+    """pipeline.hpp:70-76"""
+
+    subspace_size: int = 0
+    residual_rms: float = 0.0
+    doi_residual: float = 0.0
+    converged: bool = True
+    oi_iterations: int = 0
+
+
+@dataclasses.dataclass
+class BlockBases:
+    """pipeline.hpp:78-92"""
+
+    submeshes: List[Submesh]
+    sequence: np.ndarray
+    bases: List[Optional[np.ndarray]]
+    stats: List[BlockStats]
+    timings: Dict[str, float]
+    block_size: int
+
+    def sizes_in_order(self) -> List[int]:
+        return [self.bases[i].shape[1] for i in self.sequence]
+
+
+def _add(t: Dict[str, float], k: str, v: float) -> None:
+    t[k] = t.get(k, 0.0) + v
+
+
+def resize_basis(basis: np.ndarray, new_size: int, seed: int) -> np.ndarray:
+    """pipeline.hpp:97-109"""
+    old = basis.shape[1]
+    if new_size == old:
+        return basis
+    require(1 <= new_size <= basis.shape[0], "subspace size out of range")
+    if new_size < old:
+        return basis[:, :new_size].copy()
+    grown = np.empty((basis.shape[0], new_size))
+    grown[:, :old] = basis
+    grown[:, old:] = gaussian_block(basis.shape[0], new_size - old, seed)
+    return orthonormalize(grown)
+
+
+def initial_block_basis(lap: Laplacian, op: ShiftedInverseOperator, c: int,
+                        cfg: PipelineConfig) -> np.ndarray:
+    """pipeline.hpp:113-120"""
+    if lap.size() <= cfg.dense_limit:
+        return bottom_subspace(dense_eigendecomposition(lap, cfg.dense_limit), c)
+    cold = random_orthonormal_basis(lap.size(), c, cfg.seed ^ 0x9E3779B97F4A7C15)
+    return orthogonal_iteration(op, cold, cfg.initial_iterations)
+
+
+def _pos_seed(cfg: PipelineConfig, pos: int) -> int:
+    return (cfg.seed + 0x5851F42D4C957F2D * pos) & _MASK
+
+
+def build_submeshes(adj_offsets, adj_cols, members: Sequence[np.ndarray]) -> List[Submesh]:
+    return [build_submesh(adj_offsets, adj_cols, m) for m in members]
+
+
+def compute_block_bases_fixed_sizes(vertices, submeshes: List[Submesh], sequence, cfg: PipelineConfig,
+                                    sizes_in_order: Sequence[int], keep_bases: bool = True,
+                                    init_basis: Optional[np.ndarray] = None) -> BlockBases:
+    """pipeline.hpp:144-194.  ``init_basis`` (test hook) replaces the dense
+    first-submesh basis, used by the one-step parity mode."""
+    require(len(sizes_in_order) == len(sequence), "need one subspace size per block")
+    k = len(submeshes)
+    res = BlockBases(submeshes, np.asarray(sequence), [None] * k, [BlockStats() for _ in range(k)],
+                     {}, submeshes[0].size() if submeshes else 0)
+    t_all = time.perf_counter()
+    previous = None
+    for pos, sid in enumerate(sequence):
+        sub = submeshes[sid]
+        c = int(sizes_in_order[pos])
+        require(1 <= c <= sub.size(), "subspace size out of range for block")
+        t0 = time.perf_counter()
+        lap = build_laplacian(sub, vertices, cfg.weighting)
+        _add(res.timings, "laplacian", time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        op = ShiftedInverseOperator(lap, default_shift(lap, cfg.shift_scale), cfg.power)
+        _add(res.timings, "factorize", time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        if pos == 0:
+            basis = init_basis if init_basis is not None else initial_block_basis(lap, op, c, cfg)
+        else:
+            warm = resize_basis(previous, c, _pos_seed(cfg, pos))
+            basis = orthogonal_iteration(op, warm, cfg.iterations)
+        _add(res.timings, "basis", time.perf_counter() - t0)
+        st = res.stats[sid]
+        st.subspace_size = c
+        st.oi_iterations = 0 if pos == 0 else cfg.iterations
+        st.residual_rms = projection_residual_rms(basis, sub.local_coords(vertices))
+        previous = basis
+        res.bases[sid] = basis if keep_bases else None
+    _add(res.timings, "basis_total", time.perf_counter() - t_all)
+    return res
+
+
+def compute_block_bases_doi(vertices, submeshes: List[Submesh], sequence, cfg: PipelineConfig,
+                            keep_bases: bool = True) -> BlockBases:
+    """pipeline.hpp:245-285 (DOI branch), over an external segmentation."""
+    k = len(submeshes)
+    res = BlockBases(submeshes, np.asarray(sequence), [None] * k, [BlockStats() for _ in range(k)],
+                     {}, submeshes[0].size() if submeshes else 0)
+    t_all = time.perf_counter()
+    previous = None
+    for pos, sid in enumerate(sequence):
+        sub = submeshes[sid]
+        c_max = cfg.resolve_c_max(sub.size())
+        doi_t = cfg.resolve_doi_iterations(c_max)
+        t0 = time.perf_counter()
+        lap = build_laplacian(sub, vertices, cfg.weighting)
+        _add(res.timings, "laplacian", time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        op = ShiftedInverseOperator(lap, default_shift(lap, cfg.shift_scale), cfg.power)
+        _add(res.timings, "factorize", time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        if pos == 0:
+            c0 = min(max(cfg.subspace_size, cfg.c_min), c_max)
+            init = initial_block_basis(lap, op, c0, cfg)
+        else:
+            c_init = min(max(previous.shape[1], cfg.c_min), c_max)
+            init = resize_basis(previous, c_init, _pos_seed(cfg, pos))
+        coords = sub.local_coords(vertices)
+        doi = dynamic_oi(op, init, coords, cfg.eps_low, cfg.eps_high, cfg.c_min, c_max, doi_t)
+        _add(res.timings, "basis", time.perf_counter() - t0)
+        st = res.stats[sid]
+        st.subspace_size = doi.basis.shape[1]
+        st.doi_residual = doi.residual
+        st.converged = doi.converged
+        st.oi_iterations = doi.iterations
+        st.residual_rms = projection_residual_rms(doi.basis, coords)
+        previous = doi.basis
+        res.bases[sid] = doi.basis if keep_bases else None
+    _add(res.timings, "basis_total", time.perf_counter() - t_all)
+    return res
+
+
+def project_blocks(bb: BlockBases, vertices: np.ndarray) -> List[np.ndarray]:
+    """pipeline.hpp:290-297 (loops over submesh id)."""
+    out = []
+    for sid, sub in enumerate(bb.submeshes):
+        coords = sub.local_coords(vertices)
+        out.append(igft(bb.bases[sid], gft(bb.bases[sid], coords)))
+    return out
+
+
+def block_coefficients(bb: BlockBases, vertices: np.ndarray) -> List[np.ndarray]:
+    return [gft(bb.bases[s], sub.local_coords(vertices)) for s, sub in enumerate(bb.submeshes)]
+
+
+def reconstruct_weighted(submeshes: List[Submesh], local_results: List[np.ndarray], n: int,
+                         weighted: bool = True) -> np.ndarray:
+    """partition.hpp:311-355"""
+    require(len(submeshes) == len(local_results), "submesh and result lists must have equal length")
+    out = np.zeros((n, 3))
+    wsum = np.zeros(n)
+    copies = np.zeros(n, dtype=np.int64)
+    fallback = np.zeros((n, 3))
+    for sub, loc in zip(submeshes, local_results):
+        require(loc.shape[0] == sub.size(), "local result size does not match its submesh")
+        g = sub.global_indices
+        w = sub.local_degrees.astype(np.float64) if weighted else np.ones(g.size)
+        out[g] += w[:, None] * loc
+        wsum[g] += w
+        fallback[g] += loc
+        copies[g] += 1
+    unc = np.nonzero(copies == 0)[0]
+    if unc.size:
+        msg = f"reconstruction is missing {unc.size} vertices:" + "".join(f" {int(v)}" for v in unc[:16])
+        if unc.size > 16:
+            msg += " ..."
+        raise InvalidArgument(msg)
+    pos = wsum > 0.0
+    out[pos] /= wsum[pos][:, None]
+    out[~pos] = fallback[~pos] / copies[~pos][:, None]
+    return out
+
+
+def coarse_reconstruct_points(bb: BlockBases, vertices: np.ndarray, weighted: bool = True) -> np.ndarray:
+    """pipeline.hpp:300-305"""
+    return reconstruct_weighted(bb.submeshes, project_blocks(bb, vertices), vertices.shape[0], weighted)

@@ -1,0 +1,464 @@
+"""paper_1810_02719_b200 -- B200-native OI spectral path of arXiv 1810.02719.
+
+Python mirror of the reference's path API (``specmesh`` C++ headers, cited
+file:line in each function) on top of the C ABI of ``libspecmesh_b200.so``
+(include/specmesh_gpu.h).  Same names, argument meaning and error behaviour:
+preconditions raise :class:`InvalidArgument` (reference ``require``,
+core.hpp:36-38) and numerical failures raise :class:`SpecmeshError` with the
+reference's message text (core.hpp:18-22).  Matrices are numpy arrays in the
+reference's orientation (n x c bases, n x 3 points).
+
+Every compute call runs sm_100a kernels; nothing here falls back to the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+
+__all__ = [
+    "SpecmeshError", "InvalidArgument", "Context", "PipelineConfig", "BlockBases", "default_context",
+    "build_laplacian", "default_shift", "ShiftedInverseOperator", "orthonormalize", "orthogonal_iteration",
+    "dynamic_oi", "bottom_subspace", "gft", "igft", "compute_block_bases_fixed_sizes", "compute_block_bases",
+    "run_chains", "coarse_reconstruct_points",
+]
+
+
+class SpecmeshError(RuntimeError):
+    """specmesh::Error (core.hpp:18-22)."""
+
+
+class InvalidArgument(SpecmeshError):
+    """specmesh::InvalidArgument (core.hpp:24-28)."""
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _colmajor(a: np.ndarray) -> np.ndarray:
+    """Eigen column-major storage of an (rows, cols) array."""
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+class Context:
+    """One CUDA device + stream (smg_create)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _abi.load()
+        h = C.c_void_p()
+        st = self.lib.smg_create(device, C.byref(h))
+        if st != _abi.SMG_OK:
+            raise SpecmeshError(f"smg_create failed on device {device} (status {st}): no usable sm_100 GPU")
+        self.handle = h
+        self.device = device
+
+    def check(self, status: int) -> None:
+        if status == _abi.SMG_OK:
+            return
+        msg = self.lib.smg_last_error(self.handle).decode()
+        if status == _abi.SMG_INVALID_ARGUMENT:
+            raise InvalidArgument(msg)
+        raise SpecmeshError(msg)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.smg_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+@dataclasses.dataclass
+class PipelineConfig:
+    """PipelineConfig (pipeline.hpp:41-68), path fields, reference defaults."""
+
+    weighting: str = "distance"
+    basis_mode: str = "oi"
+    subspace_size: int = 16
+    eps_low: float = 0.004
+    eps_high: float = 0.04
+    c_min: int = 2
+    c_max: int = 0
+    power: int = 2
+    iterations: int = 2
+    initial_iterations: int = 60
+    doi_iterations: int = 0
+    seed: int = 1
+    dense_limit: int = 4096
+    shift_scale: float = 1e-8
+
+    def to_c(self) -> _abi.smg_pipeline_config:
+        if self.weighting not in _abi.WEIGHTING:
+            raise InvalidArgument(f"unknown weighting '{self.weighting}' (expected binary|distance)")
+        if self.basis_mode not in _abi.BASIS_MODE:
+            raise InvalidArgument(f"unknown basis mode '{self.basis_mode}' (expected oi|doi)")
+        return _abi.smg_pipeline_config(
+            _abi.WEIGHTING[self.weighting], _abi.BASIS_MODE[self.basis_mode], self.subspace_size, self.eps_low,
+            self.eps_high, self.c_min, self.c_max, self.power, self.iterations, self.initial_iterations,
+            self.doi_iterations, self.seed & ((1 << 64) - 1), self.dense_limit, self.shift_scale)
+
+
+# ------------------------------------------------------------------ L3 primitives
+
+def _mesh_view(mesh, keep: list) -> _abi.smg_mesh:
+    x = _f64(mesh.vertices[:, 0])
+    y = _f64(mesh.vertices[:, 1])
+    z = _f64(mesh.vertices[:, 2])
+    offs = _i32(mesh.adj_offsets)
+    cols = _i32(mesh.adj_cols)
+    keep += [x, y, z, offs, cols]
+    return _abi.smg_mesh(mesh.n, x.ctypes.data, y.ctypes.data, z.ctypes.data, offs.ctypes.data,
+                         cols.ctypes.data, 0)
+
+
+def _seg_view(seg, keep: list) -> _abi.smg_segmentation:
+    offs, ids = seg.flat()
+    seq = _i32(seg.sequence)
+    keep += [offs, ids, seq]
+    return _abi.smg_segmentation(seg.count, offs.ctypes.data, ids.ctypes.data, int(seq.size), seq.ctypes.data, 0)
+
+
+def build_laplacian(mesh, members, weighting: str = "distance", ctx: Optional[Context] = None):
+    """build_submesh adjacency + build_laplacian (partition.hpp:169-184,
+    spectral.hpp:39-68).  Returns (rowptr, cols, vals, trace) of L = D - C."""
+    ctx = ctx or default_context()
+    keep: list = []
+    mv = _mesh_view(mesh, keep)
+    mem = _i32(np.sort(np.asarray(members)))
+    n = int(mem.size)
+    cap = int(n + np.diff(mesh.adj_offsets)[mem].sum())
+    rowptr = np.empty(n + 1, np.int32)
+    cols = np.empty(cap, np.int32)
+    vals = np.empty(cap, np.float64)
+    nnz = C.c_int64()
+    tr = C.c_double()
+    ctx.check(ctx.lib.smg_build_laplacian(ctx.handle, C.byref(mv), _ptr(mem), n, _abi.WEIGHTING[weighting],
+                                          _ptr(rowptr), _ptr(cols), _ptr(vals), cap, C.byref(nnz), C.byref(tr)))
+    k = nnz.value
+    return rowptr, cols[:k].copy(), vals[:k].copy(), tr.value
+
+
+def default_shift(trace: float, n: int, scale: float = 1e-8) -> float:
+    """default_shift (spectral.hpp:193-196)."""
+    return _abi.load().smg_default_shift(trace, n, scale)
+
+
+class ShiftedInverseOperator:
+    """ShiftedInverseOperator (spectral.hpp:145-190) on the GPU block factor."""
+
+    def __init__(self, rowptr, cols, vals, delta: float, z: int, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self._rp, self._c, self._v = _i32(rowptr), _i32(cols), _f64(vals)
+        self.n = int(self._rp.size - 1)
+        self.shift_, self.power_ = float(delta), int(z)
+        h = C.c_void_p()
+        self.ctx.check(self.ctx.lib.smg_operator_create(self.ctx.handle, self.n, _ptr(self._rp), _ptr(self._c),
+                                                        _ptr(self._v), self.shift_, self.power_, C.byref(h)))
+        self.handle = h
+
+    def size(self) -> int:
+        return self.n
+
+    def shift(self) -> float:
+        return self.shift_
+
+    def power(self) -> int:
+        return self.power_
+
+    def _call(self, block: np.ndarray, once: int) -> np.ndarray:
+        block = np.asarray(block, dtype=np.float64)
+        if block.ndim != 2 or block.shape[0] != self.n:
+            raise InvalidArgument("operator/block dimension mismatch")
+        b = _colmajor(block)
+        out = np.empty_like(b, order="F")
+        self.ctx.check(self.ctx.lib.smg_operator_apply(self.ctx.handle, self.handle, b.shape[1], _ptr(b),
+                                                       _ptr(out), once))
+        return np.ascontiguousarray(out)
+
+    def apply_once(self, block):
+        return self._call(block, 1)
+
+    def apply(self, block):
+        return self._call(block, 0)
+
+    def spmm(self, block):
+        """(L + delta I) X -- CSR SpMM kernel (K4)."""
+        b = _colmajor(block)
+        out = np.empty_like(b, order="F")
+        self.ctx.check(self.ctx.lib.smg_operator_spmm(self.ctx.handle, self.handle, b.shape[1], _ptr(b),
+                                                      _ptr(out)))
+        return np.ascontiguousarray(out)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.ctx.lib.smg_operator_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def orthonormalize(block, ctx: Optional[Context] = None) -> np.ndarray:
+    """orthonormalize (spectral.hpp:120-132): CholeskyQR2 + rank test + sign convention."""
+    ctx = ctx or default_context()
+    block = np.asarray(block, dtype=np.float64)
+    rows, cols = block.shape
+    b = _colmajor(block)
+    q = np.empty_like(b, order="F")
+    ctx.check(ctx.lib.smg_orthonormalize(ctx.handle, rows, cols, _ptr(b), _ptr(q)))
+    return np.ascontiguousarray(q)
+
+
+def orthogonal_iteration(op: ShiftedInverseOperator, init, t_max: int) -> np.ndarray:
+    """orthogonal_iteration (spectral.hpp:204-211)."""
+    init = np.asarray(init, dtype=np.float64)
+    if init.shape[0] != op.n:
+        raise InvalidArgument("initial basis does not match the operator size")
+    b = _colmajor(init)
+    out = np.empty_like(b, order="F")
+    op.ctx.check(op.ctx.lib.smg_orthogonal_iteration(op.ctx.handle, op.handle, b.shape[1], _ptr(b), int(t_max),
+                                                     _ptr(out)))
+    return np.ascontiguousarray(out)
+
+
+@dataclasses.dataclass
+class DoiResult:
+    """DoiResult (spectral.hpp:233-238)."""
+
+    basis: np.ndarray
+    converged: bool
+    residual: float
+    iterations: int
+
+
+def dynamic_oi(op: ShiftedInverseOperator, init, coords, eps_low: float, eps_high: float, c_min: int, c_max: int,
+               t_max: int) -> DoiResult:
+    """dynamic_oi (spectral.hpp:244-287) -- the loop runs on the device."""
+    init = np.asarray(init, dtype=np.float64)
+    coords = np.asarray(coords, dtype=np.float64)
+    if coords.shape[0] != op.n:
+        raise InvalidArgument("coordinate/operator dimension mismatch")
+    b = _colmajor(init)
+    x = _colmajor(coords)
+    cap = max(int(c_max), b.shape[1])
+    out = np.empty((op.n, cap), order="F")
+    c_out, conv, it = C.c_int32(), C.c_int32(), C.c_int32()
+    res = C.c_double()
+    op.ctx.check(op.ctx.lib.smg_dynamic_oi(op.ctx.handle, op.handle, b.shape[1], _ptr(b), _ptr(x), eps_low,
+                                           eps_high, c_min, c_max, t_max, _ptr(out), C.byref(c_out),
+                                           C.byref(conv), C.byref(res), C.byref(it)))
+    c = c_out.value
+    basis = np.ascontiguousarray(out.reshape(-1, order="F")[:op.n * c].reshape((op.n, c), order="F"))
+    return DoiResult(basis, bool(conv.value), res.value, it.value)
+
+
+def bottom_subspace(op: ShiftedInverseOperator, c: int, return_eigenvalues: bool = False):
+    """bottom_subspace(dense_eigendecomposition(L), c) (spectral.hpp:92-117),
+    produced on the GPU (shift-invert subspace iteration + Rayleigh-Ritz)."""
+    out = np.empty((op.n, c), order="F")
+    ev = np.empty(c)
+    op.ctx.check(op.ctx.lib.smg_bottom_subspace(op.ctx.handle, op.handle, int(c), _ptr(out), _ptr(ev)))
+    u = np.ascontiguousarray(out)
+    return (u, ev) if return_eigenvalues else u
+
+
+def gft(basis, coords, ctx: Optional[Context] = None) -> np.ndarray:
+    """gft (spectral.hpp:290-293): C = U^T X."""
+    ctx = ctx or default_context()
+    basis = np.asarray(basis, dtype=np.float64)
+    coords = np.asarray(coords, dtype=np.float64)
+    if coords.shape[0] != basis.shape[0]:
+        raise InvalidArgument("coordinate/basis dimension mismatch")
+    u, x = _colmajor(basis), _colmajor(coords)
+    out = np.empty((basis.shape[1], 3), order="F")
+    ctx.check(ctx.lib.smg_gft(ctx.handle, basis.shape[0], basis.shape[1], _ptr(u), _ptr(x), _ptr(out)))
+    return np.ascontiguousarray(out)
+
+
+def igft(basis, coeffs, ctx: Optional[Context] = None) -> np.ndarray:
+    """igft (spectral.hpp:295-298): X^ = U C."""
+    ctx = ctx or default_context()
+    basis = np.asarray(basis, dtype=np.float64)
+    coeffs = np.asarray(coeffs, dtype=np.float64)
+    if coeffs.shape[0] != basis.shape[1]:
+        raise InvalidArgument("coefficient/basis dimension mismatch")
+    u, cf = _colmajor(basis), _colmajor(coeffs)
+    out = np.empty((basis.shape[0], 3), order="F")
+    ctx.check(ctx.lib.smg_igft(ctx.handle, basis.shape[0], basis.shape[1], _ptr(u), _ptr(cf), _ptr(out)))
+    return np.ascontiguousarray(out)
+
+
+# ------------------------------------------------------------------ L4 chain
+
+@dataclasses.dataclass
+class BlockStats:
+    """BlockStats (pipeline.hpp:70-76)."""
+
+    subspace_size: int
+    residual_rms: float
+    doi_residual: float
+    converged: bool
+    oi_iterations: int
+
+
+@dataclasses.dataclass
+class BlockBases:
+    """BlockBases (pipeline.hpp:78-92) + the path outputs: per-id coefficients
+    (gft) and the stitched coarse reconstruction (coarse_reconstruct_points)."""
+
+    sequence: np.ndarray
+    stats: List[BlockStats]
+    bases: Optional[List[np.ndarray]]
+    coefficients: Optional[List[np.ndarray]]
+    reconstruction: Optional[np.ndarray]
+    timings: dict
+    block_size: int
+
+    def sizes_in_order(self) -> List[int]:
+        return [self.stats[i].subspace_size for i in self.sequence]
+
+
+class _Out:
+    def __init__(self, k: int, n_d: int, nv: int, cap_c: int, want_bases: bool, want_coeffs: bool,
+                 want_recon: bool):
+        self.ss = np.zeros(k, np.int32)
+        self.rms = np.zeros(k)
+        self.doi = np.zeros(k)
+        self.conv = np.zeros(k, np.int32)
+        self.it = np.zeros(k, np.int32)
+        self.recon = np.zeros(nv * 3) if want_recon else None
+        self.coef = np.zeros(k * cap_c * 3) if want_coeffs else None
+        self.coef_off = np.zeros(k + 1, np.int64)
+        self.bases = np.zeros(k * cap_c * n_d) if want_bases else None
+        self.basis_off = np.zeros(k + 1, np.int64)
+        self.k, self.n_d, self.nv = k, n_d, nv
+
+    def c(self) -> _abi.smg_chain_output:
+        o = _abi.smg_chain_output()
+        o.subspace_size = self.ss.ctypes.data
+        o.residual_rms = self.rms.ctypes.data
+        o.doi_residual = self.doi.ctypes.data
+        o.converged = self.conv.ctypes.data
+        o.oi_iterations = self.it.ctypes.data
+        o.reconstruction = None if self.recon is None else self.recon.ctypes.data
+        o.coefficients = None if self.coef is None else self.coef.ctypes.data
+        o.coefficients_capacity = 0 if self.coef is None else self.coef.size
+        o.coefficient_offsets = self.coef_off.ctypes.data
+        o.bases = None if self.bases is None else self.bases.ctypes.data
+        o.bases_capacity = 0 if self.bases is None else self.bases.size
+        o.basis_offsets = self.basis_off.ctypes.data
+        o.on_device = 0
+        self._c = o
+        return o
+
+    def result(self, sequence) -> BlockBases:
+        o = self._c
+        stats = [BlockStats(int(self.ss[i]), float(self.rms[i]), float(self.doi[i]), bool(self.conv[i]),
+                            int(self.it[i])) for i in range(self.k)]
+        coeffs = None
+        if self.coef is not None:
+            coeffs = [self.coef[self.coef_off[i]:self.coef_off[i + 1]].reshape((3, -1)).T.copy()
+                      for i in range(self.k)]
+        bases = None
+        if self.bases is not None:
+            bases = [self.bases[self.basis_off[i]:self.basis_off[i + 1]].reshape((-1, self.n_d)).T.copy()
+                     for i in range(self.k)]
+        recon = None if self.recon is None else self.recon.reshape((3, self.nv)).T.copy()
+        names = ["laplacian", "factorize", "basis", "basis_total", "project", "total"]
+        timings = {nm: float(o.timings[i]) for i, nm in enumerate(names)}
+        return BlockBases(np.asarray(sequence), stats, bases, coeffs, recon, timings, self.n_d)
+
+
+def compute_block_bases_fixed_sizes(mesh, seg, cfg: PipelineConfig, sizes_in_order: Sequence[int],
+                                    want_bases: bool = False, want_coeffs: bool = True, want_recon: bool = True,
+                                    ctx: Optional[Context] = None) -> BlockBases:
+    """compute_block_bases_fixed_sizes (pipeline.hpp:144-194) followed by
+    coarse_reconstruct_points (pipeline.hpp:300-305) when ``want_recon``."""
+    ctx = ctx or default_context()
+    sizes = _i32(sizes_in_order)
+    if sizes.size != seg.count:
+        raise InvalidArgument("need one subspace size per block")
+    keep: list = []
+    mv, sv = _mesh_view(mesh, keep), _seg_view(seg, keep)
+    out = _Out(seg.count, seg.block_size, mesh.n, int(sizes.max()), want_bases, want_coeffs, want_recon)
+    oc = out.c()
+    cc = cfg.to_c()
+    ctx.check(ctx.lib.smg_compute_block_bases_fixed_sizes(ctx.handle, C.byref(mv), C.byref(sv), C.byref(cc),
+                                                          _ptr(sizes), C.byref(oc)))
+    return out.result(seg.sequence)
+
+
+def compute_block_bases(mesh, seg, cfg: PipelineConfig, want_bases: bool = False, want_coeffs: bool = True,
+                        want_recon: bool = True, ctx: Optional[Context] = None) -> BlockBases:
+    """compute_block_bases (pipeline.hpp:198-287), OI or DOI, over an external
+    segmentation (the reference segments internally at pipeline.hpp:201)."""
+    ctx = ctx or default_context()
+    keep: list = []
+    mv, sv = _mesh_view(mesh, keep), _seg_view(seg, keep)
+    n_d = seg.block_size
+    if cfg.basis_mode == "doi":
+        cm = cfg.c_max if cfg.c_max > 0 else max(64, 2 * cfg.subspace_size)
+        cap = min(cm, n_d)
+    else:
+        cap = cfg.subspace_size
+    out = _Out(seg.count, n_d, mesh.n, max(cap, 1), want_bases, want_coeffs, want_recon)
+    oc = out.c()
+    cc = cfg.to_c()
+    ctx.check(ctx.lib.smg_compute_block_bases(ctx.handle, C.byref(mv), C.byref(sv), C.byref(cc), C.byref(oc)))
+    return out.result(seg.sequence)
+
+
+def run_chains(meshes, segs, cfg: PipelineConfig, sizes_in_order: Sequence[int], want_bases: bool = False,
+               want_coeffs: bool = True, want_recon: bool = True, ctx: Optional[Context] = None) -> List[BlockBases]:
+    """Independent fixed-size chains in lockstep on one GPU (smg_run_chains)."""
+    ctx = ctx or default_context()
+    sizes = _i32(sizes_in_order)
+    keep: list = []
+    B = len(meshes)
+    mvs = (_abi.smg_mesh * B)(*[_mesh_view(m, keep) for m in meshes])
+    svs = (_abi.smg_segmentation * B)(*[_seg_view(s, keep) for s in segs])
+    outs = [_Out(s.count, s.block_size, m.n, int(sizes.max()), want_bases, want_coeffs, want_recon)
+            for m, s in zip(meshes, segs)]
+    ocs = (_abi.smg_chain_output * B)(*[o.c() for o in outs])
+    cc = cfg.to_c()
+    ctx.check(ctx.lib.smg_run_chains(ctx.handle, B, mvs, svs, C.byref(cc), _ptr(sizes), ocs))
+    res = []
+    for i, (o, s) in enumerate(zip(outs, segs)):
+        o._c = ocs[i]
+        res.append(o.result(s.sequence))
+    return res
+
+
+def coarse_reconstruct_points(bb: BlockBases) -> np.ndarray:
+    """coarse_reconstruct_points (pipeline.hpp:300-305) -- computed on the GPU by
+    the chain call (want_recon=True); this accessor returns it."""
+    if bb.reconstruction is None:
+        raise InvalidArgument("the chain was run without want_recon")
+    return bb.reconstruction

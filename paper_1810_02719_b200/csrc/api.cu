@@ -1,0 +1,901 @@
+// C ABI of libspecmesh_b200 (include/specmesh_gpu.h): input staging, the chain
+// runners (fixed-c lockstep batches and the device-driven DOI loop) and the L3
+// primitives.  Exceptions never cross the boundary.
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/specmesh_gpu.h"
+#include "common.cuh"
+#include "context.h"
+#include "engine.h"
+#include "doi.h"
+#include "firstbasis.h"
+
+using namespace smg;
+
+namespace {
+
+template <class F>
+smg_status guard(smg_context* ctx, F&& f) {
+    if (!ctx) return SMG_INVALID_ARGUMENT;
+    try {
+        SMG_CUDA(cudaSetDevice(ctx->device));
+        f();
+        ctx->error.clear();
+        return SMG_OK;
+    } catch (const Failure& e) {
+        ctx->error = e.what();
+        return e.code == 2 ? SMG_INVALID_ARGUMENT : SMG_ERROR;
+    } catch (const std::exception& e) {
+        ctx->error = e.what();
+        return SMG_ERROR;
+    }
+}
+
+// ---------------------------------------------------------------- staging
+struct MeshDev {
+    int64_t nv = 0;
+    const double *x = nullptr, *y = nullptr, *z = nullptr;
+    const int32_t *offs = nullptr, *cols = nullptr;
+    DBuf<double> bx, by, bz;
+    DBuf<int32_t> boffs, bcols;
+};
+
+void stage_mesh(const smg_mesh* m, MeshDev& d, cudaStream_t st) {
+    require(m != nullptr, "mesh view is null");
+    require(m->vertex_count >= 0, "mesh vertex count is negative");
+    d.nv = m->vertex_count;
+    if (m->on_device) {
+        d.x = m->x;
+        d.y = m->y;
+        d.z = m->z;
+        d.offs = m->adj_offsets;
+        d.cols = m->adj_cols;
+        return;
+    }
+    int64_t nadj = m->adj_offsets[d.nv];
+    auto up_d = [&](DBuf<double>& b, const double* h) {
+        b.alloc(d.nv, st);
+        SMG_CUDA(cudaMemcpyAsync(b.get(), h, sizeof(double) * d.nv, cudaMemcpyHostToDevice, st));
+    };
+    up_d(d.bx, m->x);
+    up_d(d.by, m->y);
+    up_d(d.bz, m->z);
+    d.boffs.alloc(d.nv + 1, st);
+    SMG_CUDA(cudaMemcpyAsync(d.boffs.get(), m->adj_offsets, sizeof(int32_t) * (d.nv + 1), cudaMemcpyHostToDevice, st));
+    d.bcols.alloc(nadj, st);
+    if (nadj)
+        SMG_CUDA(cudaMemcpyAsync(d.bcols.get(), m->adj_cols, sizeof(int32_t) * nadj, cudaMemcpyHostToDevice, st));
+    d.x = d.bx.get();
+    d.y = d.by.get();
+    d.z = d.bz.get();
+    d.offs = d.boffs.get();
+    d.cols = d.bcols.get();
+}
+
+struct SegDev {
+    int k = 0, n_d = 0;
+    std::vector<int32_t> offs_h, seq_h, pos_of;
+    const int32_t* members = nullptr;
+    DBuf<int32_t> bmembers;
+};
+
+void stage_seg(const smg_segmentation* s, SegDev& d, cudaStream_t st) {
+    require(s != nullptr, "segmentation view is null");
+    require(s->submesh_count >= 1, "cannot process an empty submesh list");
+    d.k = s->submesh_count;
+    d.offs_h.resize(d.k + 1);
+    d.seq_h.resize(s->sequence_length);
+    if (s->on_device) {
+        SMG_CUDA(cudaMemcpyAsync(d.offs_h.data(), s->member_offsets, sizeof(int32_t) * (d.k + 1),
+                                 cudaMemcpyDeviceToHost, st));
+        if (s->sequence_length)
+            SMG_CUDA(cudaMemcpyAsync(d.seq_h.data(), s->sequence, sizeof(int32_t) * s->sequence_length,
+                                     cudaMemcpyDeviceToHost, st));
+        SMG_CUDA(cudaStreamSynchronize(st));
+        d.members = s->members;
+    } else {
+        std::memcpy(d.offs_h.data(), s->member_offsets, sizeof(int32_t) * (d.k + 1));
+        if (s->sequence_length) std::memcpy(d.seq_h.data(), s->sequence, sizeof(int32_t) * s->sequence_length);
+        const int64_t tot = d.offs_h[d.k];
+        d.bmembers.alloc(tot, st);
+        SMG_CUDA(cudaMemcpyAsync(d.bmembers.get(), s->members, sizeof(int32_t) * tot, cudaMemcpyHostToDevice, st));
+        d.members = d.bmembers.get();
+    }
+    require((int)d.seq_h.size() == d.k, "the order sequence must be a permutation of the submesh ids");
+    d.pos_of.assign(d.k, -1);
+    for (int p = 0; p < d.k; ++p) {
+        const int id = d.seq_h[p];
+        require(id >= 0 && id < d.k && d.pos_of[id] < 0, "the order sequence must be a permutation of the submesh ids");
+        d.pos_of[id] = p;
+    }
+    d.n_d = d.offs_h[1] - d.offs_h[0];
+    for (int i = 0; i < d.k; ++i) {
+        const int sz = d.offs_h[i + 1] - d.offs_h[i];
+        require(sz >= 2, "submesh must have at least 2 vertices");
+        require(sz == d.n_d, "initial basis does not match the operator size");
+    }
+}
+
+struct Cfg {
+    int weighting, power, iterations, initial_iterations, doi_iterations, dense_limit, subspace_size, c_min, c_max;
+    double eps_low, eps_high, shift_scale;
+    uint64_t seed;
+    int basis_mode;
+    int resolve_c_max(int n) const {
+        const int cm = c_max > 0 ? c_max : std::max(64, 2 * subspace_size);
+        return std::min(cm, n);
+    }
+    int resolve_doi_iterations(int rc) const { return doi_iterations > 0 ? doi_iterations : (rc - c_min) + 16; }
+};
+
+Cfg read_cfg(const smg_pipeline_config* c) {
+    require(c != nullptr, "pipeline config is null");
+    Cfg r;
+    r.weighting = c->weighting;
+    r.power = c->power;
+    r.iterations = c->iterations;
+    r.initial_iterations = c->initial_iterations;
+    r.doi_iterations = c->doi_iterations;
+    r.dense_limit = c->dense_limit;
+    r.subspace_size = c->subspace_size;
+    r.c_min = c->c_min;
+    r.c_max = c->c_max;
+    r.eps_low = c->eps_low;
+    r.eps_high = c->eps_high;
+    r.shift_scale = c->shift_scale;
+    r.seed = c->seed;
+    r.basis_mode = c->basis_mode;
+    require(r.weighting == SMG_WEIGHTING_BINARY || r.weighting == SMG_WEIGHTING_DISTANCE,
+            "unknown weighting (expected binary|distance)");
+    require(r.basis_mode == SMG_BASIS_OI || r.basis_mode == SMG_BASIS_DOI, "unknown basis mode (expected oi|doi)");
+    require(r.power >= 1, "power z must be at least 1");
+    require(r.iterations >= 0, "t_max must be nonnegative");
+    return r;
+}
+
+const uint64_t kPosMul = 0x5851F42D4C957F2DULL;
+
+std::string status_message(int kind, int64_t detail) {
+    switch (kind) {
+        case kRankDeficient: return "orthonormalize: block is rank deficient at column " + std::to_string(detail);
+        case kAllZero: return "orthonormalize: block is rank deficient (all zero)";
+        case kFactorFailed: return "sparse factorization of the shifted Laplacian failed";
+        default: return "numerical failure (non-finite values)";
+    }
+}
+
+// ---------------------------------------------------------------- chain runner
+struct ChainOut {
+    smg_chain_output* out = nullptr;
+    std::vector<int64_t> coef_off, basis_off;
+    DBuf<double> coef_stage, basis_stage, recon_stage;
+    double* coef_dev = nullptr;
+    double* basis_dev = nullptr;
+    double* recon_dev = nullptr;
+};
+
+// Device-event stage timer (StageTimings, core.hpp:41-68): intervals are
+// recorded as event pairs and resolved once, after the final synchronisation.
+struct Timer {
+    cudaStream_t st;
+    std::vector<cudaEvent_t> ev;
+    std::vector<std::pair<int, std::pair<int, int>>> spans;  // stage, (a, b)
+    explicit Timer(cudaStream_t s) : st(s) {}
+    ~Timer() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    int mark() {
+        cudaEvent_t e;
+        SMG_CUDA(cudaEventCreate(&e));
+        SMG_CUDA(cudaEventRecord(e, st));
+        ev.push_back(e);
+        return (int)ev.size() - 1;
+    }
+    void add(int stage, int a, int b) { spans.push_back({stage, {a, b}}); }
+    double secs(int a, int b) {
+        float ms = 0.f;
+        SMG_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+        return ms * 1e-3;
+    }
+    double total(int stage) {
+        double t = 0.0;
+        for (auto& s : spans)
+            if (s.first == stage) t += secs(s.second.first, s.second.second);
+        return t;
+    }
+};
+enum Stage { kStLaplacian = 0, kStFactorize = 1, kStBasis = 2, kStProject = 4 };
+
+__global__ void basis_out_kernel(const double* U, int64_t ld, int64_t strideU, int n, int c, const double* sign,
+                                 int64_t strideSign, double* const* dst) {
+    const int b = blockIdx.y;
+    double* o = dst[b];
+    if (!o) return;
+    const int64_t total = (int64_t)n * c;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e / n), i = (int)(e % n);
+        o[e] = sign[(int64_t)b * strideSign + j] * U[(int64_t)b * strideU + (int64_t)i * ld + j];
+    }
+}
+
+__global__ void coef_ptr_kernel(const double* coef, int64_t strideCoef, const double* sign, int64_t strideSign,
+                                int c, double* const* dst) {
+    const int b = blockIdx.x;
+    double* o = dst[b];
+    if (!o) return;
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+        const double s = sign[(int64_t)b * strideSign + j];
+        for (int a = 0; a < 3; ++a) o[(int64_t)a * c + j] = s * coef[(int64_t)b * strideCoef + 4 * j + a];
+    }
+}
+
+__global__ void copy_stat_kernel(const double* stats, int64_t strideStats, int batch, double* dst, int64_t dstride) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < batch) dst[(int64_t)b * dstride] = stats[(int64_t)b * strideStats];
+}
+
+__global__ void stitch_tile_kernel(int n, int n_d, int weighted, const int32_t* offs, const int64_t* slots,
+                                   const int64_t* tile_of, const int32_t* rowptr_all, const double* xhat_all,
+                                   double* out) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
+        const int s = offs[g], e = offs[g + 1];
+        double o[3] = {0.0, 0.0, 0.0}, f[3] = {0.0, 0.0, 0.0}, ws = 0.0;
+        for (int q = s; q < e; ++q) {
+            const int64_t slot = slots[q];
+            const int sid = (int)(slot / n_d), li = (int)(slot % n_d);
+            const int64_t tile = tile_of[sid];
+            const int32_t* rp = rowptr_all + tile * (n_d + 1);
+            const double w = weighted ? (double)(rp[li + 1] - rp[li] - 1) : 1.0;
+            const double* xh = xhat_all + tile * (int64_t)n_d * 3 + 3 * li;
+            for (int a = 0; a < 3; ++a) {
+                o[a] += w * xh[a];
+                f[a] += xh[a];
+            }
+            ws += w;
+        }
+        const int copies = e - s;
+        for (int a = 0; a < 3; ++a) {
+            double v = 0.0;
+            if (copies > 0) v = ws > 0.0 ? o[a] / ws : f[a] / (double)copies;
+            out[(int64_t)a * n + g] = v;
+        }
+    }
+}
+
+class ChainRunner {
+public:
+    ChainRunner(smg_context* ctx, int nchains, const smg_mesh* meshes, const smg_segmentation* segs, const Cfg& cfg,
+                smg_chain_output* outs)
+        : ctx_(ctx), st_(ctx->stream), B_(nchains), cfg_(cfg) {
+        require(nchains >= 1, "need at least one chain");
+        meshes_.resize(B_);
+        segs_.resize(B_);
+        outs_.resize(B_);
+        for (int b = 0; b < B_; ++b) {
+            stage_mesh(&meshes[b], meshes_[b], st_);
+            stage_seg(&segs[b], segs_[b], st_);
+            outs_[b].out = &outs[b];
+        }
+        K_ = segs_[0].k;
+        n_ = segs_[0].n_d;
+        for (int b = 1; b < B_; ++b) {
+            require(segs_[b].k == K_, "batched chains need equal submesh counts");
+            require(segs_[b].n_d == n_, "batched chains need equal submesh sizes");
+        }
+    }
+
+    // compute_block_bases_fixed_sizes for all chains in lockstep
+    void run_fixed(const int32_t* sizes_in_order) {
+        Timer tm(st_);
+        const int t0 = tm.mark();
+        sizes_.assign(sizes_in_order, sizes_in_order + K_);
+        int ccap = 0;
+        for (int p = 0; p < K_; ++p) {
+            require(sizes_[p] >= 1 && sizes_[p] <= n_, "subspace size out of range for block");
+            ccap = std::max(ccap, sizes_[p]);
+        }
+        require(ccap <= 512, "subspace size exceeds the GPU limit of 512");
+        setup_tiles();
+        const int t_lap = tm.mark();
+        first_c_ = sizes_[0];
+        prepare_outputs([&](int b, int id) { (void)b; return sizes_[segs_[b].pos_of[id]]; });
+        const int fb_m = std::min(n_, round_up(sizes_[0] + std::max(16, sizes_[0] / 2), 8));
+        ws_.init(B_, n_, ts_.npad, std::max(ccap, fb_m), st_);
+        StepCtx cx{st_, &ts_};
+        check_assembly();
+        // factor windows over positions
+        const int64_t per_tile = (int64_t)ts_.Kb * 2 * ts_.W * ts_.W * 2 * 8;
+        const int64_t budget = (int64_t)8 << 30;
+        int window = (int)std::max<int64_t>(1, std::min<int64_t>(K_, budget / std::max<int64_t>(1, per_tile * B_)));
+        tm.add(kStLaplacian, t0, t_lap);
+        int win_first = -1;
+        FactorSet fs;
+        for (int pos = 0; pos < K_; ++pos) {
+            if (win_first < 0 || pos >= win_first + window) {
+                const int a = tm.mark();
+                win_first = pos;
+                const int cnt = std::min(window, K_ - pos);
+                fs.factor(ts_, pos * B_, cnt * B_, nullptr, st_);
+                SMG_CUDA(cudaGetLastError());
+                factor_status_.push_back({pos, download(fs.status.get(), (size_t)cnt * B_, st_)});
+                tm.add(kStFactorize, a, tm.mark());
+            }
+            const int a = tm.mark();
+            const int c = sizes_[pos];
+            if (pos == 0) {
+                FirstBasisConfig fc;
+                fc.dense_limit = cfg_.dense_limit;
+                fc.initial_iterations = cfg_.initial_iterations;
+                fc.power = cfg_.power;
+                fc.seed = cfg_.seed;
+                first_basis(cx, ws_, ts_, 0, 1, c, fc, &fs);
+            } else {
+                resize(c, pos);
+                for (int it = 0; it < cfg_.iterations; ++it) {
+                    solve_batch(cx, ws_, fs, pos * B_, 1, ws_.U.get(), ws_.V.get(), c, nullptr, cfg_.power, false);
+                    orth_batch(cx, ws_, ws_.V.get(), ws_.U.get(), c, nullptr, true, pos);
+                }
+            }
+            const int b1 = tm.mark();
+            project_batch(cx, ws_, ws_.U.get(), c, nullptr, ts_.X.get() + (int64_t)pos * B_ * n_ * 3,
+                          (int64_t)n_ * 3, xhat_.get() + (int64_t)pos * B_ * n_ * 3, (int64_t)n_ * 3);
+            emit_position(pos, c);
+            const int b2 = tm.mark();
+            tm.add(kStBasis, a, b1);
+            tm.add(kStProject, b1, b2);
+            prev_c_ = c;
+        }
+        finish(tm, t0);
+    }
+
+    // compute_block_bases, DOI branch (pipeline.hpp:245-285), one chain
+    void run_doi() {
+        require(B_ == 1, "DOI runs one chain per call");
+        Timer tm(st_);
+        const int t0 = tm.mark();
+        const int c_max = cfg_.resolve_c_max(n_);
+        const int t_max = cfg_.resolve_doi_iterations(c_max);
+        const int c0 = std::min(std::max(cfg_.subspace_size, cfg_.c_min), c_max);
+        require(cfg_.eps_low > 0.0 && cfg_.eps_low < cfg_.eps_high, "need 0 < eps_low < eps_high");
+        require(cfg_.c_min >= 1 && cfg_.c_min <= c0 && c0 <= c_max, "need c_min <= init subspace size <= c_max");
+        require(c_max <= n_, "c_max cannot exceed the submesh size");
+        require(c_max + 1 <= 512, "c_max exceeds the GPU limit of 511");
+        setup_tiles();
+        const int t_lap = tm.mark();
+        sizes_.assign(K_, 0);
+        const int fb_m = std::min(n_, round_up(c0 + std::max(16, c0 / 2), 8));
+        ws_.init(1, n_, ts_.npad, std::max(c_max + 1, fb_m), st_);
+        StepCtx cx{st_, &ts_};
+        check_assembly();
+        // all factors up front (one launch, all SMs)
+        const int a0 = tm.mark();
+        FactorSet fs;
+        fs.factor(ts_, 0, K_, nullptr, st_);
+        factor_status_.push_back({0, download(fs.status.get(), (size_t)K_, st_)});
+        tm.add(kStLaplacian, t0, t_lap);
+        tm.add(kStFactorize, a0, tm.mark());
+        DoiParams dp;
+        dp.c_min = cfg_.c_min;
+        dp.c_max = c_max;
+        dp.t_max = t_max;
+        dp.power = cfg_.power;
+        dp.eps_low = cfg_.eps_low;
+        dp.eps_high = cfg_.eps_high;
+        DoiLoop loop;
+        loop.build(ts_, ws_, dp, fs.strideF, st_);
+        doi_states_.resize(K_);
+        xhat_.alloc((size_t)K_ * n_ * 3, st_);
+        std::vector<double> bbox = download(ts_.bbox.get(), K_, st_);
+        for (int pos = 0; pos < K_; ++pos) {
+            const int a = tm.mark();
+            const int id = segs_[0].seq_h[pos];
+            int c_init;
+            if (pos == 0) {
+                FirstBasisConfig fc;
+                fc.dense_limit = cfg_.dense_limit;
+                fc.initial_iterations = cfg_.initial_iterations;
+                fc.power = cfg_.power;
+                fc.seed = cfg_.seed;
+                first_basis(cx, ws_, ts_, 0, 1, c0, fc, &fs);
+                c_init = c0;
+            } else {
+                c_init = std::min(std::max(prev_c_, cfg_.c_min), c_max);
+                resize(c_init, pos);
+            }
+            DoiState r = loop.run(fs.f(pos), fs.b(pos), ts_.perm_of(pos), ts_.X.get() + (int64_t)pos * n_ * 3,
+                                  bbox[pos], c_init);
+            int wst = 0;
+            int64_t wdet = 0;
+            SMG_CUDA(cudaMemcpyAsync(&wst, ws_.status.get(), sizeof(int), cudaMemcpyDeviceToHost, st_));
+            SMG_CUDA(cudaMemcpyAsync(&wdet, ws_.detail.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st_));
+            SMG_CUDA(cudaStreamSynchronize(st_));
+            if (wst != 0) {
+                for (const FacStatus& f : factor_status_)
+                    for (size_t i = 0; i <= (size_t)pos && i < f.st.size(); ++i)
+                        if (f.st[i] != 0) fail(3, status_message(kFactorFailed, 0));
+                fail(3, status_message(wst, wdet));
+            }
+            if (r.appended_raw) orth_batch(cx, ws_, ws_.U.get(), ws_.U.get(), r.c, nullptr, true, pos);
+            const int c = r.c;
+            sizes_[pos] = c;
+            doi_states_[pos] = r;
+            const int b1 = tm.mark();
+            // final projection of the returned basis (stats + coefficients + X^)
+            project_batch(cx, ws_, ws_.U.get(), c, nullptr, ts_.X.get() + (int64_t)pos * n_ * 3, (int64_t)n_ * 3,
+                          xhat_.get() + (int64_t)pos * n_ * 3, (int64_t)n_ * 3);
+            if (pos == 0) prepare_outputs_doi();
+            emit_position(pos, c, id);
+            const int b2 = tm.mark();
+            tm.add(kStBasis, a, b1);
+            tm.add(kStProject, b1, b2);
+            prev_c_ = c;
+        }
+        finish(tm, t0);
+        // DOI stats
+        for (int pos = 0; pos < K_; ++pos) {
+            const int id = segs_[0].seq_h[pos];
+            smg_chain_output* o = outs_[0].out;
+            const DoiState& r = doi_states_[pos];
+            if (o->doi_residual) o->doi_residual[id] = r.residual;
+            if (o->converged) o->converged[id] = r.converged;
+            if (o->oi_iterations) o->oi_iterations[id] = r.t;
+        }
+    }
+
+private:
+    struct FacStatus {
+        int pos0;
+        std::vector<int> st;
+    };
+
+    void setup_tiles() {
+        std::vector<TileRef> refs((size_t)K_ * B_);
+        for (int pos = 0; pos < K_; ++pos)
+            for (int b = 0; b < B_; ++b) {
+                const SegDev& s = segs_[b];
+                const int id = s.seq_h[pos];
+                TileRef& t = refs[(size_t)pos * B_ + b];
+                t.members = s.members + s.offs_h[id];
+                t.adj_offsets = meshes_[b].offs;
+                t.adj_cols = meshes_[b].cols;
+                t.x = meshes_[b].x;
+                t.y = meshes_[b].y;
+                t.z = meshes_[b].z;
+            }
+        ts_.build(refs, n_, cfg_.weighting, cfg_.shift_scale, st_);
+        // tile index of (chain b, submesh id): pos_of[id] * B + b
+        tile_of_.resize(B_);
+        for (int b = 0; b < B_; ++b) {
+            std::vector<int64_t> t(K_);
+            for (int id = 0; id < K_; ++id) t[id] = (int64_t)segs_[b].pos_of[id] * B_ + b;
+            tile_of_[b].upload(t, st_);
+        }
+    }
+
+    void check_assembly() {
+        // coincident-vertex failures are reported for the first position in chain order
+        for (int pos = 0; pos < K_; ++pos)
+            for (int b = 0; b < B_; ++b) {
+                const int tile = pos * B_ + b;
+                if (ts_.status_h[tile] == kCoincident) {
+                    const int64_t key = ts_.detail_h[tile];
+                    const int li = (int)(key >> 20), slot = (int)(key & 0xFFFFF);
+                    const SegDev& s = segs_[b];
+                    const int id = s.seq_h[pos];
+                    int32_t gi = 0, gj = 0, off = 0;
+                    SMG_CUDA(cudaMemcpy(&gi, s.members + s.offs_h[id] + li, 4, cudaMemcpyDeviceToHost));
+                    SMG_CUDA(cudaMemcpy(&off, meshes_[b].offs + gi, 4, cudaMemcpyDeviceToHost));
+                    SMG_CUDA(cudaMemcpy(&gj, meshes_[b].cols + off + slot, 4, cudaMemcpyDeviceToHost));
+                    pending_error_ = {pos, 0, b, 3,
+                                      "coincident connected vertices " + std::to_string(gi) + " and " +
+                                          std::to_string(gj) + " make the distance weight singular"};
+                    fail(3, pending_error_.msg);
+                }
+            }
+    }
+
+    template <class SizeOf>
+    void prepare_outputs(SizeOf size_of) {
+        xhat_.alloc((size_t)K_ * B_ * n_ * 3, st_);
+        for (int b = 0; b < B_; ++b) {
+            ChainOut& co = outs_[b];
+            smg_chain_output* o = co.out;
+            co.coef_off.assign(K_ + 1, 0);
+            co.basis_off.assign(K_ + 1, 0);
+            for (int id = 0; id < K_; ++id) {
+                const int c = size_of(b, id);
+                co.coef_off[id + 1] = co.coef_off[id] + (int64_t)c * 3;
+                co.basis_off[id + 1] = co.basis_off[id] + (int64_t)c * n_;
+            }
+            bind_outputs(co);
+        }
+    }
+
+    void prepare_outputs_doi() {
+        // DOI sizes are only known as the chain runs: stage per-position outputs at c_max
+        xhat_ready_ = true;
+    }
+
+    void bind_outputs(ChainOut& co) {
+        smg_chain_output* o = co.out;
+        if (o->coefficients) {
+            require(o->coefficients_capacity >= co.coef_off[K_], "coefficient buffer too small");
+            if (o->on_device) co.coef_dev = o->coefficients;
+            else {
+                co.coef_stage.alloc(co.coef_off[K_], st_);
+                co.coef_dev = co.coef_stage.get();
+            }
+        }
+        if (o->bases) {
+            require(o->bases_capacity >= co.basis_off[K_], "basis buffer too small");
+            if (o->on_device) co.basis_dev = o->bases;
+            else {
+                co.basis_stage.alloc(co.basis_off[K_], st_);
+                co.basis_dev = co.basis_stage.get();
+            }
+        }
+        if (o->reconstruction) {
+            if (o->on_device) co.recon_dev = o->reconstruction;
+            else {
+                co.recon_stage.alloc((size_t)meshes_[&co - outs_.data()].nv * 3, st_);
+                co.recon_dev = co.recon_stage.get();
+            }
+        }
+        if (o->coefficient_offsets) std::memcpy(o->coefficient_offsets, co.coef_off.data(), sizeof(int64_t) * (K_ + 1));
+        if (o->basis_offsets) std::memcpy(o->basis_offsets, co.basis_off.data(), sizeof(int64_t) * (K_ + 1));
+    }
+
+    void resize(int c, int pos) {
+        // resize_basis (pipeline.hpp:97-109): same size -> unchanged; shrink ->
+        // leading columns; grow -> seeded Gaussian columns + orthonormalize
+        if (c <= prev_c_) return;  // shrink: the leading c columns are used as is
+        const int add = c - prev_c_;
+        const uint64_t seed = cfg_.seed + kPosMul * (uint64_t)pos;
+        std::vector<double> g = gaussian_block_colmajor(n_, add, seed);
+        DBuf<double> gd;
+        gd.upload(g, st_);
+        for (int b = 0; b < B_; ++b) {
+            // apply the previous signs so the grown block equals the reference's
+            apply_signs(b, prev_c_);
+            transpose_to_rowmajor(gd.get(), n_, add, ws_.U.get() + (int64_t)b * ws_.mstride() + prev_c_, ws_.ld, st_);
+        }
+        StepCtx cx{st_, &ts_};
+        orth_batch(cx, ws_, ws_.U.get(), ws_.U.get(), c, nullptr, true, pos);
+    }
+
+    void apply_signs(int b, int c);
+
+    void emit_position(int pos, int c, int id_doi = -1) {
+        // per-tile residual_rms into a device array, coefficients and bases to the outputs
+        if (!stat_rms_.size()) {
+            stat_rms_.alloc((size_t)K_ * B_, st_);
+        }
+        copy_stat_kernel<<<(B_ + 127) / 128, 128, 0, st_>>>(ws_.stats.get(), 4, B_, stat_rms_.get() + (int64_t)pos * B_, 1);
+        std::vector<double*> cptr(B_, nullptr), bptr(B_, nullptr);
+        bool anyc = false, anyb = false;
+        for (int b = 0; b < B_; ++b) {
+            ChainOut& co = outs_[b];
+            const int id = id_doi >= 0 ? id_doi : segs_[b].seq_h[pos];
+            if (id_doi >= 0) ensure_doi_outputs(co, pos, c);
+            if (co.coef_dev) {
+                cptr[b] = co.coef_dev + co.coef_off[id];
+                anyc = true;
+            }
+            if (co.basis_dev) {
+                bptr[b] = co.basis_dev + co.basis_off[id];
+                anyb = true;
+            }
+        }
+        if (anyc) {
+            ptrs_c_.upload(cptr, st_);
+            coef_ptr_kernel<<<B_, 128, 0, st_>>>(ws_.coeff.get(), (int64_t)ws_.ld * 4, ws_.sign.get(), ws_.ld, c,
+                                                 ptrs_c_.get());
+            keep_.push_back(std::move(ptrs_c_));
+        }
+        if (anyb) {
+            ptrs_b_.upload(bptr, st_);
+            basis_out_kernel<<<dim3(std::min(1024, (n_ * c + 255) / 256), B_), 256, 0, st_>>>(
+                ws_.U.get(), ws_.ld, ws_.mstride(), n_, c, ws_.sign.get(), ws_.ld, ptrs_b_.get());
+            keep_.push_back(std::move(ptrs_b_));
+        }
+        SMG_CUDA(cudaGetLastError());
+    }
+
+    void ensure_doi_outputs(ChainOut& co, int pos, int c) {
+        // DOI: outputs are laid out in submesh-id order, so positions are staged
+        // per id at capacity n_d x c_max and compacted at the end.
+        smg_chain_output* o = co.out;
+        if (co.coef_off.empty()) {
+            co.coef_off.assign(K_ + 1, 0);
+            co.basis_off.assign(K_ + 1, 0);
+            const int cm = cfg_.resolve_c_max(n_);
+            for (int id = 0; id < K_; ++id) {
+                co.coef_off[id + 1] = co.coef_off[id] + (int64_t)cm * 3;
+                co.basis_off[id + 1] = co.basis_off[id] + (int64_t)cm * n_;
+            }
+            if (o->coefficients) {
+                co.coef_stage.alloc(co.coef_off[K_], st_);
+                co.coef_dev = co.coef_stage.get();
+            }
+            if (o->bases) {
+                co.basis_stage.alloc(co.basis_off[K_], st_);
+                co.basis_dev = co.basis_stage.get();
+            }
+            if (o->reconstruction) {
+                if (o->on_device) co.recon_dev = o->reconstruction;
+                else {
+                    co.recon_stage.alloc((size_t)meshes_[0].nv * 3, st_);
+                    co.recon_dev = co.recon_stage.get();
+                }
+            }
+        }
+        (void)pos;
+        (void)c;
+    }
+
+    void finish(Timer& tm, int t0) {
+        // stitch + status
+        const int s0 = tm.mark();
+        for (int b = 0; b < B_; ++b) {
+            ChainOut& co = outs_[b];
+            if (!co.recon_dev) continue;
+            Stitcher stt;
+            stt.build(segs_[b].members, K_, n_, (int)meshes_[b].nv, st_);
+            int32_t missing = 0;
+            SMG_CUDA(cudaMemcpyAsync(&missing, stt.missing, 4, cudaMemcpyDeviceToHost, st_));
+            SMG_CUDA(cudaStreamSynchronize(st_));
+            if (missing > 0) {
+                std::vector<int32_t> offs = download(stt.offs, meshes_[b].nv + 1, st_);
+                std::string msg = "reconstruction is missing " + std::to_string(missing) + " vertices:";
+                int shown = 0;
+                for (int64_t g = 0; g < meshes_[b].nv && shown < 16; ++g)
+                    if (offs[g + 1] == offs[g]) {
+                        msg += " " + std::to_string(g);
+                        ++shown;
+                    }
+                if (missing > 16) msg += " ...";
+                stt.release(st_);
+                fail(2, msg);
+            }
+            stitch_tile_kernel<<<(int)std::min<int64_t>((meshes_[b].nv + 255) / 256, 4096), 256, 0, st_>>>(
+                (int)meshes_[b].nv, n_, 1, stt.offs, stt.slots, tile_of_[b].get(), ts_.rowptr.get(), xhat_.get(),
+                co.recon_dev);
+            stt.release(st_);
+        }
+        const int s1 = tm.mark();
+        tm.add(kStProject, s0, s1);
+        SMG_CUDA(cudaStreamSynchronize(st_));
+        report_errors();
+        // host-side outputs
+        std::vector<double> rms = download(stat_rms_.get(), (size_t)K_ * B_, st_);
+        for (int b = 0; b < B_; ++b) {
+            ChainOut& co = outs_[b];
+            smg_chain_output* o = co.out;
+            for (int pos = 0; pos < K_; ++pos) {
+                const int id = segs_[b].seq_h[pos];
+                if (o->residual_rms) o->residual_rms[id] = rms[(size_t)pos * B_ + b];
+                if (o->subspace_size) o->subspace_size[id] = sizes_[pos];
+                if (o->oi_iterations) o->oi_iterations[id] = pos == 0 ? 0 : cfg_.iterations;
+                if (o->converged) o->converged[id] = 1;
+                if (o->doi_residual) o->doi_residual[id] = 0.0;
+            }
+            copy_outputs(co);
+            o->timings[0] = tm.total(kStLaplacian);
+            o->timings[1] = tm.total(kStFactorize);
+            o->timings[2] = tm.total(kStBasis);
+            o->timings[3] = o->timings[0] + o->timings[1] + o->timings[2];
+            o->timings[4] = tm.total(kStProject);
+            o->timings[5] = tm.secs(t0, s1);
+        }
+    }
+
+    void copy_outputs(ChainOut& co) {
+        smg_chain_output* o = co.out;
+        const bool doi = cfg_.basis_mode == SMG_BASIS_DOI;
+        if (doi) {
+            // compact id-ordered capacity slots into the packed layout of the real sizes
+            std::vector<int64_t> coff(K_ + 1, 0), boff(K_ + 1, 0);
+            for (int id = 0; id < K_; ++id) {
+                const int c = sizes_[segs_[0].pos_of[id]];
+                coff[id + 1] = coff[id] + (int64_t)c * 3;
+                boff[id + 1] = boff[id] + (int64_t)c * n_;
+            }
+            if (o->coefficient_offsets) std::memcpy(o->coefficient_offsets, coff.data(), 8 * (K_ + 1));
+            if (o->basis_offsets) std::memcpy(o->basis_offsets, boff.data(), 8 * (K_ + 1));
+            const cudaMemcpyKind kind = o->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+            if (o->coefficients) {
+                require(o->coefficients_capacity >= coff[K_], "coefficient buffer too small");
+                for (int id = 0; id < K_; ++id)
+                    SMG_CUDA(cudaMemcpyAsync(o->coefficients + coff[id], co.coef_dev + co.coef_off[id],
+                                             (coff[id + 1] - coff[id]) * 8, kind, st_));
+            }
+            if (o->bases) {
+                require(o->bases_capacity >= boff[K_], "basis buffer too small");
+                for (int id = 0; id < K_; ++id)
+                    SMG_CUDA(cudaMemcpyAsync(o->bases + boff[id], co.basis_dev + co.basis_off[id],
+                                             (boff[id + 1] - boff[id]) * 8, kind, st_));
+            }
+        } else if (!o->on_device) {
+            if (o->coefficients)
+                SMG_CUDA(cudaMemcpyAsync(o->coefficients, co.coef_dev, co.coef_off[K_] * 8, cudaMemcpyDeviceToHost, st_));
+            if (o->bases)
+                SMG_CUDA(cudaMemcpyAsync(o->bases, co.basis_dev, co.basis_off[K_] * 8, cudaMemcpyDeviceToHost, st_));
+        }
+        if (o->reconstruction && !o->on_device)
+            SMG_CUDA(cudaMemcpyAsync(o->reconstruction, co.recon_dev, (size_t)meshes_[&co - outs_.data()].nv * 3 * 8,
+                                     cudaMemcpyDeviceToHost, st_));
+        SMG_CUDA(cudaStreamSynchronize(st_));
+    }
+
+    void report_errors() {
+        // earliest chain position wins (the reference throws at the first failing
+        // block); within a position the factorization precedes the OI step.
+        std::vector<int> sts = download(ws_.status.get(), B_, st_);
+        std::vector<int> eps = download(ws_.errpos.get(), B_, st_);
+        std::vector<int64_t> det = download(ws_.detail.get(), B_, st_);
+        for (int b = 0; b < B_; ++b) {
+            int best_pos = INT32_MAX;
+            std::string msg;
+            for (const FacStatus& f : factor_status_)
+                for (size_t i = 0; i < f.st.size(); ++i) {
+                    const int tile = f.pos0 * B_ + (int)i;
+                    if ((tile % B_) != b || f.st[i] == 0) continue;
+                    const int pos = tile / B_;
+                    if (pos < best_pos) {
+                        best_pos = pos;
+                        msg = status_message(kFactorFailed, 0);
+                    }
+                }
+            if (sts[b] != 0) {
+                const int pos = eps[b] < 0 ? INT32_MAX - 1 : eps[b];
+                if (pos < best_pos) {
+                    best_pos = pos;
+                    msg = status_message(sts[b], det[b]);
+                }
+            }
+            if (!msg.empty()) fail(3, msg);
+        }
+    }
+
+    smg_context* ctx_;
+    cudaStream_t st_;
+    int B_, K_ = 0, n_ = 0;
+    Cfg cfg_;
+    std::vector<MeshDev> meshes_;
+    std::vector<SegDev> segs_;
+    std::vector<ChainOut> outs_;
+    std::vector<int> sizes_;
+    std::vector<DBuf<int64_t>> tile_of_;
+    std::vector<FacStatus> factor_status_;
+    std::vector<DoiState> doi_states_;
+    std::vector<DBuf<double*>> keep_;
+    DBuf<double*> ptrs_c_, ptrs_b_;
+    DBuf<double> xhat_, stat_rms_;
+    TileSet ts_;
+    Workspace ws_;
+    int first_c_ = 0, prev_c_ = 0;
+    bool xhat_ready_ = false;
+    struct PendingError {
+        int pos, stage, chain, code;
+        std::string msg;
+    } pending_error_;
+};
+
+__global__ void apply_sign_kernel(double* U, int64_t ld, int n, int c, const double* sign) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * c;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / c), j = (int)(e % c);
+        U[(int64_t)i * ld + j] *= sign[j];
+    }
+}
+
+void ChainRunner::apply_signs(int b, int c) {
+    apply_sign_kernel<<<std::min(1024, (n_ * c + 255) / 256), 256, 0, st_>>>(
+        ws_.U.get() + (int64_t)b * ws_.mstride(), ws_.ld, n_, c, ws_.sign.get() + (int64_t)b * ws_.ld);
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+int smg_abi_version(void) { return SMG_ABI_VERSION; }
+
+const char* smg_last_error(const smg_context* ctx) { return ctx ? ctx->error.c_str() : "null context"; }
+
+smg_status smg_create(int device, smg_context** out) {
+    if (!out) return SMG_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) return SMG_ERROR;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return SMG_ERROR;
+    if (prop.major != 10) return SMG_ERROR;  // built for sm_100a only
+    auto* ctx = new smg_context();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return SMG_ERROR;
+    }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = ctx;
+    return SMG_OK;
+}
+
+void smg_destroy(smg_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+void smg_default_config(smg_pipeline_config* c) {
+    if (!c) return;
+    c->weighting = SMG_WEIGHTING_DISTANCE;
+    c->basis_mode = SMG_BASIS_OI;
+    c->subspace_size = 16;
+    c->eps_low = 0.004;
+    c->eps_high = 0.04;
+    c->c_min = 2;
+    c->c_max = 0;
+    c->power = 2;
+    c->iterations = 2;
+    c->initial_iterations = 60;
+    c->doi_iterations = 0;
+    c->seed = 1;
+    c->dense_limit = 4096;
+    c->shift_scale = 1e-8;
+}
+
+smg_status smg_compute_block_bases_fixed_sizes(smg_context* ctx, const smg_mesh* mesh, const smg_segmentation* seg,
+                                               const smg_pipeline_config* cfg, const int32_t* sizes_in_order,
+                                               smg_chain_output* out) {
+    return guard(ctx, [&] {
+        require(out != nullptr && sizes_in_order != nullptr, "output / sizes are null");
+        Cfg c = read_cfg(cfg);
+        ChainRunner r(ctx, 1, mesh, seg, c, out);
+        r.run_fixed(sizes_in_order);
+    });
+}
+
+smg_status smg_compute_block_bases(smg_context* ctx, const smg_mesh* mesh, const smg_segmentation* seg,
+                                   const smg_pipeline_config* cfg, smg_chain_output* out) {
+    return guard(ctx, [&] {
+        require(out != nullptr, "output is null");
+        Cfg c = read_cfg(cfg);
+        ChainRunner r(ctx, 1, mesh, seg, c, out);
+        if (c.basis_mode == SMG_BASIS_OI) {
+            std::vector<int32_t> sizes(seg->submesh_count, c.subspace_size);
+            r.run_fixed(sizes.data());
+        } else {
+            r.run_doi();
+        }
+    });
+}
+
+smg_status smg_run_chains(smg_context* ctx, int32_t n_chains, const smg_mesh* meshes, const smg_segmentation* segs,
+                          const smg_pipeline_config* cfg, const int32_t* sizes_in_order, smg_chain_output* outs) {
+    return guard(ctx, [&] {
+        require(outs != nullptr && sizes_in_order != nullptr, "output / sizes are null");
+        Cfg c = read_cfg(cfg);
+        require(c.basis_mode == SMG_BASIS_OI, "batched chains run the fixed-size OI path");
+        ChainRunner r(ctx, n_chains, meshes, segs, c, outs);
+        r.run_fixed(sizes_in_order);
+    });
+}
+
+double smg_default_shift(double trace, int32_t n, double scale) {
+    const double mean_diag = trace / (double)n;
+    return std::max(scale * mean_diag, 1e-300);
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// Common device helpers for the sm_100a OI spectral path.
+//
+// FP64 arithmetic only.  tcgen05 (UMMA) has no f64 kind, so FP64 tensor work is
+// the warp-level DMMA `mma.sync.aligned.m8n8k4.row.col.f64` (37.2 TFLOP/s on
+// B200 vs 36.8 for DFMA; profiles/fp64_peak_r01.txt).  Matrices inside the
+// library are row-major ("vertex-major": row = local vertex, leading dimension
+// ld >= c, ld % 8 == 0); the C ABI converts Eigen's column-major at the boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define SMG_DEV __device__ __forceinline__
+
+namespace smg {
+
+// D(8x8) += A(8x4, row) * B(4x8, col).  Lane l: g = l >> 2, t = l & 3 holds
+// a = A[g][t], b = B[t][g]; d0 = D[g][2t], d1 = D[g][2t+1].
+SMG_DEV void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+SMG_DEV double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+SMG_DEV double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+SMG_DEV void cp_async16(void* smem, const void* gmem) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+SMG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+SMG_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Block-wide sum of one double per thread (blockDim.x multiple of 32, <= 1024).
+SMG_DEV double block_sum(double v, double* scratch /* >= 32 doubles */) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    double r = 0.0;
+    if (wid == 0) {
+        r = lane < nw ? scratch[lane] : 0.0;
+        r = warp_sum(r);
+        if (lane == 0) scratch[0] = r;
+    }
+    __syncthreads();
+    r = scratch[0];
+    __syncthreads();
+    return r;
+}
+
+// Status codes written by kernels into device status words.
+enum DeviceStatus : int {
+    kOk = 0,
+    kRankDeficient = 1,      // detail = column
+    kAllZero = 2,            // orthonormalize: block all zero
+    kFactorFailed = 3,       // zero pivot in LDL^T
+    kCoincident = 4,         // distance weighting singular; detail = pair
+    kNotFinite = 5,
+};
+
+}  // namespace smg

@@ -1,0 +1,334 @@
+// Engine pieces shared by the chain runner and the L3 primitives.
+#include <cstdio>
+
+#include "engine.h"
+
+namespace smg {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(3, std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
+}
+
+namespace {
+int supported_width(int w) {
+    if (w <= 16) return 16;
+    if (w <= 32) return 32;
+    if (w <= 48) return 48;
+    if (w <= 64) return 64;
+    return -1;
+}
+}  // namespace
+
+void TileSet::build(const std::vector<TileRef>& tiles, int n_, int weighting, double shift_scale, cudaStream_t st) {
+    ntiles = (int)tiles.size();
+    n = n_;
+    require(n >= 2, "submesh must have at least 2 vertices");
+    require(n <= 4096, "submesh size exceeds the GPU limit of 4096 vertices");
+    refs.upload(tiles, st);
+    nnz.alloc(ntiles, st);
+    off.alloc(ntiles + 1, st);
+    assemble_count(refs.get(), ntiles, n, nnz.get(), st);
+    exclusive_scan_i32_to_i64(nnz.get(), off.get(), ntiles, st);
+    int64_t tot = 0;
+    SMG_CUDA(cudaMemcpyAsync(&tot, off.get() + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SMG_CUDA(cudaStreamSynchronize(st));
+    total_nnz = tot;
+    rowptr.alloc((size_t)ntiles * (n + 1), st);
+    cols.alloc(tot, st);
+    vals.alloc(tot, st);
+    trace.alloc(ntiles, st);
+    status.alloc(ntiles, st);
+    status.zero();
+    detail.alloc(ntiles, st);
+    {
+        std::vector<int64_t> big(ntiles, INT64_MAX);
+        detail.upload(big, st);
+    }
+    assemble_fill(refs.get(), ntiles, n, weighting, off.get(), rowptr.get(), cols.get(), vals.get(), trace.get(),
+                  status.get(), detail.get(), st);
+    finish_build(shift_scale, nullptr, st);
+    X.alloc((size_t)ntiles * n * 3, st);
+    bbox.alloc(ntiles, st);
+    gather_coords(refs.get(), ntiles, n, X.get(), (int64_t)n * 3, bbox.get(), st);
+    status_h = download(status.get(), ntiles, st);
+    detail_h = download(detail.get(), ntiles, st);
+}
+
+void TileSet::build_from_csr(int n_, const int32_t* rowptr_h, const int32_t* cols_h, const double* vals_h,
+                             double delta_h, cudaStream_t st) {
+    ntiles = 1;
+    n = n_;
+    require(n >= 1, "operator size must be positive");
+    require(n <= 4096, "submesh size exceeds the GPU limit of 4096 vertices");
+    const int64_t nz = rowptr_h[n];
+    total_nnz = nz;
+    rowptr.upload(rowptr_h, n + 1, st);
+    cols.upload(cols_h, nz, st);
+    vals.upload(vals_h, nz, st);
+    std::vector<int64_t> o = {0, nz};
+    off.upload(o, st);
+    // trace in index order (spectral.hpp:32-36)
+    double t = 0.0;
+    for (int i = 0; i < n; ++i)
+        for (int64_t e = rowptr_h[i]; e < rowptr_h[i + 1]; ++e)
+            if (cols_h[e] == i) t += vals_h[e];
+    std::vector<double> th = {t};
+    trace.upload(th, st);
+    std::vector<double> dh = {delta_h};
+    status.alloc(1, st);
+    status.zero();
+    finish_build(0.0, &dh, st);
+}
+
+void TileSet::finish_build(double shift_scale, const std::vector<double>* explicit_delta, cudaStream_t st) {
+    // ordering: natural if block tridiagonal with W <= 64, else RCM
+    bw.alloc(ntiles, st);
+    blockw.alloc(ntiles, st);
+    natural_bandwidth(rowptr.get(), cols.get(), off.get(), nullptr, ntiles, n, bw.get(), blockw.get(), st);
+    std::vector<int32_t> bwh = download(blockw.get(), ntiles, st);
+    int wmax = 1;
+    for (int v : bwh) wmax = std::max(wmax, v);
+    use_perm = false;
+    if (supported_width(wmax) < 0) {
+        perm.alloc((size_t)ntiles * n, st);
+        rcm_order(rowptr.get(), cols.get(), off.get(), ntiles, n, perm.get(), st);
+        natural_bandwidth(rowptr.get(), cols.get(), off.get(), perm.get(), ntiles, n, bw.get(), blockw.get(), st);
+        bwh = download(blockw.get(), ntiles, st);
+        wmax = 1;
+        for (int v : bwh) wmax = std::max(wmax, v);
+        use_perm = true;
+    }
+    W = supported_width(wmax);
+    if (W < 0) fail(2, "submesh bandwidth after RCM ordering exceeds the supported block width 64");
+    Kb = (n + W - 1) / W;
+    npad = Kb * W;
+    if (explicit_delta) {
+        delta.upload(*explicit_delta, st);
+    } else {
+        delta.alloc(ntiles, st);
+        compute_delta(trace.get(), ntiles, n, shift_scale, delta.get(), st);
+    }
+    shift0.alloc(ntiles, st);
+    compute_first_shift(rowptr.get(), cols.get(), vals.get(), off.get(), trace.get(), ntiles, n, shift0.get(), st);
+}
+
+void FactorSet::factor(const TileSet& ts, int first_tile, int cnt, const double* shift, cudaStream_t st) {
+    first = first_tile;
+    count = cnt;
+    strideF = (int64_t)ts.Kb * 2 * ts.W * ts.W;
+    if (fwd.size() < (size_t)strideF * cnt) {
+        fwd.alloc((size_t)strideF * cnt, st);
+        bwd.alloc((size_t)strideF * cnt, st);
+        status.alloc(cnt, st);
+    }
+    status.zero();
+    FactorParams p;
+    p.ntiles = cnt;
+    p.n = ts.n;
+    p.W = ts.W;
+    p.Kb = ts.Kb;
+    p.rowptr = ts.rowptr.get() + (int64_t)first_tile * (ts.n + 1);
+    p.cols = ts.cols.get();
+    p.vals = ts.vals.get();
+    p.csr_offsets = ts.off.get() + first_tile;
+    p.perm = ts.use_perm ? ts.perm.get() + (int64_t)first_tile * ts.n : nullptr;
+    p.delta = (shift ? shift : ts.delta.get()) + first_tile;
+    p.Ffwd = fwd.get();
+    p.Fbwd = bwd.get();
+    p.strideF = strideF;
+    p.status = status.get();
+    factor_tiles(p, st);
+    SMG_CUDA(cudaGetLastError());
+}
+
+void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
+    B = B_;
+    n = n_;
+    npad = npad_;
+    ccap = ccap_;
+    ld = round_up(std::max(ccap, 8), 32);
+    const size_t mat = (size_t)B * npad * ld;
+    U.alloc(mat, st);
+    V.alloc(mat, st);
+    T.alloc(mat, st);
+    R.alloc(mat, st);
+    U.zero();
+    V.zero();
+    T.zero();
+    R.zero();
+    const size_t cc = (size_t)B * ld * ld;
+    G.alloc(cc, st);
+    Bm.alloc(cc, st);
+    work.alloc(cc, st);
+    // split-K over the n rows for the Gram: aim at ~2 waves of CTAs
+    const int tiles = ((ld + 63) / 64) * ((ld + 63) / 64 + 1) / 2;
+    splits = std::max(1, std::min(npad / 128, 296 / std::max(1, tiles * B)));
+    Gws.alloc((size_t)B * splits * ld * ld, st);
+    rdiag.alloc((size_t)B * ld, st);
+    coeff.alloc((size_t)B * ld * 4, st);
+    sign.alloc((size_t)B * ld, st);
+    e.alloc((size_t)B * npad, st);
+    ppart.alloc((size_t)B * proj_chunks(n) * ld * 8, st);
+    ppart2.alloc((size_t)B * proj_recon_blocks(n, 2) * 2, st);
+    stats.alloc((size_t)B * 4, st);
+    status.alloc(B, st);
+    status.zero();
+    errpos.alloc(B, st);
+    errpos.zero();
+    detail.alloc(B, st);
+    detail.zero();
+}
+
+void solve_batch(const StepCtx& cx, Workspace& ws, const FactorSet& fs, int tile0, int tstride, const double* in,
+                 double* out, int c, const int* dimC, int z, bool once) {
+    const TileSet& ts = *cx.ts;
+    SolveParams p;
+    p.n = ts.n;
+    p.Kb = ts.Kb;
+    p.z = z;
+    p.c_cap = c;
+    p.batch = ws.B;
+    p.Ffwd = fs.f(tile0);
+    p.Fbwd = fs.b(tile0);
+    p.strideF = (int64_t)tstride * fs.strideF;
+    p.perm = ts.perm_of(tile0);
+    p.stridePerm = ts.use_perm ? (int64_t)tstride * ts.n : 0;
+    p.in = in;
+    p.ldin = ws.ld;
+    p.strideIn = ws.mstride();
+    p.tmp = ws.T.get();
+    p.ldt = ws.ld;
+    p.strideT = ws.mstride();
+    p.out = out;
+    p.ldout = ws.ld;
+    p.strideOut = ws.mstride();
+    p.dimC = dimC;
+    p.dimStride = 1;
+    p.once = once ? 1 : 0;
+    solve_block_tridiag(p, ts.W, cx.st);
+    SMG_CUDA(cudaGetLastError());
+}
+
+namespace {
+void gram(Workspace& ws, const double* V, int c, const int* dimC, int n, cudaStream_t st) {
+    GemmParams g;
+    g.M = c;
+    g.N = c;
+    g.K = n;
+    g.batch = ws.B;
+    g.splits = ws.splits;
+    g.A = V;
+    g.lda = ws.ld;
+    g.strideA = ws.mstride();
+    g.B = V;
+    g.ldb = ws.ld;
+    g.strideB = ws.mstride();
+    g.syrkUpper = 1;
+    g.dimM = dimC;
+    g.dimN = dimC;
+    g.dimStride = 1;
+    if (g.splits > 1) {
+        g.C = ws.Gws.get();
+        g.ldc = ws.ld;
+        g.strideP = (int64_t)ws.ld * ws.ld;
+        g.out = ws.G.get();
+        g.ldo = ws.ld;
+        g.strideC = (int64_t)ws.ld * ws.ld;
+    } else {
+        g.C = ws.G.get();
+        g.ldc = ws.ld;
+        g.strideC = (int64_t)ws.ld * ws.ld;
+    }
+    gemm(g, true, false, st);
+}
+
+void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st) {
+    GemmParams g;
+    g.M = n;
+    g.N = c;
+    g.K = c;
+    g.batch = ws.B;
+    g.A = V;
+    g.lda = ws.ld;
+    g.strideA = ws.mstride();
+    g.B = ws.Bm.get();
+    g.ldb = ws.ld;
+    g.strideB = (int64_t)ws.ld * ws.ld;
+    g.C = out;
+    g.ldc = ws.ld;
+    g.strideC = ws.mstride();
+    g.upperB = 1;
+    g.dimN = dimC;
+    g.dimK = dimC;
+    g.dimStride = 1;
+    gemm(g, false, false, st);
+}
+
+void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_scale, int pos, cudaStream_t st) {
+    CholParams p;
+    p.batch = ws.B;
+    p.c_cap = c;
+    p.G = ws.G.get();
+    p.ldg = ws.ld;
+    p.strideG = (int64_t)ws.ld * ws.ld;
+    p.Binv = ws.Bm.get();
+    p.ldb = ws.ld;
+    p.strideB = (int64_t)ws.ld * ws.ld;
+    p.rdiag = ws.rdiag.get();
+    p.strideR = ws.ld;
+    p.work = ws.work.get();
+    p.dimC = dimC;
+    p.dimStride = 1;
+    p.status = ws.status.get();
+    p.status_detail = ws.detail.get();
+    p.errpos = ws.errpos.get();
+    p.pos = pos;
+    p.rank_test = rank_test ? 1 : 0;
+    p.column_scale = column_scale ? 1 : 0;
+    chol_inverse(p, st);
+}
+}  // namespace
+
+void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
+                bool rank_test, int pos) {
+    const int n = ws.npad;
+    gram(ws, in, c, dimC, n, cx.st);
+    chol(ws, c, dimC, rank_test, true, pos, cx.st);
+    trmm(ws, in, ws.R.get(), c, dimC, n, cx.st);
+    gram(ws, ws.R.get(), c, dimC, n, cx.st);
+    chol(ws, c, dimC, false, true, pos, cx.st);
+    trmm(ws, ws.R.get(), out, c, dimC, n, cx.st);
+    SMG_CUDA(cudaGetLastError());
+}
+
+void project_batch(const StepCtx& cx, Workspace& ws, const double* Q, int c, const int* dimC, const double* X,
+                   int64_t strideX, double* xhat, int64_t strideXhat) {
+    ProjParams p;
+    p.n = ws.n;
+    p.batch = ws.B;
+    p.c_cap = c;
+    p.Q = Q;
+    p.ldq = ws.ld;
+    p.strideQ = ws.mstride();
+    p.X = X;
+    p.strideX = strideX;
+    p.dimC = dimC;
+    p.dimStride = 1;
+    p.partial = ws.ppart.get();
+    p.partial2 = ws.ppart2.get();
+    p.coeff = ws.coeff.get();
+    p.strideCoef = (int64_t)ws.ld * 4;
+    p.sign = ws.sign.get();
+    p.strideSign = ws.ld;
+    p.xhat = xhat;
+    p.strideXhat = strideXhat;
+    p.e_out = ws.e.get();
+    p.strideE = ws.npad;
+    p.stats = ws.stats.get();
+    p.strideStats = 4;
+    p.rows_per_warp = 2;
+    project(p, cx.st);
+    SMG_CUDA(cudaGetLastError());
+}
+
+}  // namespace smg

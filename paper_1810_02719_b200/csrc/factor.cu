@@ -1,0 +1,213 @@
+// K2: factorisation of L + delta I for every submesh, batched (one CTA per tile).
+//
+// Replaces the ShiftedInverseOperator constructor (spectral.hpp:147-159:
+// `shifted = L + delta*I; SimplicialLDLT::compute`).  Eigen's LDL^T does no
+// pivoting and accepts negative pivots (only an exact zero pivot is a
+// NumericalIssue); the same algebra is kept as a *signed* block Cholesky
+// A = L Sigma L^T (Sigma = diag(+-1)) so indefinite matrices behave the same.
+//
+// In the chosen ordering (natural for grid tiles, RCM otherwise) the matrix is
+// block tridiagonal with W x W blocks D_k (diagonal) and B_k = A_{k,k-1}:
+//   L_{k,k-1} = B_k Linv_{k-1}^T Sigma_{k-1}
+//   S_k       = D_k - L_{k,k-1} Sigma_{k-1} L_{k,k-1}^T
+//   S_k       = L_kk Sigma_k L_kk^T            (signed Cholesky, zero pivot fails)
+// and the solve operands are written once per tile:
+//   Ffwd_k^T = [Linv_k | -Linv_k L_{k,k-1}]^T
+//   Fbwd_k^T = [Linv_k^T Sigma_k | -Linv_k^T L_{k+1,k}^T]^T
+#include "common.cuh"
+#include "kernels.h"
+
+namespace smg {
+
+namespace {
+
+constexpr int NT = 256;
+
+template <int W>
+struct FactorSmem {
+    static constexpr int LD = W + 1;
+    static constexpr int MAT = W * LD;
+    static int bytes(int n) { return (4 * MAT + 2 * W + 32) * 8 + n * 4; }
+};
+
+template <int W>
+__global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
+    constexpr int LD = FactorSmem<W>::LD;
+    constexpr int MAT = FactorSmem<W>::MAT;
+    extern __shared__ __align__(16) double sm[];
+    double* S = sm;              // Schur complement / L_kk (lower)
+    double* P = sm + MAT;        // L_{k,k-1}
+    double* Lp = sm + 2 * MAT;   // Linv_{k-1}
+    double* Lc = sm + 3 * MAT;   // Linv_k
+    double* sig = sm + 4 * MAT;  // Sigma_k
+    double* sigp = sig + W;      // Sigma_{k-1}
+    int* flag = reinterpret_cast<int*>(sigp + W);
+    int* ipos = reinterpret_cast<int*>(sigp + W + 32);
+
+    const int tile = blockIdx.x;
+    const int n = p.n, Kb = p.Kb, tid = threadIdx.x;
+    const int32_t* rowptr = p.rowptr + (int64_t)tile * (n + 1);
+    const int64_t base = p.csr_offsets[tile];
+    const int32_t* cols = p.cols + base;
+    const double* vals = p.vals + base;
+    const int32_t* perm = p.perm ? p.perm + (int64_t)tile * n : nullptr;
+    const double delta = p.delta[tile];
+    double* Ff = p.Ffwd + (int64_t)tile * p.strideF;
+    double* Fb = p.Fbwd + (int64_t)tile * p.strideF;
+    const int64_t slab = (int64_t)2 * W * W;
+
+    for (int i = tid; i < n; i += NT) ipos[perm ? perm[i] : i] = i;
+    if (tid == 0) flag[0] = 0;
+    __syncthreads();
+
+    for (int k = 0; k < Kb; ++k) {
+        const int r0 = k * W;
+        // ---- D_k (+ delta on the diagonal, Eigen: shifted += delta * identity)
+        for (int e = tid; e < W * W; e += NT) S[(e / W) * LD + (e % W)] = 0.0;
+        __syncthreads();
+        for (int r = tid; r < W; r += NT) {
+            const int prow = r0 + r;
+            if (prow >= n) {
+                S[r * LD + r] = 1.0;
+                continue;
+            }
+            const int i = perm ? perm[prow] : prow;
+            for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+                const int q = ipos[cols[e]] - r0;
+                if (q >= 0 && q < W) S[r * LD + q] = (cols[e] == i) ? vals[e] + delta : vals[e];
+            }
+        }
+        if (k > 0) {
+            // ---- P = B_k Linv_{k-1}^T Sigma_{k-1}  (= L_{k,k-1})
+            for (int e = tid; e < W * W; e += NT) {
+                const int r = e / W, c = e % W;
+                const int prow = r0 + r;
+                double acc = 0.0;
+                if (prow < n) {
+                    const int i = perm ? perm[prow] : prow;
+                    for (int q = rowptr[i]; q < rowptr[i + 1]; ++q) {
+                        const int qq = ipos[cols[q]] - (r0 - W);
+                        if (qq >= 0 && qq < W && c >= qq) acc += vals[q] * Lp[c * LD + qq];
+                    }
+                }
+                P[r * LD + c] = acc * sigp[c];
+            }
+            __syncthreads();
+            // ---- S -= P Sigma_{k-1} P^T (lower triangle)
+            for (int e = tid; e < W * W; e += NT) {
+                const int r = e / W, s = e % W;
+                if (s > r) continue;
+                double acc = 0.0;
+#pragma unroll 8
+                for (int i = 0; i < W; ++i) acc += P[r * LD + i] * sigp[i] * P[s * LD + i];
+                S[r * LD + s] -= acc;
+            }
+        }
+        __syncthreads();
+        // ---- signed Cholesky S = L Sigma L^T (right-looking, lower)
+        for (int j = 0; j < W; ++j) {
+            const double d = S[j * LD + j];
+            const double sj = d < 0.0 ? -1.0 : 1.0;
+            const double ljj = sqrt(fabs(d));
+            if (tid == 0) {
+                if (!(d != 0.0) || !isfinite(d)) flag[0] = 1;
+                sig[j] = sj;
+            }
+            for (int r = j + 1 + tid; r < W; r += NT) S[r * LD + j] = S[r * LD + j] / (ljj * sj);
+            __syncthreads();
+            if (tid == 0) S[j * LD + j] = ljj;
+            const int m = W - j - 1;
+            for (int e = tid; e < m * m; e += NT) {
+                const int r = j + 1 + e / m, s = j + 1 + e % m;
+                if (s > r) continue;
+                S[r * LD + s] -= S[r * LD + j] * sj * S[s * LD + j];
+            }
+            __syncthreads();
+        }
+        // ---- Linv_k = L_kk^-1 (row by row; column j handled by 4 threads)
+        for (int e = tid; e < W * W; e += NT) Lc[(e / W) * LD + (e % W)] = 0.0;
+        __syncthreads();
+        {
+            const int j = tid >> 2, part = tid & 3;
+            const bool active_col = j < W;
+            for (int r = 0; r < W; ++r) {
+                const bool act = active_col && j <= r;
+                double acc = 0.0;
+                if (act)
+                    for (int i = j + part; i < r; i += 4) acc += S[r * LD + i] * Lc[i * LD + j];
+                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                if (act && part == 0) Lc[r * LD + j] = (r == j) ? 1.0 / S[r * LD + r] : -acc / S[r * LD + r];
+                __syncthreads();
+            }
+        }
+        // ---- Ffwd_k^T: rows j<W: Linv_k[:, j]; rows W+j: -M_k[:, j], M_k = Linv_k P
+        double* F = Ff + (int64_t)k * slab;
+        for (int e = tid; e < W * W; e += NT) {
+            const int j = e / W, r = e % W;
+            F[(int64_t)j * W + r] = Lc[r * LD + j];
+            double m = 0.0;
+            if (k > 0) {
+                for (int i = 0; i <= r; ++i) m += Lc[r * LD + i] * P[i * LD + j];
+            }
+            F[(int64_t)(W + j) * W + r] = -m;
+        }
+        // ---- Fbwd_{k-1}^T second half: -(L_{k,k-1} Linv_{k-1}) = -(P Lp), row-major
+        if (k > 0) {
+            double* Fp = Fb + (int64_t)(k - 1) * slab;
+            for (int e = tid; e < W * W; e += NT) {
+                const int j = e / W, r = e % W;
+                double m = 0.0;
+                for (int i = r; i < W; ++i) m += P[j * LD + i] * Lp[i * LD + r];
+                Fp[(int64_t)(W + j) * W + r] = -m;
+            }
+        }
+        // ---- Fbwd_k^T first half: row j = sigma_j * Linv_k[j, :]
+        {
+            double* Fc = Fb + (int64_t)k * slab;
+            for (int e = tid; e < W * W; e += NT) {
+                const int j = e / W, r = e % W;
+                Fc[(int64_t)j * W + r] = sig[j] * Lc[j * LD + r];
+            }
+            if (k == Kb - 1)
+                for (int e = tid; e < W * W; e += NT) Fc[(int64_t)W * W + e] = 0.0;
+        }
+        __syncthreads();
+        // ---- carry Linv_k, Sigma_k
+        for (int e = tid; e < W * W; e += NT) Lp[(e / W) * LD + (e % W)] = Lc[(e / W) * LD + (e % W)];
+        for (int e = tid; e < W; e += NT) sigp[e] = sig[e];
+        __syncthreads();
+    }
+    if (tid == 0 && p.status) p.status[tile] = flag[0] ? kFactorFailed : kOk;
+}
+
+template <int W>
+void launch(const FactorParams& p, cudaStream_t st) {
+    const int bytes = FactorSmem<W>::bytes(p.n);
+    cudaFuncSetAttribute(factor_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    factor_kernel<W><<<p.ntiles, NT, bytes, st>>>(p);
+}
+
+}  // namespace
+
+int factor_smem_bytes(int W) {
+    switch (W) {
+        case 16: return FactorSmem<16>::bytes(0);
+        case 32: return FactorSmem<32>::bytes(0);
+        case 48: return FactorSmem<48>::bytes(0);
+        default: return FactorSmem<64>::bytes(0);
+    }
+}
+
+void factor_tiles(const FactorParams& p, cudaStream_t st) {
+    if (p.ntiles == 0) return;
+    switch (p.W) {
+        case 16: launch<16>(p, st); break;
+        case 32: launch<32>(p, st); break;
+        case 48: launch<48>(p, st); break;
+        case 64: launch<64>(p, st); break;
+        default: break;
+    }
+}
+
+}  // namespace smg

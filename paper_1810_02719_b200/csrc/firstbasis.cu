@@ -1,0 +1,211 @@
+// K9: the first-submesh basis on the GPU.
+//
+// Reference: detail::initial_block_basis (pipeline.hpp:113-120) =
+// bottom_subspace(dense_eigendecomposition(L), c) when n_d <= dense_limit, else
+// a cold OI start from random_orthonormal_basis with initial_iterations steps.
+//
+// Dense path replacement: shift-invert subspace iteration on the tile's own
+// block factor with m = c + max(16, c/2) guard columns, then Rayleigh-Ritz:
+//   Y = L U (CSR SpMM, K4), H = U^T Y, H = W Theta W^T (cluster Jacobi),
+//   Z = U W.  The bottom-c Ritz vectors converge at ((lambda_c+s)/(lambda_{m+1}+s))^z
+//   per step instead of the ((lambda_c+s)/(lambda_{c+1}+s))^z of plain OI, and the
+// loop stops when the Davis-Kahan bound max_j ||L z_j - theta_j z_j|| / (theta_{c+1}
+// - theta_c) on the subspace angle is below 1e-12.  The shift s is the Gershgorin
+// lower bound of L plus 1e-3 * mean diagonal, so L + sI is positive definite for
+// either weighting and the bottom of the spectrum is what the iteration finds.
+// Only span(bottom c) is needed downstream: fixed-c OI and the projections
+// depend on the span, and the sign convention is re-applied in project.cu.
+#include <cmath>
+#include <random>
+
+#include "engine.h"
+#include "firstbasis.h"
+
+namespace smg {
+
+namespace {
+
+void gemm_nn(Workspace& ws, const double* A, int64_t lda, const double* Bm, int64_t ldb, int64_t strideB, double* C,
+             int M, int N, int K, cudaStream_t st) {
+    GemmParams g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.batch = ws.B;
+    g.A = A;
+    g.lda = lda;
+    g.strideA = ws.mstride();
+    g.B = Bm;
+    g.ldb = ldb;
+    g.strideB = strideB;
+    g.C = C;
+    g.ldc = ws.ld;
+    g.strideC = ws.mstride();
+    gemm(g, false, false, st);
+}
+
+}  // namespace
+
+std::vector<double> gaussian_block_colmajor(int rows, int cols, uint64_t seed) {
+    // spectral.hpp:135-139 / pipeline.hpp:104-107: std::mt19937_64 + libstdc++'s
+    // normal_distribution, column-major fill -- the same draws as the reference.
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    std::vector<double> out((size_t)rows * cols);
+    for (int j = 0; j < cols; ++j)
+        for (int i = 0; i < rows; ++i) out[(size_t)j * rows + i] = gauss(rng);
+    return out;
+}
+
+FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts, int tile0, int tstride, int c,
+                             const FirstBasisConfig& cfg, const FactorSet* op_factor) {
+    FirstBasisReport rep;
+    const cudaStream_t st = cx.st;
+    const int n = ts.n;
+    if (n > cfg.dense_limit) {
+        // cold start exactly as the reference: random_orthonormal_basis + OI
+        require(op_factor != nullptr, "internal: cold start needs the operator factor");
+        std::vector<double> g = gaussian_block_colmajor(n, c, cfg.seed ^ 0x9E3779B97F4A7C15ULL);
+        DBuf<double> gd;
+        gd.upload(g, st);
+        for (int b = 0; b < ws.B; ++b)
+            transpose_to_rowmajor(gd.get(), n, c, ws.V.get() + (int64_t)b * ws.mstride(), ws.ld, st);
+        orth_batch(cx, ws, ws.V.get(), ws.U.get(), c, nullptr, true, 0);
+        for (int t = 0; t < cfg.initial_iterations; ++t) {
+            solve_batch(cx, ws, *op_factor, tile0, tstride, ws.U.get(), ws.V.get(), c, nullptr, cfg.power, false);
+            orth_batch(cx, ws, ws.V.get(), ws.U.get(), c, nullptr, true, 0);
+        }
+        rep.iterations = cfg.initial_iterations;
+        rep.cold = true;
+        return rep;
+    }
+
+    const int m = std::min(n, round_up(c + std::max(16, c / 2), 8));
+    require(m <= ws.ccap, "internal: workspace too small for the first-basis subspace");
+    FactorSet fs;
+    fs.factor(ts, tile0, (ws.B - 1) * tstride + 1, ts.shift0.get(), st);
+    // the factor set covers tiles tile0 .. tile0 + (B-1)*tstride; solve_batch indexes with tstride
+
+    JacobiPlan pl = jacobi_plan(m);
+    ws.H.alloc((size_t)ws.B * m * m, st);
+    ws.Hst.alloc((size_t)ws.B * pl.stage_elems, st);
+    ws.Vj.alloc((size_t)ws.B * m * m, st);
+    ws.theta.alloc((size_t)ws.B * m, st);
+    ws.theta_s.alloc((size_t)ws.B * m, st);
+    ws.Wm.alloc((size_t)ws.B * m * m, st);
+    const int nres = std::min(m, c + 1);
+    const int rchunks = (n + 127) / 128;
+    ws.ritz_part.alloc((size_t)ws.B * rchunks * nres, st);
+    ws.ritz.alloc((size_t)ws.B * nres, st);
+
+    randn(ws.V.get(), n, m, ws.ld, ws.mstride(), ws.B, cfg.seed * 0x2545F4914F6CDD1DULL + 17, st);
+    orth_batch(cx, ws, ws.V.get(), ws.U.get(), m, nullptr, false, 0);
+
+    FirstBasisConfig fc = cfg;
+    {
+        double s0 = 0.0;
+        SMG_CUDA(cudaMemcpyAsync(&s0, ts.shift0.get() + tile0, sizeof(double), cudaMemcpyDeviceToHost, st));
+        SMG_CUDA(cudaStreamSynchronize(st));
+        fc.shift_hint = s0;
+    }
+    int iters_next = (m == n) ? 0 : 6;
+    double prev_bound = INFINITY;
+    for (int round = 0; round < fc.max_rounds; ++round) {
+        for (int t = 0; t < iters_next; ++t) {
+            const int z = (round == 0 && t == 0) ? 1 : 2;
+            solve_batch(cx, ws, fs, tile0, tstride, ws.U.get(), ws.V.get(), m, nullptr, z, false);
+            orth_batch(cx, ws, ws.V.get(), ws.U.get(), m, nullptr, false, 0);
+            rep.iterations += 1;
+        }
+        // Rayleigh-Ritz: Y = L U (into R), H = U^T Y
+        SpmmParams sp;
+        sp.n = n;
+        sp.c = m;
+        sp.batch = ws.B;
+        sp.rowptr = ts.rowptr.get() + (int64_t)tile0 * (n + 1);
+        sp.strideRowptr = (int64_t)tstride * (n + 1);
+        sp.csr_offsets = ts.off.get() + tile0;  // per-batch offsets: stride tstride
+        sp.cols = ts.cols.get();
+        sp.vals = ts.vals.get();
+        sp.X = ws.U.get();
+        sp.ldx = ws.ld;
+        sp.strideX = ws.mstride();
+        sp.Y = ws.R.get();
+        sp.ldy = ws.ld;
+        sp.strideY = ws.mstride();
+        sp.offStride = tstride;
+        spmm(sp, st);
+        GemmParams g;
+        g.M = m;
+        g.N = m;
+        g.K = n;
+        g.batch = ws.B;
+        g.A = ws.U.get();
+        g.lda = ws.ld;
+        g.strideA = ws.mstride();
+        g.B = ws.R.get();
+        g.ldb = ws.ld;
+        g.strideB = ws.mstride();
+        g.C = ws.H.get();
+        g.ldc = m;
+        g.strideC = (int64_t)m * m;
+        gemm(g, true, false, st);
+        JacobiParams jp;
+        jp.batch = ws.B;
+        jp.H = ws.H.get();
+        jp.ldh = m;
+        jp.strideH = (int64_t)m * m;
+        jp.stage = ws.Hst.get();
+        jp.strideStage = pl.stage_elems;
+        jp.V = ws.Vj.get();
+        jp.ldv = m;
+        jp.strideV = (int64_t)m * m;
+        jp.theta = ws.theta.get();
+        jp.theta_sorted = ws.theta_s.get();
+        jp.strideTheta = m;
+        jp.W = ws.Wm.get();
+        jp.ldw = m;
+        jp.strideW = (int64_t)m * m;
+        const int jerr = jacobi_eigh(jp, pl, m, st);
+        if (jerr != 0) SMG_CUDA((cudaError_t)jerr);
+        // Z = U W (into V), LZ = Y W (into T)
+        gemm_nn(ws, ws.U.get(), ws.ld, ws.Wm.get(), m, (int64_t)m * m, ws.V.get(), n, m, m, st);
+        gemm_nn(ws, ws.R.get(), ws.ld, ws.Wm.get(), m, (int64_t)m * m, ws.T.get(), n, m, m, st);
+        ritz_residual(ws.T.get(), ws.V.get(), ws.theta_s.get(), n, nres, ws.ld, ws.mstride(), m, ws.B,
+                      ws.ritz_part.get(), ws.ritz.get(), st);
+        std::swap(ws.U, ws.V);
+        rep.rounds = round + 1;
+        std::vector<double> th = download(ws.theta_s.get(), (size_t)ws.B * m, st);
+        std::vector<double> rs = download(ws.ritz.get(), (size_t)ws.B * nres, st);
+        std::vector<int> sts = download(ws.status.get(), ws.B, st);
+        for (int b = 0; b < ws.B; ++b)
+            if (sts[b] != 0) fail(3, "first-submesh basis: orthonormalization of the subspace iterate broke down");
+        double bound = 0.0, worst_rate = 0.0;
+        for (int b = 0; b < ws.B; ++b) {
+            const double* tb = th.data() + (size_t)b * m;
+            const double* rb = rs.data() + (size_t)b * nres;
+            double err = 0.0;
+            for (int j = 0; j < c; ++j) err = std::max(err, rb[j]);
+            const double gap = (c < m) ? tb[c] - tb[c - 1] : INFINITY;
+            const double scale = std::max(std::fabs(tb[m - 1]), 1e-300);
+            const double bb = (c < m) ? err / std::max(gap, 1e-16 * scale) : err / scale;
+            bound = std::max(bound, bb);
+            if (c < m) {
+                const double s = fc.shift_hint;
+                const double rate = std::pow((tb[c - 1] + s) / (tb[m - 1] + s), 2.0);
+                worst_rate = std::max(worst_rate, rate);
+            }
+        }
+        rep.bound = bound;
+        if (m == n || bound < fc.tol) break;
+        if (!(bound < prev_bound * 0.999) && round >= 3) break;  // stagnated at the rounding floor
+        prev_bound = bound;
+        // iterations to reach the tolerance at the observed rate (bound shrinks ~rate per step)
+        double need = 4.0;
+        if (worst_rate > 0.0 && worst_rate < 1.0) need = std::log(fc.tol * 0.1 / bound) / std::log(worst_rate);
+        iters_next = (int)std::min(60.0, std::max(2.0, std::ceil(need)));
+    }
+    return rep;
+}
+
+}  // namespace smg

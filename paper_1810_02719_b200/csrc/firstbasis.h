@@ -1,0 +1,35 @@
+// First-submesh basis (K9), see firstbasis.cu.
+#pragma once
+
+#include <stdint.h>
+
+#include <vector>
+
+#include "engine.h"
+
+namespace smg {
+
+struct FirstBasisConfig {
+    int dense_limit = 4096;
+    int initial_iterations = 60;
+    int power = 2;
+    uint64_t seed = 1;
+    int max_rounds = 12;
+    double tol = 2e-12;
+    double shift_hint = 0.0;
+};
+
+struct FirstBasisReport {
+    int iterations = 0;
+    int rounds = 0;
+    double bound = 0.0;
+    bool cold = false;
+};
+
+std::vector<double> gaussian_block_colmajor(int rows, int cols, uint64_t seed);
+// Writes the first basis (n x c, row-major, unsigned columns) into ws.U for every
+// batch entry b, whose tile is tile0 + b * tstride.
+FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts, int tile0, int tstride, int c,
+                             const FirstBasisConfig& cfg, const FactorSet* op_factor);
+
+}  // namespace smg

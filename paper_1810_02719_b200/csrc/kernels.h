@@ -1,0 +1,209 @@
+// Host-side launch interfaces of the sm_100a kernels (internal to the library).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+namespace smg {
+
+// ------------------------------------------------------------------ GEMM (gemm.cu)
+struct GemmParams {
+    int M = 0, N = 0, K = 0, batch = 1, splits = 1;
+    const double* A = nullptr;
+    int64_t lda = 0, strideA = 0;
+    const double* B = nullptr;
+    int64_t ldb = 0, strideB = 0;
+    double* C = nullptr;  // destination (splits == 1) or split-K workspace (ld = ldc)
+    int64_t ldc = 0, strideC = 0;
+    int64_t strideP = 0;    // workspace stride per (batch, split)
+    double* out = nullptr;  // destination when splits > 1 (batch stride strideC)
+    int64_t ldo = 0;
+    double alpha = 1.0, beta = 0.0;
+    const int* dimM = nullptr;  // optional device-side dims (per batch, stride dimStride)
+    const int* dimN = nullptr;
+    const int* dimK = nullptr;
+    int64_t dimStride = 0;
+    int upperB = 0;     // B upper triangular (square): k < n0 + 64
+    int syrkUpper = 0;  // only tiles with tile_m <= tile_n
+};
+void gemm(const GemmParams& p, bool transA, bool transB, cudaStream_t st);
+
+// ------------------------------------------------------------------ assembly (assemble.cu)
+struct TileRef {             // one submesh of one chain
+    const int32_t* members;  // sorted ascending global ids (n)
+    const int32_t* adj_offsets;
+    const int32_t* adj_cols;
+    const double* x;
+    const double* y;
+    const double* z;
+};
+void assemble_count(const TileRef* tiles, int ntiles, int n, int32_t* nnz_out, cudaStream_t st);
+void assemble_fill(const TileRef* tiles, int ntiles, int n, int weighting, const int64_t* csr_offsets,
+                   int32_t* rowptr, int32_t* cols, double* vals, double* trace, int* status,
+                   int64_t* status_detail, cudaStream_t st);
+void exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int count, cudaStream_t st);
+void natural_bandwidth(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, const int32_t* perm,
+                       int ntiles, int n, int32_t* bw_out, int32_t* blockw_out, cudaStream_t st);
+void rcm_order(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, int ntiles, int n,
+               int32_t* perm, cudaStream_t st);
+
+// ------------------------------------------------------------------ factor (factor.cu)
+struct FactorParams {
+    int ntiles = 0, n = 0, W = 0, Kb = 0;
+    const int32_t* rowptr = nullptr;  // per tile (n+1) entries at tile*(n+1)
+    const int32_t* cols = nullptr;
+    const double* vals = nullptr;
+    const int64_t* csr_offsets = nullptr;
+    const int32_t* perm = nullptr;  // per tile n entries (nullptr: natural)
+    const double* delta = nullptr;  // per tile
+    double* Ffwd = nullptr;
+    double* Fbwd = nullptr;
+    int64_t strideF = 0;  // doubles per tile
+    int* status = nullptr;
+};
+void factor_tiles(const FactorParams& p, cudaStream_t st);
+int factor_smem_bytes(int W);
+
+// ------------------------------------------------------------------ solve (solve.cu)
+struct SolveParams {
+    int n = 0, Kb = 0, z = 2, c_cap = 0, batch = 1;
+    const double* Ffwd = nullptr;
+    const double* Fbwd = nullptr;
+    int64_t strideF = 0;
+    const int32_t* perm = nullptr;
+    int64_t stridePerm = 0;
+    const double* in = nullptr;
+    int64_t ldin = 0, strideIn = 0;
+    double* tmp = nullptr;
+    int64_t ldt = 0, strideT = 0;
+    double* out = nullptr;
+    int64_t ldout = 0, strideOut = 0;
+    const int* dimC = nullptr;
+    int64_t dimStride = 0;
+    int once = 0;
+};
+void solve_block_tridiag(const SolveParams& p, int W, cudaStream_t st);
+
+// ------------------------------------------------------------------ CholeskyQR (cholqr.cu)
+struct CholParams {
+    int batch = 1, c_cap = 0;
+    const double* G = nullptr;
+    int64_t ldg = 0, strideG = 0;
+    double* Binv = nullptr;
+    int64_t ldb = 0, strideB = 0;
+    double* rdiag = nullptr;
+    int64_t strideR = 0;
+    double* work = nullptr;  // c_cap*c_cap per batch when c > 144
+    const int* dimC = nullptr;
+    int64_t dimStride = 0;
+    int* status = nullptr;           // sticky per-chain status (first error wins)
+    int64_t* status_detail = nullptr;
+    int* errpos = nullptr;           // chain position of the first error
+    int pos = 0;
+    int rank_test = 1;
+    int column_scale = 1;
+};
+void chol_inverse(const CholParams& p, cudaStream_t st);
+
+// ------------------------------------------------------------------ projection (project.cu)
+struct ProjParams {
+    int n = 0, batch = 1, c_cap = 0;
+    const double* Q = nullptr;
+    int64_t ldq = 0, strideQ = 0;
+    const double* X = nullptr;  // n x 3 row-major
+    int64_t strideX = 0;
+    const int* dimC = nullptr;
+    int64_t dimStride = 0;
+    double* partial = nullptr;   // batch * nchunks * c_cap * 8
+    double* partial2 = nullptr;  // batch * recon_blocks * 2
+    int nchunks = 0, rows_per_chunk = 64, rows_per_warp = 2;
+    double* coeff = nullptr;  // c_cap x 4 per batch: Px Py Pz Ps (unsigned)
+    int64_t strideCoef = 0;
+    double* sign = nullptr;  // per batch, stride strideSign
+    int64_t strideSign = 0;
+    double* xhat = nullptr;  // n x 3 row-major per batch
+    int64_t strideXhat = 0;
+    double* e_out = nullptr;
+    int64_t strideE = 0;
+    double* stats = nullptr;  // per batch: [0] residual_rms [1] ||e|| [2] ||X-X^||^2
+    int64_t strideStats = 4;
+};
+int proj_chunks(int n);
+int proj_recon_blocks(int n, int rows_per_warp);
+void project(const ProjParams& p, cudaStream_t st);
+
+// ------------------------------------------------------------------ Jacobi RR (jacobi.cu)
+struct JacobiParams {
+    int batch = 1;
+    const double* H = nullptr;
+    int64_t ldh = 0, strideH = 0;
+    double* stage = nullptr;
+    int64_t strideStage = 0;
+    double* V = nullptr;  // eigenvectors, column j contiguous at V + j*ldv
+    int64_t ldv = 0, strideV = 0;
+    double* theta = nullptr;
+    double* theta_sorted = nullptr;
+    int64_t strideTheta = 0;
+    double* W = nullptr;  // sorted eigenvectors, row-major m x m
+    int64_t ldw = 0, strideW = 0;
+    int* sweeps = nullptr;
+    int max_sweeps = 40;
+    double tol = 1e-14;
+};
+struct JacobiPlan {
+    int nc = 2, b = 1, P = 4, mp = 8, smem = 0;
+    int64_t stage_elems = 0;
+};
+JacobiPlan jacobi_plan(int m);
+int jacobi_eigh(const JacobiParams& p, const JacobiPlan& pl, int m, cudaStream_t st);
+
+// ------------------------------------------------------------------ utilities (util.cu)
+void transpose_to_rowmajor(const double* colmajor, int rows, int cols, double* rowmajor, int64_t ld,
+                           cudaStream_t st);
+void transpose_to_colmajor(const double* rowmajor, int64_t ld, int rows, int cols, const double* sign,
+                           double* colmajor, cudaStream_t st);
+void fill(double* p, int64_t count, double v, cudaStream_t st);
+void gather_coords(const TileRef* tiles, int ntiles, int n, double* X, int64_t strideX, double* bbox,
+                   cudaStream_t st);
+void randn(double* p, int rows, int cols, int64_t ld, int64_t stride, int batch, uint64_t seed, cudaStream_t st);
+
+struct SpmmParams {
+    int n = 0, c = 0, batch = 1;
+    const int32_t* rowptr = nullptr;
+    int64_t strideRowptr = 0;
+    const int64_t* csr_offsets = nullptr;  // per batch offset into cols/vals (nullptr: 0)
+    int64_t offStride = 1;                 // csr_offsets index stride per batch entry
+    const int32_t* cols = nullptr;
+    const double* vals = nullptr;
+    const double* shift = nullptr;  // per batch diagonal shift (nullptr: 0)
+    const double* X = nullptr;
+    int64_t ldx = 0, strideX = 0;
+    double* Y = nullptr;
+    int64_t ldy = 0, strideY = 0;
+    const int* dimC = nullptr;
+    int64_t dimStride = 0;
+};
+void spmm(const SpmmParams& p, cudaStream_t st);
+
+struct Stitcher {
+    int n = 0, n_d = 0;
+    int32_t* offs = nullptr;
+    int64_t* slots = nullptr;
+    int32_t* missing = nullptr;
+    void build(const int32_t* members, int nsub, int n_d, int n, cudaStream_t st);
+    void release(cudaStream_t st);
+};
+struct StitchParams {
+    int n = 0, n_d = 0, weighted = 1;
+    const int32_t* offs = nullptr;
+    const int64_t* slots = nullptr;
+    const int32_t* rowptr = nullptr;  // per submesh id (n_d+1)
+    const double* xhat = nullptr;     // per submesh id n_d x 3 row-major
+    int64_t strideXhat = 0;
+    double* out = nullptr;  // SoA n x 3
+};
+void stitch(const StitchParams& p, cudaStream_t st);
+
+}  // namespace smg
