@@ -207,6 +207,15 @@ smg_status smg_gft(smg_context* ctx, int32_t rows, int32_t c, const double* basi
 smg_status smg_igft(smg_context* ctx, int32_t rows, int32_t c, const double* basis,
                     const double* coeffs, double* coords);
 
+/* ------------------------------------------------------------ diagnostics
+ * Per-stage device time (CUDA events on the context stream) of the library's
+ * kernels, the StageTimings analogue at kernel granularity.  Stages:
+ * "assemble", "factor", "solve", "orthonormalize" (= "gram" + "chol" + "trmm"
+ * + rank test), "project"; nested scopes are inclusive.  Enabling clears the
+ * record. */
+smg_status smg_profile_enable(smg_context* ctx, int32_t on);
+smg_status smg_profile_read(smg_context* ctx, const char* stage, int64_t* launches, double* total_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,7 +55,7 @@ EXPORTED = [
     "smg_compute_block_bases_fixed_sizes", "smg_compute_block_bases", "smg_run_chains",
     "smg_build_laplacian", "smg_default_shift", "smg_operator_create", "smg_operator_destroy",
     "smg_operator_apply", "smg_operator_spmm", "smg_orthonormalize", "smg_orthogonal_iteration",
-    "smg_dynamic_oi", "smg_bottom_subspace", "smg_gft", "smg_igft",
+    "smg_dynamic_oi", "smg_bottom_subspace", "smg_gft", "smg_igft", "smg_profile_enable", "smg_profile_read",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -97,6 +97,8 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_bottom_subspace": ([vp, vp, C.c_int32, vp, vp], C.c_int),
         "smg_gft": ([vp, C.c_int32, C.c_int32, vp, vp, vp], C.c_int),
         "smg_igft": ([vp, C.c_int32, C.c_int32, vp, vp, vp], C.c_int),
+        "smg_profile_enable": ([vp, C.c_int32], C.c_int),
+        "smg_profile_read": ([vp, C.c_char_p, c_int64_p, c_double_p], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

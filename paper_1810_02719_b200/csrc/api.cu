@@ -20,19 +20,7 @@ namespace {
 
 template <class F>
 smg_status guard(smg_context* ctx, F&& f) {
-    if (!ctx) return SMG_INVALID_ARGUMENT;
-    try {
-        SMG_CUDA(cudaSetDevice(ctx->device));
-        f();
-        ctx->error.clear();
-        return SMG_OK;
-    } catch (const Failure& e) {
-        ctx->error = e.what();
-        return e.code == 2 ? SMG_INVALID_ARGUMENT : SMG_ERROR;
-    } catch (const std::exception& e) {
-        ctx->error = e.what();
-        return SMG_ERROR;
-    }
+    return static_cast<smg_status>(guarded_call(ctx, std::forward<F>(f)));
 }
 
 // ---------------------------------------------------------------- staging
@@ -574,7 +562,7 @@ private:
         if (!stat_rms_.size()) {
             stat_rms_.alloc((size_t)K_ * B_, st_);
         }
-        copy_stat_kernel<<<(B_ + 127) / 128, 128, 0, st_>>>(ws_.stats.get(), 4, B_, stat_rms_.get() + (int64_t)pos * B_, 1);
+        ::smg::count_launch(), copy_stat_kernel<<<(B_ + 127) / 128, 128, 0, st_>>>(ws_.stats.get(), 4, B_, stat_rms_.get() + (int64_t)pos * B_, 1);
         std::vector<double*> cptr(B_, nullptr), bptr(B_, nullptr);
         bool anyc = false, anyb = false;
         for (int b = 0; b < B_; ++b) {
@@ -592,13 +580,13 @@ private:
         }
         if (anyc) {
             ptrs_c_.upload(cptr, st_);
-            coef_ptr_kernel<<<B_, 128, 0, st_>>>(ws_.coeff.get(), (int64_t)ws_.ld * 4, ws_.sign.get(), ws_.ld, c,
+            ::smg::count_launch(), coef_ptr_kernel<<<B_, 128, 0, st_>>>(ws_.coeff.get(), (int64_t)ws_.ld * 4, ws_.sign.get(), ws_.ld, c,
                                                  ptrs_c_.get());
             keep_.push_back(std::move(ptrs_c_));
         }
         if (anyb) {
             ptrs_b_.upload(bptr, st_);
-            basis_out_kernel<<<dim3(std::min(1024, (n_ * c + 255) / 256), B_), 256, 0, st_>>>(
+            ::smg::count_launch(), basis_out_kernel<<<dim3(std::min(1024, (n_ * c + 255) / 256), B_), 256, 0, st_>>>(
                 ws_.U.get(), ws_.ld, ws_.mstride(), n_, c, ws_.sign.get(), ws_.ld, ptrs_b_.get());
             keep_.push_back(std::move(ptrs_b_));
         }
@@ -661,7 +649,7 @@ private:
                 stt.release(st_);
                 fail(2, msg);
             }
-            stitch_tile_kernel<<<(int)std::min<int64_t>((meshes_[b].nv + 255) / 256, 4096), 256, 0, st_>>>(
+            ::smg::count_launch(), stitch_tile_kernel<<<(int)std::min<int64_t>((meshes_[b].nv + 255) / 256, 4096), 256, 0, st_>>>(
                 (int)meshes_[b].nv, n_, 1, stt.offs, stt.slots, tile_of_[b].get(), ts_.rowptr.get(), xhat_.get(),
                 co.recon_dev);
             stt.release(st_);
@@ -794,7 +782,7 @@ __global__ void apply_sign_kernel(double* U, int64_t ld, int n, int c, const dou
 }
 
 void ChainRunner::apply_signs(int b, int c) {
-    apply_sign_kernel<<<std::min(1024, (n_ * c + 255) / 256), 256, 0, st_>>>(
+    ::smg::count_launch(), apply_sign_kernel<<<std::min(1024, (n_ * c + 255) / 256), 256, 0, st_>>>(
         ws_.U.get() + (int64_t)b * ws_.mstride(), ws_.ld, n_, c, ws_.sign.get() + (int64_t)b * ws_.ld);
 }
 
@@ -891,6 +879,25 @@ smg_status smg_run_chains(smg_context* ctx, int32_t n_chains, const smg_mesh* me
         ChainRunner r(ctx, n_chains, meshes, segs, c, outs);
         r.run_fixed(sizes_in_order);
     });
+}
+
+smg_status smg_profile_enable(smg_context* ctx, int32_t on) {
+    if (!ctx) return SMG_INVALID_ARGUMENT;
+    ctx->profiling = on != 0;
+    ctx->prof.clear();
+    return SMG_OK;
+}
+
+smg_status smg_profile_read(smg_context* ctx, const char* stage, int64_t* launches, double* total_ms) {
+    if (!ctx || !stage || !launches || !total_ms) return SMG_INVALID_ARGUMENT;
+    if (std::string(stage) == "launches") {  // process-wide kernel launch counter
+        *launches = smg::launch_count();
+        *total_ms = 0.0;
+        return SMG_OK;
+    }
+    cudaSetDevice(ctx->device);
+    ctx->prof.read(stage, launches, total_ms);
+    return SMG_OK;
 }
 
 double smg_default_shift(double trace, int32_t n, double scale) {

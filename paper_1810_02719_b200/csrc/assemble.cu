@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(NT) fill_kernel(const TileRef* tiles, int n, i
                 const double dx = t.x[gi] - t.x[gj];
                 const double dy = t.y[gi] - t.y[gj];
                 const double dz = t.z[gi] - t.z[gj];
-                const double d2 = __fadd_rn(__fadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
                 const double inv = 1.0 / d2;
                 if (!(d2 > 0.0) || !isfinite(inv)) {
                     // first offending (row, neighbour slot) in the reference's loop order
@@ -280,29 +280,29 @@ __global__ void rcm_kernel(const int32_t* rowptr_all, const int32_t* cols_all, c
 }  // namespace
 
 void assemble_count(const TileRef* tiles, int ntiles, int n, int32_t* nnz_out, cudaStream_t st) {
-    if (ntiles) count_kernel<<<ntiles, NT, 0, st>>>(tiles, n, nnz_out);
+    if (ntiles) ::smg::count_launch(), count_kernel<<<ntiles, NT, 0, st>>>(tiles, n, nnz_out);
 }
 
 void assemble_fill(const TileRef* tiles, int ntiles, int n, int weighting, const int64_t* csr_offsets,
                    int32_t* rowptr, int32_t* cols, double* vals, double* trace, int* status,
                    int64_t* status_detail, cudaStream_t st) {
     if (ntiles)
-        fill_kernel<<<ntiles, NT, 0, st>>>(tiles, n, weighting, csr_offsets, rowptr, cols, vals, trace, status,
+        ::smg::count_launch(), fill_kernel<<<ntiles, NT, 0, st>>>(tiles, n, weighting, csr_offsets, rowptr, cols, vals, trace, status,
                                            status_detail);
 }
 
 void exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int count, cudaStream_t st) {
-    scan_kernel<<<1, 32, 0, st>>>(in, out, count);
+    ::smg::count_launch(), scan_kernel<<<1, 32, 0, st>>>(in, out, count);
 }
 
 void natural_bandwidth(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, const int32_t* perm,
                        int ntiles, int n, int32_t* bw_out, int32_t* blockw_out, cudaStream_t st) {
-    if (ntiles) bandwidth_kernel<<<ntiles, NT, 0, st>>>(rowptr, cols, csr_offsets, perm, n, bw_out, blockw_out);
+    if (ntiles) ::smg::count_launch(), bandwidth_kernel<<<ntiles, NT, 0, st>>>(rowptr, cols, csr_offsets, perm, n, bw_out, blockw_out);
 }
 
 void rcm_order(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, int ntiles, int n,
                int32_t* perm, cudaStream_t st) {
-    if (ntiles) rcm_kernel<<<ntiles, 128, 0, st>>>(rowptr, cols, csr_offsets, n, perm);
+    if (ntiles) ::smg::count_launch(), rcm_kernel<<<ntiles, 128, 0, st>>>(rowptr, cols, csr_offsets, n, perm);
 }
 
 }  // namespace smg

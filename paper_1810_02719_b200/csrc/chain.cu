@@ -141,34 +141,34 @@ void ritz_residual(const double* LZ, const double* Z, const double* theta, int n
                    int64_t stride, int64_t strideTheta, int batch, double* partial, double* out, cudaStream_t st) {
     const int rows = 128;
     const int chunks = (n + rows - 1) / rows;
-    ritz_partial_kernel<<<dim3(chunks, batch), 256, 0, st>>>(LZ, Z, theta, n, ncols, ld, stride, strideTheta,
+    ::smg::count_launch(), ritz_partial_kernel<<<dim3(chunks, batch), 256, 0, st>>>(LZ, Z, theta, n, ncols, ld, stride, strideTheta,
                                                               partial, rows);
-    ritz_reduce_kernel<<<batch, 256, 0, st>>>(partial, chunks, ncols, out);
+    ::smg::count_launch(), ritz_reduce_kernel<<<batch, 256, 0, st>>>(partial, chunks, ncols, out);
 }
 
 void doi_decide(DoiState* states, int batch, const double* stats, int64_t strideStats,
                 cudaGraphConditionalHandle handle, int use_handle, const int* chain_status, cudaStream_t st) {
-    doi_decide_kernel<<<1, 1, 0, st>>>(states, batch, stats, strideStats, handle, use_handle, chain_status);
+    ::smg::count_launch(), doi_decide_kernel<<<1, 1, 0, st>>>(states, batch, stats, strideStats, handle, use_handle, chain_status);
 }
 
 void doi_append(const DoiState* states, double* U, int64_t ldu, int64_t strideU, const double* e, int64_t strideE,
                 int n, int batch, cudaStream_t st) {
-    doi_append_kernel<<<dim3((n + 255) / 256, batch), 256, 0, st>>>(states, U, ldu, strideU, e, strideE, n);
+    ::smg::count_launch(), doi_append_kernel<<<dim3((n + 255) / 256, batch), 256, 0, st>>>(states, U, ldu, strideU, e, strideE, n);
 }
 
 void compute_delta(const double* trace, int ntiles, int n, double scale, double* delta, cudaStream_t st) {
-    if (ntiles) delta_kernel<<<(ntiles + 255) / 256, 256, 0, st>>>(trace, ntiles, n, scale, delta);
+    if (ntiles) ::smg::count_launch(), delta_kernel<<<(ntiles + 255) / 256, 256, 0, st>>>(trace, ntiles, n, scale, delta);
 }
 
 void compute_first_shift(const int32_t* rowptr, const int32_t* cols, const double* vals, const int64_t* csr_offsets,
                          const double* trace, int ntiles, int n, double* shift, cudaStream_t st) {
-    if (ntiles) first_shift_kernel<<<ntiles, 256, 0, st>>>(rowptr, cols, vals, csr_offsets, trace, ntiles, n, shift);
+    if (ntiles) ::smg::count_launch(), first_shift_kernel<<<ntiles, 256, 0, st>>>(rowptr, cols, vals, csr_offsets, trace, ntiles, n, shift);
 }
 
 void coeff_out(const double* coef, int64_t strideCoef, const double* sign, int64_t strideSign, const int* dimC,
                int64_t dimStride, int c_fixed, double* out, const int64_t* out_offsets, const int32_t* ids, int batch,
                cudaStream_t st) {
-    coeff_out_kernel<<<batch, 128, 0, st>>>(coef, strideCoef, sign, strideSign, dimC, dimStride, c_fixed, out,
+    ::smg::count_launch(), coeff_out_kernel<<<batch, 128, 0, st>>>(coef, strideCoef, sign, strideSign, dimC, dimStride, c_fixed, out,
                                             out_offsets, ids);
 }
 

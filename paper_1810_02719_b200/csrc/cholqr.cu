@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(NT) chol_kernel(CholParams p) {
     }
     tr = block_sum(tr, red);
     const double scale = sqrt(tr);
+    if (tid == 0 && p.vnorm) p.vnorm[b] = scale;
     if (!(scale > 0.0) || !isfinite(scale)) {
         if (tid == 0) record(scale == 0.0 ? kAllZero : kNotFinite, -1);
         return;
@@ -69,7 +70,9 @@ __global__ void __launch_bounds__(NT) chol_kernel(CholParams p) {
     for (int j = 0; j < c; ++j) {
         const double piv = A[j * ld + j];
         const double rjj = sqrt(piv);
-        const bool bad_piv = !(piv > 0.0) || !isfinite(piv) || !(d[j] > 0.0);
+        // A scaled pivot below 1e-12 means r~_jj < 1e-6: beyond what the Gram
+        // resolves, i.e. numerically dependent -- the rank-test verdict.
+        const bool bad_piv = !(piv > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(piv) || !(d[j] > 0.0);
         const double rkk = bad_piv ? 0.0 : rjj * d[j];
         if (bad_piv || (p.rank_test && rkk < thresh)) {
             if (tid == 0) {
@@ -122,7 +125,50 @@ __global__ void __launch_bounds__(NT) chol_kernel(CholParams p) {
     }
 }
 
+// partial diag(Q^T V) over a chunk of rows, threads over columns (coalesced rows)
+constexpr int RC_ROWS = 128;
+__global__ void rank_partial_kernel(RankCheckParams p) {
+    const int b = blockIdx.y, chunk = blockIdx.x;
+    if (p.status[b] != kOk) return;
+    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    const int r0 = chunk * RC_ROWS, r1 = min(p.n, r0 + RC_ROWS);
+    const double* Q = p.Q + (int64_t)b * p.stride;
+    const double* V = p.V + (int64_t)b * p.stride;
+    for (int k = threadIdx.x; k < c; k += blockDim.x) {
+        double acc = 0.0;
+        for (int i = r0; i < r1; ++i) acc = fma(Q[(int64_t)i * p.ld + k], V[(int64_t)i * p.ld + k], acc);
+        p.partial[((int64_t)b * gridDim.x + chunk) * p.c_cap + k] = acc;
+    }
+}
+
+__global__ void rank_test_kernel(RankCheckParams p, int nchunks) {
+    __shared__ int first;
+    const int b = blockIdx.x;
+    if (p.status[b] != kOk) return;
+    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    if (threadIdx.x == 0) first = c;
+    __syncthreads();
+    const double thresh = 1e-13 * p.vnorm[b];
+    for (int k = threadIdx.x; k < c; k += blockDim.x) {
+        double r = 0.0;
+        for (int ch = 0; ch < nchunks; ++ch) r += p.partial[((int64_t)b * nchunks + ch) * p.c_cap + k];
+        if (!(fabs(r) >= thresh)) atomicMin(&first, k);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && first < c) {
+        p.status[b] = kRankDeficient;
+        if (p.status_detail) p.status_detail[b] = first;
+        if (p.errpos) p.errpos[b] = p.pos;
+    }
+}
+
 }  // namespace
+
+void rank_check(const RankCheckParams& p, cudaStream_t st) {
+    const int chunks = (p.n + RC_ROWS - 1) / RC_ROWS;
+    ::smg::count_launch(), rank_partial_kernel<<<dim3(chunks, p.batch), 256, 0, st>>>(p);
+    ::smg::count_launch(), rank_test_kernel<<<p.batch, 256, 0, st>>>(p, chunks);
+}
 
 void chol_inverse(const CholParams& p, cudaStream_t st) {
     const int bytes = std::min(p.c_cap, SMEM_C) * std::min(p.c_cap, SMEM_C) * 8;
@@ -131,7 +177,7 @@ void chol_inverse(const CholParams& p, cudaStream_t st) {
         cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C * SMEM_C * 8);
         configured = 1;
     }
-    chol_kernel<<<p.batch, NT, bytes, st>>>(p);
+    ::smg::count_launch(), chol_kernel<<<p.batch, NT, bytes, st>>>(p);
 }
 
 }  // namespace smg

@@ -4,11 +4,14 @@
 #include <string>
 
 #include "engine.h"
+#include "profiler.h"
 
 struct smg_context {
     int device = 0;
     cudaStream_t stream = nullptr;
     std::string error;
+    bool profiling = false;
+    smg::Profiler prof;
 };
 
 struct smg_operator {
@@ -17,3 +20,28 @@ struct smg_operator {
     int n = 0, z = 1;
     double delta = 0.0;
 };
+
+namespace smg {
+// Runs f() for an API call: device selection, profiler activation, exception
+// to status translation (exceptions never cross the C ABI).
+template <class F>
+int guarded_call(smg_context* ctx, F&& f) {
+    if (!ctx) return 2;
+    struct Activate {
+        explicit Activate(smg_context* c) { active_profiler() = c->profiling ? &c->prof : nullptr; }
+        ~Activate() { active_profiler() = nullptr; }
+    } act(ctx);
+    try {
+        SMG_CUDA(cudaSetDevice(ctx->device));
+        f();
+        ctx->error.clear();
+        return 0;
+    } catch (const Failure& e) {
+        ctx->error = e.what();
+        return e.code == 2 ? 2 : 3;
+    } catch (const std::exception& e) {
+        ctx->error = e.what();
+        return 3;
+    }
+}
+}  // namespace smg

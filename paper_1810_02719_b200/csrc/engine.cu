@@ -2,6 +2,7 @@
 #include <cstdio>
 
 #include "engine.h"
+#include "profiler.h"
 
 namespace smg {
 
@@ -20,6 +21,7 @@ int supported_width(int w) {
 }  // namespace
 
 void TileSet::build(const std::vector<TileRef>& tiles, int n_, int weighting, double shift_scale, cudaStream_t st) {
+    ProfScope prof("assemble", st);
     ntiles = (int)tiles.size();
     n = n_;
     require(n >= 2, "submesh must have at least 2 vertices");
@@ -113,6 +115,7 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
 }
 
 void FactorSet::factor(const TileSet& ts, int first_tile, int cnt, const double* shift, cudaStream_t st) {
+    ProfScope prof("factor", st);
     first = first_tile;
     count = cnt;
     strideF = (int64_t)ts.Kb * 2 * ts.W * ts.W;
@@ -162,9 +165,12 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     work.alloc(cc, st);
     // split-K over the n rows for the Gram: aim at ~2 waves of CTAs
     const int tiles = ((ld + 63) / 64) * ((ld + 63) / 64 + 1) / 2;
-    splits = std::max(1, std::min(npad / 128, 296 / std::max(1, tiles * B)));
+    // (a function of the shape only, so results do not depend on the batch size)
+    splits = std::max(1, std::min(npad / 128, 296 / std::max(1, tiles)));
     Gws.alloc((size_t)B * splits * ld * ld, st);
     rdiag.alloc((size_t)B * ld, st);
+    vnorm.alloc(B, st);
+    rpart.alloc((size_t)B * ((npad + 127) / 128) * ld, st);
     coeff.alloc((size_t)B * ld * 4, st);
     sign.alloc((size_t)B * ld, st);
     e.alloc((size_t)B * npad, st);
@@ -181,6 +187,7 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
 
 void solve_batch(const StepCtx& cx, Workspace& ws, const FactorSet& fs, int tile0, int tstride, const double* in,
                  double* out, int c, const int* dimC, int z, bool once) {
+    ProfScope prof("solve", cx.st);
     const TileSet& ts = *cx.ts;
     SolveParams p;
     p.n = ts.n;
@@ -239,6 +246,7 @@ void gram(Workspace& ws, const double* V, int c, const int* dimC, int n, cudaStr
         g.ldc = ws.ld;
         g.strideC = (int64_t)ws.ld * ws.ld;
     }
+    ProfScope prof("gram", st);
     gemm(g, true, false, st);
 }
 
@@ -261,6 +269,7 @@ void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, i
     g.dimN = dimC;
     g.dimK = dimC;
     g.dimStride = 1;
+    ProfScope prof("trmm", st);
     gemm(g, false, false, st);
 }
 
@@ -285,24 +294,53 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
     p.pos = pos;
     p.rank_test = rank_test ? 1 : 0;
     p.column_scale = column_scale ? 1 : 0;
+    p.vnorm = rank_test ? ws.vnorm.get() : nullptr;
+    ProfScope prof("chol", st);
     chol_inverse(p, st);
 }
 }  // namespace
 
 void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
                 bool rank_test, int pos) {
+    ProfScope prof("orthonormalize", cx.st);
     const int n = ws.npad;
+    if (rank_test && in == out) {
+        // keep the input for the accurate rank test (T is free between solves)
+        SMG_CUDA(cudaMemcpyAsync(ws.T.get(), in, sizeof(double) * ws.mstride() * ws.B, cudaMemcpyDeviceToDevice,
+                                 cx.st));
+        in = ws.T.get();
+    }
     gram(ws, in, c, dimC, n, cx.st);
     chol(ws, c, dimC, rank_test, true, pos, cx.st);
     trmm(ws, in, ws.R.get(), c, dimC, n, cx.st);
     gram(ws, ws.R.get(), c, dimC, n, cx.st);
     chol(ws, c, dimC, false, true, pos, cx.st);
     trmm(ws, ws.R.get(), out, c, dimC, n, cx.st);
+    if (rank_test) {
+        RankCheckParams r;
+        r.n = ws.n;
+        r.batch = ws.B;
+        r.c_cap = c;
+        r.Q = out;
+        r.V = in;
+        r.ld = ws.ld;
+        r.stride = ws.mstride();
+        r.dimC = dimC;
+        r.dimStride = 1;
+        r.vnorm = ws.vnorm.get();
+        r.partial = ws.rpart.get();
+        r.status = ws.status.get();
+        r.status_detail = ws.detail.get();
+        r.errpos = ws.errpos.get();
+        r.pos = pos;
+        rank_check(r, cx.st);
+    }
     SMG_CUDA(cudaGetLastError());
 }
 
 void project_batch(const StepCtx& cx, Workspace& ws, const double* Q, int c, const int* dimC, const double* X,
                    int64_t strideX, double* xhat, int64_t strideXhat) {
+    ProfScope prof("project", cx.st);
     ProjParams p;
     p.n = ws.n;
     p.batch = ws.B;

@@ -61,6 +61,8 @@ public:
     }
     T* get() const { return p_; }
     size_t size() const { return n_; }
+    // free on another stream later (objects that outlive the allocating stream)
+    void rebind(cudaStream_t st) { st_ = st; }
 
 private:
     T* p_ = nullptr;
@@ -99,6 +101,11 @@ struct TileSet {
                         cudaStream_t st);
     void finish_build(double shift_scale, const std::vector<double>* explicit_delta, cudaStream_t st);
     const int32_t* perm_of(int tile) const { return use_perm ? perm.get() + (int64_t)tile * n : nullptr; }
+    void rebind(cudaStream_t st) {
+        refs.rebind(st), nnz.rebind(st), rowptr.rebind(st), cols.rebind(st), perm.rebind(st), bw.rebind(st);
+        blockw.rebind(st), off.rebind(st), detail.rebind(st), vals.rebind(st), trace.rebind(st);
+        delta.rebind(st), shift0.rebind(st), X.rebind(st), bbox.rebind(st), status.rebind(st);
+    }
 };
 
 struct FactorSet {
@@ -109,13 +116,14 @@ struct FactorSet {
     void factor(const TileSet& ts, int first_tile, int count, const double* shift, cudaStream_t st);
     const double* f(int tile) const { return fwd.get() + (int64_t)(tile - first) * strideF; }
     const double* b(int tile) const { return bwd.get() + (int64_t)(tile - first) * strideF; }
+    void rebind(cudaStream_t st) { fwd.rebind(st), bwd.rebind(st), status.rebind(st); }
 };
 
 // ------------------------------------------------------------ workspace
 struct Workspace {
     int B = 0, n = 0, npad = 0, ld = 0, ccap = 0;
     int splits = 1;
-    DBuf<double> U, V, T, R, G, Gws, Bm, work, rdiag, coeff, sign, e, ppart, ppart2, stats;
+    DBuf<double> U, V, T, R, G, Gws, Bm, work, rdiag, vnorm, rpart, coeff, sign, e, ppart, ppart2, stats;
     DBuf<int> status, errpos, scratch_status;
     DBuf<int64_t> detail;
     DBuf<double> H, Hst, Vj, theta, theta_s, Wm, ritz_part, ritz;

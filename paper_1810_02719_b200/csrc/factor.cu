@@ -185,7 +185,7 @@ template <int W>
 void launch(const FactorParams& p, cudaStream_t st) {
     const int bytes = FactorSmem<W>::bytes(p.n);
     cudaFuncSetAttribute(factor_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    factor_kernel<W><<<p.ntiles, NT, bytes, st>>>(p);
+    ::smg::count_launch(), factor_kernel<W><<<p.ntiles, NT, bytes, st>>>(p);
 }
 
 }  // namespace

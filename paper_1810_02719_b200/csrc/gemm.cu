@@ -185,13 +185,13 @@ void gemm(const GemmParams& p0, bool transA, bool transB, cudaStream_t st) {
     const int gm = (p.M + BM - 1) / BM, gn = (p.N + BN - 1) / BN;
     if (gm == 0 || gn == 0 || p.batch == 0) return;
     dim3 grid(gn, gm, p.batch * p.splits);
-    if (transA && !transB) gemm_kernel<true, false><<<grid, NT, 0, st>>>(p);
-    else if (!transA && !transB) gemm_kernel<false, false><<<grid, NT, 0, st>>>(p);
-    else if (transA && transB) gemm_kernel<true, true><<<grid, NT, 0, st>>>(p);
-    else gemm_kernel<false, true><<<grid, NT, 0, st>>>(p);
+    if (transA && !transB) ::smg::count_launch(), gemm_kernel<true, false><<<grid, NT, 0, st>>>(p);
+    else if (!transA && !transB) ::smg::count_launch(), gemm_kernel<false, false><<<grid, NT, 0, st>>>(p);
+    else if (transA && transB) ::smg::count_launch(), gemm_kernel<true, true><<<grid, NT, 0, st>>>(p);
+    else ::smg::count_launch(), gemm_kernel<false, true><<<grid, NT, 0, st>>>(p);
     if (p.splits > 1) {
         dim3 rg((unsigned)std::min<int64_t>(((int64_t)p.M * p.N + 255) / 256, 1024), p.batch);
-        gemm_reduce_kernel<<<rg, 256, 0, st>>>(p);
+        ::smg::count_launch(), gemm_reduce_kernel<<<rg, 256, 0, st>>>(p);
     }
 }
 

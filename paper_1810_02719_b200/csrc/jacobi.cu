@@ -276,10 +276,11 @@ int jacobi_eigh(const JacobiParams& p, const JacobiPlan& pl, int m, cudaStream_t
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    ::smg::count_launch();
     cudaError_t err = cudaLaunchKernelEx(&cfg, jacobi_kernel, p, sh);
     if (err != cudaSuccess) return (int)err;
     const int sbytes = m * 8 + m * 4;
-    sort_kernel<<<p.batch, 256, sbytes, st>>>(p, m);
+    ::smg::count_launch(), sort_kernel<<<p.batch, 256, sbytes, st>>>(p, m);
     return (int)cudaGetLastError();
 }
 

@@ -8,6 +8,11 @@
 
 namespace smg {
 
+// Every kernel launch site calls this (comma-prefixed); read via the
+// diagnostics API as the "launches" stage.
+int count_launch();
+int64_t launch_count();
+
 // ------------------------------------------------------------------ GEMM (gemm.cu)
 struct GemmParams {
     int M = 0, N = 0, K = 0, batch = 1, splits = 1;
@@ -102,10 +107,28 @@ struct CholParams {
     int64_t* status_detail = nullptr;
     int* errpos = nullptr;           // chain position of the first error
     int pos = 0;
+    double* vnorm = nullptr;         // ||V||_F per batch entry (rank-test scale)
     int rank_test = 1;
     int column_scale = 1;
 };
 void chol_inverse(const CholParams& p, cudaStream_t st);
+// Accurate reference rank test after CholeskyQR2: |r_kk| = |q_k^T v_k| against
+// 1e-13 ||V||_F (first failing column, sticky status).
+struct RankCheckParams {
+    int n = 0, batch = 1, c_cap = 0;
+    const double* Q = nullptr;
+    const double* V = nullptr;
+    int64_t ld = 0, stride = 0;
+    const int* dimC = nullptr;
+    int64_t dimStride = 0;
+    const double* vnorm = nullptr;
+    double* partial = nullptr;  // batch * chunks * c_cap
+    int* status = nullptr;
+    int64_t* status_detail = nullptr;
+    int* errpos = nullptr;
+    int pos = 0;
+};
+void rank_check(const RankCheckParams& p, cudaStream_t st);
 
 // ------------------------------------------------------------------ projection (project.cu)
 struct ProjParams {

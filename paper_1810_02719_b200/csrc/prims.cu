@@ -20,19 +20,7 @@ namespace {
 
 template <class F>
 smg_status guard(smg_context* ctx, F&& f) {
-    if (!ctx) return SMG_INVALID_ARGUMENT;
-    try {
-        SMG_CUDA(cudaSetDevice(ctx->device));
-        f();
-        ctx->error.clear();
-        return SMG_OK;
-    } catch (const Failure& e) {
-        ctx->error = e.what();
-        return e.code == 2 ? SMG_INVALID_ARGUMENT : SMG_ERROR;
-    } catch (const std::exception& e) {
-        ctx->error = e.what();
-        return SMG_ERROR;
-    }
+    return static_cast<smg_status>(guarded_call(ctx, std::forward<F>(f)));
 }
 
 std::string status_message(int kind, int64_t detail) {
@@ -151,6 +139,10 @@ smg_status smg_operator_create(smg_context* ctx, int32_t n, const int32_t* rowpt
         op->fs.factor(op->ts, 0, 1, nullptr, ctx->stream);
         std::vector<int> fst = download(op->fs.status.get(), 1, ctx->stream);
         if (fst[0] != 0) fail(3, "sparse factorization of the shifted Laplacian failed");
+        // the operator may outlive the context's stream: free on the default stream
+        SMG_CUDA(cudaStreamSynchronize(ctx->stream));
+        op->ts.rebind(0);
+        op->fs.rebind(0);
         *out = op.release();
     });
 }
@@ -365,7 +357,7 @@ extern "C" smg_status smg_igft(smg_context* ctx, int32_t rows, int32_t c, const 
         DBuf<double> C, out;
         C.upload(coeffs, (size_t)c * 3, st);
         out.alloc((size_t)rows * 3, st);
-        igft_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ws.U.get(), ws.ld, rows, c, C.get(), out.get());
+        ::smg::count_launch(), igft_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ws.U.get(), ws.ld, rows, c, C.get(), out.get());
         SMG_CUDA(cudaGetLastError());
         SMG_CUDA(cudaMemcpyAsync(coords, out.get(), 8 * (size_t)rows * 3, cudaMemcpyDeviceToHost, st));
         SMG_CUDA(cudaStreamSynchronize(st));

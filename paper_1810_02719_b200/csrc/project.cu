@@ -172,11 +172,11 @@ void project(const ProjParams& p0, cudaStream_t st) {
     p.rows_per_chunk = 64;
     p.nchunks = proj_chunks(p.n);
     if (p.rows_per_warp <= 0) p.rows_per_warp = 2;
-    partial_kernel<<<dim3(p.nchunks, p.batch), PNT, 0, st>>>(p);
-    reduce_kernel<<<p.batch, PNT, 0, st>>>(p);
+    ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), PNT, 0, st>>>(p);
+    ::smg::count_launch(), reduce_kernel<<<p.batch, PNT, 0, st>>>(p);
     const int nb = proj_recon_blocks(p.n, p.rows_per_warp);
-    recon_kernel<<<dim3(nb, p.batch), PNT, 0, st>>>(p);
-    stats_kernel<<<(p.batch + 127) / 128, 128, 0, st>>>(p, nb);
+    ::smg::count_launch(), recon_kernel<<<dim3(nb, p.batch), PNT, 0, st>>>(p);
+    ::smg::count_launch(), stats_kernel<<<(p.batch + 127) / 128, 128, 0, st>>>(p, nb);
 }
 
 }  // namespace smg

@@ -187,7 +187,7 @@ void launch(const SolveParams& p, cudaStream_t st) {
         configured = true;
     }
     dim3 grid((p.c_cap + CS - 1) / CS, p.batch);
-    solve_kernel<W, CS><<<grid, NT, bytes, st>>>(p);
+    ::smg::count_launch(), solve_kernel<W, CS><<<grid, NT, bytes, st>>>(p);
 }
 
 }  // namespace

@@ -72,7 +72,7 @@ __global__ void gather_kernel(const TileRef* tiles, int n, double* X, int64_t st
                 hi[a] = fmax(hi[a], red[3 + a][k]);
             }
         const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
-        bbox[blockIdx.x] = n > 0 ? sqrt(__fadd_rn(__fadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)))
+        bbox[blockIdx.x] = n > 0 ? sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)))
                                  : 0.0;
     }
 }
@@ -89,7 +89,9 @@ __global__ void randn_kernel(double* p, int rows, int cols, int64_t ld, int64_t 
     const int64_t total = (int64_t)rows * cols;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(e / cols), j = (int)(e % cols);
-        const uint64_t h1 = splitmix(seed ^ splitmix((uint64_t)b * 0x100000001ULL + (uint64_t)e * 2));
+        // the same start block for every batch entry: a chain's result must not
+        // depend on its position in a batch
+        const uint64_t h1 = splitmix(seed ^ splitmix((uint64_t)e * 2));
         const uint64_t h2 = splitmix(h1 + 0x632be59bd9b4e019ULL);
         const double u1 = ((h1 >> 11) + 1) * (1.0 / 9007199254740993.0);
         const double u2 = (h2 >> 11) * (1.0 / 9007199254740992.0);
@@ -217,31 +219,31 @@ inline int blocks_for(int64_t total, int nt) { return (int)std::min<int64_t>((to
 
 void transpose_to_rowmajor(const double* cm, int rows, int cols, double* rm, int64_t ld, cudaStream_t st) {
     const int64_t total = (int64_t)rows * cols;
-    if (total) to_rowmajor_kernel<<<blocks_for(total, 256), 256, 0, st>>>(cm, rows, cols, rm, ld);
+    if (total) ::smg::count_launch(), to_rowmajor_kernel<<<blocks_for(total, 256), 256, 0, st>>>(cm, rows, cols, rm, ld);
 }
 
 void transpose_to_colmajor(const double* rm, int64_t ld, int rows, int cols, const double* sign, double* cm,
                            cudaStream_t st) {
     const int64_t total = (int64_t)rows * cols;
-    if (total) to_colmajor_kernel<<<blocks_for(total, 256), 256, 0, st>>>(rm, ld, rows, cols, sign, cm);
+    if (total) ::smg::count_launch(), to_colmajor_kernel<<<blocks_for(total, 256), 256, 0, st>>>(rm, ld, rows, cols, sign, cm);
 }
 
 void fill(double* p, int64_t count, double v, cudaStream_t st) {
-    if (count) fill_kernel<<<blocks_for(count, 256), 256, 0, st>>>(p, count, v);
+    if (count) ::smg::count_launch(), fill_kernel<<<blocks_for(count, 256), 256, 0, st>>>(p, count, v);
 }
 
 void gather_coords(const TileRef* tiles, int ntiles, int n, double* X, int64_t strideX, double* bbox,
                    cudaStream_t st) {
-    if (ntiles) gather_kernel<<<ntiles, 256, 0, st>>>(tiles, n, X, strideX, bbox);
+    if (ntiles) ::smg::count_launch(), gather_kernel<<<ntiles, 256, 0, st>>>(tiles, n, X, strideX, bbox);
 }
 
 void randn(double* p, int rows, int cols, int64_t ld, int64_t stride, int batch, uint64_t seed, cudaStream_t st) {
     const int64_t total = (int64_t)rows * cols;
-    randn_kernel<<<dim3(blocks_for(total, 256), batch), 256, 0, st>>>(p, rows, cols, ld, stride, seed);
+    ::smg::count_launch(), randn_kernel<<<dim3(blocks_for(total, 256), batch), 256, 0, st>>>(p, rows, cols, ld, stride, seed);
 }
 
 void spmm(const SpmmParams& p, cudaStream_t st) {
-    spmm_kernel<<<dim3((p.n + SPMM_ROWS - 1) / SPMM_ROWS, p.batch), SPMM_NT, 0, st>>>(p);
+    ::smg::count_launch(), spmm_kernel<<<dim3((p.n + SPMM_ROWS - 1) / SPMM_ROWS, p.batch), SPMM_NT, 0, st>>>(p);
 }
 
 void Stitcher::build(const int32_t* members, int nsub, int n_d, int n, cudaStream_t st) {
@@ -253,18 +255,18 @@ void Stitcher::build(const int32_t* members, int nsub, int n_d, int n, cudaStrea
     int32_t* cnt;
     cudaMallocAsync(&cnt, sizeof(int32_t) * (n + 1), st);
     cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n + 1), st);
-    if (count) owner_count_kernel<<<blocks_for(count, 256), 256, 0, st>>>(members, count, cnt);
+    if (count) ::smg::count_launch(), owner_count_kernel<<<blocks_for(count, 256), 256, 0, st>>>(members, count, cnt);
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, offs, n + 1, st);
     void* tmp;
     cudaMallocAsync(&tmp, tmp_bytes, st);
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, offs, n + 1, st);
     cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n + 1), st);
-    if (count) owner_fill_kernel<<<blocks_for(count, 256), 256, 0, st>>>(members, count, n_d, offs, cnt, slots);
-    owner_sort_kernel<<<blocks_for(n, 256), 256, 0, st>>>(n, offs, slots);
+    if (count) ::smg::count_launch(), owner_fill_kernel<<<blocks_for(count, 256), 256, 0, st>>>(members, count, n_d, offs, cnt, slots);
+    ::smg::count_launch(), owner_sort_kernel<<<blocks_for(n, 256), 256, 0, st>>>(n, offs, slots);
     cudaMallocAsync(&missing, sizeof(int32_t), st);
     cudaMemsetAsync(missing, 0, sizeof(int32_t), st);
-    coverage_kernel<<<blocks_for(n, 256), 256, 0, st>>>(n, offs, missing);
+    ::smg::count_launch(), coverage_kernel<<<blocks_for(n, 256), 256, 0, st>>>(n, offs, missing);
     cudaFreeAsync(tmp, st);
     cudaFreeAsync(cnt, st);
 }
@@ -279,7 +281,7 @@ void Stitcher::release(cudaStream_t st) {
 }
 
 void stitch(const StitchParams& p, cudaStream_t st) {
-    stitch_kernel<<<blocks_for(p.n, 256), 256, 0, st>>>(p);
+    ::smg::count_launch(), stitch_kernel<<<blocks_for(p.n, 256), 256, 0, st>>>(p);
 }
 
 }  // namespace smg

@@ -118,6 +118,13 @@ def _grid_faces(W: int, H: int) -> np.ndarray:
 
 
 def grid_mesh(W: int, H: int, seed: int, sigma: float) -> Mesh:
+    faces = _grid_faces(W, H)
+    offs, cols = build_edges(faces, W * H)
+    return Mesh(grid_vertices(W, H, seed, sigma), faces, offs, cols)
+
+
+def grid_vertices(W: int, H: int, seed: int, sigma: float) -> np.ndarray:
+    """Vertices of the seeded height-field grid (connectivity is seed independent)."""
     rng = np.random.Generator(np.random.PCG64(seed))
     fx = rng.uniform(1.0, 4.0, size=3)
     fy = rng.uniform(1.0, 4.0, size=3)
@@ -129,9 +136,7 @@ def grid_mesh(W: int, H: int, seed: int, sigma: float) -> Mesh:
     for k in range(3):
         z += np.sin(2.0 * math.pi * (fx[k] * x / (W - 1) + fy[k] * y / (H - 1)) + phi[k])
     z += rng.normal(0.0, sigma, size=W * H)
-    faces = _grid_faces(W, H)
-    offs, cols = build_edges(faces, W * H)
-    return Mesh(np.stack([x, y, z], axis=1), faces, offs, cols)
+    return np.stack([x, y, z], axis=1)
 
 
 def grid_tiles(W: int, H: int, tw: int, th: int) -> Segmentation:
