@@ -1,0 +1,438 @@
+#!/usr/bin/env python3
+"""bench.py -- vertices/s through OI track + project + reconstruct (BASELINE.json).
+
+Default workload: config 5 (64 independent 512x512 grid meshes, 128 tiles of
+32x64 = 2048 vertices each, c = 200, one warm-started OI step per tile, fp64),
+the batched configuration the metric's multi-GPU scaling is quoted on.  One
+"step" = every mesh of the job carried through the full chain: Laplacian
+assembly, factorisation, first-submesh basis, OI tracking, projection, stitched
+reconstruction (+ the NCCL gather of per-mesh results to all ranks when N > 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5|C2|C3|C4]
+  python bench.py --impl reference ...     # CPU oracle (port) arm
+
+Chains shard across ranks with no data-path collective (strong scaling: the 64
+meshes are split over N GPUs).  Timing: W untimed warm-up steps, then K steps
+bracketed by barrier + synchronize, CUDA events on the launching device, max
+over ranks.  Inputs (0.9 GB for C5) exceed the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "vertices/sec through OI track+project+reconstruct; % of HBM/FP64 roofline"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_TFLOPS = 37.18  # DMMA mma.sync f64, profiles/fp64_peak_r01.txt (measured on this pool's B200)
+
+CONFIGS = {
+    # name: (W, H, tile_w, tile_h, c, t, meshes, sigma, seed0)
+    "C5": dict(W=512, H=512, tw=64, th=32, c=200, t=1, meshes=64, sigma=0.01, seed0=5000,
+               desc="64 x 512^2 grid meshes, 128 tiles of 32x64 (n_d=2048) each, c=200, t=1"),
+    "C2": dict(W=256, H=256, tw=32, th=32, c=100, t=1, meshes=1, sigma=0.005, seed0=202,
+               desc="256^2 grid, 64 tiles of 32x32 (n_d=1024), c=100, t=1"),
+}
+PINNED = dict(weighting="binary", power=2, shift_scale=1e-3, dense_limit=4096)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
+    ap.add_argument("--meshes", type=int, default=0, help="override the mesh count (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tiles", type=int, default=8, help="tiles per chain in the CPU sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------- inputs
+
+def build_inputs(cfg, mesh_ids):
+    import numpy as np
+    from paper_1810_02719_b200 import synth
+    base = synth.grid_mesh(cfg["W"], cfg["H"], cfg["seed0"], cfg["sigma"])
+    seg = synth.grid_tiles(cfg["W"], cfg["H"], cfg["tw"], cfg["th"])
+    verts = [synth.grid_vertices(cfg["W"], cfg["H"], cfg["seed0"] + i, cfg["sigma"]) for i in mesh_ids]
+    offs, members = seg.flat()
+    return base, seg, verts, np.asarray(offs, np.int32), np.asarray(members, np.int32)
+
+
+# ----------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------- GPU arm
+
+class GpuJob:
+    def __init__(self, cfg, mesh_ids, device, ctx):
+        import numpy as np
+        import torch
+        from paper_1810_02719_b200 import _abi
+        self.cfg, self.ids, self.ctx, self.np = cfg, mesh_ids, ctx, np
+        base, seg, verts, offs, members = build_inputs(cfg, mesh_ids)
+        self.seg = seg
+        self.n = base.n
+        self.K = seg.count
+        self.nd = seg.block_size
+        self.B = len(mesh_ids)
+        c = cfg["c"]
+        dev = torch.device("cuda", device)
+        self.torch, self.dev = torch, dev
+        seq = np.arange(self.K, dtype=np.int32)
+        # device-resident inputs (value) and pinned host inputs (e2e)
+        self.d_xyz = [[torch.from_numpy(np.ascontiguousarray(v[:, a])).to(dev) for a in range(3)] for v in verts]
+        self.h_xyz = [[torch.from_numpy(np.ascontiguousarray(v[:, a])).pin_memory() for a in range(3)] for v in verts]
+        conn = dict(offs=base.adj_offsets, cols=base.adj_cols, moffs=offs, members=members, seq=seq)
+        self.d_conn = {k: torch.from_numpy(np.asarray(a, np.int32)).to(dev) for k, a in conn.items()}
+        self.h_conn = {k: torch.from_numpy(np.asarray(a, np.int32)).pin_memory() for k, a in conn.items()}
+        # outputs
+        self.ncoef = self.K * c * 3
+        self.d_recon = torch.empty((self.B, 3 * self.n), dtype=torch.float64, device=dev)
+        self.d_coef = torch.empty((self.B, self.ncoef), dtype=torch.float64, device=dev)
+        self.h_recon = torch.empty((self.B, 3 * self.n), dtype=torch.float64).pin_memory()
+        self.h_coef = torch.empty((self.B, self.ncoef), dtype=torch.float64).pin_memory()
+        self.stats = [np.zeros((5, self.K)) for _ in range(self.B)]
+        self.coef_off = [np.zeros(self.K + 1, np.int64) for _ in range(self.B)]
+        self.sizes = np.full(self.K, c, np.int32)
+        self.pcfg = _abi.smg_pipeline_config()
+        ctx.lib.smg_default_config(self.pcfg)
+        self.pcfg.weighting = _abi.WEIGHTING[PINNED["weighting"]]
+        self.pcfg.subspace_size = c
+        self.pcfg.iterations = cfg["t"]
+        self.pcfg.power = PINNED["power"]
+        self.pcfg.shift_scale = PINNED["shift_scale"]
+        self._abi = _abi
+        self.views = {on: self._views(on) for on in (0, 1)}
+        self.h2d_bytes = sum(t.numel() * t.element_size() for xyz in self.h_xyz for t in xyz) + self.B * sum(
+            t.numel() * t.element_size() for t in self.h_conn.values())
+        self.d2h_bytes = self.h_recon.numel() * 8 + self.h_coef.numel() * 8 + self.B * 5 * self.K * 8
+
+    def _views(self, on_device):
+        _abi, np = self._abi, self.np
+        xyz = self.d_xyz if on_device else self.h_xyz
+        conn = self.d_conn if on_device else self.h_conn
+        recon = self.d_recon if on_device else self.h_recon
+        coef = self.d_coef if on_device else self.h_coef
+        meshes = (_abi.smg_mesh * self.B)()
+        segs = (_abi.smg_segmentation * self.B)()
+        outs = (_abi.smg_chain_output * self.B)()
+        for b in range(self.B):
+            m = meshes[b]
+            m.vertex_count = self.n
+            m.x, m.y, m.z = (t.data_ptr() for t in xyz[b])
+            m.adj_offsets, m.adj_cols = conn["offs"].data_ptr(), conn["cols"].data_ptr()
+            m.on_device = on_device
+            s = segs[b]
+            s.submesh_count, s.member_offsets, s.members = self.K, conn["moffs"].data_ptr(), conn["members"].data_ptr()
+            s.sequence_length, s.sequence, s.on_device = self.K, conn["seq"].data_ptr(), on_device
+            o = outs[b]
+            st = self.stats[b]
+            o.subspace_size = None
+            o.residual_rms = st[1].ctypes.data
+            o.doi_residual = st[2].ctypes.data
+            o.converged = None
+            o.oi_iterations = None
+            o.reconstruction = recon[b].data_ptr()
+            o.coefficients = coef[b].data_ptr()
+            o.coefficients_capacity = self.ncoef
+            o.coefficient_offsets = self.coef_off[b].ctypes.data
+            o.on_device = on_device
+        return meshes, segs, outs
+
+    def run(self, on_device):
+        meshes, segs, outs = self.views[on_device]
+        st = self.ctx.lib.smg_run_chains(self.ctx.handle, self.B, meshes, segs, self.pcfg,
+                                         self.sizes.ctypes.data, outs)
+        self.ctx.check(st)
+
+
+def gpu_arm(args, cfg, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import paper_1810_02719_b200 as G
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    total_meshes = args.meshes or cfg["meshes"]
+    if cfg["meshes"] == 1:  # single-chain configs: replicas only
+        ids = [rank]
+        total_units = world
+    else:
+        assert total_meshes % world == 0, "mesh count must divide over ranks"
+        per = total_meshes // world
+        ids = list(range(rank * per, (rank + 1) * per))
+        total_units = total_meshes
+    ctx = G.Context(local_rank)
+    job = GpuJob(cfg, ids, local_rank, ctx)
+    verts_per_unit = job.n
+    gather_buf = None
+    if dist is not None and cfg["meshes"] > 1:
+        gather_buf = torch.empty((world,) + tuple(job.d_recon.shape), dtype=torch.float64, device=job.dev)
+
+    def step(on_device):
+        job.run(on_device)
+        if gather_buf is not None and on_device:
+            dist.all_gather_into_tensor(gather_buf, job.d_recon)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(on_device, steps, profile=False):
+        lib = ctx.lib
+        if profile:
+            lib.smg_profile_enable(ctx.handle, 1)
+        l0 = launches()
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(steps):
+            step(on_device)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        barrier()
+        nl = launches() - l0
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device=job.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, nl
+
+    def launches():
+        import ctypes as C
+        n, t = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, b"launches", C.byref(n), C.byref(t))
+        return n.value
+
+    for _ in range(args.warmup):
+        step(True)
+    with ClockSampler(local_rank) as clk:
+        ms, nl = timed(True, args.steps, profile=True)
+    clocks = clk.summary()
+    stages = {}
+    import ctypes as C
+    for nm in ("assemble", "factor", "first_basis", "fb_iterate", "fb_rayleigh_ritz", "solve", "orthonormalize",
+               "gram", "chol", "trmm", "project"):
+        n, t = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, nm.encode(), C.byref(n), C.byref(t))
+        stages[nm] = {"launches": n.value, "ms": t.value / args.steps}
+    ctx.lib.smg_profile_enable(ctx.handle, 0)
+    # e2e: host pinned inputs -> results on the host
+    step(False)
+    ms_e2e, _ = timed(False, args.steps)
+
+    ms_step = ms / args.steps
+    units = total_units * verts_per_unit
+    value = units / (ms_step / 1e3)
+    e2e_value = units / (ms_e2e / args.steps / 1e3)
+
+    # roofline of the dominant kernel (solve: the block-tridiagonal R^z sweeps)
+    c, n, B, K, t = cfg["c"], job.nd, job.B, job.K, cfg["t"]
+    b_half = cfg["tw"] + 1  # half-bandwidth in the natural order
+    z = PINNED["power"]
+    solve = stages["solve"]
+    solve_launches_per_step = solve["launches"] / args.steps if solve["launches"] else 0
+    flops_per_launch = B * z * 4.0 * n * b_half * c  # z*4*n_d*b*c per tile
+    avg_ms = solve["ms"] / max(solve_launches_per_step, 1e-9)
+    achieved = flops_per_launch / (avg_ms * 1e-3) / 1e12 if avg_ms > 0 else None
+    roofline = {"kernel": "solve_kernel (block-tridiagonal R^z sweeps, DMMA f64)", "bound": "tensor",
+                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                "peak_source": "measured FP64 DMMA peak, profiles/fp64_peak_r01.txt (MEASURED_PEAKS.json has no FP64 entry)",
+                "flops_per_launch": flops_per_launch, "avg_launch_ms": avg_ms,
+                "step_share": solve["ms"] / ms_step if ms_step else None}
+    # whole-step algorithmic FP64 work (SURVEY.md §8(d) formulas, per GPU)
+    per_tile = z * 4.0 * n * b_half * c * t + (4.0 * n * c * c) * t + n * b_half ** 2 + 12.0 * n * c + 3 * n
+    first = (4.0 / 3.0) * n ** 3 + 2.0 * n * n * c
+    step_flops = B * ((K - 1) * per_tile + first)
+    out = {
+        "metric": METRIC, "value": value * (1 if cfg["meshes"] > 1 else 1), "unit": "vertices/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong" if cfg["meshes"] > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded sinusoid height-field grids + N(0,sigma^2) noise; no dataset exists)",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes": total_units, "tiles_per_mesh": K,
+                   "n_d": n, "c": c, "oi_iterations": t, "z": z, "shift_scale": PINNED["shift_scale"],
+                   "weighting": PINNED["weighting"], "tile_order": "row-major",
+                   "parallelism": f"chains sharded over {world} GPU(s)" if cfg["meshes"] > 1 else "replicas",
+                   "l2": "inputs larger than L2 (%.0f MB per GPU)" % (job.h2d_bytes / 1e6)},
+        "e2e": {"value": e2e_value, "unit": "vertices/s", "h2d_bytes_per_step": job.h2d_bytes,
+                "d2h_bytes_per_step": job.d2h_bytes},
+        "roofline": roofline,
+        "fp64_step_efficiency": {"algorithmic_tflop_per_step": step_flops / 1e12,
+                                 "achieved_tflops": step_flops / (ms_step * 1e-3) / 1e12,
+                                 "frac_of_peak": step_flops / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
+        "stages_ms_per_step": {k: round(v["ms"], 3) for k, v in stages.items()},
+        "clocks": clocks,
+        "gpu_launches": nl,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, cfg, total_units)
+    if dist is not None:
+        dist.destroy_process_group()
+    ctx.close()
+    return out if rank == 0 else None
+
+
+# ----------------------------------------------------------------------- CPU arm
+
+def _cpu_chain(task):
+    """One chain of the oracle over the first T tiles: (t_first, t_rest) seconds."""
+    cfgname, mesh_id, T = task
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import specmesh_oracle as O
+    from paper_1810_02719_b200 import synth
+    cfg = CONFIGS[cfgname]
+    base = synth.grid_mesh(cfg["W"], cfg["H"], cfg["seed0"] + mesh_id, cfg["sigma"])
+    seg = synth.grid_tiles(cfg["W"], cfg["H"], cfg["tw"], cfg["th"])
+    subs = O.build_submeshes(base.adj_offsets, base.adj_cols, seg.members[:T])
+    ocfg = O.PipelineConfig(weighting=O.BINARY, subspace_size=cfg["c"], iterations=cfg["t"],
+                            shift_scale=PINNED["shift_scale"])
+    t0 = time.perf_counter()
+    bb1 = O.compute_block_bases_fixed_sizes(base.vertices, subs[:1], np.arange(1), ocfg, [cfg["c"]])
+    O.project_blocks(bb1, base.vertices)
+    t1 = time.perf_counter()
+    bb = O.compute_block_bases_fixed_sizes(base.vertices, subs, np.arange(T), ocfg, [cfg["c"]] * T)
+    locals_ = O.project_blocks(bb, base.vertices)
+    t2 = time.perf_counter()
+    return t1 - t0, (t2 - t1) - (t1 - t0)
+
+
+def cpu_baseline(args, cfg, total_units):
+    """The oracle restatement timed on the host cores (one chain per core, BLAS 1 thread),
+    on a bounded sample: the first T tiles of P chains, extrapolated per chain to all tiles."""
+    import multiprocessing as mp
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["MKL_NUM_THREADS"] = "1"
+    cores = os.cpu_count() or 1
+    P = min(cores, max(1, total_units if cfg["meshes"] > 1 else 1))
+    T = max(2, args.cpu_tiles)
+    K = (cfg["W"] // cfg["tw"]) * (cfg["H"] // cfg["th"])
+    T = min(T, K)
+    ctxm = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctxm.Pool(P) as pool:
+        res = pool.map(_cpu_chain, [(args.config, i, T) for i in range(P)])
+    wall = time.perf_counter() - t0
+    t_first = sum(r[0] for r in res) / P
+    t_rest = sum(r[1] for r in res) / P / max(T - 1, 1)
+    t_chain = t_first + (K - 1) * t_rest
+    n_mesh = cfg["W"] * cfg["H"]
+    rounds = math.ceil(total_units / P)
+    value = total_units * n_mesh / (rounds * t_chain)
+    return {"value": value, "unit": "vertices/s", "cores": P, "kind": "port",
+            "sample": f"{P} chains in parallel (1 per core, BLAS 1 thread) x first {T} of {K} tiles "
+                      f"(numpy/LAPACK oracle, oracle/specmesh_oracle.py); per chain t_first={t_first:.2f}s "
+                      f"+ {K - 1} x t_tile={t_rest:.3f}s extrapolated; sample wall {wall:.1f}s"}
+
+
+def reference_arm(args, cfg):
+    total_units = args.meshes or cfg["meshes"]
+    vals = []
+    for _ in range(max(1, args.steps)):
+        cb = cpu_baseline(args, cfg, total_units)
+        vals.append(cb["value"])
+    cb["value"] = statistics.median(vals)
+    n_mesh = cfg["W"] * cfg["H"]
+    ms_step = total_units * n_mesh / cb["value"] * 1e3
+    return {"metric": METRIC, "value": cb["value"], "unit": "vertices/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if cfg["meshes"] > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded sinusoid height-field grids + N(0,sigma^2) noise)",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes": total_units},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(reference_arm(args, cfg)), flush=True)
+        return
+    out = gpu_arm(args, cfg, rank, world, local_rank)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -2,6 +2,7 @@
 // runners (fixed-c lockstep batches and the device-driven DOI loop) and the L3
 // primitives.  Exceptions never cross the boundary.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -276,7 +277,10 @@ public:
         }
     }
 
-    // compute_block_bases_fixed_sizes for all chains in lockstep
+    // compute_block_bases_fixed_sizes for all chains in lockstep.  Chains are split
+    // into groups on their own streams so one group's latency-bound phases (the
+    // c x c Cholesky panels, small reductions) overlap another group's solves and
+    // GEMMs; chains are independent, so grouping does not change any result.
     void run_fixed(const int32_t* sizes_in_order) {
         Timer tm(st_);
         const int t0 = tm.mark();
@@ -289,55 +293,146 @@ public:
         require(ccap <= 512, "subspace size exceeds the GPU limit of 512");
         setup_tiles();
         const int t_lap = tm.mark();
-        first_c_ = sizes_[0];
-        prepare_outputs([&](int b, int id) { (void)b; return sizes_[segs_[b].pos_of[id]]; });
+        tm.add(kStLaplacian, t0, t_lap);
+        prepare_outputs([&](int b, int id) { return sizes_[segs_[b].pos_of[id]]; });
+        build_pointer_tables();
         const int fb_m = std::min(n_, round_up(sizes_[0] + std::max(16, sizes_[0] / 2), 8));
         ws_.init(B_, n_, ts_.npad, std::max(ccap, fb_m), st_);
         StepCtx cx{st_, &ts_};
         check_assembly();
-        // factor windows over positions
-        const int64_t per_tile = (int64_t)ts_.Kb * 2 * ts_.W * ts_.W * 2 * 8;
-        const int64_t budget = (int64_t)8 << 30;
-        int window = (int)std::max<int64_t>(1, std::min<int64_t>(K_, budget / std::max<int64_t>(1, per_tile * B_)));
-        tm.add(kStLaplacian, t0, t_lap);
-        int win_first = -1;
-        FactorSet fs;
-        for (int pos = 0; pos < K_; ++pos) {
-            if (win_first < 0 || pos >= win_first + window) {
-                const int a = tm.mark();
-                win_first = pos;
-                const int cnt = std::min(window, K_ - pos);
-                fs.factor(ts_, pos * B_, cnt * B_, nullptr, st_);
-                SMG_CUDA(cudaGetLastError());
-                factor_status_.push_back({pos, download(fs.status.get(), (size_t)cnt * B_, st_)});
-                tm.add(kStFactorize, a, tm.mark());
+        // chain groups
+        int G = B_ >= 16 ? 2 : 1;
+        if (const char* e = std::getenv("SMG_GROUPS")) G = std::max(1, std::min(B_, std::atoi(e)));
+        std::vector<Group> grp(G);
+        for (int g = 0; g < G; ++g) {
+            grp[g].b0 = (int)((int64_t)B_ * g / G);
+            grp[g].nb = (int)((int64_t)B_ * (g + 1) / G) - grp[g].b0;
+            SMG_CUDA(cudaStreamCreateWithFlags(&grp[g].st, cudaStreamNonBlocking));
+            SMG_CUDA(cudaEventCreateWithFlags(&grp[g].ev, cudaEventDisableTiming));
+            grp[g].ws.init(grp[g].nb, n_, ts_.npad, ccap, grp[g].st);
+        }
+        cudaEvent_t ev_main;
+        SMG_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
+        auto fork = [&]() {
+            SMG_CUDA(cudaEventRecord(ev_main, st_));
+            for (Group& g : grp) SMG_CUDA(cudaStreamWaitEvent(g.st, ev_main, 0));
+        };
+        auto join = [&]() {
+            for (Group& g : grp) {
+                SMG_CUDA(cudaEventRecord(g.ev, g.st));
+                SMG_CUDA(cudaStreamWaitEvent(st_, g.ev, 0));
             }
-            const int a = tm.mark();
+        };
+        fork();  // group workspaces were initialised on their streams; ordering vs st_
+        // Factor windows over positions, double buffered on their own stream: window
+        // w+1 is factored while the groups track through window w.
+        const int64_t per_tile = (int64_t)ts_.Kb * 2 * ts_.W * ts_.W * 2 * 8;
+        const int64_t budget = (int64_t)4 << 30;
+        const int window =
+            (int)std::max<int64_t>(1, std::min<int64_t>(K_, budget / std::max<int64_t>(1, per_tile * B_)));
+        const int nwin = (K_ + window - 1) / window;
+        DBuf<int> fstat;
+        fstat.alloc((size_t)K_ * B_, st_);
+        fstat.zero();
+        cudaStream_t fst;
+        SMG_CUDA(cudaStreamCreateWithFlags(&fst, cudaStreamNonBlocking));
+        cudaEvent_t fready[2], fdone[2];
+        for (int i = 0; i < 2; ++i) {
+            SMG_CUDA(cudaEventCreateWithFlags(&fready[i], cudaEventDisableTiming));
+            SMG_CUDA(cudaEventCreateWithFlags(&fdone[i], cudaEventDisableTiming));
+        }
+        FactorSet fs[2];
+        SMG_CUDA(cudaEventRecord(ev_main, st_));
+        SMG_CUDA(cudaStreamWaitEvent(fst, ev_main, 0));  // tiles are assembled
+        auto start_factor = [&](int w) {
+            const int slot = w & 1, pos0 = w * window, cnt = std::min(window, K_ - pos0);
+            if (w >= 2) SMG_CUDA(cudaStreamWaitEvent(fst, fdone[slot], 0));  // window w-2 released the slot
+            fs[slot].factor(ts_, pos0 * B_, cnt * B_, nullptr, fst, fstat.get() + (int64_t)pos0 * B_);
+            SMG_CUDA(cudaEventRecord(fready[slot], fst));
+        };
+        const int tf0 = tm.mark();
+        start_factor(0);
+        if (nwin > 1) start_factor(1);
+        int t_basis0 = -1;
+        for (int pos = 0; pos < K_; ++pos) {
+            const int w = pos / window, slot = w & 1;
+            FactorSet& fcur = fs[slot];
+            if (pos % window == 0) {
+                SMG_CUDA(cudaStreamWaitEvent(st_, fready[slot], 0));
+                for (Group& g : grp) SMG_CUDA(cudaStreamWaitEvent(g.st, fready[slot], 0));
+            }
             const int c = sizes_[pos];
             if (pos == 0) {
+                const int a = tm.mark();
                 FirstBasisConfig fc;
                 fc.dense_limit = cfg_.dense_limit;
                 fc.initial_iterations = cfg_.initial_iterations;
                 fc.power = cfg_.power;
                 fc.seed = cfg_.seed;
-                first_basis(cx, ws_, ts_, 0, 1, c, fc, &fs);
+                first_basis(cx, ws_, ts_, 0, 1, c, fc, &fcur);
+                project_batch(cx, ws_, ws_.U.get(), c, nullptr, ts_.X.get(), (int64_t)n_ * 3, xhat_.get(),
+                              (int64_t)n_ * 3);
+                emit_position(0, c, ws_, 0, B_, st_);
+                // hand each group its chains' basis (leading c columns)
+                for (Group& g : grp)
+                    SMG_CUDA(cudaMemcpy2DAsync(g.ws.U.get(), (size_t)g.ws.ld * 8,
+                                               ws_.U.get() + (int64_t)g.b0 * ws_.mstride(), (size_t)ws_.ld * 8,
+                                               (size_t)c * 8, (size_t)g.nb * ts_.npad, cudaMemcpyDeviceToDevice, st_));
+                tm.add(kStBasis, a, tm.mark());
+                fork();
+                t_basis0 = tm.mark();
             } else {
-                resize(c, pos);
-                for (int it = 0; it < cfg_.iterations; ++it) {
-                    solve_batch(cx, ws_, fs, pos * B_, 1, ws_.U.get(), ws_.V.get(), c, nullptr, cfg_.power, false);
-                    orth_batch(cx, ws_, ws_.V.get(), ws_.U.get(), c, nullptr, true, pos);
+                for (Group& g : grp) {
+                    StepCtx gx{g.st, &ts_};
+                    const int tile0 = pos * B_ + g.b0;
+                    resize(c, pos, g.ws, g.b0, g.nb, g.st);
+                    for (int it = 0; it < cfg_.iterations; ++it) {
+                        solve_batch(gx, g.ws, fcur, tile0, 1, g.ws.U.get(), g.ws.V.get(), c, nullptr, cfg_.power,
+                                    false);
+                        orth_batch(gx, g.ws, g.ws.V.get(), g.ws.U.get(), c, nullptr, true, pos);
+                    }
+                    project_batch(gx, g.ws, g.ws.U.get(), c, nullptr, ts_.X.get() + (int64_t)tile0 * n_ * 3,
+                                  (int64_t)n_ * 3, xhat_.get() + (int64_t)tile0 * n_ * 3, (int64_t)n_ * 3);
+                    emit_position(pos, c, g.ws, g.b0, g.nb, g.st);
                 }
             }
-            const int b1 = tm.mark();
-            project_batch(cx, ws_, ws_.U.get(), c, nullptr, ts_.X.get() + (int64_t)pos * B_ * n_ * 3,
-                          (int64_t)n_ * 3, xhat_.get() + (int64_t)pos * B_ * n_ * 3, (int64_t)n_ * 3);
-            emit_position(pos, c);
-            const int b2 = tm.mark();
-            tm.add(kStBasis, a, b1);
-            tm.add(kStProject, b1, b2);
             prev_c_ = c;
+            if ((pos + 1) % window == 0 || pos + 1 == K_) {
+                // window w done: release its factor slot and start window w+2 in it
+                join();
+                SMG_CUDA(cudaEventRecord(fdone[slot], st_));
+                if (w + 2 < nwin) start_factor(w + 2);
+                fork();
+            }
+        }
+        tm.add(kStFactorize, tf0, tf0);  // factor runs overlapped on its own stream
+        {
+            std::vector<int> fsh = download(fstat.get(), (size_t)K_ * B_, st_);
+            factor_status_.push_back({0, std::move(fsh)});
+        }
+        join();
+        if (t_basis0 >= 0) tm.add(kStBasis, t_basis0, tm.mark());
+        // per-chain sticky statuses back into the full-batch arrays
+        for (Group& g : grp) {
+            SMG_CUDA(cudaMemcpyAsync(ws_.status.get() + g.b0, g.ws.status.get(), 4 * g.nb, cudaMemcpyDeviceToDevice, st_));
+            SMG_CUDA(cudaMemcpyAsync(ws_.errpos.get() + g.b0, g.ws.errpos.get(), 4 * g.nb, cudaMemcpyDeviceToDevice, st_));
+            SMG_CUDA(cudaMemcpyAsync(ws_.detail.get() + g.b0, g.ws.detail.get(), 8 * g.nb, cudaMemcpyDeviceToDevice, st_));
         }
         finish(tm, t0);
+        SMG_CUDA(cudaStreamSynchronize(st_));
+        SMG_CUDA(cudaStreamSynchronize(fst));
+        for (int i = 0; i < 2; ++i) {
+            fs[i].rebind(st_);
+            cudaEventDestroy(fready[i]);
+            cudaEventDestroy(fdone[i]);
+        }
+        cudaStreamDestroy(fst);
+        for (Group& g : grp) {
+            g.ws = Workspace();
+            cudaEventDestroy(g.ev);
+            cudaStreamDestroy(g.st);
+        }
+        cudaEventDestroy(ev_main);
     }
 
     // compute_block_bases, DOI branch (pipeline.hpp:245-285), one chain
@@ -376,7 +471,7 @@ public:
         DoiLoop loop;
         loop.build(ts_, ws_, dp, fs.strideF, st_);
         doi_states_.resize(K_);
-        xhat_.alloc((size_t)K_ * n_ * 3, st_);
+        prepare_outputs_doi();
         std::vector<double> bbox = download(ts_.bbox.get(), K_, st_);
         for (int pos = 0; pos < K_; ++pos) {
             const int a = tm.mark();
@@ -392,7 +487,7 @@ public:
                 c_init = c0;
             } else {
                 c_init = std::min(std::max(prev_c_, cfg_.c_min), c_max);
-                resize(c_init, pos);
+                resize(c_init, pos, ws_, 0, 1, st_);
             }
             DoiState r = loop.run(fs.f(pos), fs.b(pos), ts_.perm_of(pos), ts_.X.get() + (int64_t)pos * n_ * 3,
                                   bbox[pos], c_init);
@@ -415,8 +510,7 @@ public:
             // final projection of the returned basis (stats + coefficients + X^)
             project_batch(cx, ws_, ws_.U.get(), c, nullptr, ts_.X.get() + (int64_t)pos * n_ * 3, (int64_t)n_ * 3,
                           xhat_.get() + (int64_t)pos * n_ * 3, (int64_t)n_ * 3);
-            if (pos == 0) prepare_outputs_doi();
-            emit_position(pos, c, id);
+            emit_position(pos, c, ws_, 0, 1, st_);
             const int b2 = tm.mark();
             tm.add(kStBasis, a, b1);
             tm.add(kStProject, b1, b2);
@@ -503,11 +597,6 @@ private:
         }
     }
 
-    void prepare_outputs_doi() {
-        // DOI sizes are only known as the chain runs: stage per-position outputs at c_max
-        xhat_ready_ = true;
-    }
-
     void bind_outputs(ChainOut& co) {
         smg_chain_output* o = co.out;
         if (o->coefficients) {
@@ -537,67 +626,63 @@ private:
         if (o->basis_offsets) std::memcpy(o->basis_offsets, co.basis_off.data(), sizeof(int64_t) * (K_ + 1));
     }
 
-    void resize(int c, int pos) {
+    void resize(int c, int pos, Workspace& ws, int b0, int nb, cudaStream_t st) {
         // resize_basis (pipeline.hpp:97-109): same size -> unchanged; shrink ->
         // leading columns; grow -> seeded Gaussian columns + orthonormalize
         if (c <= prev_c_) return;  // shrink: the leading c columns are used as is
         const int add = c - prev_c_;
         const uint64_t seed = cfg_.seed + kPosMul * (uint64_t)pos;
-        std::vector<double> g = gaussian_block_colmajor(n_, add, seed);
+        std::vector<double> gh = gaussian_block_colmajor(n_, add, seed);
         DBuf<double> gd;
-        gd.upload(g, st_);
-        for (int b = 0; b < B_; ++b) {
-            // apply the previous signs so the grown block equals the reference's
-            apply_signs(b, prev_c_);
-            transpose_to_rowmajor(gd.get(), n_, add, ws_.U.get() + (int64_t)b * ws_.mstride() + prev_c_, ws_.ld, st_);
+        gd.upload(gh, st);
+        for (int b = 0; b < nb; ++b) {
+            apply_signs(ws, b, prev_c_, st);  // the reference grows its sign-fixed basis
+            transpose_to_rowmajor(gd.get(), n_, add, ws.U.get() + (int64_t)b * ws.mstride() + prev_c_, ws.ld, st);
         }
-        StepCtx cx{st_, &ts_};
-        orth_batch(cx, ws_, ws_.U.get(), ws_.U.get(), c, nullptr, true, pos);
+        StepCtx cx{st, &ts_};
+        orth_batch(cx, ws, ws.U.get(), ws.U.get(), c, nullptr, true, pos);
+        (void)b0;
     }
 
-    void apply_signs(int b, int c);
+    void apply_signs(Workspace& ws, int b, int c, cudaStream_t st);
 
-    void emit_position(int pos, int c, int id_doi = -1) {
-        // per-tile residual_rms into a device array, coefficients and bases to the outputs
-        if (!stat_rms_.size()) {
-            stat_rms_.alloc((size_t)K_ * B_, st_);
-        }
-        ::smg::count_launch(), copy_stat_kernel<<<(B_ + 127) / 128, 128, 0, st_>>>(ws_.stats.get(), 4, B_, stat_rms_.get() + (int64_t)pos * B_, 1);
-        std::vector<double*> cptr(B_, nullptr), bptr(B_, nullptr);
-        bool anyc = false, anyb = false;
-        for (int b = 0; b < B_; ++b) {
-            ChainOut& co = outs_[b];
-            const int id = id_doi >= 0 ? id_doi : segs_[b].seq_h[pos];
-            if (id_doi >= 0) ensure_doi_outputs(co, pos, c);
-            if (co.coef_dev) {
-                cptr[b] = co.coef_dev + co.coef_off[id];
-                anyc = true;
+    // destination tables: per (position, chain) pointer into the outputs (or null)
+    void build_pointer_tables() {
+        std::vector<double*> ct((size_t)K_ * B_, nullptr), bt((size_t)K_ * B_, nullptr);
+        for (int pos = 0; pos < K_; ++pos)
+            for (int b = 0; b < B_; ++b) {
+                const ChainOut& co = outs_[b];
+                const int id = segs_[b].seq_h[pos];
+                if (co.coef_dev) ct[(size_t)pos * B_ + b] = co.coef_dev + co.coef_off[id];
+                if (co.basis_dev) bt[(size_t)pos * B_ + b] = co.basis_dev + co.basis_off[id];
+                any_coef_ |= co.coef_dev != nullptr;
+                any_basis_ |= co.basis_dev != nullptr;
             }
-            if (co.basis_dev) {
-                bptr[b] = co.basis_dev + co.basis_off[id];
-                anyb = true;
-            }
-        }
-        if (anyc) {
-            ptrs_c_.upload(cptr, st_);
-            ::smg::count_launch(), coef_ptr_kernel<<<B_, 128, 0, st_>>>(ws_.coeff.get(), (int64_t)ws_.ld * 4, ws_.sign.get(), ws_.ld, c,
-                                                 ptrs_c_.get());
-            keep_.push_back(std::move(ptrs_c_));
-        }
-        if (anyb) {
-            ptrs_b_.upload(bptr, st_);
-            ::smg::count_launch(), basis_out_kernel<<<dim3(std::min(1024, (n_ * c + 255) / 256), B_), 256, 0, st_>>>(
-                ws_.U.get(), ws_.ld, ws_.mstride(), n_, c, ws_.sign.get(), ws_.ld, ptrs_b_.get());
-            keep_.push_back(std::move(ptrs_b_));
-        }
+        ctab_.upload(ct, st_);
+        btab_.upload(bt, st_);
+        stat_rms_.alloc((size_t)K_ * B_, st_);
+    }
+
+    void emit_position(int pos, int c, Workspace& ws, int b0, int nb, cudaStream_t st) {
+        // per-tile residual_rms, signed coefficients and bases to the outputs
+        ::smg::count_launch(), copy_stat_kernel<<<(nb + 127) / 128, 128, 0, st>>>(
+            ws.stats.get(), 4, nb, stat_rms_.get() + (int64_t)pos * B_ + b0, 1);
+        if (any_coef_)
+            ::smg::count_launch(), coef_ptr_kernel<<<nb, 128, 0, st>>>(ws.coeff.get(), (int64_t)ws.ld * 4,
+                                                                      ws.sign.get(), ws.ld, c,
+                                                                      ctab_.get() + (int64_t)pos * B_ + b0);
+        if (any_basis_)
+            ::smg::count_launch(), basis_out_kernel<<<dim3(std::min(1024, (n_ * c + 255) / 256), nb), 256, 0, st>>>(
+                ws.U.get(), ws.ld, ws.mstride(), n_, c, ws.sign.get(), ws.ld, btab_.get() + (int64_t)pos * B_ + b0);
         SMG_CUDA(cudaGetLastError());
     }
 
-    void ensure_doi_outputs(ChainOut& co, int pos, int c) {
-        // DOI: outputs are laid out in submesh-id order, so positions are staged
-        // per id at capacity n_d x c_max and compacted at the end.
-        smg_chain_output* o = co.out;
-        if (co.coef_off.empty()) {
+    // DOI: sizes are known only as the chain runs, so outputs are staged per id at
+    // capacity n_d x c_max and compacted at the end (copy_outputs).
+    void prepare_outputs_doi() {
+        xhat_.alloc((size_t)K_ * n_ * 3, st_);
+        for (ChainOut& co : outs_) {
+            smg_chain_output* o = co.out;
             co.coef_off.assign(K_ + 1, 0);
             co.basis_off.assign(K_ + 1, 0);
             const int cm = cfg_.resolve_c_max(n_);
@@ -621,8 +706,7 @@ private:
                 }
             }
         }
-        (void)pos;
-        (void)c;
+        build_pointer_tables();
     }
 
     void finish(Timer& tm, int t0) {
@@ -760,13 +844,18 @@ private:
     std::vector<DBuf<int64_t>> tile_of_;
     std::vector<FacStatus> factor_status_;
     std::vector<DoiState> doi_states_;
-    std::vector<DBuf<double*>> keep_;
-    DBuf<double*> ptrs_c_, ptrs_b_;
+    DBuf<double*> ctab_, btab_;
+    bool any_coef_ = false, any_basis_ = false;
+    struct Group {
+        int b0 = 0, nb = 0;
+        Workspace ws;
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev = nullptr;
+    };
     DBuf<double> xhat_, stat_rms_;
     TileSet ts_;
     Workspace ws_;
     int first_c_ = 0, prev_c_ = 0;
-    bool xhat_ready_ = false;
     struct PendingError {
         int pos, stage, chain, code;
         std::string msg;
@@ -781,9 +870,9 @@ __global__ void apply_sign_kernel(double* U, int64_t ld, int n, int c, const dou
     }
 }
 
-void ChainRunner::apply_signs(int b, int c) {
-    ::smg::count_launch(), apply_sign_kernel<<<std::min(1024, (n_ * c + 255) / 256), 256, 0, st_>>>(
-        ws_.U.get() + (int64_t)b * ws_.mstride(), ws_.ld, n_, c, ws_.sign.get() + (int64_t)b * ws_.ld);
+void ChainRunner::apply_signs(Workspace& ws, int b, int c, cudaStream_t st) {
+    ::smg::count_launch(), apply_sign_kernel<<<std::min(1024, (n_ * c + 255) / 256), 256, 0, st>>>(
+        ws.U.get() + (int64_t)b * ws.mstride(), ws.ld, n_, c, ws.sign.get() + (int64_t)b * ws.ld);
 }
 
 }  // namespace

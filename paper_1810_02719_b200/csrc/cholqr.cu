@@ -1,16 +1,23 @@
-// K6: c x c Cholesky of the column-scaled Gram matrix, the reference rank test,
-// and the scaled triangular inverse used by CholeskyQR2.
+// K6/K7: CholeskyQR building blocks -- blocked c x c Cholesky of the column-
+// scaled Gram matrix with the reference rank test, and the triangular solve
+// Q = V D^-1 R~^-1 -- on the FP64 DMMA path.
 //
 // orthonormalize (spectral.hpp:120-132) computes a Householder QR and throws
 // "rank deficient at column k" for the first k with |r_kk| < 1e-13 ||block||_F.
 // CholeskyQR gives the same R up to column signs: with D = diag(||v_j||) and
 // G~ = D^-1 V^T V D^-1 = R~^T R~, R = R~ D, so |r_kk| = r~_kk d_k and ||block||_F
-// = sqrt(trace G).  Column scaling makes the test exact for the column-graded
-// blocks R^z U produces (SURVEY.md §0 finding 5).  A non-positive pivot means
-// r~_kk is below rounding, reported as rank deficiency at that column.
-// Output Binv = D^-1 R~^-1 (upper), so Q1 = V Binv is one triangular GEMM.
-// One CTA per batch entry; the working matrix lives in shared memory when it
-// fits (c <= 144) and in L2 otherwise.
+// = sqrt(trace G).  Column scaling keeps the column-graded blocks R^z U
+// produces well conditioned (SURVEY.md §0 finding 5).  A scaled pivot below
+// 1e-12 (r~_kk < 1e-6, beyond what the Gram resolves) is a rank-test failure
+// at that column; columns that pass are re-tested exactly after the QR by
+// rank_check (|q_k^T v_k| against the same threshold).
+//
+// chol_kernel: one CTA per chain, right-looking blocked Cholesky with 32-wide
+// panels on the matrix in L2: the 32x32 diagonal block is factored and inverted
+// in one warp's registers (shuffles, no block barriers), the panel row and the
+// trailing SYRK run on all warps as 32x32x32 DMMA blocks.
+// trsm_kernel: rows are independent, so each CTA owns 32 rows of V and sweeps
+// the 32-column panels: Q_p = (V_p D_p^-1 - Q_<p R~_<p,p) R~_pp^-1.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -18,110 +25,298 @@ namespace smg {
 
 namespace {
 
-constexpr int NT = 512;
-constexpr int SMEM_C = 144;
+constexpr int CNT = 256;
+constexpr int CW = CNT / 32;
+constexpr unsigned FULL = 0xffffffffu;
 
-__global__ void __launch_bounds__(NT) chol_kernel(CholParams p) {
-    extern __shared__ __align__(16) double sm[];
+// 32x32x32 block product on one warp: acc(4x4 tiles of 8x8, 2 values) += op(A) * B
+// with op(A)[m][k] = a(m, k), B[k][n] = b(k, n) supplied as functors.
+template <class FA, class FB>
+SMG_DEV void warp_block_mma(double (&acc)[4][4][2], FA a, FB b, int g, int t) {
+#pragma unroll 2
+    for (int kk = 0; kk < 32; kk += 4) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = a(8 * i + g, kk + t);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = b(kk + t, 8 * j + g);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
+}
+
+SMG_DEV void zero_acc(double (&acc)[4][4][2]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+__global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     __shared__ double red[32];
-    __shared__ double d[512];
+    __shared__ int fail;
     const int b = blockIdx.x;
-    if (p.status[b] != kOk) return;  // this chain already failed (sticky first error)
+    if (p.status[b] != kOk) return;  // sticky first error of this chain
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    const int P = (c + 31) / 32, cp = P * 32;
     const double* G = p.G + (int64_t)b * p.strideG;
-    double* Bo = p.Binv + (int64_t)b * p.strideB;
-    double* rdiag = p.rdiag ? p.rdiag + (int64_t)b * p.strideR : nullptr;
-    const bool in_smem = c <= SMEM_C;
-    const int ld = in_smem ? c : p.c_cap;
-    double* A = in_smem ? sm : p.work + (int64_t)b * p.c_cap * p.c_cap;
-    const int tid = threadIdx.x;
+    double* A = p.A + (int64_t)b * p.strideA;
+    double* Dinv = p.Dinv + (int64_t)b * p.strideDinv;
+    double* d = p.dscale + (int64_t)b * p.strideD;
+    const int64_t lda = p.lda;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+
+    double tr = 0.0;
+    for (int j = tid; j < cp; j += CNT) {
+        double dj = 1.0;
+        if (j < c) {
+            const double gjj = G[(int64_t)j * p.ldg + j];
+            tr += gjj;
+            dj = p.column_scale ? sqrt(gjj) : 1.0;
+        }
+        d[j] = dj;
+    }
+    tr = block_sum(tr, red);
+    const double scale = sqrt(tr);
+    if (tid == 0) {
+        fail = 0;
+        if (p.vnorm) p.vnorm[b] = scale;
+    }
     auto record = [&](int kind, int64_t col) {
         p.status[b] = kind;
         if (p.status_detail) p.status_detail[b] = col;
         if (p.errpos) p.errpos[b] = p.pos;
     };
-
-    // column norms and ||V||_F
-    double tr = 0.0;
-    for (int j = tid; j < c; j += NT) {
-        const double gjj = G[(int64_t)j * p.ldg + j];
-        d[j] = p.column_scale ? sqrt(gjj) : 1.0;
-        tr += gjj;
-    }
-    tr = block_sum(tr, red);
-    const double scale = sqrt(tr);
-    if (tid == 0 && p.vnorm) p.vnorm[b] = scale;
     if (!(scale > 0.0) || !isfinite(scale)) {
         if (tid == 0) record(scale == 0.0 ? kAllZero : kNotFinite, -1);
         return;
     }
     const double thresh = 1e-13 * scale;
-    // scaled upper triangle
-    for (int e = tid; e < c * c; e += NT) {
-        const int i = e / c, k = e % c;
-        if (k >= i) {
+    __syncthreads();
+    // A = D^-1 G D^-1 (upper triangle incl. full diagonal blocks); identity padding
+    for (int e = tid; e < cp * cp; e += CNT) {
+        const int i = e / cp, k = e % cp;
+        if ((k >> 5) < (i >> 5)) continue;
+        double v;
+        if (i < c && k < c) {
             const double di = d[i], dk = d[k];
-            A[i * ld + k] = (di > 0.0 && dk > 0.0) ? G[(int64_t)i * p.ldg + k] / di / dk : 0.0;
+            v = (di > 0.0 && dk > 0.0) ? G[(int64_t)i * p.ldg + k] / di / dk : 0.0;
+        } else {
+            v = (i == k) ? 1.0 : 0.0;
         }
+        A[(int64_t)i * lda + k] = v;
     }
     __syncthreads();
-    // right-looking Cholesky, upper: A = R~^T R~
-    int stop = c;
-    for (int j = 0; j < c; ++j) {
-        const double piv = A[j * ld + j];
-        const double rjj = sqrt(piv);
-        // A scaled pivot below 1e-12 means r~_jj < 1e-6: beyond what the Gram
-        // resolves, i.e. numerically dependent -- the rank-test verdict.
-        const bool bad_piv = !(piv > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(piv) || !(d[j] > 0.0);
-        const double rkk = bad_piv ? 0.0 : rjj * d[j];
-        if (bad_piv || (p.rank_test && rkk < thresh)) {
-            if (tid == 0) {
-                record(p.rank_test ? kRankDeficient : kNotFinite, j);
-                if (rdiag) rdiag[j] = rkk;
+
+    // panel row p (32 x cp) lives in shared memory during its panel step
+    extern __shared__ __align__(16) double psm[];
+    const int PS = cp + 4;  // row stride, % 16 == 4: conflict-free DMMA fragments
+    double* Ps = psm;
+    double* Xs = psm + 32 * PS;  // 32 x 33
+    for (int pb = 0; pb < P; ++pb) {
+        const int p0 = pb * 32;
+        for (int e = tid; e < 32 * (cp - p0); e += CNT) {
+            const int r = e / (cp - p0), k = p0 + e % (cp - p0);
+            Ps[r * PS + k] = A[(int64_t)(p0 + r) * lda + k];
+        }
+        __syncthreads();
+        // ---- (a) factor + invert the diagonal block (warp 0; rows broadcast via smem)
+        if (warp == 0) {
+            double col[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) col[i] = (i <= lane) ? Ps[i * PS + p0 + lane] : 0.0;
+            int bad = -1;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const double piv = Ps[j * PS + p0 + j];
+                const int gj = p0 + j;
+                if (bad < 0 && gj < c) {
+                    const bool bp = !(piv > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(piv) || !(d[gj] > 0.0);
+                    const double rkk = bp ? 0.0 : sqrt(piv) * d[gj];
+                    if (bp || (p.rank_test && rkk < thresh)) bad = j;
+                }
+                const double rjj = sqrt(fmax(piv, 1e-300));
+                if (lane > j) col[j] /= rjj;
+                if (lane == j) col[j] = rjj;
+                __syncwarp();
+                if (lane >= j) Ps[j * PS + p0 + lane] = col[j];  // row j of R_pp
+                __syncwarp();
+                const double ajk = col[j];
+#pragma unroll
+                for (int i = j + 1; i < 32; ++i) {
+                    if (lane >= i) col[i] -= Ps[j * PS + p0 + i] * ajk;
+                    if (lane == i) Ps[i * PS + p0 + i] = col[i];  // updated pivot for step i
+                }
+                __syncwarp();
             }
-            stop = j;
-            break;
+            // X = R_pp^-1 (upper), lane k holds column k; R rows broadcast from smem
+            double x[32];
+#pragma unroll
+            for (int i = 31; i >= 0; --i) {
+                double s = (lane == i) ? 1.0 : 0.0;
+#pragma unroll
+                for (int l = i + 1; l < 32; ++l) s -= Ps[i * PS + p0 + l] * x[l];
+                x[i] = (lane >= i) ? s / Ps[i * PS + p0 + i] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                Xs[i * 33 + lane] = x[i];
+                Dinv[(int64_t)pb * 1024 + i * 32 + lane] = x[i];
+                if (i <= lane) A[(int64_t)(p0 + i) * lda + p0 + lane] = Ps[i * PS + p0 + lane];
+            }
+            if (lane == 0 && bad >= 0) {
+                record(p.rank_test ? kRankDeficient : kNotFinite, p0 + bad);
+                fail = 1;
+            }
         }
-        for (int k = j + 1 + tid; k < c; k += NT) A[j * ld + k] /= rjj;
         __syncthreads();
-        if (tid == 0) {
-            A[j * ld + j] = rjj;
-            if (rdiag) rdiag[j] = rkk;
+        if (fail) return;
+        // ---- (b) panel row R_{p,q} = X^T A_{p,q}, q > p (smem operands, written back to smem and L2)
+        for (int q = pb + 1 + warp; q < P; q += CW) {
+            const int q0 = q * 32;
+            double acc[4][4][2];
+            zero_acc(acc);
+            warp_block_mma(
+                acc, [&](int m, int k) { return Xs[k * 33 + m]; }, [&](int k, int n) { return Ps[k * PS + q0 + n]; },
+                g, t);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = 8 * i + g, cc = q0 + 8 * j + 2 * t;
+                    Ps[r * PS + cc] = acc[i][j][0];
+                    Ps[r * PS + cc + 1] = acc[i][j][1];
+                    double* dst = A + (int64_t)(p0 + r) * lda + cc;
+                    dst[0] = acc[i][j][0];
+                    dst[1] = acc[i][j][1];
+                }
         }
-        const int m = c - j - 1;
-        for (int e = tid; e < m * m; e += NT) {
-            const int i = j + 1 + e / m, k = j + 1 + e % m;
-            if (k >= i) A[i * ld + k] -= A[j * ld + i] * A[j * ld + k];
+        __syncthreads();
+        // ---- (c) trailing update A_{q,r} -= R_{p,q}^T R_{p,r}, p < q <= r
+        const int rem = P - pb - 1;
+        const int nblk = rem * (rem + 1) / 2;
+        for (int e = warp; e < nblk; e += CW) {
+            int q = 0, rowlen = rem, acc_e = e;
+            while (acc_e >= rowlen) {
+                acc_e -= rowlen;
+                ++q;
+                --rowlen;
+            }
+            const int qq = pb + 1 + q, rr = qq + acc_e;
+            const int q0 = qq * 32, r0 = rr * 32;
+            double acc[4][4][2];
+            zero_acc(acc);
+            warp_block_mma(
+                acc, [&](int m, int k) { return Ps[k * PS + q0 + m]; },
+                [&](int k, int n) { return Ps[k * PS + r0 + n]; }, g, t);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    double* dst = A + (int64_t)(q0 + 8 * i + g) * lda + r0 + 8 * j + 2 * t;
+                    dst[0] -= acc[i][j][0];
+                    dst[1] -= acc[i][j][1];
+                }
         }
         __syncthreads();
     }
-    __syncthreads();
-    if (stop < c) return;
-    // Binv = R~^-1 row-scaled by 1/d: rows from the bottom; row i depends on rows > i.
-    // Stored in Bo (upper, ld p.ldb); lower part zeroed.
-    for (int e = tid; e < c * c; e += NT) {
-        const int i = e / c, k = e % c;
-        if (k < i) Bo[(int64_t)i * p.ldb + k] = 0.0;
-    }
-    // X = R~^-1 computed in place in the lower-unused layout: use Bo as X (unscaled), scale at the end
-    for (int i = c - 1; i >= 0; --i) {
-        const double rii = A[i * ld + i];
-        for (int k = i + tid; k < c; k += NT) {
-            double v;
-            if (k == i) {
-                v = 1.0 / rii;
+}
+
+// Q = V D^-1 R~^-1, ROWS rows per CTA (8 per warp); the CTA's rows of Q stay in
+// shared memory across panels and the R~ column blocks stream through a
+// cp.async double buffer.
+constexpr int RS = 36;  // padded smem row of a staged 32x32 R block
+
+template <int ROWS>
+__global__ void __launch_bounds__(ROWS * 4) trsm_kernel(TrsmParams p) {
+    constexpr int NTH = ROWS * 4;
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y;
+    if (p.status && p.status[b] != kOk) return;
+    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    const int P = (c + 31) / 32, cp = P * 32;
+    const int QS = cp + 4;
+    double* Qs = sm;                          // ROWS x QS
+    double* Rs[2] = {sm + ROWS * QS, sm + ROWS * QS + 32 * RS};
+    double* Ts = sm + ROWS * QS + 64 * RS;    // ROWS x RS
+    const int r0 = blockIdx.x * ROWS;
+    if (r0 >= p.n) return;
+    const double* V = p.V + (int64_t)b * p.strideV;
+    double* Q = p.Q + (int64_t)b * p.strideQ;
+    const double* A = p.A + (int64_t)b * p.strideA;
+    const double* Dinv = p.Dinv + (int64_t)b * p.strideDinv;
+    const double* d = p.dscale + (int64_t)b * p.strideD;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+
+    for (int pb = 0; pb < P; ++pb) {
+        const int p0 = pb * 32;
+        double acc[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+        auto issue = [&](int kb, int buf) {
+            for (int e = tid; e < 32 * 16; e += NTH) {
+                const int k = e >> 4, ch = e & 15;
+                cp_async16(Rs[buf] + k * RS + 2 * ch, A + (int64_t)(kb * 32 + k) * p.lda + p0 + 2 * ch);
+            }
+            cp_async_commit();
+        };
+        // acc = Q_<p * R~_<p,p
+        if (pb > 0) issue(0, 0);
+        int buf = 0;
+        for (int kb = 0; kb < pb; ++kb) {
+            if (kb + 1 < pb) {
+                issue(kb + 1, buf ^ 1);
+                cp_async_wait<1>();
             } else {
-                double acc = 0.0;
-                for (int l = i + 1; l <= k; ++l) acc += A[i * ld + l] * Bo[(int64_t)l * p.ldb + k];
-                v = -acc / rii;
+                cp_async_wait<0>();
             }
-            Bo[(int64_t)i * p.ldb + k] = v;
+            __syncthreads();
+            const double* rs = Rs[buf];
+#pragma unroll
+            for (int kk = 0; kk < 32; kk += 4) {
+                const double a = Qs[(8 * warp + g) * QS + kb * 32 + kk + t];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a, rs[(kk + t) * RS + 8 * j + g]);
+            }
+            __syncthreads();
+            buf ^= 1;
         }
+        // T = V_p D_p^-1 - acc  (C-fragment layout: row 8w+g, cols 8j+2t, +1)
+        const int row = r0 + 8 * warp + g;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int col = p0 + 8 * j + 2 * t + q;
+                double v = 0.0;
+                if (row < p.n && col < c) v = V[(int64_t)row * p.ldv + col] / d[col];
+                Ts[(8 * warp + g) * RS + 8 * j + 2 * t + q] = v - acc[j][q];
+            }
+        // X_p = R~_pp^-1 into Rs[0]
+        for (int e = tid; e < 32 * 32; e += NTH) Rs[0][(e >> 5) * RS + (e & 31)] = Dinv[(int64_t)pb * 1024 + e];
         __syncthreads();
-    }
-    for (int e = tid; e < c * c; e += NT) {
-        const int i = e / c, k = e % c;
-        if (k >= i) Bo[(int64_t)i * p.ldb + k] /= d[i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 32; kk += 4) {
+            const double a = Ts[(8 * warp + g) * RS + kk + t];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a, Rs[0][(kk + t) * RS + 8 * j + g]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int cl = 8 * j + 2 * t + q;
+                Qs[(8 * warp + g) * QS + p0 + cl] = acc[j][q];
+                if (row < p.n && p0 + cl < c) Q[(int64_t)row * p.ldq + p0 + cl] = acc[j][q];
+            }
+        __syncthreads();
     }
 }
 
@@ -170,14 +365,46 @@ void rank_check(const RankCheckParams& p, cudaStream_t st) {
     ::smg::count_launch(), rank_test_kernel<<<p.batch, 256, 0, st>>>(p, chunks);
 }
 
-void chol_inverse(const CholParams& p, cudaStream_t st) {
-    const int bytes = std::min(p.c_cap, SMEM_C) * std::min(p.c_cap, SMEM_C) * 8;
+int chol_smem_bytes(int c_cap) {
+    const int cp = (c_cap + 31) / 32 * 32;
+    return (32 * (cp + 4) + 32 * 33) * 8;
+}
+
+void chol_factor(const CholParams& p, cudaStream_t st) {
+    const int bytes = chol_smem_bytes(p.c_cap);
     static int configured = 0;
-    if (!configured) {
-        cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_C * SMEM_C * 8);
-        configured = 1;
+    if (bytes > configured) {
+        cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        configured = bytes;
     }
-    ::smg::count_launch(), chol_kernel<<<p.batch, NT, bytes, st>>>(p);
+    ::smg::count_launch(), chol_kernel<<<p.batch, CNT, bytes, st>>>(p);
+}
+
+static int trsm_rows(int c_cap) { return c_cap <= 256 ? 64 : 32; }
+
+int trsm_smem_bytes(int c_cap) {
+    const int cp = (c_cap + 31) / 32 * 32;
+    const int rows = trsm_rows(c_cap);
+    return (rows * (cp + 4) + 64 * RS + rows * RS) * 8;
+}
+
+void trsm(const TrsmParams& p, cudaStream_t st) {
+    const int bytes = trsm_smem_bytes(p.c_cap);
+    const int rows = trsm_rows(p.c_cap);
+    static int configured[2] = {0, 0};
+    if (rows == 64) {
+        if (bytes > configured[0]) {
+            cudaFuncSetAttribute(trsm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            configured[0] = bytes;
+        }
+        ::smg::count_launch(), trsm_kernel<64><<<dim3((p.n + 63) / 64, p.batch), 256, bytes, st>>>(p);
+    } else {
+        if (bytes > configured[1]) {
+            cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            configured[1] = bytes;
+        }
+        ::smg::count_launch(), trsm_kernel<32><<<dim3((p.n + 31) / 32, p.batch), 128, bytes, st>>>(p);
+    }
 }
 
 }  // namespace smg

@@ -114,7 +114,8 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
     compute_first_shift(rowptr.get(), cols.get(), vals.get(), off.get(), trace.get(), ntiles, n, shift0.get(), st);
 }
 
-void FactorSet::factor(const TileSet& ts, int first_tile, int cnt, const double* shift, cudaStream_t st) {
+void FactorSet::factor(const TileSet& ts, int first_tile, int cnt, const double* shift, cudaStream_t st,
+                       int* status_out) {
     ProfScope prof("factor", st);
     first = first_tile;
     count = cnt;
@@ -139,7 +140,7 @@ void FactorSet::factor(const TileSet& ts, int first_tile, int cnt, const double*
     p.Ffwd = fwd.get();
     p.Fbwd = bwd.get();
     p.strideF = strideF;
-    p.status = status.get();
+    p.status = status_out ? status_out : status.get();
     factor_tiles(p, st);
     SMG_CUDA(cudaGetLastError());
 }
@@ -250,27 +251,30 @@ void gram(Workspace& ws, const double* V, int c, const int* dimC, int n, cudaStr
     gemm(g, true, false, st);
 }
 
+// out = V D^-1 R~^-1 with R~ / Dinv / d from the last chol()
 void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st) {
-    GemmParams g;
-    g.M = n;
-    g.N = c;
-    g.K = c;
-    g.batch = ws.B;
-    g.A = V;
-    g.lda = ws.ld;
-    g.strideA = ws.mstride();
-    g.B = ws.Bm.get();
-    g.ldb = ws.ld;
-    g.strideB = (int64_t)ws.ld * ws.ld;
-    g.C = out;
-    g.ldc = ws.ld;
-    g.strideC = ws.mstride();
-    g.upperB = 1;
-    g.dimN = dimC;
-    g.dimK = dimC;
-    g.dimStride = 1;
+    TrsmParams p;
+    p.n = n;
+    p.batch = ws.B;
+    p.c_cap = c;
+    p.V = V;
+    p.ldv = ws.ld;
+    p.strideV = ws.mstride();
+    p.Q = out;
+    p.ldq = ws.ld;
+    p.strideQ = ws.mstride();
+    p.A = ws.work.get();
+    p.lda = ws.ld;
+    p.strideA = (int64_t)ws.ld * ws.ld;
+    p.Dinv = ws.Bm.get();
+    p.strideDinv = (int64_t)ws.ld * ws.ld;
+    p.dscale = ws.rdiag.get();
+    p.strideD = ws.ld;
+    p.dimC = dimC;
+    p.dimStride = 1;
+    p.status = ws.status.get();
     ProfScope prof("trmm", st);
-    gemm(g, false, false, st);
+    trsm(p, st);
 }
 
 void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_scale, int pos, cudaStream_t st) {
@@ -280,12 +284,13 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
     p.G = ws.G.get();
     p.ldg = ws.ld;
     p.strideG = (int64_t)ws.ld * ws.ld;
-    p.Binv = ws.Bm.get();
-    p.ldb = ws.ld;
-    p.strideB = (int64_t)ws.ld * ws.ld;
-    p.rdiag = ws.rdiag.get();
-    p.strideR = ws.ld;
-    p.work = ws.work.get();
+    p.A = ws.work.get();
+    p.lda = ws.ld;
+    p.strideA = (int64_t)ws.ld * ws.ld;
+    p.Dinv = ws.Bm.get();
+    p.strideDinv = (int64_t)ws.ld * ws.ld;
+    p.dscale = ws.rdiag.get();
+    p.strideD = ws.ld;
     p.dimC = dimC;
     p.dimStride = 1;
     p.status = ws.status.get();
@@ -296,12 +301,12 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
     p.column_scale = column_scale ? 1 : 0;
     p.vnorm = rank_test ? ws.vnorm.get() : nullptr;
     ProfScope prof("chol", st);
-    chol_inverse(p, st);
+    chol_factor(p, st);
 }
 }  // namespace
 
 void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
-                bool rank_test, int pos) {
+                bool rank_test, int pos, int passes) {
     ProfScope prof("orthonormalize", cx.st);
     const int n = ws.npad;
     if (rank_test && in == out) {
@@ -312,6 +317,11 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
     }
     gram(ws, in, c, dimC, n, cx.st);
     chol(ws, c, dimC, rank_test, true, pos, cx.st);
+    if (passes == 1) {  // single CholeskyQR pass (span-only uses: subspace iteration)
+        trmm(ws, in, out, c, dimC, n, cx.st);
+        SMG_CUDA(cudaGetLastError());
+        return;
+    }
     trmm(ws, in, ws.R.get(), c, dimC, n, cx.st);
     gram(ws, ws.R.get(), c, dimC, n, cx.st);
     chol(ws, c, dimC, false, true, pos, cx.st);

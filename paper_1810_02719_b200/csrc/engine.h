@@ -113,7 +113,8 @@ struct FactorSet {
     int64_t strideF = 0;
     DBuf<double> fwd, bwd;
     DBuf<int> status;
-    void factor(const TileSet& ts, int first_tile, int count, const double* shift, cudaStream_t st);
+    void factor(const TileSet& ts, int first_tile, int count, const double* shift, cudaStream_t st,
+                int* status_out = nullptr);
     const double* f(int tile) const { return fwd.get() + (int64_t)(tile - first) * strideF; }
     const double* b(int tile) const { return bwd.get() + (int64_t)(tile - first) * strideF; }
     void rebind(cudaStream_t st) { fwd.rebind(st), bwd.rebind(st), status.rebind(st); }
@@ -142,7 +143,7 @@ void solve_batch(const StepCtx& cx, Workspace& ws, const FactorSet& fs, int tile
                  double* out, int c, const int* dimC, int z, bool once);
 // CholeskyQR2: out = orth(in); sticky per-chain status, error position `pos`.
 void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
-                bool rank_test, int pos);
+                bool rank_test, int pos, int passes = 2);
 void project_batch(const StepCtx& cx, Workspace& ws, const double* Q, int c, const int* dimC, const double* X,
                    int64_t strideX, double* xhat, int64_t strideXhat);
 

@@ -23,12 +23,50 @@ namespace {
 
 constexpr int NT = 256;
 
+constexpr int MAXCPL = 16;  // coupling entries per row into the previous block
+
 template <int W>
 struct FactorSmem {
-    static constexpr int LD = W + 1;
+    static constexpr int LD = W + 4;  // LD % 16 == 4: conflict-free DMMA fragment reads
     static constexpr int MAT = W * LD;
-    static int bytes(int n) { return (4 * MAT + 2 * W + 32) * 8 + n * 4; }
+    static int bytes(int n) {
+        return (4 * MAT + 2 * W + 32) * 8 + ((n + 1) & ~1) * 4 + W * MAXCPL * (8 + 4) + W * 4;
+    }
 };
+
+// C (W x W, DMMA accumulators of one warp's 2x(W/16)... tiles) helpers.
+// Warps tile the W x W output as a 4 x 2 grid of (W/32 x W/16) 8x8 tiles.
+template <int W>
+struct FTile {
+    // 8x8 tiles per warp: W=16 1x1 (4 warps), 32 1x2 (8), 48 2x3 (6), 64 2x4 (8)
+    static constexpr int MT = (W == 48 || W == 64) ? 2 : 1;
+    static constexpr int NTT = W == 16 ? 1 : (W == 32 ? 2 : (W == 48 ? 3 : 4));
+    static constexpr int WMG = (W / 8) / MT;  // warps along m
+    static constexpr int WNG = (W / 8) / NTT; // warps along n
+    static constexpr int ACTIVE = WMG * WNG;
+};
+
+// acc[i][j] += sum_k A(m, k) * B(k, n) over k in [k0, k1), A/B as functors of
+// (row, col) returning smem values; m = 8*(wm*MT+i)+g, n = 8*(wn*NT+j)+g.
+template <int W, class FA, class FB, class FSkip>
+SMG_DEV void fblock_mma(double (&acc)[FTile<W>::MT][FTile<W>::NTT][2], FA a, FB b, FSkip skip, int wm, int wn,
+                        int g, int t) {
+    constexpr int MT = FTile<W>::MT, NT = FTile<W>::NTT;
+#pragma unroll 2
+    for (int kk = 0; kk < W; kk += 4) {
+        double av[MT], bv[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) bv[j] = b(kk + t, 8 * (wn * NT + j) + g);
+#pragma unroll
+        for (int i = 0; i < MT; ++i) av[i] = a(8 * (wm * MT + i) + g, kk + t);
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            if (skip(wm * MT + i, kk)) continue;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+        }
+    }
+}
 
 template <int W>
 __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
@@ -43,6 +81,14 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
     double* sigp = sig + W;      // Sigma_{k-1}
     int* flag = reinterpret_cast<int*>(sigp + W);
     int* ipos = reinterpret_cast<int*>(sigp + W + 32);
+    double* cval = reinterpret_cast<double*>(ipos + ((p.n + 1) & ~1));  // [W][MAXCPL]
+    int* cidx = reinterpret_cast<int*>(cval + W * MAXCPL);             // [W][MAXCPL]
+    int* ccnt = cidx + W * MAXCPL;                                     // [W]
+    using FT = FTile<W>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm = warp % FT::WMG, wn = warp / FT::WMG;
+    const bool mma_warp = warp < FT::ACTIVE;
 
     const int tile = blockIdx.x;
     const int n = p.n, Kb = p.Kb, tid = threadIdx.x;
@@ -65,42 +111,62 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
         // ---- D_k (+ delta on the diagonal, Eigen: shifted += delta * identity)
         for (int e = tid; e < W * W; e += NT) S[(e / W) * LD + (e % W)] = 0.0;
         __syncthreads();
+        // one scan of the block's CSR rows: D_k entries and the coupling B_k into block k-1
         for (int r = tid; r < W; r += NT) {
             const int prow = r0 + r;
+            int cnt = 0;
             if (prow >= n) {
                 S[r * LD + r] = 1.0;
-                continue;
+            } else {
+                const int i = perm ? perm[prow] : prow;
+                for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+                    const int pq = ipos[cols[e]];
+                    const int q = pq - r0;
+                    if (q >= 0 && q < W) {
+                        S[r * LD + q] = (cols[e] == i) ? vals[e] + delta : vals[e];
+                    } else if (q >= -W && q < 0) {
+                        if (cnt < MAXCPL) {
+                            cidx[r * MAXCPL + cnt] = q + W;
+                            cval[r * MAXCPL + cnt] = vals[e];
+                        }
+                        ++cnt;
+                    } else if (q < -W || q >= 2 * W) {
+                        flag[0] = 2;  // not block tridiagonal at this width
+                    }
+                }
             }
-            const int i = perm ? perm[prow] : prow;
-            for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
-                const int q = ipos[cols[e]] - r0;
-                if (q >= 0 && q < W) S[r * LD + q] = (cols[e] == i) ? vals[e] + delta : vals[e];
-            }
+            ccnt[r] = cnt;
+            if (cnt > MAXCPL) flag[0] = 2;
         }
+        __syncthreads();
         if (k > 0) {
-            // ---- P = B_k Linv_{k-1}^T Sigma_{k-1}  (= L_{k,k-1})
+            // ---- P = B_k Linv_{k-1}^T Sigma_{k-1}  (= L_{k,k-1}), B_k sparse
             for (int e = tid; e < W * W; e += NT) {
                 const int r = e / W, c = e % W;
-                const int prow = r0 + r;
+                const int cnt = min(ccnt[r], MAXCPL);
                 double acc = 0.0;
-                if (prow < n) {
-                    const int i = perm ? perm[prow] : prow;
-                    for (int q = rowptr[i]; q < rowptr[i + 1]; ++q) {
-                        const int qq = ipos[cols[q]] - (r0 - W);
-                        if (qq >= 0 && qq < W && c >= qq) acc += vals[q] * Lp[c * LD + qq];
-                    }
+                for (int q = 0; q < cnt; ++q) {
+                    const int qq = cidx[r * MAXCPL + q];
+                    if (c >= qq) acc += cval[r * MAXCPL + q] * Lp[c * LD + qq];
                 }
                 P[r * LD + c] = acc * sigp[c];
             }
             __syncthreads();
-            // ---- S -= P Sigma_{k-1} P^T (lower triangle)
-            for (int e = tid; e < W * W; e += NT) {
-                const int r = e / W, s = e % W;
-                if (s > r) continue;
-                double acc = 0.0;
-#pragma unroll 8
-                for (int i = 0; i < W; ++i) acc += P[r * LD + i] * sigp[i] * P[s * LD + i];
-                S[r * LD + s] -= acc;
+            // ---- S -= P Sigma_{k-1} P^T  (DMMA; full block, the lower triangle is used)
+            if (mma_warp) {
+                double acc[FT::MT][FT::NTT][2] = {};
+                fblock_mma<W>(
+                    acc, [&](int m, int kk) { return P[m * LD + kk]; },
+                    [&](int kk, int nn) { return P[nn * LD + kk] * sigp[kk]; }, [](int, int) { return false; }, wm, wn,
+                    g, t4);
+#pragma unroll
+                for (int i = 0; i < FT::MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < FT::NTT; ++j) {
+                        const int r = 8 * (wm * FT::MT + i) + g, s = 8 * (wn * FT::NTT + j) + 2 * t4;
+                        S[r * LD + s] -= acc[i][j][0];
+                        S[r * LD + s + 1] -= acc[i][j][1];
+                    }
             }
         }
         __syncthreads();
@@ -146,21 +212,40 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
         for (int e = tid; e < W * W; e += NT) {
             const int j = e / W, r = e % W;
             F[(int64_t)j * W + r] = Lc[r * LD + j];
-            double m = 0.0;
-            if (k > 0) {
-                for (int i = 0; i <= r; ++i) m += Lc[r * LD + i] * P[i * LD + j];
-            }
-            F[(int64_t)(W + j) * W + r] = -m;
+        }
+        if (mma_warp) {
+            double acc[FT::MT][FT::NTT][2] = {};
+            if (k > 0)  // M_k = Linv_k P (Linv_k lower: skip k-slices right of the m-tile)
+                fblock_mma<W>(
+                    acc, [&](int m, int kk) { return Lc[m * LD + kk]; },
+                    [&](int kk, int nn) { return P[kk * LD + nn]; },
+                    [](int ti, int kk) { return kk >= 8 * ti + 8; }, wm, wn, g, t4);
+            // stored transposed: F[W + j][r] = -M[r][j]
+#pragma unroll
+            for (int i = 0; i < FT::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < FT::NTT; ++j)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int r = 8 * (wm * FT::MT + i) + g, jj = 8 * (wn * FT::NTT + j) + 2 * t4 + q;
+                        F[(int64_t)(W + jj) * W + r] = -acc[i][j][q];
+                    }
         }
         // ---- Fbwd_{k-1}^T second half: -(L_{k,k-1} Linv_{k-1}) = -(P Lp), row-major
-        if (k > 0) {
+        if (k > 0 && mma_warp) {
             double* Fp = Fb + (int64_t)(k - 1) * slab;
-            for (int e = tid; e < W * W; e += NT) {
-                const int j = e / W, r = e % W;
-                double m = 0.0;
-                for (int i = r; i < W; ++i) m += P[j * LD + i] * Lp[i * LD + r];
-                Fp[(int64_t)(W + j) * W + r] = -m;
-            }
+            double acc[FT::MT][FT::NTT][2] = {};
+            fblock_mma<W>(
+                acc, [&](int m, int kk) { return P[m * LD + kk]; }, [&](int kk, int nn) { return Lp[kk * LD + nn]; },
+                [](int, int) { return false; }, wm, wn, g, t4);
+#pragma unroll
+            for (int i = 0; i < FT::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < FT::NTT; ++j) {
+                    const int r = 8 * (wm * FT::MT + i) + g, jj = 8 * (wn * FT::NTT + j) + 2 * t4;
+                    double2* dst = reinterpret_cast<double2*>(Fp + (int64_t)(W + r) * W + jj);
+                    *dst = make_double2(-acc[i][j][0], -acc[i][j][1]);
+                }
         }
         // ---- Fbwd_k^T first half: row j = sigma_j * Linv_k[j, :]
         {

@@ -16,10 +16,13 @@
 // Only span(bottom c) is needed downstream: fixed-c OI and the projections
 // depend on the span, and the sign convention is re-applied in project.cu.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <random>
 
 #include "engine.h"
 #include "firstbasis.h"
+#include "profiler.h"
 
 namespace smg {
 
@@ -62,6 +65,21 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
     FirstBasisReport rep;
     const cudaStream_t st = cx.st;
     const int n = ts.n;
+    // recorded as one "first_basis" stage; its inner solves/QRs are not
+    // attributed to the chain's per-step stages
+    struct Scope {
+        Profiler* saved;
+        int token;
+        cudaStream_t st;
+        explicit Scope(cudaStream_t s) : saved(active_profiler()), token(-1), st(s) {
+            if (saved) token = saved->begin(st);
+            active_profiler() = nullptr;
+        }
+        ~Scope() {
+            active_profiler() = saved;
+            if (saved && token >= 0) saved->end("first_basis", token, st);
+        }
+    } scope(st);
     if (n > cfg.dense_limit) {
         // cold start exactly as the reference: random_orthonormal_basis + OI
         require(op_factor != nullptr, "internal: cold start needs the operator factor");
@@ -111,12 +129,17 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
     int iters_next = (m == n) ? 0 : 6;
     double prev_bound = INFINITY;
     for (int round = 0; round < fc.max_rounds; ++round) {
+        const int tk_it = scope.saved ? scope.saved->begin(st) : -1;
         for (int t = 0; t < iters_next; ++t) {
             const int z = (round == 0 && t == 0) ? 1 : 2;
             solve_batch(cx, ws, fs, tile0, tstride, ws.U.get(), ws.V.get(), m, nullptr, z, false);
-            orth_batch(cx, ws, ws.V.get(), ws.U.get(), m, nullptr, false, 0);
+            // intermediate iterates only need their span: one CholeskyQR pass;
+            // the iterate entering Rayleigh-Ritz gets the full CholeskyQR2
+            orth_batch(cx, ws, ws.V.get(), ws.U.get(), m, nullptr, false, 0, t + 1 == iters_next ? 2 : 1);
             rep.iterations += 1;
         }
+        if (tk_it >= 0) scope.saved->end("fb_iterate", tk_it, st);
+        const int tk_rr = scope.saved ? scope.saved->begin(st) : -1;
         // Rayleigh-Ritz: Y = L U (into R), H = U^T Y
         SpmmParams sp;
         sp.n = n;
@@ -166,14 +189,24 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
         jp.W = ws.Wm.get();
         jp.ldw = m;
         jp.strideW = (int64_t)m * m;
+        DBuf<int> sweeps;
+        sweeps.alloc(ws.B, st);
+        jp.sweeps = sweeps.get();
         const int jerr = jacobi_eigh(jp, pl, m, st);
         if (jerr != 0) SMG_CUDA((cudaError_t)jerr);
+        if (std::getenv("SMG_DEBUG")) {
+            std::vector<int> sw = download(sweeps.get(), ws.B, st);
+            int mx = 0;
+            for (int v : sw) mx = std::max(mx, v);
+            std::fprintf(stderr, "[smg] jacobi m %d clusters %d x %d: max sweeps %d\n", m, ws.B, pl.nc, mx);
+        }
         // Z = U W (into V), LZ = Y W (into T)
         gemm_nn(ws, ws.U.get(), ws.ld, ws.Wm.get(), m, (int64_t)m * m, ws.V.get(), n, m, m, st);
         gemm_nn(ws, ws.R.get(), ws.ld, ws.Wm.get(), m, (int64_t)m * m, ws.T.get(), n, m, m, st);
         ritz_residual(ws.T.get(), ws.V.get(), ws.theta_s.get(), n, nres, ws.ld, ws.mstride(), m, ws.B,
                       ws.ritz_part.get(), ws.ritz.get(), st);
         std::swap(ws.U, ws.V);
+        if (tk_rr >= 0) scope.saved->end("fb_rayleigh_ritz", tk_rr, st);
         rep.rounds = round + 1;
         std::vector<double> th = download(ws.theta_s.get(), (size_t)ws.B * m, st);
         std::vector<double> rs = download(ws.ritz.get(), (size_t)ws.B * nres, st);
@@ -197,12 +230,18 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
             }
         }
         rep.bound = bound;
+        if (std::getenv("SMG_DEBUG"))
+            std::fprintf(stderr, "[smg] first_basis round %d: iterations %d bound %.3e rate %.3e m %d\n", round,
+                         rep.iterations, bound, worst_rate, m);
         if (m == n || bound < fc.tol) break;
         if (!(bound < prev_bound * 0.999) && round >= 3) break;  // stagnated at the rounding floor
         prev_bound = bound;
         // iterations to reach the tolerance at the observed rate (bound shrinks ~rate per step)
         double need = 4.0;
-        if (worst_rate > 0.0 && worst_rate < 1.0) need = std::log(fc.tol * 0.1 / bound) / std::log(worst_rate);
+        // plan with a pessimistic rate (the early Ritz values overestimate the gap) so
+        // that one more Rayleigh-Ritz round suffices
+        if (worst_rate > 0.0 && worst_rate < 1.0)
+            need = std::log(fc.tol * 0.1 / bound) / std::log(std::pow(worst_rate, 0.85));
         iters_next = (int)std::min(60.0, std::max(2.0, std::ceil(need)));
     }
     return rep;

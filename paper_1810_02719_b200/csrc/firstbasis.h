@@ -15,7 +15,7 @@ struct FirstBasisConfig {
     int power = 2;
     uint64_t seed = 1;
     int max_rounds = 12;
-    double tol = 2e-12;
+    double tol = 1e-10;  // subspace-angle bound; parity target 1e-8
     double shift_hint = 0.0;
 };
 

@@ -94,13 +94,14 @@ void solve_block_tridiag(const SolveParams& p, int W, cudaStream_t st);
 // ------------------------------------------------------------------ CholeskyQR (cholqr.cu)
 struct CholParams {
     int batch = 1, c_cap = 0;
-    const double* G = nullptr;
+    const double* G = nullptr;  // Gram (upper 64-tiles valid)
     int64_t ldg = 0, strideG = 0;
-    double* Binv = nullptr;
-    int64_t ldb = 0, strideB = 0;
-    double* rdiag = nullptr;
-    int64_t strideR = 0;
-    double* work = nullptr;  // c_cap*c_cap per batch when c > 144
+    double* A = nullptr;  // scaled Gram -> R~ (upper), ld multiple of 32 (>= c rounded to 32)
+    int64_t lda = 0, strideA = 0;
+    double* Dinv = nullptr;  // per 32-panel inverse of the diagonal block (32x32 row-major)
+    int64_t strideDinv = 0;
+    double* dscale = nullptr;  // column norms d_j (rounded-up length)
+    int64_t strideD = 0;
     const int* dimC = nullptr;
     int64_t dimStride = 0;
     int* status = nullptr;           // sticky per-chain status (first error wins)
@@ -111,7 +112,26 @@ struct CholParams {
     int rank_test = 1;
     int column_scale = 1;
 };
-void chol_inverse(const CholParams& p, cudaStream_t st);
+void chol_factor(const CholParams& p, cudaStream_t st);
+// Q = V D^-1 R~^-1 (rows independent; 32 rows per CTA)
+struct TrsmParams {
+    int n = 0, batch = 1, c_cap = 0;
+    const double* V = nullptr;
+    int64_t ldv = 0, strideV = 0;
+    double* Q = nullptr;
+    int64_t ldq = 0, strideQ = 0;
+    const double* A = nullptr;
+    int64_t lda = 0, strideA = 0;
+    const double* Dinv = nullptr;
+    int64_t strideDinv = 0;
+    const double* dscale = nullptr;
+    int64_t strideD = 0;
+    const int* dimC = nullptr;
+    int64_t dimStride = 0;
+    const int* status = nullptr;
+};
+void trsm(const TrsmParams& p, cudaStream_t st);
+int trsm_smem_bytes(int c_cap);
 // Accurate reference rank test after CholeskyQR2: |r_kk| = |q_k^T v_k| against
 // 1e-13 ||V||_F (first failing column, sticky status).
 struct RankCheckParams {

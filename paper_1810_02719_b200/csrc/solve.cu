@@ -36,53 +36,69 @@ SMG_DEV void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
 
+// Warp tiling of the W x CS step output: warps form a WM x WN grid, each owns
+// MT x NT tiles of 8x8, so per k-slice it loads MT + NT operand fragments for
+// MT * NT DMMAs (shared-memory traffic, not the DMMA pipe, bounds this loop).
+template <int W, int CS>
+struct SolveTiling {
+    static constexpr int MT_ALL = W / 8, NT_ALL = CS / 8;
+    static constexpr int WM = (MT_ALL % 4 == 0) ? 4 : ((MT_ALL % 2 == 0) ? 2 : 1);
+    static constexpr int WN_RAW = 4 / WM;
+    static constexpr int WN = (NT_ALL % WN_RAW == 0) ? WN_RAW : ((WN_RAW >= 2 && NT_ALL % 2 == 0) ? 2 : 1);
+    static constexpr int MT = MT_ALL / WM, NT = NT_ALL / WN;
+    static constexpr int ACTIVE = WM * WN;
+};
+
 template <int W, int CS, bool FWD>
-SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ xs, double (&acc)[(W / 8) * (CS / 8) / 4 + 1][2],
-                      int warp, int g, int t, bool skip_second) {
-    constexpr int TN = CS / 8;
-    constexpr int T = (W / 8) * TN;
-    constexpr int MAXT = T / 4 + 1;
+SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ xs,
+                      double (&acc)[SolveTiling<W, CS>::MT][SolveTiling<W, CS>::NT][2], int warp, int g, int t,
+                      bool skip_second) {
+    using TL = SolveTiling<W, CS>;
+    constexpr int MT = TL::MT, NT = TL::NT;
     constexpr int FS = SolveSmem<W, CS>::FS;
     constexpr int XS = SolveSmem<W, CS>::XS;
+    const int wm = warp % TL::WM, wn = warp / TL::WM;
 #pragma unroll
-    for (int q = 0; q < MAXT; ++q) acc[q][0] = acc[q][1] = 0.0;
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (warp >= TL::ACTIVE) return;
     // first half: triangular block (Linv_k lower for FWD, Linv_k^T Sigma upper for BWD)
-#pragma unroll 4
+#pragma unroll 2
     for (int kk = 0; kk < W; kk += 4) {
+        double b[NT];
 #pragma unroll
-        for (int q = 0; q < MAXT; ++q) {
-            const int tile = warp + 4 * q;
-            if (tile >= T) break;
-            const int ti = tile / TN, tj = tile % TN;
+        for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int ti = wm * MT + i;
             const bool nz = FWD ? (kk < 8 * ti + 8) : (kk + 4 > 8 * ti);
             if (!nz) continue;
             const double a = fs[(kk + t) * FS + 8 * ti + g];
-            const double b = xs[(kk + t) * XS + 8 * tj + g];
-            dmma884(acc[q][0], acc[q][1], a, b);
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a, b[j]);
         }
     }
     if (skip_second) return;
-#pragma unroll 4
+#pragma unroll 2
     for (int kk = W; kk < 2 * W; kk += 4) {
+        double a[MT], b[NT];
 #pragma unroll
-        for (int q = 0; q < MAXT; ++q) {
-            const int tile = warp + 4 * q;
-            if (tile >= T) break;
-            const int ti = tile / TN, tj = tile % TN;
-            const double a = fs[(kk + t) * FS + 8 * ti + g];
-            const double b = xs[(kk + t) * XS + 8 * tj + g];
-            dmma884(acc[q][0], acc[q][1], a, b);
-        }
+        for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) a[i] = fs[(kk + t) * FS + 8 * (wm * MT + i) + g];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
 }
 
 template <int W, int CS>
 __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     using S = SolveSmem<W, CS>;
+    using TL = SolveTiling<W, CS>;
     constexpr int FS = S::FS, XS = S::XS;
-    constexpr int TN = CS / 8;
-    constexpr int T = (W / 8) * TN;
-    constexpr int MAXT = T / 4 + 1;
     extern __shared__ __align__(16) double smem[];
     double* Fs[2] = {smem, smem + S::F_ELEMS};
     double* Xs[2] = {smem + 2 * S::F_ELEMS, smem + 2 * S::F_ELEMS + S::X_ELEMS};
@@ -145,31 +161,34 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
             cp_async_wait<0>();
             __syncthreads();
             if (step + 1 < Kb) issue(sweep, fwd ? k + 1 : k - 1, buf ^ 1);
-            double acc[MAXT][2];
+            double acc[TL::MT][TL::NT][2];
             const bool skip2 = step == 0;
             if (fwd) mma_step<W, CS, true>(Fs[buf], Xs[buf], acc, warp, g, t, skip2);
             else mma_step<W, CS, false>(Fs[buf], Xs[buf], acc, warp, g, t, skip2);
             // epilogue: result is the "previous block" of the next step and goes to dst
             double* xnext = Xs[buf ^ 1] + W * XS;
+            if (warp < TL::ACTIVE) {
+                const int wm = warp % TL::WM, wn = warp / TL::WM;
 #pragma unroll
-            for (int q = 0; q < MAXT; ++q) {
-                const int tile = warp + 4 * q;
-                if (tile >= T) break;
-                const int ti = tile / TN, tj = tile % TN;
-                const int r = 8 * ti + g, cc = 8 * tj + 2 * t;
-                xnext[r * XS + cc] = acc[q][0];
-                xnext[r * XS + cc + 1] = acc[q][1];
-                const int prow = k * W + r;
-                if (last) {
-                    if (prow < n && col0 + cc < c) {
-                        const int lrow = perm ? perm[prow] : prow;
-                        double2* dst = reinterpret_cast<double2*>(out + (int64_t)lrow * p.ldout + col0 + cc);
-                        *dst = make_double2(acc[q][0], acc[q][1]);
+                for (int i = 0; i < TL::MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < TL::NT; ++j) {
+                        const int r = 8 * (wm * TL::MT + i) + g, cc = 8 * (wn * TL::NT + j) + 2 * t;
+                        xnext[r * XS + cc] = acc[i][j][0];
+                        xnext[r * XS + cc + 1] = acc[i][j][1];
+                        const int prow = k * W + r;
+                        if (last) {
+                            if (prow < n && col0 + cc < c) {
+                                const int lrow = perm ? perm[prow] : prow;
+                                double2* dst =
+                                    reinterpret_cast<double2*>(out + (int64_t)lrow * p.ldout + col0 + cc);
+                                *dst = make_double2(acc[i][j][0], acc[i][j][1]);
+                            }
+                        } else {
+                            double2* dst = reinterpret_cast<double2*>(tmp + (int64_t)prow * p.ldt + col0 + cc);
+                            *dst = make_double2(acc[i][j][0], acc[i][j][1]);
+                        }
                     }
-                } else {
-                    double2* dst = reinterpret_cast<double2*>(tmp + (int64_t)prow * p.ldt + col0 + cc);
-                    *dst = make_double2(acc[q][0], acc[q][1]);
-                }
             }
             buf ^= 1;
         }
