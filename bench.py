@@ -216,6 +216,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     import numpy as np
     import torch
     import paper_1810_02719_b200 as G
+    from paper_1810_02719_b200 import shard
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
@@ -226,21 +227,18 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         ids = [rank]
         total_units = world
     else:
-        assert total_meshes % world == 0, "mesh count must divide over ranks"
-        per = total_meshes // world
-        ids = list(range(rank * per, (rank + 1) * per))
+        ids = shard.shard_meshes(total_meshes, world, rank)
         total_units = total_meshes
     ctx = G.Context(local_rank)
     job = GpuJob(cfg, ids, local_rank, ctx)
     verts_per_unit = job.n
-    gather_buf = None
-    if dist is not None and cfg["meshes"] > 1:
-        gather_buf = torch.empty((world,) + tuple(job.d_recon.shape), dtype=torch.float64, device=job.dev)
+    gather = dist is not None and cfg["meshes"] > 1
 
     def step(on_device):
         job.run(on_device)
-        if gather_buf is not None and on_device:
-            dist.all_gather_into_tensor(gather_buf, job.d_recon)
+        if gather and on_device:
+            # per-mesh reconstructions to every rank (NCCL over NVLink)
+            shard.gather_meshes(job.d_recon, total_meshes)
 
     def barrier():
         torch.cuda.synchronize()

@@ -95,15 +95,16 @@ __global__ void delta_kernel(const double* trace, int ntiles, int n, double scal
     }
 }
 
-// first-basis shift: Gershgorin lower bound of L, then + 1e-3 * mean diagonal
+// first-basis shift: Gershgorin lower bound of L, then + 1e-3 * mean diagonal;
+// shift[ntiles + t] = Gershgorin upper bound (Chebyshev filter interval end)
 __global__ void first_shift_kernel(const int32_t* rowptr, const int32_t* cols, const double* vals,
                                    const int64_t* csr_offsets, const double* trace, int ntiles, int n, double* shift) {
-    __shared__ double red[32];
+    __shared__ double red[32], redh[32];
     const int t = blockIdx.x;
     const int32_t* rp = rowptr + (int64_t)t * (n + 1);
     const double* v = vals + csr_offsets[t];
     const int32_t* c = cols + csr_offsets[t];
-    double lo = INFINITY;
+    double lo = INFINITY, hi = -INFINITY;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         double diag = 0.0, off = 0.0;
         for (int e = rp[i]; e < rp[i + 1]; ++e) {
@@ -111,14 +112,25 @@ __global__ void first_shift_kernel(const int32_t* rowptr, const int32_t* cols, c
             else off += fabs(v[e]);
         }
         lo = fmin(lo, diag - off);
+        hi = fmax(hi, diag + off);
     }
-    for (int o = 16; o > 0; o >>= 1) lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lo;
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5] = lo;
+        redh[threadIdx.x >> 5] = hi;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double m = INFINITY;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, red[w]);
+        double m = INFINITY, h = -INFINITY;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            m = fmin(m, red[w]);
+            h = fmax(h, redh[w]);
+        }
         shift[t] = fmax(0.0, -m) + 1e-3 * (trace[t] / (double)n) + 1e-300;
+        shift[ntiles + t] = h;
     }
 }
 

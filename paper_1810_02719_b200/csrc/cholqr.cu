@@ -1,6 +1,6 @@
-// K6/K7: CholeskyQR building blocks -- blocked c x c Cholesky of the column-
-// scaled Gram matrix with the reference rank test, and the triangular solve
-// Q = V D^-1 R~^-1 -- on the FP64 DMMA path.
+// K6: CholeskyQR building block -- blocked c x c Cholesky of the column-scaled
+// Gram matrix with the reference rank test, and B = D^-1 R~^-1 so that the
+// orthonormal factor is one triangular GEMM Q = V B (gemm.cu, upperB).
 //
 // orthonormalize (spectral.hpp:120-132) computes a Householder QR and throws
 // "rank deficient at column k" for the first k with |r_kk| < 1e-13 ||block||_F.
@@ -13,11 +13,11 @@
 // rank_check (|q_k^T v_k| against the same threshold).
 //
 // chol_kernel: one CTA per chain, right-looking blocked Cholesky with 32-wide
-// panels on the matrix in L2: the 32x32 diagonal block is factored and inverted
-// in one warp's registers (shuffles, no block barriers), the panel row and the
-// trailing SYRK run on all warps as 32x32x32 DMMA blocks.
-// trsm_kernel: rows are independent, so each CTA owns 32 rows of V and sweeps
-// the 32-column panels: Q_p = (V_p D_p^-1 - Q_<p R~_<p,p) R~_pp^-1.
+// panels; the panel row sits in shared memory, its 32x32 diagonal block is
+// factored and inverted by one warp in shared memory, the panel row solve and
+// the trailing SYRK are 32x32x32 DMMA blocks on all warps; finally the block
+// upper-triangular inverse X = R~^-1 is formed by block back-substitution
+// (DMMA) and stored row-scaled as B = D^-1 X.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -27,7 +27,6 @@ namespace {
 
 constexpr int CNT = 256;
 constexpr int CW = CNT / 32;
-constexpr unsigned FULL = 0xffffffffu;
 
 // 32x32x32 block product on one warp: acc(4x4 tiles of 8x8, 2 values) += op(A) * B
 // with op(A)[m][k] = a(m, k), B[k][n] = b(k, n) supplied as functors.
@@ -57,17 +56,22 @@ SMG_DEV void zero_acc(double (&acc)[4][4][2]) {
 __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     __shared__ double red[32];
     __shared__ int fail;
+    extern __shared__ __align__(16) double psm[];
     const int b = blockIdx.x;
     if (p.status[b] != kOk) return;  // sticky first error of this chain
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const int P = (c + 31) / 32, cp = P * 32;
     const double* G = p.G + (int64_t)b * p.strideG;
     double* A = p.A + (int64_t)b * p.strideA;
-    double* Dinv = p.Dinv + (int64_t)b * p.strideDinv;
+    double* Bo = p.Binv + (int64_t)b * p.strideB;
     double* d = p.dscale + (int64_t)b * p.strideD;
-    const int64_t lda = p.lda;
+    const int64_t lda = p.lda, ldb = p.ldb;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
+    const int PS = cp + 4;         // panel row stride (% 16 == 4: conflict-free fragments)
+    double* Ps = psm;              // 32 x PS panel row
+    double* Xs = psm + 32 * PS;    // 32 x 33 diagonal-block inverse
+    double* Ts = Xs + 32 * 33;     // CW x 32 x 33 per-warp staging
 
     double tr = 0.0;
     for (int j = tid; j < cp; j += CNT) {
@@ -111,11 +115,6 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     }
     __syncthreads();
 
-    // panel row p (32 x cp) lives in shared memory during its panel step
-    extern __shared__ __align__(16) double psm[];
-    const int PS = cp + 4;  // row stride, % 16 == 4: conflict-free DMMA fragments
-    double* Ps = psm;
-    double* Xs = psm + 32 * PS;  // 32 x 33
     for (int pb = 0; pb < P; ++pb) {
         const int p0 = pb * 32;
         for (int e = tid; e < 32 * (cp - p0); e += CNT) {
@@ -123,15 +122,12 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             Ps[r * PS + k] = A[(int64_t)(p0 + r) * lda + k];
         }
         __syncthreads();
-        // ---- (a) factor + invert the diagonal block (warp 0; rows broadcast via smem)
+        // ---- (a) factor + invert the diagonal block: warp 0, lane k owns column k
         if (warp == 0) {
-            double col[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) col[i] = (i <= lane) ? Ps[i * PS + p0 + lane] : 0.0;
             int bad = -1;
-#pragma unroll
+            double* D = Ps + p0;  // D[i * PS + k]
             for (int j = 0; j < 32; ++j) {
-                const double piv = Ps[j * PS + p0 + j];
+                const double piv = D[j * PS + j];
                 const int gj = p0 + j;
                 if (bad < 0 && gj < c) {
                     const bool bp = !(piv > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(piv) || !(d[gj] > 0.0);
@@ -139,34 +135,25 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                     if (bp || (p.rank_test && rkk < thresh)) bad = j;
                 }
                 const double rjj = sqrt(fmax(piv, 1e-300));
-                if (lane > j) col[j] /= rjj;
-                if (lane == j) col[j] = rjj;
                 __syncwarp();
-                if (lane >= j) Ps[j * PS + p0 + lane] = col[j];  // row j of R_pp
+                if (lane > j) D[j * PS + lane] /= rjj;
+                if (lane == j) D[j * PS + j] = rjj;
                 __syncwarp();
-                const double ajk = col[j];
-#pragma unroll
-                for (int i = j + 1; i < 32; ++i) {
-                    if (lane >= i) col[i] -= Ps[j * PS + p0 + i] * ajk;
-                    if (lane == i) Ps[i * PS + p0 + i] = col[i];  // updated pivot for step i
+                if (lane > j) {
+                    const double ajk = D[j * PS + lane];
+                    for (int i = j + 1; i <= lane; ++i) D[i * PS + lane] -= D[j * PS + i] * ajk;
                 }
                 __syncwarp();
             }
-            // X = R_pp^-1 (upper), lane k holds column k; R rows broadcast from smem
-            double x[32];
-#pragma unroll
+            // X = R_pp^-1 (upper), lane k computes column k bottom-up
             for (int i = 31; i >= 0; --i) {
                 double s = (lane == i) ? 1.0 : 0.0;
-#pragma unroll
-                for (int l = i + 1; l < 32; ++l) s -= Ps[i * PS + p0 + l] * x[l];
-                x[i] = (lane >= i) ? s / Ps[i * PS + p0 + i] : 0.0;
+                for (int l = i + 1; l <= lane; ++l) s -= D[i * PS + l] * Xs[l * 33 + lane];
+                Xs[i * 33 + lane] = (lane >= i) ? s / D[i * PS + i] : 0.0;
             }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                Xs[i * 33 + lane] = x[i];
-                Dinv[(int64_t)pb * 1024 + i * 32 + lane] = x[i];
-                if (i <= lane) A[(int64_t)(p0 + i) * lda + p0 + lane] = Ps[i * PS + p0 + lane];
-            }
+            __syncwarp();
+            for (int i = 0; i < 32; ++i)
+                if (i <= lane) A[(int64_t)(p0 + i) * lda + p0 + lane] = D[i * PS + lane];
             if (lane == 0 && bad >= 0) {
                 record(p.rank_test ? kRankDeficient : kNotFinite, p0 + bad);
                 fail = 1;
@@ -194,6 +181,15 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                     dst[0] = acc[i][j][0];
                     dst[1] = acc[i][j][1];
                 }
+        }
+        // diagonal block of B: X_pp scaled by 1/d (rows), lower blocks of this row zero
+        for (int e = tid; e < 32 * 32; e += CNT) {
+            const int i = e >> 5, k = e & 31;
+            Bo[(int64_t)(p0 + i) * ldb + p0 + k] = Xs[i * 33 + k] / d[p0 + i];
+        }
+        for (int e = tid; e < 32 * p0; e += CNT) {
+            const int i = e / p0, k = e % p0;
+            Bo[(int64_t)(p0 + i) * ldb + k] = 0.0;
         }
         __syncthreads();
         // ---- (c) trailing update A_{q,r} -= R_{p,q}^T R_{p,r}, p < q <= r
@@ -224,98 +220,45 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         }
         __syncthreads();
     }
-}
-
-// Q = V D^-1 R~^-1, ROWS rows per CTA (8 per warp); the CTA's rows of Q stay in
-// shared memory across panels and the R~ column blocks stream through a
-// cp.async double buffer.
-constexpr int RS = 36;  // padded smem row of a staged 32x32 R block
-
-template <int ROWS>
-__global__ void __launch_bounds__(ROWS * 4) trsm_kernel(TrsmParams p) {
-    constexpr int NTH = ROWS * 4;
-    extern __shared__ __align__(16) double sm[];
-    const int b = blockIdx.y;
-    if (p.status && p.status[b] != kOk) return;
-    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
-    const int P = (c + 31) / 32, cp = P * 32;
-    const int QS = cp + 4;
-    double* Qs = sm;                          // ROWS x QS
-    double* Rs[2] = {sm + ROWS * QS, sm + ROWS * QS + 32 * RS};
-    double* Ts = sm + ROWS * QS + 64 * RS;    // ROWS x RS
-    const int r0 = blockIdx.x * ROWS;
-    if (r0 >= p.n) return;
-    const double* V = p.V + (int64_t)b * p.strideV;
-    double* Q = p.Q + (int64_t)b * p.strideQ;
-    const double* A = p.A + (int64_t)b * p.strideA;
-    const double* Dinv = p.Dinv + (int64_t)b * p.strideDinv;
-    const double* d = p.dscale + (int64_t)b * p.strideD;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, t = lane & 3;
-
-    for (int pb = 0; pb < P; ++pb) {
+    // ---- (d) X = R~^-1 by block back-substitution: X_pq = -X_pp sum_{s=p+1..q} R_ps X_sq.
+    // B holds D^-1 X, so X_sq = d_row * B_sq on read.
+    double* Tw = Ts + warp * 32 * 33;
+    for (int pb = P - 2; pb >= 0; --pb) {
         const int p0 = pb * 32;
-        double acc[4][2];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
-        auto issue = [&](int kb, int buf) {
-            for (int e = tid; e < 32 * 16; e += NTH) {
-                const int k = e >> 4, ch = e & 15;
-                cp_async16(Rs[buf] + k * RS + 2 * ch, A + (int64_t)(kb * 32 + k) * p.lda + p0 + 2 * ch);
+        for (int q = pb + 1 + warp; q < P; q += CW) {
+            const int q0 = q * 32;
+            double acc[4][4][2];
+            zero_acc(acc);
+            for (int s = pb + 1; s <= q; ++s) {
+                const int s0 = s * 32;
+                warp_block_mma(
+                    acc, [&](int m, int k) { return A[(int64_t)(p0 + m) * lda + s0 + k]; },
+                    [&](int k, int n) { return Bo[(int64_t)(s0 + k) * ldb + q0 + n] * d[s0 + k]; }, g, t);
             }
-            cp_async_commit();
-        };
-        // acc = Q_<p * R~_<p,p
-        if (pb > 0) issue(0, 0);
-        int buf = 0;
-        for (int kb = 0; kb < pb; ++kb) {
-            if (kb + 1 < pb) {
-                issue(kb + 1, buf ^ 1);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncthreads();
-            const double* rs = Rs[buf];
 #pragma unroll
-            for (int kk = 0; kk < 32; kk += 4) {
-                const double a = Qs[(8 * warp + g) * QS + kb * 32 + kk + t];
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a, rs[(kk + t) * RS + 8 * j + g]);
-            }
-            __syncthreads();
-            buf ^= 1;
+                for (int j = 0; j < 4; ++j) {
+                    Tw[(8 * i + g) * 33 + 8 * j + 2 * t] = acc[i][j][0];
+                    Tw[(8 * i + g) * 33 + 8 * j + 2 * t + 1] = acc[i][j][1];
+                }
+            __syncwarp();
+            // X_pp from the stored diagonal block of B (row-scaled)
+            zero_acc(acc);
+            warp_block_mma(
+                acc, [&](int m, int k) { return Bo[(int64_t)(p0 + m) * ldb + p0 + k] * d[p0 + m]; },
+                [&](int k, int n) { return Tw[k * 33 + n]; }, g, t);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = p0 + 8 * i + g;
+                    double* dst = Bo + (int64_t)r * ldb + q0 + 8 * j + 2 * t;
+                    dst[0] = -acc[i][j][0] / d[r];
+                    dst[1] = -acc[i][j][1] / d[r];
+                }
         }
-        // T = V_p D_p^-1 - acc  (C-fragment layout: row 8w+g, cols 8j+2t, +1)
-        const int row = r0 + 8 * warp + g;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int col = p0 + 8 * j + 2 * t + q;
-                double v = 0.0;
-                if (row < p.n && col < c) v = V[(int64_t)row * p.ldv + col] / d[col];
-                Ts[(8 * warp + g) * RS + 8 * j + 2 * t + q] = v - acc[j][q];
-            }
-        // X_p = R~_pp^-1 into Rs[0]
-        for (int e = tid; e < 32 * 32; e += NTH) Rs[0][(e >> 5) * RS + (e & 31)] = Dinv[(int64_t)pb * 1024 + e];
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 32; kk += 4) {
-            const double a = Ts[(8 * warp + g) * RS + kk + t];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a, Rs[0][(kk + t) * RS + 8 * j + g]);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int cl = 8 * j + 2 * t + q;
-                Qs[(8 * warp + g) * QS + p0 + cl] = acc[j][q];
-                if (row < p.n && p0 + cl < c) Q[(int64_t)row * p.ldq + p0 + cl] = acc[j][q];
-            }
         __syncthreads();
     }
 }
@@ -367,7 +310,7 @@ void rank_check(const RankCheckParams& p, cudaStream_t st) {
 
 int chol_smem_bytes(int c_cap) {
     const int cp = (c_cap + 31) / 32 * 32;
-    return (32 * (cp + 4) + 32 * 33) * 8;
+    return (32 * (cp + 4) + 32 * 33 + CW * 32 * 33) * 8;
 }
 
 void chol_factor(const CholParams& p, cudaStream_t st) {
@@ -378,33 +321,6 @@ void chol_factor(const CholParams& p, cudaStream_t st) {
         configured = bytes;
     }
     ::smg::count_launch(), chol_kernel<<<p.batch, CNT, bytes, st>>>(p);
-}
-
-static int trsm_rows(int c_cap) { return c_cap <= 256 ? 64 : 32; }
-
-int trsm_smem_bytes(int c_cap) {
-    const int cp = (c_cap + 31) / 32 * 32;
-    const int rows = trsm_rows(c_cap);
-    return (rows * (cp + 4) + 64 * RS + rows * RS) * 8;
-}
-
-void trsm(const TrsmParams& p, cudaStream_t st) {
-    const int bytes = trsm_smem_bytes(p.c_cap);
-    const int rows = trsm_rows(p.c_cap);
-    static int configured[2] = {0, 0};
-    if (rows == 64) {
-        if (bytes > configured[0]) {
-            cudaFuncSetAttribute(trsm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-            configured[0] = bytes;
-        }
-        ::smg::count_launch(), trsm_kernel<64><<<dim3((p.n + 63) / 64, p.batch), 256, bytes, st>>>(p);
-    } else {
-        if (bytes > configured[1]) {
-            cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-            configured[1] = bytes;
-        }
-        ::smg::count_launch(), trsm_kernel<32><<<dim3((p.n + 31) / 32, p.batch), 128, bytes, st>>>(p);
-    }
 }
 
 }  // namespace smg

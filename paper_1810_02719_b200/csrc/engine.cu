@@ -110,7 +110,7 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
         delta.alloc(ntiles, st);
         compute_delta(trace.get(), ntiles, n, shift_scale, delta.get(), st);
     }
-    shift0.alloc(ntiles, st);
+    shift0.alloc((size_t)2 * ntiles, st);  // [shift | Gershgorin upper bound]
     compute_first_shift(rowptr.get(), cols.get(), vals.get(), off.get(), trace.get(), ntiles, n, shift0.get(), st);
 }
 
@@ -166,8 +166,8 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     work.alloc(cc, st);
     // split-K over the n rows for the Gram: aim at ~2 waves of CTAs
     const int tiles = ((ld + 63) / 64) * ((ld + 63) / 64 + 1) / 2;
-    // (a function of the shape only, so results do not depend on the batch size)
-    splits = std::max(1, std::min(npad / 128, 296 / std::max(1, tiles)));
+    // ~4 waves of CTAs, each split at least 256 rows deep
+    splits = std::max(1, std::min(npad / 256, (592 + tiles * B - 1) / std::max(1, tiles * B)));
     Gws.alloc((size_t)B * splits * ld * ld, st);
     rdiag.alloc((size_t)B * ld, st);
     vnorm.alloc(B, st);
@@ -253,28 +253,26 @@ void gram(Workspace& ws, const double* V, int c, const int* dimC, int n, cudaStr
 
 // out = V D^-1 R~^-1 with R~ / Dinv / d from the last chol()
 void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st) {
-    TrsmParams p;
-    p.n = n;
-    p.batch = ws.B;
-    p.c_cap = c;
-    p.V = V;
-    p.ldv = ws.ld;
-    p.strideV = ws.mstride();
-    p.Q = out;
-    p.ldq = ws.ld;
-    p.strideQ = ws.mstride();
-    p.A = ws.work.get();
-    p.lda = ws.ld;
-    p.strideA = (int64_t)ws.ld * ws.ld;
-    p.Dinv = ws.Bm.get();
-    p.strideDinv = (int64_t)ws.ld * ws.ld;
-    p.dscale = ws.rdiag.get();
-    p.strideD = ws.ld;
-    p.dimC = dimC;
-    p.dimStride = 1;
-    p.status = ws.status.get();
+    GemmParams g;
+    g.M = n;
+    g.N = c;
+    g.K = c;
+    g.batch = ws.B;
+    g.A = V;
+    g.lda = ws.ld;
+    g.strideA = ws.mstride();
+    g.B = ws.Bm.get();
+    g.ldb = ws.ld;
+    g.strideB = (int64_t)ws.ld * ws.ld;
+    g.C = out;
+    g.ldc = ws.ld;
+    g.strideC = ws.mstride();
+    g.upperB = 1;
+    g.dimN = dimC;
+    g.dimK = dimC;
+    g.dimStride = 1;
     ProfScope prof("trmm", st);
-    trsm(p, st);
+    gemm(g, false, false, st);
 }
 
 void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_scale, int pos, cudaStream_t st) {
@@ -287,8 +285,9 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
     p.A = ws.work.get();
     p.lda = ws.ld;
     p.strideA = (int64_t)ws.ld * ws.ld;
-    p.Dinv = ws.Bm.get();
-    p.strideDinv = (int64_t)ws.ld * ws.ld;
+    p.Binv = ws.Bm.get();
+    p.ldb = ws.ld;
+    p.strideB = (int64_t)ws.ld * ws.ld;
     p.dscale = ws.rdiag.get();
     p.strideD = ws.ld;
     p.dimC = dimC;

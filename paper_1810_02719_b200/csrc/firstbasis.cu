@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <random>
+#include <string>
 
 #include "engine.h"
 #include "firstbasis.h"
@@ -126,17 +127,74 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
         SMG_CUDA(cudaStreamSynchronize(st));
         fc.shift_hint = s0;
     }
-    int iters_next = (m == n) ? 0 : 6;
+    // Gershgorin upper bounds of L (Chebyshev interval end), per batch entry
+    std::vector<double> upper(ws.B);
+    for (int b = 0; b < ws.B; ++b)
+        SMG_CUDA(cudaMemcpyAsync(&upper[b], ts.shift0.get() + ts.ntiles + tile0 + (int64_t)b * tstride,
+                                 sizeof(double), cudaMemcpyDeviceToHost, st));
+    SMG_CUDA(cudaStreamSynchronize(st));
+    const bool use_cheb = !(std::getenv("SMG_FIRST_BASIS") && std::string(std::getenv("SMG_FIRST_BASIS")) == "si");
+    const int deg = 30;
+    DBuf<double> dcoef;          // [deg][B] alpha | [deg][B] gamma | [B] shift
+    int iters_next = (m == n) ? 0 : (use_cheb ? 4 : 6);
+    int cheb_apps = 0;
     double prev_bound = INFINITY;
     for (int round = 0; round < fc.max_rounds; ++round) {
         const int tk_it = scope.saved ? scope.saved->begin(st) : -1;
-        for (int t = 0; t < iters_next; ++t) {
-            const int z = (round == 0 && t == 0) ? 1 : 2;
-            solve_batch(cx, ws, fs, tile0, tstride, ws.U.get(), ws.V.get(), m, nullptr, z, false);
-            // intermediate iterates only need their span: one CholeskyQR pass;
-            // the iterate entering Rayleigh-Ritz gets the full CholeskyQR2
-            orth_batch(cx, ws, ws.V.get(), ws.U.get(), m, nullptr, false, 0, t + 1 == iters_next ? 2 : 1);
-            rep.iterations += 1;
+        if (cheb_apps > 0) {
+            // Chebyshev-filtered subspace iteration on L (SpMM only): p_d damps
+            // [a, b] = [theta_m, Gershgorin bound] and keeps the bottom of the spectrum
+            double* bufs[3] = {ws.U.get(), ws.V.get(), ws.T.get()};
+            for (int app = 0; app < cheb_apps; ++app) {
+                int x = 0, y = 1;
+                for (int i = 1; i <= deg; ++i) {
+                    const int z = (i == 1) ? 1 : 3 - x - y;
+                    SpmmParams sp;
+                    sp.n = n;
+                    sp.c = m;
+                    sp.batch = ws.B;
+                    sp.rowptr = ts.rowptr.get() + (int64_t)tile0 * (n + 1);
+                    sp.strideRowptr = (int64_t)tstride * (n + 1);
+                    sp.csr_offsets = ts.off.get() + tile0;
+                    sp.offStride = tstride;
+                    sp.cols = ts.cols.get();
+                    sp.vals = ts.vals.get();
+                    sp.shift = dcoef.get() + (size_t)2 * deg * ws.B;
+                    sp.alpha = dcoef.get() + (size_t)(i - 1) * ws.B;
+                    sp.X = bufs[i == 1 ? 0 : y];
+                    sp.ldx = ws.ld;
+                    sp.strideX = ws.mstride();
+                    if (i > 1) {
+                        sp.gamma = dcoef.get() + (size_t)deg * ws.B + (size_t)(i - 1) * ws.B;
+                        sp.Z = bufs[x];
+                        sp.ldz = ws.ld;
+                        sp.strideZ = ws.mstride();
+                    }
+                    sp.Y = bufs[z];
+                    sp.ldy = ws.ld;
+                    sp.strideY = ws.mstride();
+                    spmm(sp, st);
+                    if (i == 1) {
+                        x = 0;
+                        y = 1;
+                    } else {
+                        x = y;
+                        y = z;
+                    }
+                }
+                const bool last = app + 1 == cheb_apps;
+                orth_batch(cx, ws, bufs[y], ws.U.get(), m, nullptr, false, 0, (last || y == 0) ? 2 : 1);
+                rep.iterations += deg;
+            }
+        } else {
+            for (int t = 0; t < iters_next; ++t) {
+                const int z = (round == 0 && t == 0) ? 1 : 2;
+                solve_batch(cx, ws, fs, tile0, tstride, ws.U.get(), ws.V.get(), m, nullptr, z, false);
+                // intermediate iterates only need their span: one CholeskyQR pass;
+                // the iterate entering Rayleigh-Ritz gets the full CholeskyQR2
+                orth_batch(cx, ws, ws.V.get(), ws.U.get(), m, nullptr, false, 0, t + 1 == iters_next ? 2 : 1);
+                rep.iterations += 1;
+            }
         }
         if (tk_it >= 0) scope.saved->end("fb_iterate", tk_it, st);
         const int tk_rr = scope.saved ? scope.saved->begin(st) : -1;
@@ -236,13 +294,54 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
         if (m == n || bound < fc.tol) break;
         if (!(bound < prev_bound * 0.999) && round >= 3) break;  // stagnated at the rounding floor
         prev_bound = bound;
-        // iterations to reach the tolerance at the observed rate (bound shrinks ~rate per step)
-        double need = 4.0;
-        // plan with a pessimistic rate (the early Ritz values overestimate the gap) so
-        // that one more Rayleigh-Ritz round suffices
-        if (worst_rate > 0.0 && worst_rate < 1.0)
-            need = std::log(fc.tol * 0.1 / bound) / std::log(std::pow(worst_rate, 0.85));
-        iters_next = (int)std::min(60.0, std::max(2.0, std::ceil(need)));
+        // Chebyshev plan from the Ritz values: cut a = theta_m, a0 = theta_1
+        cheb_apps = 0;
+        if (use_cheb && c < m) {
+            std::vector<double> coef((size_t)2 * deg * ws.B + ws.B);
+            double worst = 0.0;
+            bool ok = true;
+            for (int b = 0; b < ws.B && ok; ++b) {
+                const double* tb = th.data() + (size_t)b * m;
+                const double a = tb[m - 1], a0 = tb[0], up = upper[b];
+                if (!(up > a && a > a0 && a > tb[c - 1])) {
+                    ok = false;
+                    break;
+                }
+                const double e = 0.5 * (up - a), cen = 0.5 * (up + a);
+                const double sigma1 = e / (a0 - cen), tau = 2.0 / sigma1;
+                double sigma = sigma1;
+                coef[(size_t)0 * ws.B + b] = sigma1 / e;
+                coef[(size_t)deg * ws.B + b] = 0.0;
+                for (int i = 2; i <= deg; ++i) {
+                    const double sn = 1.0 / (tau - sigma);
+                    coef[(size_t)(i - 1) * ws.B + b] = 2.0 * sn / e;
+                    coef[(size_t)deg * ws.B + (size_t)(i - 1) * ws.B + b] = -sigma * sn;
+                    sigma = sn;
+                }
+                coef[(size_t)2 * deg * ws.B + b] = -cen;
+                const double xi = std::fabs((tb[c - 1] - cen) / e);
+                worst = std::max(worst, 1.0 / std::cosh(deg * std::acosh(std::max(xi, 1.0 + 1e-15))));
+            }
+            if (ok && worst < 0.5) {
+                dcoef.upload(coef, st);
+                // a conservative rate: eigenvalues between lambda_m and the cut are
+                // amplified as well, so count each application as sqrt(worst)
+                const double need = std::log(fc.tol * 0.1 / bound) / std::log(std::sqrt(worst));
+                cheb_apps = (int)std::min(8.0, std::max(1.0, std::ceil(need)));
+            }
+        }
+        if (cheb_apps == 0) {
+            // shift-invert iterations to reach the tolerance at the observed rate
+            double need = 4.0;
+            // plan with a pessimistic rate (the early Ritz values overestimate the gap) so
+            // that one more Rayleigh-Ritz round suffices
+            if (worst_rate > 0.0 && worst_rate < 1.0)
+                need = std::log(fc.tol * 0.1 / bound) / std::log(std::pow(worst_rate, 0.85));
+            iters_next = (int)std::min(60.0, std::max(2.0, std::ceil(need)));
+        }
+        if (std::getenv("SMG_DEBUG"))
+            std::fprintf(stderr, "[smg] first_basis plan: chebyshev applications %d (degree %d), si iterations %d\n",
+                         cheb_apps, deg, cheb_apps ? 0 : iters_next);
     }
     return rep;
 }

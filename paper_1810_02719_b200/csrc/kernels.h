@@ -98,8 +98,8 @@ struct CholParams {
     int64_t ldg = 0, strideG = 0;
     double* A = nullptr;  // scaled Gram -> R~ (upper), ld multiple of 32 (>= c rounded to 32)
     int64_t lda = 0, strideA = 0;
-    double* Dinv = nullptr;  // per 32-panel inverse of the diagonal block (32x32 row-major)
-    int64_t strideDinv = 0;
+    double* Binv = nullptr;  // B = D^-1 R~^-1 (upper, lower blocks zero), ld = ldb
+    int64_t ldb = 0, strideB = 0;
     double* dscale = nullptr;  // column norms d_j (rounded-up length)
     int64_t strideD = 0;
     const int* dimC = nullptr;
@@ -113,25 +113,7 @@ struct CholParams {
     int column_scale = 1;
 };
 void chol_factor(const CholParams& p, cudaStream_t st);
-// Q = V D^-1 R~^-1 (rows independent; 32 rows per CTA)
-struct TrsmParams {
-    int n = 0, batch = 1, c_cap = 0;
-    const double* V = nullptr;
-    int64_t ldv = 0, strideV = 0;
-    double* Q = nullptr;
-    int64_t ldq = 0, strideQ = 0;
-    const double* A = nullptr;
-    int64_t lda = 0, strideA = 0;
-    const double* Dinv = nullptr;
-    int64_t strideDinv = 0;
-    const double* dscale = nullptr;
-    int64_t strideD = 0;
-    const int* dimC = nullptr;
-    int64_t dimStride = 0;
-    const int* status = nullptr;
-};
-void trsm(const TrsmParams& p, cudaStream_t st);
-int trsm_smem_bytes(int c_cap);
+int chol_smem_bytes(int c_cap);
 // Accurate reference rank test after CholeskyQR2: |r_kk| = |q_k^T v_k| against
 // 1e-13 ||V||_F (first failing column, sticky status).
 struct RankCheckParams {
@@ -221,6 +203,11 @@ struct SpmmParams {
     const int32_t* cols = nullptr;
     const double* vals = nullptr;
     const double* shift = nullptr;  // per batch diagonal shift (nullptr: 0)
+    // Chebyshev-step form Y = alpha_b (L + shift_b I) X + gamma_b Z (nullptr: alpha 1, no Z term)
+    const double* alpha = nullptr;
+    const double* gamma = nullptr;
+    const double* Z = nullptr;
+    int64_t ldz = 0, strideZ = 0;
     const double* X = nullptr;
     int64_t ldx = 0, strideX = 0;
     double* Y = nullptr;

@@ -18,7 +18,8 @@ namespace smg {
 
 namespace {
 
-constexpr int NT = 128;
+constexpr int NT = 256;
+constexpr int kSolveWarps = NT / 32;
 
 template <int W, int CS>
 struct SolveSmem {
@@ -42,9 +43,14 @@ SMG_DEV void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
 template <int W, int CS>
 struct SolveTiling {
     static constexpr int MT_ALL = W / 8, NT_ALL = CS / 8;
-    static constexpr int WM = (MT_ALL % 4 == 0) ? 4 : ((MT_ALL % 2 == 0) ? 2 : 1);
-    static constexpr int WN_RAW = 4 / WM;
-    static constexpr int WN = (NT_ALL % WN_RAW == 0) ? WN_RAW : ((WN_RAW >= 2 && NT_ALL % 2 == 0) ? 2 : 1);
+    // 8 warps (two per SM sub-partition hide the DMMA issue latency); prefer a
+    // 4 x 2 warp grid, a full m-column of warps when there is one n-tile
+    static constexpr int NW = kSolveWarps;
+    static constexpr int WM = (NT_ALL == 1) ? (MT_ALL < NW ? MT_ALL : NW)
+                                            : ((MT_ALL % 4 == 0) ? 4 : ((MT_ALL % 2 == 0) ? 2 : 1));
+    static constexpr int WN_RAW = NW / WM;
+    static constexpr int WN = (NT_ALL % WN_RAW == 0) ? WN_RAW
+                                                     : ((NT_ALL % 4 == 0 && WN_RAW >= 4) ? 4 : ((NT_ALL % 2 == 0 && WN_RAW >= 2) ? 2 : 1));
     static constexpr int MT = MT_ALL / WM, NT = NT_ALL / WN;
     static constexpr int ACTIVE = WM * WN;
 };

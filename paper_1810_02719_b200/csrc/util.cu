@@ -115,11 +115,16 @@ __global__ void __launch_bounds__(SPMM_NT) spmm_kernel(SpmmParams p) {
     const double shift = p.shift ? p.shift[b] : 0.0;
     const double* X = p.X + (int64_t)b * p.strideX;
     double* Y = p.Y + (int64_t)b * p.strideY;
+    const double alpha = p.alpha ? p.alpha[b] : 1.0;
+    const double gam = p.gamma ? p.gamma[b] : 0.0;
+    const double* Zb = p.Z ? p.Z + (int64_t)b * p.strideZ : nullptr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i = blockIdx.x * SPMM_ROWS + warp;
+    int s = 0, nzt = 0;
     if (i < p.n) {
-        const int s = rowptr[i], e = rowptr[i + 1];
-        const int nz = min(e - s, SPMM_MAXNZ);
+        s = rowptr[i];
+        nzt = rowptr[i + 1] - s;
+        const int nz = min(nzt, SPMM_MAXNZ);
         for (int q = lane; q < nz; q += 32) {
             scol[warp][q] = cols[s + q];
             sval[warp][q] = vals[s + q] + (cols[s + q] == i ? shift : 0.0);
@@ -129,6 +134,11 @@ __global__ void __launch_bounds__(SPMM_NT) spmm_kernel(SpmmParams p) {
     __syncthreads();
     if (i >= p.n) return;
     const int nz = snz[warp];
+    // entries past the staged ones (rows with > SPMM_MAXNZ neighbours) come from L2
+    auto col_of = [&](int q) { return q < SPMM_MAXNZ ? scol[warp][q] : cols[s + q]; };
+    auto val_of = [&](int q) {
+        return q < SPMM_MAXNZ ? sval[warp][q] : vals[s + q] + (cols[s + q] == i ? shift : 0.0);
+    };
     if ((c & 1) == 0 && (p.ldx & 1) == 0 && (p.ldy & 1) == 0) {
         for (int j = 2 * lane; j < c; j += 64) {
             double2 acc = make_double2(0.0, 0.0);
@@ -138,12 +148,27 @@ __global__ void __launch_bounds__(SPMM_NT) spmm_kernel(SpmmParams p) {
                 acc.x = fma(v, x.x, acc.x);
                 acc.y = fma(v, x.y, acc.y);
             }
+            for (int q = nz; q < nzt; ++q) {
+                const double v = val_of(q);
+                const double2 x = *reinterpret_cast<const double2*>(X + (int64_t)col_of(q) * p.ldx + j);
+                acc.x = fma(v, x.x, acc.x);
+                acc.y = fma(v, x.y, acc.y);
+            }
+            acc.x *= alpha;
+            acc.y *= alpha;
+            if (Zb) {
+                const double2 z = *reinterpret_cast<const double2*>(Zb + (int64_t)i * p.ldz + j);
+                acc.x = fma(gam, z.x, acc.x);
+                acc.y = fma(gam, z.y, acc.y);
+            }
             *reinterpret_cast<double2*>(Y + (int64_t)i * p.ldy + j) = acc;
         }
     } else {
         for (int j = lane; j < c; j += 32) {
             double acc = 0.0;
-            for (int q = 0; q < nz; ++q) acc = fma(sval[warp][q], X[(int64_t)scol[warp][q] * p.ldx + j], acc);
+            for (int q = 0; q < nzt; ++q) acc = fma(val_of(q), X[(int64_t)col_of(q) * p.ldx + j], acc);
+            acc *= alpha;
+            if (Zb) acc = fma(gam, Zb[(int64_t)i * p.ldz + j], acc);
             Y[(int64_t)i * p.ldy + j] = acc;
         }
     }
