@@ -296,7 +296,7 @@ public:
         tm.add(kStLaplacian, t0, t_lap);
         prepare_outputs([&](int b, int id) { return sizes_[segs_[b].pos_of[id]]; });
         build_pointer_tables();
-        const int fb_m = std::min(n_, round_up(sizes_[0] + std::max(16, sizes_[0] / 2), 8));
+        const int fb_m = first_basis_width(n_, sizes_[0]);
         ws_.init(B_, n_, ts_.npad, std::max(ccap, fb_m), st_);
         StepCtx cx{st_, &ts_};
         check_assembly();
@@ -450,7 +450,7 @@ public:
         setup_tiles();
         const int t_lap = tm.mark();
         sizes_.assign(K_, 0);
-        const int fb_m = std::min(n_, round_up(c0 + std::max(16, c0 / 2), 8));
+        const int fb_m = first_basis_width(n_, c0);
         ws_.init(1, n_, ts_.npad, std::max(c_max + 1, fb_m), st_);
         StepCtx cx{st_, &ts_};
         check_assembly();

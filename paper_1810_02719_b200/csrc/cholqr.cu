@@ -14,7 +14,7 @@
 //
 // chol_kernel: one CTA per chain, right-looking blocked Cholesky with 32-wide
 // panels; the panel row sits in shared memory, its 32x32 diagonal block is
-// factored and inverted by one warp in shared memory, the panel row solve and
+// factored and inverted by all threads (one barrier per column), the panel row solve and
 // the trailing SYRK are 32x32x32 DMMA blocks on all warps; finally the block
 // upper-triangular inverse X = R~^-1 is formed by block back-substitution
 // (DMMA) and stored row-scaled as B = D^-1 X.
@@ -27,6 +27,8 @@ namespace {
 
 constexpr int CNT = 256;
 constexpr int CW = CNT / 32;
+constexpr int XS = 36;
+constexpr int kMaxPanels = 16;  // c <= 512 (the library-wide column limit)  // 32-wide block stride (% 16 == 4: conflict-free fragments)
 
 // 32x32x32 block product on one warp: acc(4x4 tiles of 8x8, 2 values) += op(A) * B
 // with op(A)[m][k] = a(m, k), B[k][n] = b(k, n) supplied as functors.
@@ -53,8 +55,33 @@ SMG_DEV void zero_acc(double (&acc)[4][4][2]) {
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 }
 
+// Upper-triangle element ownership for the 32x32 diagonal block: the 528
+// elements (i <= k) are enumerated row by row and thread t owns e = t, t + 256,
+// t + 512 (at most three).
+struct DiagOwn {
+    int n = 0;
+    int i[3], k[3];
+    SMG_DEV void init(int tid) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            int e = tid + q * CNT;
+            i[q] = k[q] = 0;
+            if (e >= 528) continue;
+            int r = 0;
+            while (e >= 32 - r) {
+                e -= 32 - r;
+                ++r;
+            }
+            i[q] = r;
+            k[q] = r + e;
+            n = q + 1;
+        }
+    }
+};
+
 __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     __shared__ double red[32];
+    __shared__ double pivs[32];
     __shared__ int fail;
     extern __shared__ __align__(16) double psm[];
     const int b = blockIdx.x;
@@ -68,10 +95,12 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     const int64_t lda = p.lda, ldb = p.ldb;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int PS = cp + 4;         // panel row stride (% 16 == 4: conflict-free fragments)
-    double* Ps = psm;              // 32 x PS panel row
-    double* Xs = psm + 32 * PS;    // 32 x 33 diagonal-block inverse
-    double* Ts = Xs + 32 * 33;     // CW x 32 x 33 per-warp staging
+    const int PS = cp + 4;             // panel row stride (% 16 == 4: conflict-free fragments)
+    double* Ps = psm;                  // 32 x PS panel row
+    double* Xs = psm + 32 * PS;        // 32 x XS diagonal-block inverse
+    double* Ts = Xs + 32 * XS;         // CW x 32 x XS per-warp staging
+    double* ds = Ts + CW * 32 * XS;    // d_j (cp)
+    double* rds = ds + cp;             // 1 / d_j (cp)
 
     double tr = 0.0;
     for (int j = tid; j < cp; j += CNT) {
@@ -82,6 +111,8 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             dj = p.column_scale ? sqrt(gjj) : 1.0;
         }
         d[j] = dj;
+        ds[j] = dj;
+        rds[j] = dj > 0.0 ? 1.0 / dj : 0.0;
     }
     tr = block_sum(tr, red);
     const double scale = sqrt(tr);
@@ -100,74 +131,98 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     }
     const double thresh = 1e-13 * scale;
     __syncthreads();
-    // A = D^-1 G D^-1 (upper triangle incl. full diagonal blocks); identity padding
-    for (int e = tid; e < cp * cp; e += CNT) {
-        const int i = e / cp, k = e % cp;
-        if ((k >> 5) < (i >> 5)) continue;
-        double v;
-        if (i < c && k < c) {
-            const double di = d[i], dk = d[k];
-            v = (di > 0.0 && dk > 0.0) ? G[(int64_t)i * p.ldg + k] / di / dk : 0.0;
-        } else {
-            v = (i == k) ? 1.0 : 0.0;
+    // A = D^-1 G D^-1 (upper triangle incl. full diagonal 32-blocks); identity padding
+    for (int i = warp; i < cp; i += CW) {
+        const double ri = rds[i];
+        const int k0 = (i & ~31) + lane;
+        double v[kMaxPanels];
+#pragma unroll
+        for (int u = 0; u < kMaxPanels; ++u) {  // all loads of the row in flight at once
+            const int k = k0 + 32 * u;
+            v[u] = (k < cp && i < c && k < c) ? G[(int64_t)i * p.ldg + k] : 0.0;
         }
-        A[(int64_t)i * lda + k] = v;
+#pragma unroll
+        for (int u = 0; u < kMaxPanels; ++u) {
+            const int k = k0 + 32 * u;
+            if (k < cp) A[(int64_t)i * lda + k] = (i < c && k < c) ? v[u] * ri * rds[k] : (i == k ? 1.0 : 0.0);
+        }
     }
+    DiagOwn own;
+    own.init(tid);
     __syncthreads();
 
     for (int pb = 0; pb < P; ++pb) {
         const int p0 = pb * 32;
-        for (int e = tid; e < 32 * (cp - p0); e += CNT) {
-            const int r = e / (cp - p0), k = p0 + e % (cp - p0);
-            Ps[r * PS + k] = A[(int64_t)(p0 + r) * lda + k];
-        }
+        for (int r = warp; r < 32; r += CW)
+            for (int k = p0 + lane; k < cp; k += 32) Ps[r * PS + k] = A[(int64_t)(p0 + r) * lda + k];
         __syncthreads();
-        // ---- (a) factor + invert the diagonal block: warp 0, lane k owns column k
-        if (warp == 0) {
-            int bad = -1;
-            double* D = Ps + p0;  // D[i * PS + k]
-            for (int j = 0; j < 32; ++j) {
-                const double piv = D[j * PS + j];
+        // ---- (a) factor the diagonal block with all threads (right-looking, LDL^T
+        // form: the pivots are kept and the rows scaled at the end), then invert it.
+        double* D = Ps + p0;  // D[i * PS + k]
+        for (int j = 0; j < 32; ++j) {
+            const double pj = D[j * PS + j];
+            if (tid == 0) {
+                pivs[j] = pj;
                 const int gj = p0 + j;
-                if (bad < 0 && gj < c) {
-                    const bool bp = !(piv > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(piv) || !(d[gj] > 0.0);
-                    const double rkk = bp ? 0.0 : sqrt(piv) * d[gj];
-                    if (bp || (p.rank_test && rkk < thresh)) bad = j;
+                if (!fail && gj < c) {
+                    const bool bp = !(pj > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(pj) || !(ds[gj] > 0.0);
+                    const double rkk = bp ? 0.0 : sqrt(pj) * ds[gj];
+                    if (bp || (p.rank_test && rkk < thresh)) {
+                        record(p.rank_test ? kRankDeficient : kNotFinite, gj);
+                        fail = 1;
+                    }
                 }
-                const double rjj = sqrt(fmax(piv, 1e-300));
-                __syncwarp();
-                if (lane > j) D[j * PS + lane] /= rjj;
-                if (lane == j) D[j * PS + j] = rjj;
-                __syncwarp();
-                if (lane > j) {
-                    const double ajk = D[j * PS + lane];
-                    for (int i = j + 1; i <= lane; ++i) D[i * PS + lane] -= D[j * PS + i] * ajk;
+            }
+            const double inv = 1.0 / fmax(pj, 1e-300);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (q < own.n && own.i[q] > j) {
+                    const double l = D[j * PS + own.i[q]] * inv;
+                    D[own.i[q] * PS + own.k[q]] = fma(-l, D[j * PS + own.k[q]], D[own.i[q] * PS + own.k[q]]);
                 }
-                __syncwarp();
             }
-            // X = R_pp^-1 (upper), lane k computes column k bottom-up
-            for (int i = 31; i >= 0; --i) {
-                double s = (lane == i) ? 1.0 : 0.0;
-                for (int l = i + 1; l <= lane; ++l) s -= D[i * PS + l] * Xs[l * 33 + lane];
-                Xs[i * 33 + lane] = (lane >= i) ? s / D[i * PS + i] : 0.0;
-            }
-            __syncwarp();
-            for (int i = 0; i < 32; ++i)
-                if (i <= lane) A[(int64_t)(p0 + i) * lda + p0 + lane] = D[i * PS + lane];
-            if (lane == 0 && bad >= 0) {
-                record(p.rank_test ? kRankDeficient : kNotFinite, p0 + bad);
-                fail = 1;
+            __syncthreads();
+        }
+        if (fail) return;
+        // rows scaled: R[i][k] = D[i][k] / sqrt(piv_i); X = R^-1 accumulators
+        double xacc[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            xacc[q] = 0.0;
+            if (q < own.n) {
+                const int i = own.i[q], k = own.k[q];
+                const double rii = sqrt(fmax(pivs[i], 1e-300));
+                const double r = (i == k) ? rii : D[i * PS + k] / rii;
+                D[i * PS + k] = r;
+                A[(int64_t)(p0 + i) * lda + p0 + k] = r;
+                xacc[q] = (i == k) ? 1.0 : 0.0;
             }
         }
+        for (int e = tid; e < 32 * 32; e += CNT) {
+            const int i = e >> 5, k = e & 31;
+            if (i > k) Xs[i * XS + k] = 0.0;
+        }
         __syncthreads();
-        if (fail) return;
+        // X = R_pp^-1 by rows, bottom-up: X[l][k] = acc / R[l][l], then
+        // acc[i][k] -= R[i][l] X[l][k] for i < l <= k
+        for (int l = 31; l >= 0; --l) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (q < own.n && own.i[q] == l) Xs[l * XS + own.k[q]] = xacc[q] / D[l * PS + l];
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (q < own.n && own.i[q] < l && own.k[q] >= l)
+                    xacc[q] = fma(-D[own.i[q] * PS + l], Xs[l * XS + own.k[q]], xacc[q]);
+        }
+        __syncthreads();
         // ---- (b) panel row R_{p,q} = X^T A_{p,q}, q > p (smem operands, written back to smem and L2)
         for (int q = pb + 1 + warp; q < P; q += CW) {
             const int q0 = q * 32;
             double acc[4][4][2];
             zero_acc(acc);
             warp_block_mma(
-                acc, [&](int m, int k) { return Xs[k * 33 + m]; }, [&](int k, int n) { return Ps[k * PS + q0 + n]; },
+                acc, [&](int m, int k) { return Xs[k * XS + m]; }, [&](int k, int n) { return Ps[k * PS + q0 + n]; },
                 g, t);
             __syncwarp();
 #pragma unroll
@@ -183,13 +238,9 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                 }
         }
         // diagonal block of B: X_pp scaled by 1/d (rows), lower blocks of this row zero
-        for (int e = tid; e < 32 * 32; e += CNT) {
-            const int i = e >> 5, k = e & 31;
-            Bo[(int64_t)(p0 + i) * ldb + p0 + k] = Xs[i * 33 + k] / d[p0 + i];
-        }
-        for (int e = tid; e < 32 * p0; e += CNT) {
-            const int i = e / p0, k = e % p0;
-            Bo[(int64_t)(p0 + i) * ldb + k] = 0.0;
+        for (int r = warp; r < 32; r += CW) {
+            Bo[(int64_t)(p0 + r) * ldb + p0 + lane] = Xs[r * XS + lane] * rds[p0 + r];
+            for (int k = lane; k < p0; k += 32) Bo[(int64_t)(p0 + r) * ldb + k] = 0.0;
         }
         __syncthreads();
         // ---- (c) trailing update A_{q,r} -= R_{p,q}^T R_{p,r}, p < q <= r
@@ -204,7 +255,15 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             }
             const int qq = pb + 1 + q, rr = qq + acc_e;
             const int q0 = qq * 32, r0 = rr * 32;
-            double acc[4][4][2];
+            double acc[4][4][2], old[4][4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)  // the block's current values load while the product runs
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double2 o = *reinterpret_cast<const double2*>(A + (int64_t)(q0 + 8 * i + g) * lda + r0 + 8 * j + 2 * t);
+                    old[i][j][0] = o.x;
+                    old[i][j][1] = o.y;
+                }
             zero_acc(acc);
             warp_block_mma(
                 acc, [&](int m, int k) { return Ps[k * PS + q0 + m]; },
@@ -213,51 +272,60 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    double* dst = A + (int64_t)(q0 + 8 * i + g) * lda + r0 + 8 * j + 2 * t;
-                    dst[0] -= acc[i][j][0];
-                    dst[1] -= acc[i][j][1];
+                    double2* dst = reinterpret_cast<double2*>(A + (int64_t)(q0 + 8 * i + g) * lda + r0 + 8 * j + 2 * t);
+                    *dst = make_double2(old[i][j][0] - acc[i][j][0], old[i][j][1] - acc[i][j][1]);
                 }
         }
         __syncthreads();
     }
     // ---- (d) X = R~^-1 by block back-substitution: X_pq = -X_pp sum_{s=p+1..q} R_ps X_sq.
-    // B holds D^-1 X, so X_sq = d_row * B_sq on read.
-    double* Tw = Ts + warp * 32 * 33;
+    // B holds D^-1 X, so X_sq = d_row * B_sq on read.  R's panel row and X_pp sit
+    // in shared memory; each X_sq block is staged into the warp's buffer with
+    // one coalesced burst before its DMMA block product.
+    double* Tw = Ts + warp * 32 * XS;
     for (int pb = P - 2; pb >= 0; --pb) {
         const int p0 = pb * 32;
+        for (int r = warp; r < 32; r += CW) {
+            for (int k = p0 + lane; k < cp; k += 32) Ps[r * PS + k] = A[(int64_t)(p0 + r) * lda + k];
+            Xs[r * XS + lane] = Bo[(int64_t)(p0 + r) * ldb + p0 + lane] * ds[p0 + r];
+        }
+        __syncthreads();
         for (int q = pb + 1 + warp; q < P; q += CW) {
             const int q0 = q * 32;
             double acc[4][4][2];
             zero_acc(acc);
             for (int s = pb + 1; s <= q; ++s) {
                 const int s0 = s * 32;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 32; ++k) Tw[k * XS + lane] = Bo[(int64_t)(s0 + k) * ldb + q0 + lane] * ds[s0 + k];
+                __syncwarp();
                 warp_block_mma(
-                    acc, [&](int m, int k) { return A[(int64_t)(p0 + m) * lda + s0 + k]; },
-                    [&](int k, int n) { return Bo[(int64_t)(s0 + k) * ldb + q0 + n] * d[s0 + k]; }, g, t);
+                    acc, [&](int m, int k) { return Ps[m * PS + s0 + k]; }, [&](int k, int n) { return Tw[k * XS + n]; },
+                    g, t);
             }
+            __syncwarp();
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    Tw[(8 * i + g) * 33 + 8 * j + 2 * t] = acc[i][j][0];
-                    Tw[(8 * i + g) * 33 + 8 * j + 2 * t + 1] = acc[i][j][1];
+                    Tw[(8 * i + g) * XS + 8 * j + 2 * t] = acc[i][j][0];
+                    Tw[(8 * i + g) * XS + 8 * j + 2 * t + 1] = acc[i][j][1];
                 }
             __syncwarp();
-            // X_pp from the stored diagonal block of B (row-scaled)
             zero_acc(acc);
             warp_block_mma(
-                acc, [&](int m, int k) { return Bo[(int64_t)(p0 + m) * ldb + p0 + k] * d[p0 + m]; },
-                [&](int k, int n) { return Tw[k * 33 + n]; }, g, t);
-            __syncwarp();
+                acc, [&](int m, int k) { return Xs[m * XS + k]; }, [&](int k, int n) { return Tw[k * XS + n]; }, g, t);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int r = p0 + 8 * i + g;
                     double* dst = Bo + (int64_t)r * ldb + q0 + 8 * j + 2 * t;
-                    dst[0] = -acc[i][j][0] / d[r];
-                    dst[1] = -acc[i][j][1] / d[r];
+                    dst[0] = -acc[i][j][0] * rds[r];
+                    dst[1] = -acc[i][j][1] * rds[r];
                 }
+            __syncwarp();
         }
         __syncthreads();
     }
@@ -310,7 +378,7 @@ void rank_check(const RankCheckParams& p, cudaStream_t st) {
 
 int chol_smem_bytes(int c_cap) {
     const int cp = (c_cap + 31) / 32 * 32;
-    return (32 * (cp + 4) + 32 * 33 + CW * 32 * 33) * 8;
+    return (32 * (cp + 4) + 32 * XS + CW * 32 * XS + 2 * cp) * 8;
 }
 
 void chol_factor(const CholParams& p, cudaStream_t st) {

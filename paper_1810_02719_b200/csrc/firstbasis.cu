@@ -99,7 +99,8 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
         return rep;
     }
 
-    const int m = std::min(n, round_up(c + std::max(16, c / 2), 8));
+    const int m = first_basis_width(n, c);
+    require(m <= kFirstBasisMaxCols, "first-submesh subspace size exceeds the GPU limit of 480");
     require(m <= ws.ccap, "internal: workspace too small for the first-basis subspace");
     FactorSet fs;
     fs.factor(ts, tile0, (ws.B - 1) * tstride + 1, ts.shift0.get(), st);

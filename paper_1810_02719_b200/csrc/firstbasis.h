@@ -3,6 +3,7 @@
 
 #include <stdint.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "engine.h"
@@ -25,6 +26,14 @@ struct FirstBasisReport {
     double bound = 0.0;
     bool cold = false;
 };
+
+// Columns of the first-basis subspace: c plus max(16, c/2) guard columns,
+// capped at the 480-column limit of the cluster Jacobi (16 CTAs x 2 blocks of 15).
+constexpr int kFirstBasisMaxCols = 480;
+inline int first_basis_width(int n, int c) {
+    const int want = round_up(c + std::max(16, c / 2), 8);
+    return std::min(n, std::max(c, std::min(kFirstBasisMaxCols, want)));
+}
 
 std::vector<double> gaussian_block_colmajor(int rows, int cols, uint64_t seed);
 // Writes the first basis (n x c, row-major, unsigned columns) into ws.U for every

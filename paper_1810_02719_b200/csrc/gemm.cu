@@ -91,6 +91,20 @@ __global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p) {
 
     // op(A) element (m, k): TA ? A[k*lda + m] : A[m*lda + k]  -> k-major iff TA
     // op(B) element (k, n): TB ? B[n*ldb + k] : B[k*ldb + n]  -> k-major iff !TB
+    // fragments (8x8 of the warp's 32x32) that carry no output are skipped on the
+    // DMMA pipe: rows >= M, cols >= N, and for syrkUpper the 32-blocks below the
+    // diagonal (the Cholesky reads the upper triangle incl. full 32x32 diagonal blocks)
+    unsigned fmask = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = m0 + wm + 8 * i, cc = n0 + wn + 8 * j;
+            bool on = r < M && cc < N;
+            if (p.syrkUpper && (r >> 5) > (cc >> 5)) on = false;
+            if (on) fmask |= 1u << (4 * i + j);
+        }
+
     TileLoader<TA> la;
     TileLoader<!TB> lb;
     int buf = 0;
@@ -116,10 +130,17 @@ __global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p) {
             for (int i = 0; i < 4; ++i) a[i] = as[(kk + t) * SP + wm + 8 * i + g];
 #pragma unroll
             for (int j = 0; j < 4; ++j) bb[j] = bs[(kk + t) * SP + wn + 8 * j + g];
+            unsigned m = fmask;
+            if (p.upperB) {  // B[k][col] = 0 for k > col: fragment column block must reach k0 + kk
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (n0 + wn + 8 * j + 7 < k0 + kk) m &= ~(0x1111u << j);
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+                for (int j = 0; j < 4; ++j)
+                    if (m & (1u << (4 * i + j))) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
         }
         if (more) {
             la.store(As[buf ^ 1]);

@@ -248,7 +248,7 @@ JacobiPlan jacobi_plan(int m) {
     auto fits = [&](int ncv) {
         const int b = (m + 2 * ncv - 1) / (2 * ncv);
         const int mp = ((2 * ncv * b) + 7) / 8 * 8;
-        return (int64_t)4 * b * mp * 8 <= 200 * 1024;
+        return (int64_t)4 * b * mp * 8 <= 227 * 1024;
     };
     while (nc < 16 && !fits(nc)) nc *= 2;
     pl.nc = nc;

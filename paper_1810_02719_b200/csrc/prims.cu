@@ -290,7 +290,7 @@ smg_status smg_bottom_subspace(smg_context* ctx, const smg_operator* op, int32_t
         require(c >= 1 && c <= op->n, "subspace size out of range");
         const cudaStream_t st = ctx->stream;
         const int n = op->n;
-        const int m = std::min(n, round_up(c + std::max(16, c / 2), 8));
+        const int m = first_basis_width(n, c);
         require(m <= 512, "subspace size exceeds the GPU limit");
         Workspace ws;
         ws.init(1, n, op->ts.npad, m, st);

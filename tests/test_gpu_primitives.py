@@ -123,6 +123,16 @@ def test_orthonormalize_rank_deficiency_error_parity(ctx, col):
     assert str(eg.value) == str(eo.value) == f"orthonormalize: block is rank deficient at column {col}"
 
 
+@pytest.mark.parametrize("c", [33, 300, 512])
+def test_orthonormalize_wide_blocks(ctx, c):
+    """Multi-panel CholeskyQR2 up to the 512-column limit, graded column norms."""
+    rng = np.random.default_rng(c)
+    b = rng.standard_normal((2048, c)) * np.logspace(0, -6, c)
+    q = G.orthonormalize(b, ctx=ctx)
+    assert np.abs(q.T @ q - np.eye(c)).max() < 1e-12
+    assert np.abs(q - O.orthonormalize(b)).max() < 1e-10
+
+
 def test_orthonormalize_errors(ctx):
     with pytest.raises(G.SpecmeshError, match=r"rank deficient \(all zero\)"):
         G.orthonormalize(np.zeros((5, 2)), ctx=ctx)
@@ -145,7 +155,8 @@ def test_orthogonal_iteration(ctx, grid):
         G.orthogonal_iteration(g, init, -1)
 
 
-@pytest.mark.parametrize("case,c", [("grid", 40), ("grid", 100), ("sphere", 60), ("wide", 200)])
+@pytest.mark.parametrize("case,c", [("grid", 40), ("grid", 100), ("sphere", 60), ("wide", 200), ("grid", 400),
+                                    ("wide", 440)])
 def test_first_basis_matches_dense_eig(ctx, grid, sphere, case, c):
     """bottom_subspace(dense_eigendecomposition(L), c) (spectral.hpp:92-117)."""
     if case == "wide":
