@@ -301,7 +301,7 @@ public:
         StepCtx cx{st_, &ts_};
         check_assembly();
         // chain groups
-        int G = B_ >= 16 ? 2 : 1;
+        int G = B_ >= 4 ? 2 : 1;
         if (const char* e = std::getenv("SMG_GROUPS")) G = std::max(1, std::min(B_, std::atoi(e)));
         std::vector<Group> grp(G);
         for (int g = 0; g < G; ++g) {

@@ -131,6 +131,29 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     }
     const double thresh = 1e-13 * scale;
     __syncthreads();
+    if (p.near_identity) {
+        double e = 0.0;
+        for (int i = warp; i < c; i += CW)
+            for (int k = i + lane; k < c; k += 32) {
+                const double x = fabs(fma(G[(int64_t)i * p.ldg + k] * rds[i], rds[k], (i == k) ? -1.0 : 0.0));
+                e = (x <= e) ? e : (x == x ? x : INFINITY);  // NaN -> full path
+            }
+        for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+        if (lane == 0) red[warp] = e;
+        __syncthreads();
+        e = red[0];
+        for (int w = 1; w < CW; ++w) e = fmax(e, red[w]);
+        if (e <= 1e-9) {
+            for (int i = warp; i < cp; i += CW)
+                for (int k = lane; k < cp; k += 32) {
+                    double v = (k == i) ? 1.0 : 0.0;
+                    if (k > i && k < c) v = -G[(int64_t)i * p.ldg + k] * rds[i] * rds[k];
+                    Bo[(int64_t)i * ldb + k] = v * rds[i];
+                }
+            return;
+        }
+        __syncthreads();
+    }
     // A = D^-1 G D^-1 (upper triangle incl. full diagonal 32-blocks); identity padding
     for (int i = warp; i < cp; i += CW) {
         const double ri = rds[i];
@@ -332,7 +355,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
 }
 
 // partial diag(Q^T V) over a chunk of rows, threads over columns (coalesced rows)
-constexpr int RC_ROWS = 128;
+constexpr int RC_ROWS = 32;
 __global__ void rank_partial_kernel(RankCheckParams p) {
     const int b = blockIdx.y, chunk = blockIdx.x;
     if (p.status[b] != kOk) return;

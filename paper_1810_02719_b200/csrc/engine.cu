@@ -171,7 +171,7 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     Gws.alloc((size_t)B * splits * ld * ld, st);
     rdiag.alloc((size_t)B * ld, st);
     vnorm.alloc(B, st);
-    rpart.alloc((size_t)B * ((npad + 127) / 128) * ld, st);
+    rpart.alloc((size_t)B * ((npad + 31) / 32) * ld, st);  // rank_check chunks of 32 rows
     coeff.alloc((size_t)B * ld * 4, st);
     sign.alloc((size_t)B * ld, st);
     e.alloc((size_t)B * npad, st);
@@ -275,7 +275,8 @@ void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, i
     gemm(g, false, false, st);
 }
 
-void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_scale, int pos, cudaStream_t st) {
+void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_scale, int pos, cudaStream_t st,
+          bool near_identity = false) {
     CholParams p;
     p.batch = ws.B;
     p.c_cap = c;
@@ -299,6 +300,7 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
     p.rank_test = rank_test ? 1 : 0;
     p.column_scale = column_scale ? 1 : 0;
     p.vnorm = rank_test ? ws.vnorm.get() : nullptr;
+    p.near_identity = near_identity ? 1 : 0;
     ProfScope prof("chol", st);
     chol_factor(p, st);
 }
@@ -323,7 +325,7 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
     }
     trmm(ws, in, ws.R.get(), c, dimC, n, cx.st);
     gram(ws, ws.R.get(), c, dimC, n, cx.st);
-    chol(ws, c, dimC, false, true, pos, cx.st);
+    chol(ws, c, dimC, false, true, pos, cx.st, true);
     trmm(ws, ws.R.get(), out, c, dimC, n, cx.st);
     if (rank_test) {
         RankCheckParams r;

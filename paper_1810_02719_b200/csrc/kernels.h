@@ -111,6 +111,10 @@ struct CholParams {
     double* vnorm = nullptr;         // ||V||_F per batch entry (rank-test scale)
     int rank_test = 1;
     int column_scale = 1;
+    // second CholeskyQR pass: when max|G~ - I| <= 1e-9 the factor is taken to
+    // first order, R~ = I + triu(G~ - I, 1) (error O(|E|^2) <= c * 1e-18), and
+    // B = D^-1 (I - triu(G~ - I, 1)) is written without the serial Cholesky
+    int near_identity = 0;
 };
 void chol_factor(const CholParams& p, cudaStream_t st);
 int chol_smem_bytes(int c_cap);
