@@ -30,7 +30,7 @@ struct FactorSmem {
     static constexpr int LD = W + 4;  // LD % 16 == 4: conflict-free DMMA fragment reads
     static constexpr int MAT = W * LD;
     static int bytes(int n) {
-        return (4 * MAT + 2 * W + 32) * 8 + ((n + 1) & ~1) * 4 + W * MAXCPL * (8 + 4) + W * 4;
+        return (4 * MAT + 4 * W + 32) * 8 + ((n + 1) & ~1) * 4 + W * MAXCPL * (8 + 4) + W * 4;
     }
 };
 
@@ -79,8 +79,10 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
     double* Lc = sm + 3 * MAT;   // Linv_k
     double* sig = sm + 4 * MAT;  // Sigma_k
     double* sigp = sig + W;      // Sigma_{k-1}
-    int* flag = reinterpret_cast<int*>(sigp + W);
-    int* ipos = reinterpret_cast<int*>(sigp + W + 32);
+    double* piv = sigp + W;      // pivots of the current block
+    double* rsc = piv + W;       // 1 / (l_jj sigma_j)
+    int* flag = reinterpret_cast<int*>(rsc + W);
+    int* ipos = reinterpret_cast<int*>(rsc + W + 32);
     double* cval = reinterpret_cast<double*>(ipos + ((p.n + 1) & ~1));  // [W][MAXCPL]
     int* cidx = reinterpret_cast<int*>(cval + W * MAXCPL);             // [W][MAXCPL]
     int* ccnt = cidx + W * MAXCPL;                                     // [W]
@@ -104,6 +106,22 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
 
     for (int i = tid; i < n; i += NT) ipos[perm ? perm[i] : i] = i;
     if (tid == 0) flag[0] = 0;
+    // ownership of the W x W upper triangle (a <= b), enumerated row by row
+    constexpr int NOWN = (W * (W + 1) / 2 + NT - 1) / NT;
+    int own_a[NOWN], own_b[NOWN], nown = 0;
+#pragma unroll
+    for (int q = 0; q < NOWN; ++q) {
+        int e = tid + q * NT, a = 0;
+        own_a[q] = own_b[q] = 0;
+        if (e >= W * (W + 1) / 2) continue;
+        while (e >= W - a) {
+            e -= W - a;
+            ++a;
+        }
+        own_a[q] = a;
+        own_b[q] = a + e;
+        nown = q + 1;
+    }
     __syncthreads();
 
     for (int k = 0; k < Kb; ++k) {
@@ -170,43 +188,60 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
             }
         }
         __syncthreads();
-        // ---- signed Cholesky S = L Sigma L^T (right-looking, lower)
+        // ---- signed Cholesky S = L Sigma L^T, right-looking in LDL^T form on the
+        // upper triangle (row j is read contiguously): every thread updates the
+        // elements it owns, one barrier per column; pivots kept, rows scaled at the end
         for (int j = 0; j < W; ++j) {
             const double d = S[j * LD + j];
-            const double sj = d < 0.0 ? -1.0 : 1.0;
-            const double ljj = sqrt(fabs(d));
             if (tid == 0) {
                 if (!(d != 0.0) || !isfinite(d)) flag[0] = 1;
-                sig[j] = sj;
+                piv[j] = d;
             }
-            for (int r = j + 1 + tid; r < W; r += NT) S[r * LD + j] = S[r * LD + j] / (ljj * sj);
-            __syncthreads();
-            if (tid == 0) S[j * LD + j] = ljj;
-            const int m = W - j - 1;
-            for (int e = tid; e < m * m; e += NT) {
-                const int r = j + 1 + e / m, s = j + 1 + e % m;
-                if (s > r) continue;
-                S[r * LD + s] -= S[r * LD + j] * sj * S[s * LD + j];
+            const double rd = 1.0 / d;
+#pragma unroll
+            for (int q = 0; q < NOWN; ++q) {
+                const int a = own_a[q], b = own_b[q];
+                if (q < nown && a > j) S[a * LD + b] = fma(-S[j * LD + a] * rd, S[j * LD + b], S[a * LD + b]);
             }
             __syncthreads();
         }
-        // ---- Linv_k = L_kk^-1 (row by row; column j handled by 4 threads)
+        // L (lower) = scaled transpose of the upper rows; Sigma = sign(pivots)
+#pragma unroll
+        for (int q = 0; q < NOWN; ++q) {
+            if (q >= nown) continue;
+            const int a = own_a[q], b = own_b[q];
+            const double d = piv[a];
+            const double la = sqrt(fabs(d));
+            if (a == b) S[a * LD + a] = la;
+            else S[b * LD + a] = S[a * LD + b] / (la * (d < 0.0 ? -1.0 : 1.0));
+        }
+        for (int e = tid; e < W; e += NT) {
+            sig[e] = piv[e] < 0.0 ? -1.0 : 1.0;
+            rsc[e] = 1.0 / (sqrt(fabs(piv[e])) * (piv[e] < 0.0 ? -1.0 : 1.0));
+        }
+        // ---- Linv_k = L_kk^-1 by rows (update form, X[b][a] accumulated by the owner of (a, b))
         for (int e = tid; e < W * W; e += NT) Lc[(e / W) * LD + (e % W)] = 0.0;
         __syncthreads();
         {
-            const int j = tid >> 2, part = tid & 3;
-            const bool active_col = j < W;
-            for (int r = 0; r < W; ++r) {
-                const bool act = active_col && j <= r;
-                double acc = 0.0;
-                if (act)
-                    for (int i = j + part; i < r; i += 4) acc += S[r * LD + i] * Lc[i * LD + j];
-                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-                acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-                if (act && part == 0) Lc[r * LD + j] = (r == j) ? 1.0 / S[r * LD + r] : -acc / S[r * LD + r];
+            double xacc[NOWN];
+#pragma unroll
+            for (int q = 0; q < NOWN; ++q) xacc[q] = (q < nown && own_a[q] == own_b[q]) ? 1.0 : 0.0;
+            for (int i = 0; i < W; ++i) {
+                const double rii = 1.0 / S[i * LD + i];
+#pragma unroll
+                for (int q = 0; q < NOWN; ++q)
+                    if (q < nown && own_b[q] == i) Lc[i * LD + own_a[q]] = xacc[q] * rii;
                 __syncthreads();
+                const double ri = rsc[i];
+#pragma unroll
+                for (int q = 0; q < NOWN; ++q) {
+                    const int a = own_a[q], b = own_b[q];
+                    // L[b][i] = U_raw[i][b] / (l_ii sigma_i), read from the upper row i
+                    if (q < nown && b > i && a <= i) xacc[q] = fma(-S[i * LD + b] * ri, Lc[i * LD + a], xacc[q]);
+                }
             }
         }
+        __syncthreads();
         // ---- Ffwd_k^T: rows j<W: Linv_k[:, j]; rows W+j: -M_k[:, j], M_k = Linv_k P
         double* F = Ff + (int64_t)k * slab;
         for (int e = tid; e < W * W; e += NT) {

@@ -251,6 +251,9 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
         DBuf<int> sweeps;
         sweeps.alloc(ws.B, st);
         jp.sweeps = sweeps.get();
+        // the bootstrap round only plans the Chebyshev filter (interval ends, rate);
+        // the filter input needs the span, not converged Ritz vectors
+        if (round == 0 && use_cheb && c < m) jp.max_sweeps = 3;
         const int jerr = jacobi_eigh(jp, pl, m, st);
         if (jerr != 0) SMG_CUDA((cudaError_t)jerr);
         if (std::getenv("SMG_DEBUG")) {
