@@ -2,11 +2,18 @@
 //
 // C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b], row-major operands.
 // Used for the Gram V^T V (K5, split-K over the n_d rows, upper tiles only),
-// the triangular right-multiply V * R^-1 (K7, B upper triangular so the K loop
+// the triangular right-multiply V * B with B upper triangular (K7, the K loop
 // stops at the tile's last column), and the Rayleigh-Ritz products of the
-// first-submesh basis (K9).  64x64x16 CTA tiles, 4 warps of 32x32, register
-// prefetch of the next K slab while the current one is multiplied; split-K
-// partials are summed in a fixed order by gemm_reduce (deterministic).
+// first-submesh basis (K9).
+//
+// CTA tile 64 x BN (BN = 16 * NJ), four warps of 32 x 8NJ, register prefetch of
+// the next K slab while the current one is multiplied.  The column range is
+// launched as 64-wide tiles plus one tail tile (BN = 16, 32, 48 or 64) so
+// c = 200 does not pay for 56 padded columns: DMMAs that are predicated off
+// still occupy the pipe, so padding is removed structurally, and the masked
+// (predicated) inner loop only runs where the tile crosses a row/column edge,
+// the Gram's diagonal or B's diagonal block.  Split-K partials are summed in a
+// fixed order by gemm_reduce (deterministic).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -14,58 +21,66 @@ namespace smg {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 128, SP = 68;  // SP: padded smem row (68 % 16 == 4)
+constexpr int BM = 64, BK = 16, NT = 128;
+constexpr int SPX = BK + 4;  // x-major slab row (k contiguous): 20 % 16 == 4, conflict-free
 
-template <bool KMAJOR>
-struct TileLoader {
-    // Loads the BK x 64 slab (k in [k0,k0+BK), x in [x0,x0+64)) of an operand whose
-    // element (k, x) lives at ptr[k*ld + x] (KMAJOR) or ptr[x*ld + k] (!KMAJOR).
-    double r[8];
-    SMG_DEV void load(const double* __restrict__ ptr, int64_t ld, int k0, int x0, int kmax, int xmax) {
-        const int tid = threadIdx.x;
+// Shared-memory slab of one operand: BK x XW (k, x).  k-major operands (x
+// contiguous in global memory) are stored [k][x], x-major ones [x][k]; both
+// strides are 4 mod 16 doubles so fragment reads and stores avoid bank conflicts.
+template <int XW, bool KMAJOR>
+struct Slab {
+    static constexpr int S = KMAJOR ? XW + 4 : SPX;
+    static constexpr int ELEMS = KMAJOR ? BK * (XW + 4) : XW * SPX;
+    static constexpr int PER = XW * BK / NT;  // elements per thread
+    double r[PER];
+    SMG_DEV static double at(const double* s, int k, int x) { return KMAJOR ? s[k * S + x] : s[x * S + k]; }
+    SMG_DEV static void coords(int e, int& k, int& x) {
         if (KMAJOR) {
-            const int x = tid & 63, kb = tid >> 6;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int k = kb + 2 * j;
-                const int gk = k0 + k, gx = x0 + x;
-                r[j] = (gk < kmax && gx < xmax) ? __ldg(ptr + (int64_t)gk * ld + gx) : 0.0;
-            }
+            k = e / XW;
+            x = e % XW;
         } else {
-            const int k = tid & 15, xb = tid >> 4;
+            k = e % BK;
+            x = e / BK;
+        }
+    }
+    // element (k, x) lives at ptr[k*ld + x] (KMAJOR) or ptr[x*ld + k]
+    SMG_DEV void load(const double* __restrict__ ptr, int64_t ld, int k0, int x0, int kmax, int xmax) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int x = xb + 8 * j;
-                const int gk = k0 + k, gx = x0 + x;
-                r[j] = (gk < kmax && gx < xmax) ? __ldg(ptr + (int64_t)gx * ld + gk) : 0.0;
-            }
+        for (int j = 0; j < PER; ++j) {
+            int k, x;
+            coords(threadIdx.x + j * NT, k, x);
+            const int gk = k0 + k, gx = x0 + x;
+            r[j] = (gk < kmax && gx < xmax) ? __ldg(KMAJOR ? ptr + (int64_t)gk * ld + gx : ptr + (int64_t)gx * ld + gk)
+                                            : 0.0;
         }
     }
     SMG_DEV void store(double* __restrict__ s) const {
-        const int tid = threadIdx.x;
-        if (KMAJOR) {
-            const int x = tid & 63, kb = tid >> 6;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) s[(kb + 2 * j) * SP + x] = r[j];
-        } else {
-            const int k = tid & 15, xb = tid >> 4;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) s[k * SP + xb + 8 * j] = r[j];
+        for (int j = 0; j < PER; ++j) {
+            int k, x;
+            coords(threadIdx.x + j * NT, k, x);
+            if (KMAJOR) s[k * S + x] = r[j];
+            else s[x * S + k] = r[j];
         }
     }
 };
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p) {
+template <bool TA, bool TB, int NJ>
+__global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p, int n_base) {
+    constexpr int BN = 16 * NJ;
+    // op(A) element (m, k): TA ? A[k*lda + m] : A[m*lda + k]  -> k-major iff TA
+    // op(B) element (k, n): TB ? B[n*ldb + k] : B[k*ldb + n]  -> k-major iff !TB
+    using SA = Slab<BM, TA>;
+    using SB = Slab<BN, !TB>;
     const int splits = p.splits > 0 ? p.splits : 1;
     const int b = blockIdx.z / splits;
     const int s = blockIdx.z % splits;
     const int M = p.dimM ? p.dimM[(int64_t)b * p.dimStride] : p.M;
     const int N = p.dimN ? p.dimN[(int64_t)b * p.dimStride] : p.N;
     const int K = p.dimK ? p.dimK[(int64_t)b * p.dimStride] : p.K;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int m0 = blockIdx.y * BM, n0 = n_base + blockIdx.x * BN;
     if (m0 >= M || n0 >= N) return;
-    if (p.syrkUpper && blockIdx.y > blockIdx.x) return;
+    if (p.syrkUpper && m0 > n0) return;
 
     int kEnd = K;
     if (p.upperB) kEnd = min(kEnd, n0 + BN);
@@ -76,37 +91,38 @@ __global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p) {
     const double* A = p.A + (int64_t)b * p.strideA;
     const double* B = p.B + (int64_t)b * p.strideB;
 
-    __shared__ __align__(16) double As[2][BK * SP];
-    __shared__ __align__(16) double Bs[2][BK * SP];
+    __shared__ __align__(16) double As[2][SA::ELEMS];
+    __shared__ __align__(16) double Bs[2][SB::ELEMS];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * (8 * NJ);
 
-    double acc[4][4][2];
+    double acc[4][NJ][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    // op(A) element (m, k): TA ? A[k*lda + m] : A[m*lda + k]  -> k-major iff TA
-    // op(B) element (k, n): TB ? B[n*ldb + k] : B[k*ldb + n]  -> k-major iff !TB
-    // fragments (8x8 of the warp's 32x32) that carry no output are skipped on the
-    // DMMA pipe: rows >= M, cols >= N, and for syrkUpper the 32-blocks below the
-    // diagonal (the Cholesky reads the upper triangle incl. full 32x32 diagonal blocks)
+    // fragments that carry output: rows < M, cols < N, and for syrkUpper not in a
+    // 32-block below the diagonal (the Cholesky reads the upper triangle incl.
+    // full 32x32 diagonal blocks)
+    constexpr unsigned kFull = (1u << (4 * NJ)) - 1u;
     unsigned fmask = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             const int r = m0 + wm + 8 * i, cc = n0 + wn + 8 * j;
             bool on = r < M && cc < N;
             if (p.syrkUpper && (r >> 5) > (cc >> 5)) on = false;
-            if (on) fmask |= 1u << (4 * i + j);
+            if (on) fmask |= 1u << (NJ * i + j);
         }
+    // first k of the warp's diagonal region of an upper-triangular B (k > col is zero)
+    const int kdiag = p.upperB ? n0 + wn : 1 << 30;
 
-    TileLoader<TA> la;
-    TileLoader<!TB> lb;
+    SA la;
+    SB lb;
     int buf = 0;
     if (kBeg < kStop) {
         la.load(A, p.lda, kBeg, m0, kStop, M);
@@ -123,24 +139,44 @@ __global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p) {
         }
         const double* as = As[buf];
         const double* bs = Bs[buf];
+        if (fmask == kFull && k0 + BK <= kdiag) {
+            // interior: every fragment active, no predication
 #pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double a[4], bb[4];
+            for (int kk = 0; kk < BK; kk += 4) {
+                double a[4], bb[NJ];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = as[(kk + t) * SP + wm + 8 * i + g];
+                for (int i = 0; i < 4; ++i) a[i] = SA::at(as, kk + t, wm + 8 * i + g);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bb[j] = bs[(kk + t) * SP + wn + 8 * j + g];
-            unsigned m = fmask;
-            if (p.upperB) {  // B[k][col] = 0 for k > col: fragment column block must reach k0 + kk
+                for (int j = 0; j < NJ; ++j) bb[j] = SB::at(bs, kk + t, wn + 8 * j + g);
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (n0 + wn + 8 * j + 7 < k0 + kk) m &= ~(0x1111u << j);
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
             }
+        } else if (fmask != 0 && k0 < kdiag + 8 * NJ) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int kk = 0; kk < BK; kk += 4) {
+                unsigned m = fmask;
+                if (p.upperB) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (m & (1u << (4 * i + j))) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+                    for (int j = 0; j < NJ; ++j)
+                        if (kdiag + 8 * j + 7 < k0 + kk) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) m &= ~(1u << (NJ * i + j));
+                        }
+                }
+                if (m == 0) continue;
+                double a[4], bb[NJ];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = SA::at(as, kk + t, wm + 8 * i + g);
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) bb[j] = SB::at(bs, kk + t, wn + 8 * j + g);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j)
+                        if (m & (1u << (NJ * i + j))) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+            }
         }
         if (more) {
             la.store(As[buf ^ 1]);
@@ -164,7 +200,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p) {
         const int row = m0 + wm + 8 * i + g;
         if (row >= M) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int col = n0 + wn + 8 * j + 2 * t + q;
@@ -188,7 +224,7 @@ __global__ void gemm_reduce_kernel(GemmParams p) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(e / N), j = (int)(e % N);
-        if (p.syrkUpper && (i / BM) > (j / BN)) continue;
+        if (p.syrkUpper && (i / BM) > (j / BM)) continue;
         double sum = 0.0;
         for (int s = 0; s < p.splits; ++s) sum += W[(int64_t)s * p.strideP + (int64_t)i * p.ldc + j];
         double v = p.alpha * sum;
@@ -198,18 +234,38 @@ __global__ void gemm_reduce_kernel(GemmParams p) {
     }
 }
 
+template <bool TA, bool TB, int NJ>
+void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
+    constexpr int BN = 16 * NJ;
+    const int gm = (p.M + BM - 1) / BM, gn = (width + BN - 1) / BN;
+    dim3 grid(gn, gm, p.batch * p.splits);
+    ::smg::count_launch();
+    gemm_kernel<TA, TB, NJ><<<grid, NT, 0, st>>>(p, n_base);
+}
+
+template <bool TA, bool TB>
+void launch_split(const GemmParams& p, cudaStream_t st) {
+    const int main = p.N / 64 * 64, tail = p.N - main;
+    if (main > 0) launch_tiles<TA, TB, 4>(p, 0, main, st);
+    switch ((tail + 15) / 16) {
+        case 1: launch_tiles<TA, TB, 1>(p, main, tail, st); break;
+        case 2: launch_tiles<TA, TB, 2>(p, main, tail, st); break;
+        case 3: launch_tiles<TA, TB, 3>(p, main, tail, st); break;
+        case 4: launch_tiles<TA, TB, 4>(p, main, tail, st); break;
+        default: break;
+    }
+}
+
 }  // namespace
 
 void gemm(const GemmParams& p0, bool transA, bool transB, cudaStream_t st) {
     GemmParams p = p0;
     if (p.splits < 1) p.splits = 1;
-    const int gm = (p.M + BM - 1) / BM, gn = (p.N + BN - 1) / BN;
-    if (gm == 0 || gn == 0 || p.batch == 0) return;
-    dim3 grid(gn, gm, p.batch * p.splits);
-    if (transA && !transB) ::smg::count_launch(), gemm_kernel<true, false><<<grid, NT, 0, st>>>(p);
-    else if (!transA && !transB) ::smg::count_launch(), gemm_kernel<false, false><<<grid, NT, 0, st>>>(p);
-    else if (transA && transB) ::smg::count_launch(), gemm_kernel<true, true><<<grid, NT, 0, st>>>(p);
-    else ::smg::count_launch(), gemm_kernel<false, true><<<grid, NT, 0, st>>>(p);
+    if (p.M <= 0 || p.N <= 0 || p.batch == 0) return;
+    if (transA && !transB) launch_split<true, false>(p, st);
+    else if (!transA && !transB) launch_split<false, false>(p, st);
+    else if (transA && transB) launch_split<true, true>(p, st);
+    else launch_split<false, true>(p, st);
     if (p.splits > 1) {
         dim3 rg((unsigned)std::min<int64_t>(((int64_t)p.M * p.N + 255) / 256, 1024), p.batch);
         ::smg::count_launch(), gemm_reduce_kernel<<<rg, 256, 0, st>>>(p);
