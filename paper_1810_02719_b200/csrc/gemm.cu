@@ -8,8 +8,8 @@
 //
 // CTA tile 64 x BN (BN = 16 * NJ), four warps of 32 x 8NJ, register prefetch of
 // the next K slab while the current one is multiplied.  The column range is
-// launched as 64-wide tiles plus one tail tile (BN = 16, 32, 48 or 64) so
-// c = 200 does not pay for 56 padded columns: DMMAs that are predicated off
+// launched as 64-wide tiles plus one narrow tail tile (BN = 16..64), so c = 200
+// does not pay for 56 padded columns: DMMAs that are predicated off
 // still occupy the pipe, so padding is removed structurally, and the masked
 // (predicated) inner loop only runs where the tile crosses a row/column edge,
 // the Gram's diagonal or B's diagonal block.  Split-K partials are summed in a
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p, int n_base) {
     const int K = p.dimK ? p.dimK[(int64_t)b * p.dimStride] : p.K;
     const int m0 = blockIdx.y * BM, n0 = n_base + blockIdx.x * BN;
     if (m0 >= M || n0 >= N) return;
-    if (p.syrkUpper && m0 > n0) return;
+    if (p.syrkUpper && m0 > n0 + BN - 1) return;  // tile entirely below the diagonal
 
     int kEnd = K;
     if (p.upperB) kEnd = min(kEnd, n0 + BN);
@@ -246,6 +246,10 @@ void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
 template <bool TA, bool TB>
 void launch_split(const GemmParams& p, cudaStream_t st) {
     const int main = p.N / 64 * 64, tail = p.N - main;
+    if (tail == 0) {
+        launch_tiles<TA, TB, 4>(p, 0, main, st);
+        return;
+    }
     if (main > 0) launch_tiles<TA, TB, 4>(p, 0, main, st);
     switch ((tail + 15) / 16) {
         case 1: launch_tiles<TA, TB, 1>(p, main, tail, st); break;
