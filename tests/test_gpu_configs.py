@@ -1,0 +1,99 @@
+"""Parity on the five BASELINE.json configs at their full sizes.
+
+C1-C3 run end to end on the GPU and in the oracle (seconds each).  C5 runs a
+two-mesh shard of the real 512^2 / 128-tile / c=200 workload on the GPU,
+checked against the oracle on a chain prefix, and against itself run one chain
+at a time.  C4's saturating DOI chain (tile 0 grows c from 20 to ~330 in ~300
+steps on n_d = 4096) is too long for the oracle in a test, and long DOI runs
+are rounding-chaotic, so the full run is checked through
+size-independent properties of the controller (spectral.hpp:259-283); the
+decision-level parity lives in test_gpu_chain.test_doi_chain_decisions_match.
+Seeded synthetic inputs stand in for the configs (no dataset exists).
+"""
+import numpy as np
+import pytest
+
+import specmesh_oracle as O
+from paper_1810_02719_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+G = pytest.importorskip("paper_1810_02719_b200")
+
+from test_gpu_chain import check_parity, run_both  # noqa: E402
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_config_end_to_end(ctx, name):
+    w = synth.config(name)
+    bb, ob = run_both(ctx, w.mesh, w.seg, w.c, t=w.iterations)
+    check_parity(w.mesh, bb, ob)
+
+
+def test_config5_shard_prefix_matches_oracle(ctx):
+    """First 6 tiles of two C5 meshes (n_d = 2048, c = 200, first basis from the
+    GPU subspace iteration) against the oracle's dense-eigendecomposition chain."""
+    T = 6
+    ws = [synth.config("C5", mesh_index=i) for i in (0, 1)]
+    seg = synth.Segmentation(ws[0].seg.members[:T], np.arange(T, dtype=np.int32))
+    cfg = G.PipelineConfig(weighting="binary", subspace_size=200, iterations=1, shift_scale=1e-3)
+    out = G.run_chains([w.mesh for w in ws], [seg] * 2, cfg, [200] * T, want_bases=True, want_recon=False,
+                       ctx=ctx)
+    for w, bb in zip(ws, out):
+        subs = O.build_submeshes(w.mesh.adj_offsets, w.mesh.adj_cols, seg.members)
+        ocfg = O.PipelineConfig(weighting=O.BINARY, subspace_size=200, iterations=1, shift_scale=1e-3)
+        ob = O.compute_block_bases_fixed_sizes(w.mesh.vertices, subs, seg.sequence, ocfg, [200] * T)
+        for i in range(T):
+            assert O.max_principal_angle(bb.bases[i], ob.bases[i]) < 1e-8
+            assert abs(bb.stats[i].residual_rms - ob.stats[i].residual_rms) <= 1e-9 * ob.stats[i].residual_rms
+            co = O.gft(ob.bases[i], ob.submeshes[i].local_coords(w.mesh.vertices))
+            s = np.sign(np.sum(bb.bases[i] * ob.bases[i], axis=0))
+            assert np.abs(bb.coefficients[i] * s[:, None] - co).max() <= 1e-8 * np.abs(co).max()
+
+
+def test_config5_full_chains_batched_equal_single(ctx):
+    """The real C5 chain (128 tiles) on a 2-mesh shard: the batched path equals
+    each chain run alone, and the stitched reconstruction of every mesh is the
+    weighted average of its tiles' projections (tiles are disjoint here)."""
+    ws = [synth.config("C5", mesh_index=i) for i in (3, 4)]
+    cfg = G.PipelineConfig(weighting="binary", subspace_size=200, iterations=1, shift_scale=1e-3)
+    sizes = [200] * ws[0].seg.count
+    batch = G.run_chains([w.mesh for w in ws], [w.seg for w in ws], cfg, sizes, ctx=ctx)
+    for w, b in zip(ws, batch):
+        single = G.compute_block_bases_fixed_sizes(w.mesh, w.seg, cfg, sizes, ctx=ctx)
+        r = single.reconstruction
+        assert np.linalg.norm(b.reconstruction - r, axis=1).max() <= 1e-10 * np.linalg.norm(r, axis=1).max()
+        for i in range(w.seg.count):
+            assert abs(single.stats[i].residual_rms - b.stats[i].residual_rms) <= 1e-10 * single.stats[i].residual_rms
+        # reconstruction error is bounded by the per-tile projection residuals
+        err2 = np.sum((b.reconstruction - w.mesh.vertices) ** 2)
+        bound2 = sum(3 * w.seg.block_size * b.stats[i].residual_rms ** 2 for i in range(w.seg.count))
+        assert abs(err2 - bound2) <= 1e-8 * bound2
+
+
+def test_config4_doi_controller_properties(ctx):
+    """Full C4 (1024^2 grid, 256 tiles of 64x64, DOI c in [20, 400], band
+    1e-5 / 1e-4): every block ends inside the band or at a bound, the size
+    stays in [c_min, c_max], and the carry starts each block at the previous
+    block's size (pipeline.hpp:266-270)."""
+    w = synth.config("C4")
+    kw = dict(subspace_size=w.c, c_min=w.c_min, c_max=w.c_max, eps_low=w.eps_low, eps_high=w.eps_high,
+              shift_scale=1e-3)
+    cfg = G.PipelineConfig(weighting="binary", basis_mode="doi", **kw)
+    bb = G.compute_block_bases(w.mesh, w.seg, cfg, want_bases=False, ctx=ctx)
+    grew = False
+    for i in range(w.seg.count):
+        st = bb.stats[i]
+        assert w.c_min <= st.subspace_size <= w.c_max
+        assert st.oi_iterations >= 1
+        if st.converged:
+            assert st.doi_residual <= w.eps_high
+            assert st.doi_residual >= w.eps_low or st.subspace_size == w.c_min
+        else:
+            assert st.subspace_size == w.c_max or st.oi_iterations == O.PipelineConfig(**kw).resolve_doi_iterations(w.c_max)
+        assert np.all(np.isfinite(bb.coefficients[i]))
+        grew |= st.subspace_size > w.c
+    assert grew
+    assert np.all(np.isfinite(bb.reconstruction))
+    rel = np.linalg.norm(bb.reconstruction - w.mesh.vertices, axis=1).max() / np.abs(w.mesh.vertices).max()
+    assert rel < 1e-2
