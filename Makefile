@@ -25,7 +25,22 @@ oracle/_ref/rng_ref: oracle/rng_ref.cpp
 	@mkdir -p oracle/_ref
 	g++ -O2 -std=c++17 -o $@ $<
 
+# standalone kernel timing tools (not part of the library)
+tools: build/solve_bench build/solve_bench_noload build/solve_bench_nomma
+
+build/solve_bench: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -o $@ $<
+
+build/solve_bench_noload: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_LOAD -o $@ $<
+
+build/solve_bench_nomma: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_MMA -o $@ $<
+
 clean:
 	rm -rf build $(LIB) oracle/_ref
 
-.PHONY: all clean oracle
+.PHONY: all clean oracle tools

@@ -296,20 +296,36 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     value = units / (ms_step / 1e3)
     e2e_value = units / (ms_e2e / args.steps / 1e3)
 
-    # roofline of the dominant kernel (solve: the block-tridiagonal R^z sweeps)
+    # roofline of the dominant kernel (solve: the block-tridiagonal R^z sweeps).
+    # Algorithmic flops: z*4*n_d*b*c per tile and OI iteration,
+    # b = half-bandwidth in the natural order; the "solve" stage also holds the
+    # first basis's shift-invert bootstrap (4 iterations on m columns, the first
+    # with z = 1).  Launch durations are CUDA-event spans on the launching
+    # stream inside the timed region; two chain groups share the GPU, so a
+    # launch's span includes time the other group's kernels occupy SMs.
     c, n, B, K, t = cfg["c"], job.nd, job.B, job.K, cfg["t"]
-    b_half = cfg["tw"] + 1  # half-bandwidth in the natural order
+    b_half = cfg["tw"] + 1
     z = PINNED["power"]
+    m_fb = min(n, max(c, min(480, -(-(c + max(16, c // 2)) // 8) * 8)))
     solve = stages["solve"]
     solve_launches_per_step = solve["launches"] / args.steps if solve["launches"] else 0
-    flops_per_launch = B * z * 4.0 * n * b_half * c  # z*4*n_d*b*c per tile
+    solve_flops_step = B * ((K - 1) * t * z * 4.0 * n * b_half * c + (1 + 3 * z) * 4.0 * n * b_half * m_fb)
+    flops_per_launch = solve_flops_step / max(solve_launches_per_step, 1e-9)
     avg_ms = solve["ms"] / max(solve_launches_per_step, 1e-9)
-    achieved = flops_per_launch / (avg_ms * 1e-3) / 1e12 if avg_ms > 0 else None
+    achieved = solve_flops_step / (solve["ms"] * 1e-3) / 1e12 if solve["ms"] > 0 else None
+    traffic = None
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "solve_traffic_r01.json")) as f:
+            traffic = json.load(f)["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        pass
     roofline = {"kernel": "solve_kernel (block-tridiagonal R^z sweeps, DMMA f64)", "bound": "tensor",
                 "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
+                "traffic_source": "profiles/solve_traffic_r01.json (bytes per launch of 32 chains)",
                 "peak_source": "measured FP64 DMMA peak, profiles/fp64_peak_r01.txt (MEASURED_PEAKS.json has no FP64 entry)",
                 "flops_per_launch": flops_per_launch, "avg_launch_ms": avg_ms,
+                "launches_per_step": solve_launches_per_step,
                 "step_share": solve["ms"] / ms_step if ms_step else None}
     # whole-step algorithmic FP64 work (SURVEY.md §8(d) formulas, per GPU)
     per_tile = z * 4.0 * n * b_half * c * t + (4.0 * n * c * c) * t + n * b_half ** 2 + 12.0 * n * c + 3 * n

@@ -16,8 +16,11 @@ namespace smg {
 
 // D(8x8) += A(8x4, row) * B(4x8, col).  Lane l: g = l >> 2, t = l & 3 holds
 // a = A[g][t], b = B[t][g]; d0 = D[g][2t], d1 = D[g][2t+1].
+#ifndef SMG_DMMA_ASM
+#define SMG_DMMA_ASM asm volatile
+#endif
 SMG_DEV void dmma884(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    SMG_DMMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }

@@ -53,6 +53,12 @@ struct SolveTiling {
                                                      : ((NT_ALL % 4 == 0 && WN_RAW >= 4) ? 4 : ((NT_ALL % 2 == 0 && WN_RAW >= 2) ? 2 : 1));
     static constexpr int MT = MT_ALL / WM, NT = NT_ALL / WN;
     static constexpr int ACTIVE = WM * WN;
+    // Row-tile of the warp's i-th m tile.  The first half of every step is a
+    // triangular block, so contiguous row tiles would give the bottom warps up
+    // to 4x the DMMAs of the top ones; pairing tile r with MT_ALL-1-r balances
+    // every warp (and so every SM sub-partition).
+    static constexpr bool PAIRED = (MT == 2 && MT_ALL == 2 * WM);
+    SMG_DEV static int tile(int wm, int i) { return PAIRED ? (i == 0 ? wm : MT_ALL - 1 - wm) : wm * MT + i; }
 };
 
 template <int W, int CS, bool FWD>
@@ -70,6 +76,45 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     if (warp >= TL::ACTIVE) return;
     // first half: triangular block (Linv_k lower for FWD, Linv_k^T Sigma upper for BWD)
+    if constexpr (TL::PAIRED) {
+        // row tiles lo = wm and hi = MT_ALL-1-wm; the k ranges where a tile's
+        // block is nonzero are loop bounds, not predicates (a predicated-off
+        // DMMA still occupies the pipe): FWD tile r needs kk < 8r+8, BWD kk >= 8r
+        const int lo = wm, hi = TL::MT_ALL - 1 - wm;
+        auto both = [&](int k0, int k1) {
+#pragma unroll 2
+            for (int kk = k0; kk < k1; kk += 4) {
+                double a0, a1, b[NT];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
+                a0 = fs[(kk + t) * FS + 8 * lo + g];
+                a1 = fs[(kk + t) * FS + 8 * hi + g];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    dmma884(acc[0][j][0], acc[0][j][1], a0, b[j]);
+                    dmma884(acc[1][j][0], acc[1][j][1], a1, b[j]);
+                }
+            }
+        };
+        auto one = [&](int k0, int k1, int i, int r) {
+#pragma unroll 2
+            for (int kk = k0; kk < k1; kk += 4) {
+                double b[NT];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
+                const double a = fs[(kk + t) * FS + 8 * r + g];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a, b[j]);
+            }
+        };
+        if (FWD) {
+            both(0, 8 * lo + 8);
+            one(8 * lo + 8, 8 * hi + 8, 1, hi);
+        } else {
+            one(8 * lo, 8 * hi, 0, lo);
+            both(8 * hi, W);
+        }
+    } else {
 #pragma unroll 2
     for (int kk = 0; kk < W; kk += 4) {
         double b[NT];
@@ -77,13 +122,14 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
         for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
-            const int ti = wm * MT + i;
+            const int ti = TL::tile(wm, i);
             const bool nz = FWD ? (kk < 8 * ti + 8) : (kk + 4 > 8 * ti);
             if (!nz) continue;
             const double a = fs[(kk + t) * FS + 8 * ti + g];
 #pragma unroll
             for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a, b[j]);
         }
+    }
     }
     if (skip_second) return;
 #pragma unroll 2
@@ -92,7 +138,7 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
 #pragma unroll
         for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
 #pragma unroll
-        for (int i = 0; i < MT; ++i) a[i] = fs[(kk + t) * FS + 8 * (wm * MT + i) + g];
+        for (int i = 0; i < MT; ++i) a[i] = fs[(kk + t) * FS + 8 * TL::tile(wm, i) + g];
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -128,6 +174,9 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
 
     // issue async loads of factor slab k and rhs rows of block k for `sweep`
     auto issue = [&](int sweep, int k, int buf) {
+#ifdef SMG_SOLVE_NO_LOAD
+        return;
+#endif
         const double* F = ((sweep & 1) ? Fbwd : Ffwd) + (int64_t)k * slab;
         double* fs = Fs[buf];
         // 2W rows x W doubles -> W/2 16-byte chunks per row
@@ -169,8 +218,13 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
             if (step + 1 < Kb) issue(sweep, fwd ? k + 1 : k - 1, buf ^ 1);
             double acc[TL::MT][TL::NT][2];
             const bool skip2 = step == 0;
+#ifndef SMG_SOLVE_NO_MMA
             if (fwd) mma_step<W, CS, true>(Fs[buf], Xs[buf], acc, warp, g, t, skip2);
             else mma_step<W, CS, false>(Fs[buf], Xs[buf], acc, warp, g, t, skip2);
+#else
+            for (int i = 0; i < TL::MT; ++i)
+                for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Xs[buf][tid];
+#endif
             // epilogue: result is the "previous block" of the next step and goes to dst
             double* xnext = Xs[buf ^ 1] + W * XS;
             if (warp < TL::ACTIVE) {
@@ -179,7 +233,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 for (int i = 0; i < TL::MT; ++i)
 #pragma unroll
                     for (int j = 0; j < TL::NT; ++j) {
-                        const int r = 8 * (wm * TL::MT + i) + g, cc = 8 * (wn * TL::NT + j) + 2 * t;
+                        const int r = 8 * TL::tile(wm, i) + g, cc = 8 * (wn * TL::NT + j) + 2 * t;
                         xnext[r * XS + cc] = acc[i][j][0];
                         xnext[r * XS + cc + 1] = acc[i][j][1];
                         const int prow = k * W + r;
