@@ -119,7 +119,7 @@ void FactorSet::factor(const TileSet& ts, int first_tile, int cnt, const double*
     ProfScope prof("factor", st);
     first = first_tile;
     count = cnt;
-    strideF = (int64_t)ts.Kb * 2 * ts.W * ts.W;
+    strideF = (int64_t)ts.Kb * 2 * ts.W * factor_row(ts.W);
     if (fwd.size() < (size_t)strideF * cnt) {
         fwd.alloc((size_t)strideF * cnt, st);
         bwd.alloc((size_t)strideF * cnt, st);

@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
     const double delta = p.delta[tile];
     double* Ff = p.Ffwd + (int64_t)tile * p.strideF;
     double* Fb = p.Fbwd + (int64_t)tile * p.strideF;
-    const int64_t slab = (int64_t)2 * W * W;
+    constexpr int FR = factor_row(W);
+    const int64_t slab = (int64_t)2 * W * FR;
 
     for (int i = tid; i < n; i += NT) ipos[perm ? perm[i] : i] = i;
     if (tid == 0) flag[0] = 0;
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
         double* F = Ff + (int64_t)k * slab;
         for (int e = tid; e < W * W; e += NT) {
             const int j = e / W, r = e % W;
-            F[(int64_t)j * W + r] = Lc[r * LD + j];
+            F[(int64_t)j * FR + r] = Lc[r * LD + j];
         }
         if (mma_warp) {
             double acc[FT::MT][FT::NTT][2] = {};
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         const int r = 8 * (wm * FT::MT + i) + g, jj = 8 * (wn * FT::NTT + j) + 2 * t4 + q;
-                        F[(int64_t)(W + jj) * W + r] = -acc[i][j][q];
+                        F[(int64_t)(W + jj) * FR + r] = -acc[i][j][q];
                     }
         }
         // ---- Fbwd_{k-1}^T second half: -(L_{k,k-1} Linv_{k-1}) = -(P Lp), row-major
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
 #pragma unroll
                 for (int j = 0; j < FT::NTT; ++j) {
                     const int r = 8 * (wm * FT::MT + i) + g, jj = 8 * (wn * FT::NTT + j) + 2 * t4;
-                    double2* dst = reinterpret_cast<double2*>(Fp + (int64_t)(W + r) * W + jj);
+                    double2* dst = reinterpret_cast<double2*>(Fp + (int64_t)(W + r) * FR + jj);
                     *dst = make_double2(-acc[i][j][0], -acc[i][j][1]);
                 }
         }
@@ -287,10 +288,10 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
             double* Fc = Fb + (int64_t)k * slab;
             for (int e = tid; e < W * W; e += NT) {
                 const int j = e / W, r = e % W;
-                Fc[(int64_t)j * W + r] = sig[j] * Lc[j * LD + r];
+                Fc[(int64_t)j * FR + r] = sig[j] * Lc[j * LD + r];
             }
             if (k == Kb - 1)
-                for (int e = tid; e < W * W; e += NT) Fc[(int64_t)W * W + e] = 0.0;
+                for (int e = tid; e < W * W; e += NT) Fc[(int64_t)(W + e / W) * FR + e % W] = 0.0;
         }
         __syncthreads();
         // ---- carry Linv_k, Sigma_k

@@ -55,6 +55,10 @@ void rcm_order(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_of
                int32_t* perm, cudaStream_t st);
 
 // ------------------------------------------------------------------ factor (factor.cu)
+// Row stride of the (2W x W) solve operand slabs in global memory: padded to
+// W + 4 doubles (% 16 == 4) so one bulk copy lands a slab in the solve's
+// bank-conflict-free shared-memory layout.
+__host__ __device__ constexpr int factor_row(int W) { return W + 4; }
 struct FactorParams {
     int ntiles = 0, n = 0, W = 0, Kb = 0;
     const int32_t* rowptr = nullptr;  // per tile (n+1) entries at tile*(n+1)

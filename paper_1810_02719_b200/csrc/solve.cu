@@ -18,8 +18,17 @@ namespace smg {
 
 namespace {
 
-constexpr int NT = 256;
-constexpr int kSolveWarps = NT / 32;
+// 8 DMMA warps + 2 producer warps.  The producers move each step's factor slab
+// (one bulk async copy on the TMA engine) and right-hand-side rows (cp.async),
+// completion tracked by an mbarrier; the DMMA warps never have loads in flight, so
+// their shared-memory fragment reads do not wait on the long scoreboard
+// (cp.async issued by the DMMA warps themselves serialised the next slab's
+// transfer with the current step's products).
+constexpr int kSolveWarps = 8;
+constexpr int kProdWarps = 2;
+constexpr int NT_MMA = kSolveWarps * 32;
+constexpr int NT = NT_MMA + kProdWarps * 32;
+constexpr int NT_PROD = kProdWarps * 32;
 
 template <int W, int CS>
 struct SolveSmem {
@@ -146,6 +155,32 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
     }
 }
 
+// ---- bulk async copies (TMA engine) with mbarrier completion
+SMG_DEV uint32_t smem_u32(const void* ptr) { return static_cast<uint32_t>(__cvta_generic_to_shared(ptr)); }
+SMG_DEV void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+SMG_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+SMG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+SMG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int W, int CS>
 __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     using S = SolveSmem<W, CS>;
@@ -163,7 +198,8 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int n = p.n, Kb = p.Kb;
-    const int64_t slab = (int64_t)2 * W * W;  // doubles per block in Ffwd/Fbwd
+    const int64_t slab = (int64_t)2 * W * factor_row(W);  // doubles per block in Ffwd/Fbwd (padded rows)
+    static_assert(FS == factor_row(W), "smem slab rows match the global padded rows");
     const double* Ffwd = p.Ffwd + (int64_t)b * p.strideF;
     const double* Fbwd = p.Fbwd + (int64_t)b * p.strideF;
     const int32_t* perm = p.perm ? p.perm + (int64_t)b * p.stridePerm : nullptr;
@@ -172,33 +208,56 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     double* out = p.out + (int64_t)b * p.strideOut;
     const int sweeps = p.once ? 2 : 2 * p.z;
 
-    // issue async loads of factor slab k and rhs rows of block k for `sweep`
+    const bool producer = tid >= NT_MMA;
+    const int ptid = tid - NT_MMA;
+    __shared__ __align__(8) uint64_t full[2];
+    uint32_t phase[2] = {0u, 0u};
+    if (tid == 0) {
+        mbar_init(&full[0], kProdWarps);  // one arrive per producer warp (+ tx bytes, cp.async)
+        mbar_init(&full[1], kProdWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // producer warp: factor slab k and rhs rows of block k for `sweep` into
+    // buffer buf (one bulk copy for the slab, cp.async for the rhs rows),
+    // completing on full[buf]
     auto issue = [&](int sweep, int k, int buf) {
-#ifdef SMG_SOLVE_NO_LOAD
-        return;
-#endif
         const double* F = ((sweep & 1) ? Fbwd : Ffwd) + (int64_t)k * slab;
         double* fs = Fs[buf];
-        // 2W rows x W doubles -> W/2 16-byte chunks per row
-        constexpr int CH = W / 2;
-        for (int e = tid; e < 2 * W * CH; e += NT) {
-            const int r = e / CH, ch = e % CH;
-            cp_async16(fs + r * FS + 2 * ch, F + (int64_t)r * W + 2 * ch);
-        }
         double* xs = Xs[buf];
+        const int nvalid = max(0, min(W, n - k * W));  // rhs rows of the block inside the tile
+#ifdef SMG_SOLVE_NO_LOAD
+        if (lane == 0) mbar_arrive_expect_tx(&full[buf], 0);
+        (void)ptid;
+        (void)F;
+        (void)fs;
+        (void)xs;
+        (void)nvalid;
+        return;
+#endif
+        // rhs rows: 16-byte cp.async chunks from the producer lanes, tracked by
+        // the same mbarrier (cp.async.mbarrier.arrive, before the expect_tx arrive)
         constexpr int CCH = CS / 2;
-        for (int e = tid; e < W * CCH; e += NT) {
+        for (int e = ptid; e < W * CCH; e += NT_PROD) {
             const int r = e / CCH, ch = e % CCH;
             const int prow = k * W + r;
-            if (sweep == 0) {
-                const bool valid = prow < n;
-                const int lrow = valid ? (perm ? perm[prow] : prow) : 0;
-                cp_async16_zfill(xs + r * XS + 2 * ch, in + (int64_t)lrow * p.ldin + col0 + 2 * ch, valid);
+            if (r < nvalid) {
+                const double* src = (sweep == 0) ? in + (int64_t)(perm ? perm[prow] : prow) * p.ldin + col0
+                                                 : tmp + (int64_t)prow * p.ldt + col0;
+                cp_async16(xs + r * XS + 2 * ch, src + 2 * ch);
             } else {
-                cp_async16(xs + r * XS + 2 * ch, tmp + (int64_t)prow * p.ldt + col0 + 2 * ch);
+                cp_async16_zfill(xs + r * XS + 2 * ch, in, false);  // padded rows past n
             }
         }
-        cp_async_commit();
+        asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[buf])) : "memory");
+        __syncwarp();
+        if (ptid == 0) {
+            mbar_arrive_expect_tx(&full[buf], (uint32_t)(2 * W * FS * 8));
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            bulk_g2s(fs, F, 2 * W * FS * 8, &full[buf]);
+        } else if (lane == 0) {
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&full[buf])) : "memory");
+        }
     };
 
     for (int sweep = 0; sweep < sweeps; ++sweep) {
@@ -207,15 +266,20 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
         int buf = 0;
         {
             const int k = fwd ? 0 : Kb - 1;
-            issue(sweep, k, 0);
+            if (producer) issue(sweep, k, 0);
             // previous-block rows of the first step are zero
             for (int e = tid; e < W * XS; e += NT) Xs[0][W * XS + e] = 0.0;
         }
         for (int step = 0; step < Kb; ++step) {
             const int k = fwd ? step : Kb - 1 - step;
-            cp_async_wait<0>();
             __syncthreads();
-            if (step + 1 < Kb) issue(sweep, fwd ? k + 1 : k - 1, buf ^ 1);
+            if (producer) {
+                if (step + 1 < Kb) issue(sweep, fwd ? k + 1 : k - 1, buf ^ 1);
+                buf ^= 1;
+                continue;
+            }
+            mbar_wait(&full[buf], phase[buf]);
+            phase[buf] ^= 1u;
             double acc[TL::MT][TL::NT][2];
             const bool skip2 = step == 0;
 #ifndef SMG_SOLVE_NO_MMA
@@ -252,6 +316,8 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
             }
             buf ^= 1;
         }
+        // the next sweep's bulk copies (async proxy) read this sweep's rows of tmp
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
         __threadfence_block();
         __syncthreads();
     }
