@@ -309,24 +309,33 @@ public:
             grp[g].nb = (int)((int64_t)B_ * (g + 1) / G) - grp[g].b0;
             SMG_CUDA(cudaStreamCreateWithFlags(&grp[g].st, cudaStreamNonBlocking));
             SMG_CUDA(cudaEventCreateWithFlags(&grp[g].ev, cudaEventDisableTiming));
+            SMG_CUDA(cudaStreamCreateWithFlags(&grp[g].pst, cudaStreamNonBlocking));
+            SMG_CUDA(cudaEventCreateWithFlags(&grp[g].ev_orth, cudaEventDisableTiming));
+            SMG_CUDA(cudaEventCreateWithFlags(&grp[g].ev_proj, cudaEventDisableTiming));
             grp[g].ws.init(grp[g].nb, n_, ts_.npad, ccap, grp[g].st);
         }
         cudaEvent_t ev_main;
         SMG_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
         auto fork = [&]() {
             SMG_CUDA(cudaEventRecord(ev_main, st_));
-            for (Group& g : grp) SMG_CUDA(cudaStreamWaitEvent(g.st, ev_main, 0));
+            for (Group& g : grp) {
+                SMG_CUDA(cudaStreamWaitEvent(g.st, ev_main, 0));
+                SMG_CUDA(cudaStreamWaitEvent(g.pst, ev_main, 0));
+            }
         };
         auto join = [&]() {
             for (Group& g : grp) {
                 SMG_CUDA(cudaEventRecord(g.ev, g.st));
                 SMG_CUDA(cudaStreamWaitEvent(st_, g.ev, 0));
+                SMG_CUDA(cudaEventRecord(g.ev, g.pst));
+                SMG_CUDA(cudaStreamWaitEvent(st_, g.ev, 0));
+                g.proj_pending = false;
             }
         };
         fork();  // group workspaces were initialised on their streams; ordering vs st_
         // Factor windows over positions, double buffered on their own stream: window
         // w+1 is factored while the groups track through window w.
-        const int64_t per_tile = (int64_t)ts_.Kb * 2 * ts_.W * ts_.W * 2 * 8;
+        const int64_t per_tile = (int64_t)ts_.Kb * 2 * ts_.W * factor_row(ts_.W) * 2 * 8;
         const int64_t budget = (int64_t)4 << 30;
         const int window =
             (int)std::max<int64_t>(1, std::min<int64_t>(K_, budget / std::max<int64_t>(1, per_tile * B_)));
@@ -385,15 +394,28 @@ public:
                 for (Group& g : grp) {
                     StepCtx gx{g.st, &ts_};
                     const int tile0 = pos * B_ + g.b0;
+                    // the previous projection reads U and writes the signs: resize and
+                    // the next orthonormalisation (which overwrites U) wait for it
+                    auto wait_proj = [&]() {
+                        if (g.proj_pending) SMG_CUDA(cudaStreamWaitEvent(g.st, g.ev_proj, 0));
+                        g.proj_pending = false;
+                    };
+                    if (c > prev_c_) wait_proj();
                     resize(c, pos, g.ws, g.b0, g.nb, g.st);
                     for (int it = 0; it < cfg_.iterations; ++it) {
                         solve_batch(gx, g.ws, fcur, tile0, 1, g.ws.U.get(), g.ws.V.get(), c, nullptr, cfg_.power,
                                     false);
+                        wait_proj();
                         orth_batch(gx, g.ws, g.ws.V.get(), g.ws.U.get(), c, nullptr, true, pos);
                     }
-                    project_batch(gx, g.ws, g.ws.U.get(), c, nullptr, ts_.X.get() + (int64_t)tile0 * n_ * 3,
+                    SMG_CUDA(cudaEventRecord(g.ev_orth, g.st));
+                    SMG_CUDA(cudaStreamWaitEvent(g.pst, g.ev_orth, 0));
+                    StepCtx px{g.pst, &ts_};
+                    project_batch(px, g.ws, g.ws.U.get(), c, nullptr, ts_.X.get() + (int64_t)tile0 * n_ * 3,
                                   (int64_t)n_ * 3, xhat_.get() + (int64_t)tile0 * n_ * 3, (int64_t)n_ * 3);
-                    emit_position(pos, c, g.ws, g.b0, g.nb, g.st);
+                    emit_position(pos, c, g.ws, g.b0, g.nb, g.pst);
+                    SMG_CUDA(cudaEventRecord(g.ev_proj, g.pst));
+                    g.proj_pending = true;
                 }
             }
             prev_c_ = c;
@@ -430,7 +452,10 @@ public:
         for (Group& g : grp) {
             g.ws = Workspace();
             cudaEventDestroy(g.ev);
+            cudaEventDestroy(g.ev_orth);
+            cudaEventDestroy(g.ev_proj);
             cudaStreamDestroy(g.st);
+            cudaStreamDestroy(g.pst);
         }
         cudaEventDestroy(ev_main);
     }
@@ -851,6 +876,10 @@ private:
         Workspace ws;
         cudaStream_t st = nullptr;
         cudaEvent_t ev = nullptr;
+        // projection of position p on its own stream, overlapping the solve of p+1
+        cudaStream_t pst = nullptr;
+        cudaEvent_t ev_orth = nullptr, ev_proj = nullptr;
+        bool proj_pending = false;
     };
     DBuf<double> xhat_, stat_rms_;
     TileSet ts_;
