@@ -329,8 +329,10 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
             if (ok && worst < 0.5) {
                 dcoef.upload(coef, st);
                 // a conservative rate: eigenvalues between lambda_m and the cut are
-                // amplified as well, so count each application as sqrt(worst)
-                const double need = std::log(fc.tol * 0.1 / bound) / std::log(std::sqrt(worst));
+                // amplified as well (and the bootstrap Ritz values are rough), so
+                // count each application as worst^0.4 -- an extra filter application
+                // is far cheaper than another Rayleigh-Ritz round
+                const double need = std::log(fc.tol * 0.1 / bound) / std::log(std::pow(worst, 0.4));
                 cheb_apps = (int)std::min(8.0, std::max(1.0, std::ceil(need)));
             }
         }

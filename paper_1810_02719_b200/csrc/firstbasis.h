@@ -31,7 +31,7 @@ struct FirstBasisReport {
 // capped at the 480-column limit of the cluster Jacobi (16 CTAs x 2 blocks of 15).
 constexpr int kFirstBasisMaxCols = 480;
 inline int first_basis_width(int n, int c) {
-    const int want = round_up(c + std::max(16, c / 2), 8);
+    const int want = round_up(c + std::max(16, c / 4), 8);
     return std::min(n, std::max(c, std::min(kFirstBasisMaxCols, want)));
 }
 
