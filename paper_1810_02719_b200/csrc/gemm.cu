@@ -8,8 +8,8 @@
 //
 // CTA tile 64 x BN (BN = 16 * NJ), four warps of 32 x 8NJ, register prefetch of
 // the next K slab while the current one is multiplied.  The column range is
-// launched as 64-wide tiles plus one narrow tail tile (BN = 16..64), so c = 200
-// does not pay for 56 padded columns: DMMAs that are predicated off
+// launched as 64-wide tiles plus one narrow tile (BN = 16..64) over c mod 64
+// columns, so c = 200 does not pay for 56 padded columns: DMMAs that are predicated off
 // still occupy the pipe, so padding is removed structurally, and the masked
 // (predicated) inner loop only runs where the tile crosses a row/column edge,
 // the Gram's diagonal or B's diagonal block.  Split-K partials are summed in a
@@ -66,7 +66,7 @@ struct Slab {
 };
 
 template <bool TA, bool TB, int NJ>
-__global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p, int n_base) {
+__global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p, int n_base, int n_end) {
     constexpr int BN = 16 * NJ;
     // op(A) element (m, k): TA ? A[k*lda + m] : A[m*lda + k]  -> k-major iff TA
     // op(B) element (k, n): TB ? B[n*ldb + k] : B[k*ldb + n]  -> k-major iff !TB
@@ -76,11 +76,11 @@ __global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p, int n_base) {
     const int b = blockIdx.z / splits;
     const int s = blockIdx.z % splits;
     const int M = p.dimM ? p.dimM[(int64_t)b * p.dimStride] : p.M;
-    const int N = p.dimN ? p.dimN[(int64_t)b * p.dimStride] : p.N;
+    const int N = min(p.dimN ? p.dimN[(int64_t)b * p.dimStride] : p.N, n_end);  // this launch's columns
     const int K = p.dimK ? p.dimK[(int64_t)b * p.dimStride] : p.K;
     const int m0 = blockIdx.y * BM, n0 = n_base + blockIdx.x * BN;
     if (m0 >= M || n0 >= N) return;
-    if (p.syrkUpper && m0 > n0 + BN - 1) return;  // tile entirely below the diagonal
+    if (p.syrkUpper && (m0 >> 5) > ((n0 + BN - 1) >> 5)) return;  // tile entirely below the diagonal 32-blocks
 
     int kEnd = K;
     if (p.upperB) kEnd = min(kEnd, n0 + BN);
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p, int n_base) {
         for (int j = 0; j < NJ; ++j) {
             const int r = m0 + wm + 8 * i, cc = n0 + wn + 8 * j;
             bool on = r < M && cc < N;
-            if (p.syrkUpper && (r >> 5) > (cc >> 5)) on = false;
+            if (p.syrkUpper && (r >> 5) > ((cc + 7) >> 5)) on = false;  // tiles need not be 32-aligned
             if (on) fmask |= 1u << (NJ * i + j);
         }
     // first k of the warp's diagonal region of an upper-triangular B (k > col is zero)
@@ -224,7 +224,7 @@ __global__ void gemm_reduce_kernel(GemmParams p) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(e / N), j = (int)(e % N);
-        if (p.syrkUpper && (i / BM) > (j / BM)) continue;
+        if (p.syrkUpper && (i >> 5) > (j >> 5)) continue;  // the Cholesky reads upper 32-blocks only
         double sum = 0.0;
         for (int s = 0; s < p.splits; ++s) sum += W[(int64_t)s * p.strideP + (int64_t)i * p.ldc + j];
         double v = p.alpha * sum;
@@ -240,24 +240,24 @@ void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
     const int gm = (p.M + BM - 1) / BM, gn = (width + BN - 1) / BN;
     dim3 grid(gn, gm, p.batch * p.splits);
     ::smg::count_launch();
-    gemm_kernel<TA, TB, NJ><<<grid, NT, 0, st>>>(p, n_base);
+    gemm_kernel<TA, TB, NJ><<<grid, NT, 0, st>>>(p, n_base, n_base + width);
 }
 
 template <bool TA, bool TB>
 void launch_split(const GemmParams& p, cudaStream_t st) {
-    const int main = p.N / 64 * 64, tail = p.N - main;
-    if (tail == 0) {
-        launch_tiles<TA, TB, 4>(p, 0, main, st);
-        return;
-    }
-    if (main > 0) launch_tiles<TA, TB, 4>(p, 0, main, st);
+    // V * B with B upper triangular: the narrow tile takes the FIRST columns, so
+    // its K range is `tail` instead of all of K.  The Gram keeps 32-aligned
+    // tiles (unaligned ones straddle the diagonal blocks) and its narrow tile last.
+    const int tail = p.N % 64, main = p.N - tail;
+    const int t0 = p.upperB ? 0 : main, m0 = p.upperB ? tail : 0;
     switch ((tail + 15) / 16) {
-        case 1: launch_tiles<TA, TB, 1>(p, main, tail, st); break;
-        case 2: launch_tiles<TA, TB, 2>(p, main, tail, st); break;
-        case 3: launch_tiles<TA, TB, 3>(p, main, tail, st); break;
-        case 4: launch_tiles<TA, TB, 4>(p, main, tail, st); break;
+        case 1: launch_tiles<TA, TB, 1>(p, t0, tail, st); break;
+        case 2: launch_tiles<TA, TB, 2>(p, t0, tail, st); break;
+        case 3: launch_tiles<TA, TB, 3>(p, t0, tail, st); break;
+        case 4: launch_tiles<TA, TB, 4>(p, t0, tail, st); break;
         default: break;
     }
+    if (main > 0) launch_tiles<TA, TB, 4>(p, m0, main, st);
 }
 
 }  // namespace
