@@ -26,7 +26,7 @@ oracle/_ref/rng_ref: oracle/rng_ref.cpp
 	g++ -O2 -std=c++17 -o $@ $<
 
 # standalone kernel timing tools (not part of the library)
-tools: build/solve_bench build/solve_bench_noload build/solve_bench_nomma
+tools: build/solve_bench build/solve_bench_noload build/solve_bench_nomma build/chol_bench
 
 build/solve_bench: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
@@ -39,6 +39,10 @@ build/solve_bench_noload: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 build/solve_bench_nomma: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_MMA -o $@ $<
+
+build/chol_bench: tools/chol_bench.cu $(SRC_DIR)/cholqr.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_CHOL_TIMING -o $@ $<
 
 clean:
 	rm -rf build $(LIB) oracle/_ref

@@ -23,6 +23,18 @@
 
 namespace smg {
 
+#ifdef SMG_CHOL_TIMING
+__device__ long long g_chol_t[128];
+#define SMG_CHOL_T(i) \
+    do { \
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_chol_t[(i)] = clock64(); \
+    } while (0)
+#else
+#define SMG_CHOL_T(i) \
+    do { \
+    } while (0)
+#endif
+
 namespace {
 
 constexpr int CNT = 256;
@@ -82,6 +94,7 @@ struct DiagOwn {
 __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     __shared__ double red[32];
     __shared__ double pivs[32];
+    __shared__ double rinvd[32];  // 1 / r_ii of the current diagonal block
     __shared__ int fail;
     extern __shared__ __align__(16) double psm[];
     const int b = blockIdx.x;
@@ -89,6 +102,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const int P = (c + 31) / 32, cp = P * 32;
     const double* G = p.G + (int64_t)b * p.strideG;
+    SMG_CHOL_T(0);
     double* A = p.A + (int64_t)b * p.strideA;
     double* Bo = p.Binv + (int64_t)b * p.strideB;
     double* d = p.dscale + (int64_t)b * p.strideD;
@@ -173,29 +187,20 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     DiagOwn own;
     own.init(tid);
     __syncthreads();
+    SMG_CHOL_T(1);
 
     for (int pb = 0; pb < P; ++pb) {
         const int p0 = pb * 32;
         for (int r = warp; r < 32; r += CW)
             for (int k = p0 + lane; k < cp; k += 32) Ps[r * PS + k] = A[(int64_t)(p0 + r) * lda + k];
         __syncthreads();
+        SMG_CHOL_T(2 + pb * 5);
         // ---- (a) factor the diagonal block with all threads (right-looking, LDL^T
         // form: the pivots are kept and the rows scaled at the end), then invert it.
         double* D = Ps + p0;  // D[i * PS + k]
         for (int j = 0; j < 32; ++j) {
             const double pj = D[j * PS + j];
-            if (tid == 0) {
-                pivs[j] = pj;
-                const int gj = p0 + j;
-                if (!fail && gj < c) {
-                    const bool bp = !(pj > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(pj) || !(ds[gj] > 0.0);
-                    const double rkk = bp ? 0.0 : sqrt(pj) * ds[gj];
-                    if (bp || (p.rank_test && rkk < thresh)) {
-                        record(p.rank_test ? kRankDeficient : kNotFinite, gj);
-                        fail = 1;
-                    }
-                }
-            }
+            if (tid == 0) pivs[j] = pj;
             const double inv = 1.0 / fmax(pj, 1e-300);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
@@ -206,7 +211,27 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             }
             __syncthreads();
         }
+        // rank test on the block's pivots, off the per-column critical path: first
+        // failing column of the block (the pivots do not depend on the test)
+        if (warp == 0) {
+            const int gj = p0 + lane;
+            bool badc = false;
+            if (gj < c) {
+                const double pj = pivs[lane];
+                const bool bp = !(pj > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(pj) || !(ds[gj] > 0.0);
+                const double rkk = bp ? 0.0 : sqrt(pj) * ds[gj];
+                badc = bp || (p.rank_test && rkk < thresh);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, badc);
+            if (lane == 0 && m) {
+                record(p.rank_test ? kRankDeficient : kNotFinite, p0 + __ffs(m) - 1);
+                fail = 1;
+            }
+            rinvd[lane] = 1.0 / sqrt(fmax(pivs[lane], 1e-300));
+        }
+        __syncthreads();
         if (fail) return;
+        SMG_CHOL_T(3 + pb * 5);
         // rows scaled: R[i][k] = D[i][k] / sqrt(piv_i); X = R^-1 accumulators
         double xacc[3];
 #pragma unroll
@@ -215,7 +240,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             if (q < own.n) {
                 const int i = own.i[q], k = own.k[q];
                 const double rii = sqrt(fmax(pivs[i], 1e-300));
-                const double r = (i == k) ? rii : D[i * PS + k] / rii;
+                const double r = (i == k) ? rii : D[i * PS + k] * rinvd[i];
                 D[i * PS + k] = r;
                 A[(int64_t)(p0 + i) * lda + p0 + k] = r;
                 xacc[q] = (i == k) ? 1.0 : 0.0;
@@ -231,7 +256,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         for (int l = 31; l >= 0; --l) {
 #pragma unroll
             for (int q = 0; q < 3; ++q)
-                if (q < own.n && own.i[q] == l) Xs[l * XS + own.k[q]] = xacc[q] / D[l * PS + l];
+                if (q < own.n && own.i[q] == l) Xs[l * XS + own.k[q]] = xacc[q] * rinvd[l];
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < 3; ++q)
@@ -239,6 +264,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                     xacc[q] = fma(-D[own.i[q] * PS + l], Xs[l * XS + own.k[q]], xacc[q]);
         }
         __syncthreads();
+        SMG_CHOL_T(4 + pb * 5);
         // ---- (b) panel row R_{p,q} = X^T A_{p,q}, q > p (smem operands, written back to smem and L2)
         for (int q = pb + 1 + warp; q < P; q += CW) {
             const int q0 = q * 32;
@@ -266,6 +292,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             for (int k = lane; k < p0; k += 32) Bo[(int64_t)(p0 + r) * ldb + k] = 0.0;
         }
         __syncthreads();
+        SMG_CHOL_T(5 + pb * 5);
         // ---- (c) trailing update A_{q,r} -= R_{p,q}^T R_{p,r}, p < q <= r
         const int rem = P - pb - 1;
         const int nblk = rem * (rem + 1) / 2;
@@ -300,6 +327,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                 }
         }
         __syncthreads();
+        SMG_CHOL_T(6 + pb * 5);
     }
     // ---- (d) X = R~^-1 by block back-substitution: X_pq = -X_pp sum_{s=p+1..q} R_ps X_sq.
     // B holds D^-1 X, so X_sq = d_row * B_sq on read.  R's panel row and X_pp sit
@@ -352,6 +380,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         }
         __syncthreads();
     }
+    SMG_CHOL_T(127);
 }
 
 // partial diag(Q^T V) over a chunk of rows, threads over columns (coalesced rows)
