@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         __syncthreads();
         SMG_CHOL_T(6 + pb * 5);
     }
+    if (p.skip_inverse) return;
     // ---- (d) X = R~^-1 by block back-substitution: X_pq = -X_pp sum_{s=p+1..q} R_ps X_sq.
     // B holds D^-1 X, so X_sq = d_row * B_sq on read.  R's panel row and X_pp sit
     // in shared memory; each X_sq block is staged into the warp's buffer with

@@ -1,6 +1,8 @@
 // Engine pieces shared by the chain runner and the L3 primitives.
 #include <cstdio>
 
+#include <cstdlib>
+
 #include "engine.h"
 #include "profiler.h"
 
@@ -252,6 +254,42 @@ void gram(Workspace& ws, const double* V, int c, const int* dimC, int n, cudaStr
 }
 
 // out = V D^-1 R~^-1 with R~ / Dinv / d from the last chol()
+// Q = V D^-1 R~^-1 from the pass-1 Cholesky (skip_inverse) by the row-parallel solve
+void trsm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st) {
+    TrsmParams t;
+    t.n = n;
+    t.batch = ws.B;
+    t.c_cap = c;
+    t.V = V;
+    t.ldv = ws.ld;
+    t.strideV = ws.mstride();
+    t.Q = out;
+    t.ldq = ws.ld;
+    t.strideQ = ws.mstride();
+    t.R = ws.work.get();
+    t.ldr = ws.ld;
+    t.strideR = (int64_t)ws.ld * ws.ld;
+    t.Binv = ws.Bm.get();
+    t.ldb = ws.ld;
+    t.strideB = (int64_t)ws.ld * ws.ld;
+    t.dscale = ws.rdiag.get();
+    t.strideD = ws.ld;
+    t.dimC = dimC;
+    t.dimStride = 1;
+    t.status = ws.status.get();
+    ProfScope prof("trmm", st);
+    trsm_right_upper(t, st);
+}
+
+// The solve replaces the Cholesky's serial back-substitution by row-parallel
+// work; it pays when few chains leave SMs idle during that single-CTA phase
+// (small batches), while at large batches the plain GEMM with B = D^-1 R~^-1
+// is faster (the back-substitution overlaps the other chain group's kernels).
+bool use_trsm(int c, int batch) {
+    static const bool off = std::getenv("SMG_NO_TRSM") != nullptr;
+    return !off && batch <= 4 && trsm_supported(c);
+}
+
 void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st) {
     GemmParams g;
     g.M = n;
@@ -276,7 +314,7 @@ void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, i
 }
 
 void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_scale, int pos, cudaStream_t st,
-          bool near_identity = false) {
+          bool near_identity = false, bool skip_inverse = false) {
     CholParams p;
     p.batch = ws.B;
     p.c_cap = c;
@@ -301,6 +339,7 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
     p.column_scale = column_scale ? 1 : 0;
     p.vnorm = rank_test ? ws.vnorm.get() : nullptr;
     p.near_identity = near_identity ? 1 : 0;
+    p.skip_inverse = skip_inverse ? 1 : 0;
     ProfScope prof("chol", st);
     chol_factor(p, st);
 }
@@ -317,13 +356,18 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
         in = ws.T.get();
     }
     gram(ws, in, c, dimC, n, cx.st);
-    chol(ws, c, dimC, rank_test, true, pos, cx.st);
+    const bool ts = use_trsm(c, ws.B);
+    chol(ws, c, dimC, rank_test, true, pos, cx.st, false, ts);
+    auto pass1 = [&](double* dst) {
+        if (ts) trsm(ws, in, dst, c, dimC, n, cx.st);
+        else trmm(ws, in, dst, c, dimC, n, cx.st);
+    };
     if (passes == 1) {  // single CholeskyQR pass (span-only uses: subspace iteration)
-        trmm(ws, in, out, c, dimC, n, cx.st);
+        pass1(out);
         SMG_CUDA(cudaGetLastError());
         return;
     }
-    trmm(ws, in, ws.R.get(), c, dimC, n, cx.st);
+    pass1(ws.R.get());
     gram(ws, ws.R.get(), c, dimC, n, cx.st);
     chol(ws, c, dimC, false, true, pos, cx.st, true);
     trmm(ws, ws.R.get(), out, c, dimC, n, cx.st);

@@ -119,9 +119,33 @@ struct CholParams {
     // first order, R~ = I + triu(G~ - I, 1) (error O(|E|^2) <= c * 1e-18), and
     // B = D^-1 (I - triu(G~ - I, 1)) is written without the serial Cholesky
     int near_identity = 0;
+    // skip the block back-substitution for R~^-1 (off-diagonal blocks of B); the
+    // caller forms Q with trsm_right_upper instead
+    int skip_inverse = 0;
 };
 void chol_factor(const CholParams& p, cudaStream_t st);
 int chol_smem_bytes(int c_cap);
+// Q = V D^-1 R~^-1 by a row-parallel right triangular solve (trsm.cu), from the
+// Cholesky's R~ (upper blocks in R) and diagonal-block inverses (diag of Binv).
+struct TrsmParams {
+    int n = 0, batch = 1, c_cap = 0;
+    const double* V = nullptr;
+    int64_t ldv = 0, strideV = 0;
+    double* Q = nullptr;
+    int64_t ldq = 0, strideQ = 0;
+    const double* R = nullptr;
+    int64_t ldr = 0, strideR = 0;
+    const double* Binv = nullptr;
+    int64_t ldb = 0, strideB = 0;
+    const double* dscale = nullptr;
+    int64_t strideD = 0;
+    const int* dimC = nullptr;
+    int64_t dimStride = 0;
+    const int* status = nullptr;
+};
+void trsm_right_upper(const TrsmParams& p, cudaStream_t st);
+bool trsm_supported(int c_cap);
+int trsm_smem_bytes(int c_cap);
 // Accurate reference rank test after CholeskyQR2: |r_kk| = |q_k^T v_k| against
 // 1e-13 ||V||_F (first failing column, sticky status).
 struct RankCheckParams {
