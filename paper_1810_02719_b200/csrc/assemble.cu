@@ -154,9 +154,9 @@ __global__ void scan_kernel(const int32_t* in, int64_t* out, int count) {
 // else b.
 __global__ void __launch_bounds__(NT) bandwidth_kernel(const int32_t* rowptr_all, const int32_t* cols_all,
                                                        const int64_t* csr_offsets, const int32_t* perm_all, int n,
-                                                       int32_t* bw_out, int32_t* blockw_out) {
+                                                       int32_t* bw_out, int32_t* blockw_out, int32_t* lower_out) {
     __shared__ int32_t pos[MAXN];
-    __shared__ int red_i[2];
+    __shared__ int red_i[3];
     const int tile = blockIdx.x;
     const int32_t* rowptr = rowptr_all + (int64_t)tile * (n + 1);
     const int32_t* cols = cols_all + csr_offsets[tile];
@@ -165,12 +165,20 @@ __global__ void __launch_bounds__(NT) bandwidth_kernel(const int32_t* rowptr_all
     if (threadIdx.x == 0) {
         red_i[0] = 0;
         red_i[1] = 0;
+        red_i[2] = 0;
     }
     __syncthreads();
-    int bw = 0;
-    for (int i = threadIdx.x; i < n; i += NT)
-        for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) bw = max(bw, abs(pos[i] - pos[cols[e]]));
+    int bw = 0, low = 0;
+    for (int i = threadIdx.x; i < n; i += NT) {
+        int li = 0;
+        for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+            bw = max(bw, abs(pos[i] - pos[cols[e]]));
+            li += pos[cols[e]] < pos[i];
+        }
+        low = max(low, li);
+    }
     atomicMax(&red_i[0], bw);
+    atomicMax(&red_i[2], low);
     __syncthreads();
     const int b = red_i[0];
     const int w = b - 1;
@@ -187,6 +195,7 @@ __global__ void __launch_bounds__(NT) bandwidth_kernel(const int32_t* rowptr_all
     if (threadIdx.x == 0) {
         bw_out[tile] = b;
         blockw_out[tile] = red_i[1] ? max(b, 1) : w;
+        if (lower_out) lower_out[tile] = red_i[2];
     }
 }
 
@@ -296,8 +305,10 @@ void exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int count, cudaS
 }
 
 void natural_bandwidth(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, const int32_t* perm,
-                       int ntiles, int n, int32_t* bw_out, int32_t* blockw_out, cudaStream_t st) {
-    if (ntiles) ::smg::count_launch(), bandwidth_kernel<<<ntiles, NT, 0, st>>>(rowptr, cols, csr_offsets, perm, n, bw_out, blockw_out);
+                       int ntiles, int n, int32_t* bw_out, int32_t* blockw_out, int32_t* lower_out, cudaStream_t st) {
+    if (ntiles)
+        ::smg::count_launch(), bandwidth_kernel<<<ntiles, NT, 0, st>>>(rowptr, cols, csr_offsets, perm, n, bw_out,
+                                                                      blockw_out, lower_out);
 }
 
 void rcm_order(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, int ntiles, int n,

@@ -88,7 +88,9 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
     // ordering: natural if block tridiagonal with W <= 64, else RCM
     bw.alloc(ntiles, st);
     blockw.alloc(ntiles, st);
-    natural_bandwidth(rowptr.get(), cols.get(), off.get(), nullptr, ntiles, n, bw.get(), blockw.get(), st);
+    DBuf<int32_t> lower;
+    lower.alloc(ntiles, st);
+    natural_bandwidth(rowptr.get(), cols.get(), off.get(), nullptr, ntiles, n, bw.get(), blockw.get(), lower.get(), st);
     std::vector<int32_t> bwh = download(blockw.get(), ntiles, st);
     int wmax = 1;
     for (int v : bwh) wmax = std::max(wmax, v);
@@ -96,11 +98,18 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
     if (supported_width(wmax) < 0) {
         perm.alloc((size_t)ntiles * n, st);
         rcm_order(rowptr.get(), cols.get(), off.get(), ntiles, n, perm.get(), st);
-        natural_bandwidth(rowptr.get(), cols.get(), off.get(), perm.get(), ntiles, n, bw.get(), blockw.get(), st);
+        natural_bandwidth(rowptr.get(), cols.get(), off.get(), perm.get(), ntiles, n, bw.get(), blockw.get(),
+                          lower.get(), st);
         bwh = download(blockw.get(), ntiles, st);
         wmax = 1;
         for (int v : bwh) wmax = std::max(wmax, v);
         use_perm = true;
+    }
+    {
+        std::vector<int32_t> lh = download(lower.get(), ntiles, st);
+        int lm = 1;
+        for (int v : lh) lm = std::max(lm, v);
+        cpl = round_up(lm, 2);  // couplings into the previous block <= lower neighbours
     }
     W = supported_width(wmax);
     if (W < 0) fail(2, "submesh bandwidth after RCM ordering exceeds the supported block width 64");
@@ -142,6 +151,7 @@ void FactorSet::factor(const TileSet& ts, int first_tile, int cnt, const double*
     p.Ffwd = fwd.get();
     p.Fbwd = bwd.get();
     p.strideF = strideF;
+    p.cpl = ts.cpl;
     p.status = status_out ? status_out : status.get();
     factor_tiles(p, st);
     SMG_CUDA(cudaGetLastError());

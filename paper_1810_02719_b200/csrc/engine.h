@@ -84,6 +84,7 @@ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 struct TileSet {
     int ntiles = 0, n = 0;
     int W = 0, Kb = 0, npad = 0;
+    int cpl = 16;  // bound on a row's couplings into the previous block (factor smem stride)
     bool use_perm = false;
     int64_t total_nnz = 0;
     DBuf<TileRef> refs;

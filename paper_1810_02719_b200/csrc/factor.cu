@@ -23,14 +23,17 @@ namespace {
 
 constexpr int NT = 256;
 
-constexpr int MAXCPL = 16;  // coupling entries per row into the previous block
-
+// Shared memory: three W x W matrices (S, P and L, where L holds Linv_{k-1}
+// until -P Linv_{k-1} is written and then receives Linv_k), the coupling lists
+// with a runtime stride (cpl = bound on a row's lower neighbours, from the
+// ordering pass) and the inverse permutation only for RCM-ordered tiles -- at
+// W = 64 in natural order that is ~106 KB, two CTAs per SM.
 template <int W>
 struct FactorSmem {
     static constexpr int LD = W + 4;  // LD % 16 == 4: conflict-free DMMA fragment reads
     static constexpr int MAT = W * LD;
-    static int bytes(int n) {
-        return (4 * MAT + 4 * W + 32) * 8 + ((n + 1) & ~1) * 4 + W * MAXCPL * (8 + 4) + W * 4;
+    static int bytes(int n, int cpl, bool permuted) {
+        return (3 * MAT + 4 * W + 32) * 8 + (permuted ? ((n + 1) & ~1) * 4 : 0) + W * cpl * (8 + 4) + W * 4;
     }
 };
 
@@ -75,17 +78,18 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
     extern __shared__ __align__(16) double sm[];
     double* S = sm;              // Schur complement / L_kk (lower)
     double* P = sm + MAT;        // L_{k,k-1}
-    double* Lp = sm + 2 * MAT;   // Linv_{k-1}
-    double* Lc = sm + 3 * MAT;   // Linv_k
-    double* sig = sm + 4 * MAT;  // Sigma_k
+    double* Lp = sm + 2 * MAT;   // Linv_{k-1}, then (same buffer) Linv_k
+    double* Lc = Lp;
+    double* sig = sm + 3 * MAT;  // Sigma_k
     double* sigp = sig + W;      // Sigma_{k-1}
     double* piv = sigp + W;      // pivots of the current block
     double* rsc = piv + W;       // 1 / (l_jj sigma_j)
     int* flag = reinterpret_cast<int*>(rsc + W);
-    int* ipos = reinterpret_cast<int*>(rsc + W + 32);
-    double* cval = reinterpret_cast<double*>(ipos + ((p.n + 1) & ~1));  // [W][MAXCPL]
-    int* cidx = reinterpret_cast<int*>(cval + W * MAXCPL);             // [W][MAXCPL]
-    int* ccnt = cidx + W * MAXCPL;                                     // [W]
+    const int CPL = p.cpl;
+    int* ipos = reinterpret_cast<int*>(rsc + W + 32);                                  // RCM only
+    double* cval = reinterpret_cast<double*>(ipos + (p.perm ? ((p.n + 1) & ~1) : 0));  // [W][CPL]
+    int* cidx = reinterpret_cast<int*>(cval + W * CPL);                                // [W][CPL]
+    int* ccnt = cidx + W * CPL;                                                        // [W]
     using FT = FTile<W>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t4 = lane & 3;
@@ -105,7 +109,8 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
     constexpr int FR = factor_row(W);
     const int64_t slab = (int64_t)2 * W * FR;
 
-    for (int i = tid; i < n; i += NT) ipos[perm ? perm[i] : i] = i;
+    if (perm)
+        for (int i = tid; i < n; i += NT) ipos[perm[i]] = i;
     if (tid == 0) flag[0] = 0;
     // ownership of the W x W upper triangle (a <= b), enumerated row by row
     constexpr int NOWN = (W * (W + 1) / 2 + NT - 1) / NT;
@@ -139,14 +144,14 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
             } else {
                 const int i = perm ? perm[prow] : prow;
                 for (int e = rowptr[i]; e < rowptr[i + 1]; ++e) {
-                    const int pq = ipos[cols[e]];
+                    const int pq = perm ? ipos[cols[e]] : cols[e];
                     const int q = pq - r0;
                     if (q >= 0 && q < W) {
                         S[r * LD + q] = (cols[e] == i) ? vals[e] + delta : vals[e];
                     } else if (q >= -W && q < 0) {
-                        if (cnt < MAXCPL) {
-                            cidx[r * MAXCPL + cnt] = q + W;
-                            cval[r * MAXCPL + cnt] = vals[e];
+                        if (cnt < CPL) {
+                            cidx[r * CPL + cnt] = q + W;
+                            cval[r * CPL + cnt] = vals[e];
                         }
                         ++cnt;
                     } else if (q < -W || q >= 2 * W) {
@@ -155,22 +160,39 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
                 }
             }
             ccnt[r] = cnt;
-            if (cnt > MAXCPL) flag[0] = 2;
+            if (cnt > CPL) flag[0] = 2;
         }
         __syncthreads();
         if (k > 0) {
             // ---- P = B_k Linv_{k-1}^T Sigma_{k-1}  (= L_{k,k-1}), B_k sparse
             for (int e = tid; e < W * W; e += NT) {
                 const int r = e / W, c = e % W;
-                const int cnt = min(ccnt[r], MAXCPL);
+                const int cnt = min(ccnt[r], CPL);
                 double acc = 0.0;
                 for (int q = 0; q < cnt; ++q) {
-                    const int qq = cidx[r * MAXCPL + q];
-                    if (c >= qq) acc += cval[r * MAXCPL + q] * Lp[c * LD + qq];
+                    const int qq = cidx[r * CPL + q];
+                    if (c >= qq) acc += cval[r * CPL + q] * Lp[c * LD + qq];
                 }
                 P[r * LD + c] = acc * sigp[c];
             }
             __syncthreads();
+        // ---- Fbwd_{k-1}^T second half: -(L_{k,k-1} Linv_{k-1}) = -(P Lp), row-major
+        if (mma_warp) {
+            double* Fp = Fb + (int64_t)(k - 1) * slab;
+            double acc[FT::MT][FT::NTT][2] = {};
+            fblock_mma<W>(
+                acc, [&](int m, int kk) { return P[m * LD + kk]; }, [&](int kk, int nn) { return Lp[kk * LD + nn]; },
+                [](int, int) { return false; }, wm, wn, g, t4);
+#pragma unroll
+            for (int i = 0; i < FT::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < FT::NTT; ++j) {
+                    const int r = 8 * (wm * FT::MT + i) + g, jj = 8 * (wn * FT::NTT + j) + 2 * t4;
+                    double2* dst = reinterpret_cast<double2*>(Fp + (int64_t)(W + r) * FR + jj);
+                    *dst = make_double2(-acc[i][j][0], -acc[i][j][1]);
+                }
+        }
+
             // ---- S -= P Sigma_{k-1} P^T  (DMMA; full block, the lower triangle is used)
             if (mma_warp) {
                 double acc[FT::MT][FT::NTT][2] = {};
@@ -267,22 +289,6 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
                         F[(int64_t)(W + jj) * FR + r] = -acc[i][j][q];
                     }
         }
-        // ---- Fbwd_{k-1}^T second half: -(L_{k,k-1} Linv_{k-1}) = -(P Lp), row-major
-        if (k > 0 && mma_warp) {
-            double* Fp = Fb + (int64_t)(k - 1) * slab;
-            double acc[FT::MT][FT::NTT][2] = {};
-            fblock_mma<W>(
-                acc, [&](int m, int kk) { return P[m * LD + kk]; }, [&](int kk, int nn) { return Lp[kk * LD + nn]; },
-                [](int, int) { return false; }, wm, wn, g, t4);
-#pragma unroll
-            for (int i = 0; i < FT::MT; ++i)
-#pragma unroll
-                for (int j = 0; j < FT::NTT; ++j) {
-                    const int r = 8 * (wm * FT::MT + i) + g, jj = 8 * (wn * FT::NTT + j) + 2 * t4;
-                    double2* dst = reinterpret_cast<double2*>(Fp + (int64_t)(W + r) * FR + jj);
-                    *dst = make_double2(-acc[i][j][0], -acc[i][j][1]);
-                }
-        }
         // ---- Fbwd_k^T first half: row j = sigma_j * Linv_k[j, :]
         {
             double* Fc = Fb + (int64_t)k * slab;
@@ -294,8 +300,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
                 for (int e = tid; e < W * W; e += NT) Fc[(int64_t)(W + e / W) * FR + e % W] = 0.0;
         }
         __syncthreads();
-        // ---- carry Linv_k, Sigma_k
-        for (int e = tid; e < W * W; e += NT) Lp[(e / W) * LD + (e % W)] = Lc[(e / W) * LD + (e % W)];
+        // ---- carry Sigma_k (Linv_k already sits in the L buffer)
         for (int e = tid; e < W; e += NT) sigp[e] = sig[e];
         __syncthreads();
     }
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
 
 template <int W>
 void launch(const FactorParams& p, cudaStream_t st) {
-    const int bytes = FactorSmem<W>::bytes(p.n);
+    const int bytes = FactorSmem<W>::bytes(p.n, p.cpl, p.perm != nullptr);
     cudaFuncSetAttribute(factor_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     ::smg::count_launch(), factor_kernel<W><<<p.ntiles, NT, bytes, st>>>(p);
 }
@@ -313,10 +318,10 @@ void launch(const FactorParams& p, cudaStream_t st) {
 
 int factor_smem_bytes(int W) {
     switch (W) {
-        case 16: return FactorSmem<16>::bytes(0);
-        case 32: return FactorSmem<32>::bytes(0);
-        case 48: return FactorSmem<48>::bytes(0);
-        default: return FactorSmem<64>::bytes(0);
+        case 16: return FactorSmem<16>::bytes(0, 16, false);
+        case 32: return FactorSmem<32>::bytes(0, 16, false);
+        case 48: return FactorSmem<48>::bytes(0, 16, false);
+        default: return FactorSmem<64>::bytes(0, 16, false);
     }
 }
 

@@ -50,7 +50,7 @@ void assemble_fill(const TileRef* tiles, int ntiles, int n, int weighting, const
                    int64_t* status_detail, cudaStream_t st);
 void exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int count, cudaStream_t st);
 void natural_bandwidth(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, const int32_t* perm,
-                       int ntiles, int n, int32_t* bw_out, int32_t* blockw_out, cudaStream_t st);
+                       int ntiles, int n, int32_t* bw_out, int32_t* blockw_out, int32_t* lower_out, cudaStream_t st);
 void rcm_order(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, int ntiles, int n,
                int32_t* perm, cudaStream_t st);
 
@@ -71,6 +71,7 @@ struct FactorParams {
     double* Fbwd = nullptr;
     int64_t strideF = 0;  // doubles per tile
     int* status = nullptr;
+    int cpl = 16;  // bound on a row's couplings into the previous block (lower neighbours)
 };
 void factor_tiles(const FactorParams& p, cudaStream_t st);
 int factor_smem_bytes(int W);
