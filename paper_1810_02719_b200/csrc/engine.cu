@@ -178,8 +178,9 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     work.alloc(cc, st);
     // split-K over the n rows for the Gram: aim at ~2 waves of CTAs
     const int tiles = ((ld + 63) / 64) * ((ld + 63) / 64 + 1) / 2;
-    // ~4 waves of CTAs, each split at least 256 rows deep
-    splits = std::max(1, std::min(npad / 256, (592 + tiles * B - 1) / std::max(1, tiles * B)));
+    // ~8 waves of CTAs, each split at least 256 rows deep (measured best at C5)
+    splits = std::max(1, std::min(npad / 256, (1184 + tiles * B - 1) / std::max(1, tiles * B)));
+    if (const char* e = std::getenv("SMG_GRAM_SPLITS")) splits = std::max(1, std::min(npad / 64, std::atoi(e)));
     Gws.alloc((size_t)B * splits * ld * ld, st);
     rdiag.alloc((size_t)B * ld, st);
     vnorm.alloc(B, st);
