@@ -66,7 +66,7 @@ struct Slab {
 };
 
 template <bool TA, bool TB, int NJ>
-__global__ void __launch_bounds__(NT) gemm_kernel(GemmParams p, int n_base, int n_end) {
+__global__ void __launch_bounds__(NT, 4) gemm_kernel(GemmParams p, int n_base, int n_end) {
     constexpr int BN = 16 * NJ;
     // op(A) element (m, k): TA ? A[k*lda + m] : A[m*lda + k]  -> k-major iff TA
     // op(B) element (k, n): TB ? B[n*ldb + k] : B[k*ldb + n]  -> k-major iff !TB
