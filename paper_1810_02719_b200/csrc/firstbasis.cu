@@ -138,6 +138,7 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
     const int deg = 30;
     DBuf<double> dcoef;          // [deg][B] alpha | [deg][B] gamma | [B] shift
     int iters_next = (m == n) ? 0 : (use_cheb ? 4 : 6);
+    if (const char* e = std::getenv("SMG_FB_BOOT")) iters_next = std::max(1, std::atoi(e));
     int cheb_apps = 0;
     double prev_bound = INFINITY;
     for (int round = 0; round < fc.max_rounds; ++round) {

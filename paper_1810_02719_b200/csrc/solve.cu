@@ -11,6 +11,8 @@
 // one chain and runs every sweep with only CTA barriers; no grid-wide sync.
 // The W x 2W factor slab of the next block streams into shared memory with
 // cp.async while the current one is multiplied (double buffer).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -181,7 +183,56 @@ SMG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
         : "memory");
 }
 
-template <int W, int CS>
+SMG_DEV void bulk_multicast(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+        "%4;\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+SMG_DEV void mbar_arrive_local(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrive on the mbarrier at the same offset in cluster CTA `rank`
+SMG_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+    asm volatile(
+        "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, %1;\n"
+        " mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(smem_u32(bar)),
+        "r"(rank)
+        : "memory");
+}
+SMG_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAITC_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+SMG_DEV uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+SMG_DEV uint32_t cluster_size() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
+    return r;
+}
+SMG_DEV void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// named barrier over the DMMA warps only (the producers run ahead on mbarriers)
+SMG_DEV void mma_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT_MMA) : "memory"); }
+
+// Warp-specialised: the DMMA warps run the steps (named barrier among
+// themselves for the epilogue rows), the producer warps run one step ahead
+// and never meet them at a CTA barrier -- they wait for a buffer to be
+// released (consumed[buf], one arrive per DMMA warp) and fill it (full[buf]).
+// MC: the column-slice CTAs of one chain form a cluster; every CTA releases a
+// buffer by arriving on rank 0's empty[buf], and rank 0 multicasts the factor
+// slab (read from L2 once per cluster) into every CTA's buffer.
+template <int W, int CS, bool MC>
 __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     using S = SolveSmem<W, CS>;
     using TL = SolveTiling<W, CS>;
@@ -193,7 +244,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     const int b = blockIdx.y;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const int col0 = blockIdx.x * CS;
-    if (col0 >= c) return;
+    if (!MC && col0 >= c) return;  // (MC launches only with every slice in range)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -207,81 +258,91 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     double* tmp = p.tmp + (int64_t)b * p.strideT;
     double* out = p.out + (int64_t)b * p.strideOut;
     const int sweeps = p.once ? 2 : 2 * p.z;
+    const int total = sweeps * Kb;
 
     const bool producer = tid >= NT_MMA;
     const int ptid = tid - NT_MMA;
-    __shared__ __align__(8) uint64_t full[2];
-    uint32_t phase[2] = {0u, 0u};
+    __shared__ __align__(8) uint64_t full[2], consumed[2], empty[2];
+    uint32_t csz = 1, crank = 0;
+    if (MC) {
+        csz = cluster_size();
+        crank = cluster_rank();
+    }
     if (tid == 0) {
-        mbar_init(&full[0], kProdWarps);  // one arrive per producer warp (+ tx bytes, cp.async)
-        mbar_init(&full[1], kProdWarps);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&full[i], kProdWarps);        // one arrive per producer warp (+ tx bytes, cp.async)
+            mbar_init(&consumed[i], kSolveWarps);  // one arrive per DMMA warp
+            mbar_init(&empty[i], (int)csz);        // rank 0 (MC): one arrive per cluster CTA
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    // producer warp: factor slab k and rhs rows of block k for `sweep` into
-    // buffer buf (one bulk copy for the slab, cp.async for the rhs rows),
-    // completing on full[buf]
-    auto issue = [&](int sweep, int k, int buf) {
-        const double* F = ((sweep & 1) ? Fbwd : Ffwd) + (int64_t)k * slab;
-        double* fs = Fs[buf];
-        double* xs = Xs[buf];
-        const int nvalid = max(0, min(W, n - k * W));  // rhs rows of the block inside the tile
-#ifdef SMG_SOLVE_NO_LOAD
-        if (lane == 0) mbar_arrive_expect_tx(&full[buf], 0);
-        (void)ptid;
-        (void)F;
-        (void)fs;
-        (void)xs;
-        (void)nvalid;
-        return;
-#endif
-        // rhs rows: 16-byte cp.async chunks from the producer lanes, tracked by
-        // the same mbarrier (cp.async.mbarrier.arrive, before the expect_tx arrive)
-        constexpr int CCH = CS / 2;
-        for (int e = ptid; e < W * CCH; e += NT_PROD) {
-            const int r = e / CCH, ch = e % CCH;
-            const int prow = k * W + r;
-            if (r < nvalid) {
-                const double* src = (sweep == 0) ? in + (int64_t)(perm ? perm[prow] : prow) * p.ldin + col0
-                                                 : tmp + (int64_t)prow * p.ldt + col0;
-                cp_async16(xs + r * XS + 2 * ch, src + 2 * ch);
-            } else {
-                cp_async16_zfill(xs + r * XS + 2 * ch, in, false);  // padded rows past n
-            }
-        }
-        asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[buf])) : "memory");
-        __syncwarp();
-        if (ptid == 0) {
-            mbar_arrive_expect_tx(&full[buf], (uint32_t)(2 * W * FS * 8));
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            bulk_g2s(fs, F, 2 * W * FS * 8, &full[buf]);
-        } else if (lane == 0) {
-            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&full[buf])) : "memory");
-        }
+    if (MC) cluster_sync_all();  // every CTA's barriers exist before the first remote arrive
+
+    auto block_of = [&](int gs) {
+        const int sweep = gs / Kb, step = gs % Kb;
+        return (sweep & 1) ? Kb - 1 - step : step;
     };
 
-    for (int sweep = 0; sweep < sweeps; ++sweep) {
-        const bool fwd = (sweep & 1) == 0;
-        const bool last = sweep == sweeps - 1;
-        int buf = 0;
-        {
-            const int k = fwd ? 0 : Kb - 1;
-            if (producer) issue(sweep, k, 0);
-            // previous-block rows of the first step are zero
-            for (int e = tid; e < W * XS; e += NT) Xs[0][W * XS + e] = 0.0;
-        }
-        for (int step = 0; step < Kb; ++step) {
-            const int k = fwd ? step : Kb - 1 - step;
-            __syncthreads();
-            if (producer) {
-                if (step + 1 < Kb) issue(sweep, fwd ? k + 1 : k - 1, buf ^ 1);
-                buf ^= 1;
-                continue;
+    if (producer) {
+        uint32_t cph[2] = {0u, 0u}, eph[2] = {0u, 0u};
+        for (int gs = 0; gs < total; ++gs) {
+            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), buf = gs & 1;
+            // the buffer's previous contents (step gs-2) are consumed; at a sweep's
+            // first step the previous sweep (its tmp rows) is complete
+            if (gs >= 2) {
+                mbar_wait(&consumed[buf], cph[buf]);
+                cph[buf] ^= 1u;
             }
-            mbar_wait(&full[buf], phase[buf]);
-            phase[buf] ^= 1u;
+            if (step == 0 && gs > 0)  // step gs-1 (the sweep's end) is consumed; the regular
+                mbar_wait(&consumed[buf ^ 1], cph[buf ^ 1]);  // wait of step gs+1 re-checks this phase
+            const double* F = ((sweep & 1) ? Fbwd : Ffwd) + (int64_t)k * slab;
+            double* fs = Fs[buf];
+            double* xs = Xs[buf];
+            const int nvalid = max(0, min(W, n - k * W));  // rhs rows of the block inside the tile
+            constexpr int CCH = CS / 2;
+            for (int e = ptid; e < W * CCH; e += NT_PROD) {
+                const int r = e / CCH, ch = e % CCH;
+                const int prow = k * W + r;
+                if (r < nvalid) {
+                    const double* src = (sweep == 0) ? in + (int64_t)(perm ? perm[prow] : prow) * p.ldin + col0
+                                                     : tmp + (int64_t)prow * p.ldt + col0;
+                    cp_async16(xs + r * XS + 2 * ch, src + 2 * ch);
+                } else {
+                    cp_async16_zfill(xs + r * XS + 2 * ch, in, false);  // padded rows past n
+                }
+            }
+            asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[buf])) : "memory");
+            __syncwarp();
+            if (ptid == 0) {
+                mbar_arrive_expect_tx(&full[buf], (uint32_t)(2 * W * FS * 8));
+                if constexpr (MC) {
+                    mbar_arrive_remote(&empty[buf], 0);  // this CTA's buffer is free and armed
+                    if (crank == 0) {
+                        mbar_wait_cluster(&empty[buf], eph[buf]);
+                        eph[buf] ^= 1u;
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        bulk_multicast(fs, F, 2 * W * FS * 8, &full[buf], (uint16_t)((1u << csz) - 1u));
+                    }
+                } else {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    bulk_g2s(fs, F, 2 * W * FS * 8, &full[buf]);
+                }
+            } else if (lane == 0) {
+                mbar_arrive_local(&full[buf]);
+            }
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+    } else {
+        uint32_t fph[2] = {0u, 0u};
+        for (int gs = 0; gs < total; ++gs) {
+            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), buf = gs & 1;
+            const bool fwd = (sweep & 1) == 0;
+            const bool last = sweep == sweeps - 1;
+            mbar_wait(&full[buf], fph[buf]);
+            fph[buf] ^= 1u;
             double acc[TL::MT][TL::NT][2];
-            const bool skip2 = step == 0;
+            const bool skip2 = step == 0;  // previous-block rows of a sweep's first step are zero
 #ifndef SMG_SOLVE_NO_MMA
             if (fwd) mma_step<W, CS, true>(Fs[buf], Xs[buf], acc, warp, g, t, skip2);
             else mma_step<W, CS, false>(Fs[buf], Xs[buf], acc, warp, g, t, skip2);
@@ -304,8 +365,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                         if (last) {
                             if (prow < n && col0 + cc < c) {
                                 const int lrow = perm ? perm[prow] : prow;
-                                double2* dst =
-                                    reinterpret_cast<double2*>(out + (int64_t)lrow * p.ldout + col0 + cc);
+                                double2* dst = reinterpret_cast<double2*>(out + (int64_t)lrow * p.ldout + col0 + cc);
                                 *dst = make_double2(acc[i][j][0], acc[i][j][1]);
                             }
                         } else {
@@ -314,25 +374,61 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                         }
                     }
             }
-            buf ^= 1;
+            if (step + 1 == Kb) {
+                // the next sweep's rhs rows (read by the producers) are this sweep's tmp rows
+                __threadfence_block();
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            }
+            mma_bar();  // xnext complete before the next step reads it; buf fully read
+            if (lane == 0) mbar_arrive_local(&consumed[buf]);
         }
-        // the next sweep's bulk copies (async proxy) read this sweep's rows of tmp
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        __threadfence_block();
+    }
+    if (MC) {
         __syncthreads();
+        cluster_sync_all();  // no CTA leaves while cluster peers may still address its barriers
     }
 }
 
 template <int W, int CS>
 void launch(const SolveParams& p, cudaStream_t st) {
     const int bytes = SolveSmem<W, CS>::BYTES;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(solve_kernel<W, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        configured = true;
+    const int slices = (p.c_cap + CS - 1) / CS;
+    int csz = 0;  // cluster size: largest divisor of the slice count in [2, 8]
+    // opt-in (SMG_SOLVE_MC=1): with two slab buffers the per-step cross-CTA
+    // release/multicast round trip sits on the critical path and the cluster
+    // runs slower than independent CTAs (1.48 ms vs 0.83 ms per C5 launch)
+    if (p.dimC == nullptr && std::getenv("SMG_SOLVE_MC"))
+        for (int d = 8; d >= 2; --d)
+            if (slices % d == 0) {
+                csz = d;
+                break;
+            }
+    static bool configured[2] = {false, false};
+    const bool mc = csz >= 2;
+    if (!configured[mc]) {
+        if (mc) cudaFuncSetAttribute(solve_kernel<W, CS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        else cudaFuncSetAttribute(solve_kernel<W, CS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        configured[mc] = true;
     }
-    dim3 grid((p.c_cap + CS - 1) / CS, p.batch);
-    ::smg::count_launch(), solve_kernel<W, CS><<<grid, NT, bytes, st>>>(p);
+    dim3 grid(slices, p.batch);
+    ::smg::count_launch();
+    if (!mc) {
+        solve_kernel<W, CS, false><<<grid, NT, bytes, st>>>(p);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csz;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, solve_kernel<W, CS, true>, p);
 }
 
 }  // namespace
@@ -341,8 +437,13 @@ void launch(const SolveParams& p, cudaStream_t st) {
 // wide slices when many chains already fill the 148 SMs.
 void solve_block_tridiag(const SolveParams& p, int W, cudaStream_t st) {
     const int slices8 = (p.c_cap + 7) / 8;
-    const bool wide = (int64_t)p.batch * ((p.c_cap + 31) / 32) >= 148;
-    const bool mid = (int64_t)p.batch * ((p.c_cap + 15) / 16) >= 148;
+    bool wide = (int64_t)p.batch * ((p.c_cap + 31) / 32) >= 148;
+    bool mid = (int64_t)p.batch * ((p.c_cap + 15) / 16) >= 148;
+    if (const char* e = std::getenv("SMG_SOLVE_CS")) {  // tuning override: 8, 16 or 32
+        const int cs = std::atoi(e);
+        wide = cs >= 32;
+        mid = cs >= 16;
+    }
     (void)slices8;
     switch (W) {
         case 16: launch<16, 8>(p, st); break;

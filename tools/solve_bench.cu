@@ -16,7 +16,7 @@ int main(int argc, char** argv) {
     const int c = argc > 2 ? atoi(argv[2]) : 200;
     const int reps = argc > 3 ? atoi(argv[3]) : 20;
     const int n = 2048, W = 64, Kb = n / W, ld = (c + 31) / 32 * 32;
-    const int64_t strideF = (int64_t)Kb * 2 * W * W;
+    const int64_t strideF = (int64_t)Kb * 2 * W * smg::factor_row(W);
     double *Ff, *Fb, *in, *tmp, *out;
     cudaMalloc(&Ff, sizeof(double) * strideF * B);
     cudaMalloc(&Fb, sizeof(double) * strideF * B);
