@@ -199,6 +199,102 @@ __global__ void __launch_bounds__(NT) bandwidth_kernel(const int32_t* rowptr_all
     }
 }
 
+
+// Geometric ordering candidate: local vertices sorted by their coordinate along
+// the axis of largest extent, ties by the second-largest axis, then by index.
+// On a grid tile this is the lexicographic order along the long side, whose
+// bandwidth is the short side + 1 (a 32 x 64 tile: W = 32 instead of 64).
+// One CTA per tile, bitonic sort of (key1, key2, index) in shared memory.
+__global__ void __launch_bounds__(512) axis_order_kernel(const double* X_all, int64_t strideX, int n, int32_t* perm_all) {
+    extern __shared__ __align__(16) double asort[];
+    int N2 = 1;
+    while (N2 < n) N2 <<= 1;
+    double* k1 = asort;
+    double* k2 = k1 + N2;
+    int* id = reinterpret_cast<int*>(k2 + N2);
+    __shared__ double wlo[16][3], whi[16][3];
+    __shared__ int axes[2];
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    const double* X = X_all + (int64_t)tile * strideX;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int i = tid; i < n; i += blockDim.x)
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = fmin(lo[d], X[(int64_t)i * 3 + d]);
+            hi[d] = fmax(hi[d], X[(int64_t)i * 3 + d]);
+        }
+    for (int d = 0; d < 3; ++d)
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+            hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+        }
+    if ((tid & 31) == 0)
+        for (int d = 0; d < 3; ++d) {
+            wlo[tid >> 5][d] = lo[d];
+            whi[tid >> 5][d] = hi[d];
+        }
+    __syncthreads();
+    if (tid == 0) {
+        double e[3];
+        for (int d = 0; d < 3; ++d) {
+            double l = INFINITY, h = -INFINITY;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                l = fmin(l, wlo[w][d]);
+                h = fmax(h, whi[w][d]);
+            }
+            e[d] = h - l;
+        }
+        int a0 = 0;
+        for (int d = 1; d < 3; ++d)
+            if (e[d] > e[a0]) a0 = d;
+        int a1 = (a0 == 0) ? 1 : 0;
+        for (int d = 0; d < 3; ++d)
+            if (d != a0 && e[d] > e[a1]) a1 = d;
+        axes[0] = a0;
+        axes[1] = a1;
+    }
+    __syncthreads();
+    const int a0 = axes[0], a1 = axes[1];
+    for (int i = tid; i < N2; i += blockDim.x) {
+        if (i < n) {
+            k1[i] = X[(int64_t)i * 3 + a0];
+            k2[i] = X[(int64_t)i * 3 + a1];
+        } else {
+            k1[i] = INFINITY;
+            k2[i] = INFINITY;
+        }
+        id[i] = i;
+    }
+    __syncthreads();
+    auto less = [&](int x, int y) {
+        if (k1[x] != k1[y]) return k1[x] < k1[y];
+        if (k2[x] != k2[y]) return k2[x] < k2[y];
+        return id[x] < id[y];
+    };
+    for (int size = 2; size <= N2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < N2; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    if (less(j, i) == up) {
+                        double t1 = k1[i];
+                        k1[i] = k1[j];
+                        k1[j] = t1;
+                        double t2 = k2[i];
+                        k2[i] = k2[j];
+                        k2[j] = t2;
+                        int ti = id[i];
+                        id[i] = id[j];
+                        id[j] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    int32_t* perm = perm_all + (int64_t)tile * n;
+    for (int r = tid; r < n; r += blockDim.x) perm[r] = id[r];
+}
+
 // Reverse Cuthill-McKee per tile (single-thread BFS in shared memory).
 // Start vertex: George-Liu pseudo-peripheral search from the lowest-degree
 // vertex; neighbours enqueued by (degree, index); every component restarts
@@ -309,6 +405,18 @@ void natural_bandwidth(const int32_t* rowptr, const int32_t* cols, const int64_t
     if (ntiles)
         ::smg::count_launch(), bandwidth_kernel<<<ntiles, NT, 0, st>>>(rowptr, cols, csr_offsets, perm, n, bw_out,
                                                                       blockw_out, lower_out);
+}
+
+void axis_order(const double* X, int64_t strideX, int ntiles, int n, int32_t* perm, cudaStream_t st) {
+    int N2 = 1;
+    while (N2 < n) N2 <<= 1;
+    const int bytes = N2 * (8 + 8 + 4);
+    static int configured = 0;
+    if (bytes > configured) {
+        cudaFuncSetAttribute(axis_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        configured = bytes;
+    }
+    if (ntiles) ::smg::count_launch(), axis_order_kernel<<<ntiles, 512, bytes, st>>>(X, strideX, n, perm);
 }
 
 void rcm_order(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, int ntiles, int n,

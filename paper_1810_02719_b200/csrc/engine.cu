@@ -50,10 +50,10 @@ void TileSet::build(const std::vector<TileRef>& tiles, int n_, int weighting, do
     }
     assemble_fill(refs.get(), ntiles, n, weighting, off.get(), rowptr.get(), cols.get(), vals.get(), trace.get(),
                   status.get(), detail.get(), st);
-    finish_build(shift_scale, nullptr, st);
     X.alloc((size_t)ntiles * n * 3, st);
     bbox.alloc(ntiles, st);
     gather_coords(refs.get(), ntiles, n, X.get(), (int64_t)n * 3, bbox.get(), st);
+    finish_build(shift_scale, nullptr, st, X.get());
     status_h = download(status.get(), ntiles, st);
     detail_h = download(detail.get(), ntiles, st);
 }
@@ -84,27 +84,55 @@ void TileSet::build_from_csr(int n_, const int32_t* rowptr_h, const int32_t* col
     finish_build(0.0, &dh, st);
 }
 
-void TileSet::finish_build(double shift_scale, const std::vector<double>* explicit_delta, cudaStream_t st) {
-    // ordering: natural if block tridiagonal with W <= 64, else RCM
+void TileSet::finish_build(double shift_scale, const std::vector<double>* explicit_delta, cudaStream_t st,
+                           const double* coords) {
+    // ordering: the narrowest block-tridiagonal width among the natural order,
+    // the geometric order along the tile's longest axis (when coordinates are
+    // known) and, if neither is supported, RCM
     bw.alloc(ntiles, st);
     blockw.alloc(ntiles, st);
     DBuf<int32_t> lower;
     lower.alloc(ntiles, st);
-    natural_bandwidth(rowptr.get(), cols.get(), off.get(), nullptr, ntiles, n, bw.get(), blockw.get(), lower.get(), st);
-    std::vector<int32_t> bwh = download(blockw.get(), ntiles, st);
-    int wmax = 1;
-    for (int v : bwh) wmax = std::max(wmax, v);
+    auto widest = [&](const int32_t* pm) {
+        natural_bandwidth(rowptr.get(), cols.get(), off.get(), pm, ntiles, n, bw.get(), blockw.get(), lower.get(), st);
+        std::vector<int32_t> h = download(blockw.get(), ntiles, st);
+        int w = 1;
+        for (int v : h) w = std::max(w, v);
+        return w;
+    };
+    int wmax = widest(nullptr);
     use_perm = false;
-    if (supported_width(wmax) < 0) {
-        perm.alloc((size_t)ntiles * n, st);
-        rcm_order(rowptr.get(), cols.get(), off.get(), ntiles, n, perm.get(), st);
-        natural_bandwidth(rowptr.get(), cols.get(), off.get(), perm.get(), ntiles, n, bw.get(), blockw.get(),
-                          lower.get(), st);
-        bwh = download(blockw.get(), ntiles, st);
-        wmax = 1;
-        for (int v : bwh) wmax = std::max(wmax, v);
-        use_perm = true;
+    // A narrower W halves the solve's flops and shrinks its per-step slabs, but
+    // doubles its sequential steps: worth it when many tiles keep the GPU
+    // throughput-bound, not for a few latency-bound chains whose natural order works.
+    if (coords && (supported_width(wmax) < 0 || ntiles >= 2048)) {
+        DBuf<int32_t> ap;
+        ap.alloc((size_t)ntiles * n, st);
+        axis_order(coords, (int64_t)n * 3, ntiles, n, ap.get(), st);
+        const int wa = widest(ap.get());
+        const int sn = supported_width(wmax), sa = supported_width(wa);
+        if (sa > 0 && (sn < 0 || sa < sn)) {
+            perm = std::move(ap);
+            use_perm = true;
+            wmax = wa;
+        }
     }
+    if (supported_width(widest(nullptr)) < 0) {
+        // the natural order is not block tridiagonal at W <= 64: RCM competes too
+        DBuf<int32_t> rp;
+        rp.alloc((size_t)ntiles * n, st);
+        rcm_order(rowptr.get(), cols.get(), off.get(), ntiles, n, rp.get(), st);
+        const int sr = supported_width(widest(rp.get()));
+        const int sc = use_perm ? supported_width(wmax) : -1;
+        if (sr > 0 && (sc < 0 || sr <= sc)) {
+            perm = std::move(rp);
+            use_perm = true;
+        } else if (sc < 0) {
+            perm = std::move(rp);  // unsupported either way: reported below
+            use_perm = true;
+        }
+    }
+    wmax = widest(use_perm ? perm.get() : nullptr);  // final order: width and coupling bound
     {
         std::vector<int32_t> lh = download(lower.get(), ntiles, st);
         int lm = 1;

@@ -100,7 +100,8 @@ struct TileSet {
     // one tile from a host CSR (operator primitives); delta given explicitly
     void build_from_csr(int n, const int32_t* rowptr, const int32_t* cols, const double* vals, double delta,
                         cudaStream_t st);
-    void finish_build(double shift_scale, const std::vector<double>* explicit_delta, cudaStream_t st);
+    void finish_build(double shift_scale, const std::vector<double>* explicit_delta, cudaStream_t st,
+                      const double* coords = nullptr);
     const int32_t* perm_of(int tile) const { return use_perm ? perm.get() + (int64_t)tile * n : nullptr; }
     void rebind(cudaStream_t st) {
         refs.rebind(st), nnz.rebind(st), rowptr.rebind(st), cols.rebind(st), perm.rebind(st), bw.rebind(st);

@@ -51,6 +51,7 @@ void assemble_fill(const TileRef* tiles, int ntiles, int n, int weighting, const
 void exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int count, cudaStream_t st);
 void natural_bandwidth(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, const int32_t* perm,
                        int ntiles, int n, int32_t* bw_out, int32_t* blockw_out, int32_t* lower_out, cudaStream_t st);
+void axis_order(const double* X, int64_t strideX, int ntiles, int n, int32_t* perm, cudaStream_t st);
 void rcm_order(const int32_t* rowptr, const int32_t* cols, const int64_t* csr_offsets, int ntiles, int n,
                int32_t* perm, cudaStream_t st);
 

@@ -125,6 +125,19 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
             one(8 * lo, 8 * hi, 0, lo);
             both(8 * hi, W);
         }
+    } else if constexpr (MT == 1) {
+        // one row tile: its nonzero k range is a loop bound
+        const int r = TL::tile(wm, 0);
+        const int k0 = FWD ? 0 : 8 * r, k1 = FWD ? 8 * r + 8 : W;
+#pragma unroll 2
+        for (int kk = k0; kk < k1; kk += 4) {
+            double b[NT];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
+            const double a = fs[(kk + t) * FS + 8 * r + g];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma884(acc[0][j][0], acc[0][j][1], a, b[j]);
+        }
     } else {
 #pragma unroll 2
     for (int kk = 0; kk < W; kk += 4) {
