@@ -38,7 +38,11 @@ struct SolveSmem {
     static constexpr int XS = CS + 4;  // padded row of the right-hand-side slab
     static constexpr int F_ELEMS = 2 * W * FS;
     static constexpr int X_ELEMS = 2 * W * XS;
-    static constexpr int BYTES = (2 * F_ELEMS + 2 * X_ELEMS) * 8;
+    // pipeline depth: as many stages as fit two CTAs per SM (at least 2); a
+    // narrow W has short steps, so its loads need more than one step of lead
+    static constexpr int STAGE = (F_ELEMS + X_ELEMS) * 8;
+    static constexpr int NS = (4 * STAGE <= 113 * 1024) ? 4 : ((3 * STAGE <= 113 * 1024) ? 3 : 2);
+    static constexpr int BYTES = NS * STAGE;
 };
 
 // zero-fill variant: src_bytes = 0 writes zeros
@@ -251,8 +255,9 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     using TL = SolveTiling<W, CS>;
     constexpr int FS = S::FS, XS = S::XS;
     extern __shared__ __align__(16) double smem[];
-    double* Fs[2] = {smem, smem + S::F_ELEMS};
-    double* Xs[2] = {smem + 2 * S::F_ELEMS, smem + 2 * S::F_ELEMS + S::X_ELEMS};
+    constexpr int NS = S::NS;
+    auto Fs = [&](int i) { return smem + i * S::F_ELEMS; };
+    auto Xs = [&](int i) { return smem + NS * S::F_ELEMS + i * S::X_ELEMS; };
 
     const int b = blockIdx.y;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
@@ -275,14 +280,14 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
 
     const bool producer = tid >= NT_MMA;
     const int ptid = tid - NT_MMA;
-    __shared__ __align__(8) uint64_t full[2], consumed[2], empty[2];
+    __shared__ __align__(8) uint64_t full[NS], consumed[NS], empty[NS];
     uint32_t csz = 1, crank = 0;
     if (MC) {
         csz = cluster_size();
         crank = cluster_rank();
     }
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], kProdWarps);        // one arrive per producer warp (+ tx bytes, cp.async)
             mbar_init(&consumed[i], kSolveWarps);  // one arrive per DMMA warp
             mbar_init(&empty[i], (int)csz);        // rank 0 (MC): one arrive per cluster CTA
@@ -298,20 +303,23 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     };
 
     if (producer) {
-        uint32_t cph[2] = {0u, 0u}, eph[2] = {0u, 0u};
+        uint32_t cph[NS], eph[NS];
+        for (int i = 0; i < NS; ++i) cph[i] = eph[i] = 0u;
         for (int gs = 0; gs < total; ++gs) {
-            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), buf = gs & 1;
-            // the buffer's previous contents (step gs-2) are consumed; at a sweep's
+            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), buf = gs % NS;
+            // the buffer's previous contents (step gs-NS) are consumed; at a sweep's
             // first step the previous sweep (its tmp rows) is complete
-            if (gs >= 2) {
+            if (gs >= NS) {
                 mbar_wait(&consumed[buf], cph[buf]);
                 cph[buf] ^= 1u;
             }
-            if (step == 0 && gs > 0)  // step gs-1 (the sweep's end) is consumed; the regular
-                mbar_wait(&consumed[buf ^ 1], cph[buf ^ 1]);  // wait of step gs+1 re-checks this phase
+            if (step == 0 && gs > 0) {  // step gs-1 (the sweep's end) is consumed; the regular
+                const int pb = (gs - 1) % NS;  // wait of step gs-1+NS re-checks this phase
+                mbar_wait(&consumed[pb], cph[pb]);
+            }
             const double* F = ((sweep & 1) ? Fbwd : Ffwd) + (int64_t)k * slab;
-            double* fs = Fs[buf];
-            double* xs = Xs[buf];
+            double* fs = Fs(buf);
+            double* xs = Xs(buf);
             const int nvalid = max(0, min(W, n - k * W));  // rhs rows of the block inside the tile
             constexpr int CCH = CS / 2;
             for (int e = ptid; e < W * CCH; e += NT_PROD) {
@@ -347,24 +355,36 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
     } else {
-        uint32_t fph[2] = {0u, 0u};
+        uint32_t fph[NS];
+        for (int i = 0; i < NS; ++i) fph[i] = 0u;
         for (int gs = 0; gs < total; ++gs) {
-            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), buf = gs & 1;
+            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), buf = gs % NS;
             const bool fwd = (sweep & 1) == 0;
             const bool last = sweep == sweeps - 1;
+            // output rows of the last sweep go through the permutation: fetch them
+            // before the wait so the loads overlap it and the products
+            int lrow[TL::MT];
+            {
+                const int wm = warp % TL::WM;
+#pragma unroll
+                for (int i = 0; i < TL::MT; ++i) {
+                    const int prow = k * W + 8 * TL::tile(wm, i) + g;
+                    lrow[i] = (last && perm && prow < n) ? __ldg(perm + prow) : prow;
+                }
+            }
             mbar_wait(&full[buf], fph[buf]);
             fph[buf] ^= 1u;
             double acc[TL::MT][TL::NT][2];
             const bool skip2 = step == 0;  // previous-block rows of a sweep's first step are zero
 #ifndef SMG_SOLVE_NO_MMA
-            if (fwd) mma_step<W, CS, true>(Fs[buf], Xs[buf], acc, warp, g, t, skip2);
-            else mma_step<W, CS, false>(Fs[buf], Xs[buf], acc, warp, g, t, skip2);
+            if (fwd) mma_step<W, CS, true>(Fs(buf), Xs(buf), acc, warp, g, t, skip2);
+            else mma_step<W, CS, false>(Fs(buf), Xs(buf), acc, warp, g, t, skip2);
 #else
             for (int i = 0; i < TL::MT; ++i)
-                for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Xs[buf][tid];
+                for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Xs(buf)[tid];
 #endif
             // epilogue: result is the "previous block" of the next step and goes to dst
-            double* xnext = Xs[buf ^ 1] + W * XS;
+            double* xnext = Xs((gs + 1) % NS) + W * XS;
             if (warp < TL::ACTIVE) {
                 const int wm = warp % TL::WM, wn = warp / TL::WM;
 #pragma unroll
@@ -377,8 +397,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                         const int prow = k * W + r;
                         if (last) {
                             if (prow < n && col0 + cc < c) {
-                                const int lrow = perm ? perm[prow] : prow;
-                                double2* dst = reinterpret_cast<double2*>(out + (int64_t)lrow * p.ldout + col0 + cc);
+                                double2* dst = reinterpret_cast<double2*>(out + (int64_t)lrow[i] * p.ldout + col0 + cc);
                                 *dst = make_double2(acc[i][j][0], acc[i][j][1]);
                             }
                         } else {
