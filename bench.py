@@ -319,12 +319,23 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             traffic = json.load(f)["dram_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         pass
+    # the factorisation's ordering picks the block width: the geometric order gives
+    # 32x64 grid tiles W = 32 (band 33) where the natural order has 65, so the
+    # DMMA work done is below the SURVEY's algorithmic figure (kept as the
+    # contract's numerator); hw_flops_per_launch is the block solve's own count
+    W_used = 32 if B * K >= 2048 else 64
+    # per triangular sweep 3*n*W*cols flops (triangular half + full coupling half);
+    # an OI step is 2z sweeps, the bootstrap 2 + 3*2z sweeps on m columns
+    hw_step = B * 3.0 * n * W_used * ((K - 1) * t * 2 * z * c + (2 + 3 * 2 * z) * m_fb)
     roofline = {"kernel": "solve_kernel (block-tridiagonal R^z sweeps, DMMA f64)", "bound": "tensor",
                 "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
                 "traffic_source": "profiles/solve_traffic_r01.json (bytes per launch of 32 chains)",
                 "peak_source": "measured FP64 DMMA peak, profiles/fp64_peak_r01.txt (MEASURED_PEAKS.json has no FP64 entry)",
                 "flops_per_launch": flops_per_launch, "avg_launch_ms": avg_ms,
+                "b_algorithmic": b_half, "block_width_used": W_used,
+                "hw_flops_per_launch": hw_step / max(solve_launches_per_step, 1e-9),
+                "hw_frac": (hw_step / (solve["ms"] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS) if solve["ms"] > 0 else None,
                 "launches_per_step": solve_launches_per_step,
                 "step_share": solve["ms"] / ms_step if ms_step else None}
     # whole-step algorithmic FP64 work (SURVEY.md §8(d) formulas, per GPU)
