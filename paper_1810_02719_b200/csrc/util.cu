@@ -140,28 +140,41 @@ __global__ void __launch_bounds__(SPMM_NT) spmm_kernel(SpmmParams p) {
         return q < SPMM_MAXNZ ? sval[warp][q] : vals[s + q] + (cols[s + q] == i ? shift : 0.0);
     };
     if ((c & 1) == 0 && (p.ldx & 1) == 0 && (p.ldy & 1) == 0) {
-        for (int j = 2 * lane; j < c; j += 64) {
-            double2 acc = make_double2(0.0, 0.0);
-            for (int q = 0; q < nz; ++q) {
-                const double v = sval[warp][q];
-                const double2 x = *reinterpret_cast<const double2*>(X + (int64_t)scol[warp][q] * p.ldx + j);
-                acc.x = fma(v, x.x, acc.x);
-                acc.y = fma(v, x.y, acc.y);
+        // U column groups of 64 per pass: every neighbour row contributes U
+        // independent double2 loads per lane, so up to nz*U loads are in flight
+        constexpr int U = 4;
+        for (int j0 = 2 * lane; j0 < c; j0 += 64 * U) {
+            double2 acc[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] = make_double2(0.0, 0.0);
+            auto add_row = [&](double v, int col) {
+                const double* xr = X + (int64_t)col * p.ldx;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + 64 * u;
+                    if (j < c) {
+                        const double2 x = *reinterpret_cast<const double2*>(xr + j);
+                        acc[u].x = fma(v, x.x, acc[u].x);
+                        acc[u].y = fma(v, x.y, acc[u].y);
+                    }
+                }
+            };
+            for (int q = 0; q < nz; ++q) add_row(sval[warp][q], scol[warp][q]);
+            for (int q = nz; q < nzt; ++q) add_row(val_of(q), col_of(q));
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + 64 * u;
+                if (j >= c) continue;
+                double2 a = acc[u];
+                a.x *= alpha;
+                a.y *= alpha;
+                if (Zb) {
+                    const double2 z = *reinterpret_cast<const double2*>(Zb + (int64_t)i * p.ldz + j);
+                    a.x = fma(gam, z.x, a.x);
+                    a.y = fma(gam, z.y, a.y);
+                }
+                *reinterpret_cast<double2*>(Y + (int64_t)i * p.ldy + j) = a;
             }
-            for (int q = nz; q < nzt; ++q) {
-                const double v = val_of(q);
-                const double2 x = *reinterpret_cast<const double2*>(X + (int64_t)col_of(q) * p.ldx + j);
-                acc.x = fma(v, x.x, acc.x);
-                acc.y = fma(v, x.y, acc.y);
-            }
-            acc.x *= alpha;
-            acc.y *= alpha;
-            if (Zb) {
-                const double2 z = *reinterpret_cast<const double2*>(Zb + (int64_t)i * p.ldz + j);
-                acc.x = fma(gam, z.x, acc.x);
-                acc.y = fma(gam, z.y, acc.y);
-            }
-            *reinterpret_cast<double2*>(Y + (int64_t)i * p.ldy + j) = acc;
         }
     } else {
         for (int j = lane; j < c; j += 32) {
