@@ -140,18 +140,30 @@ __global__ void __launch_bounds__(NT, 4) gemm_kernel(GemmParams p, int n_base, i
         const double* as = As[buf];
         const double* bs = Bs[buf];
         if (fmask == kFull && k0 + BK <= kdiag) {
-            // interior: every fragment active, no predication
+            // interior: every fragment active, no predication; m16n8k8 (4x the
+            // work per instruction of m8n8k4, same accumulator registers)
 #pragma unroll
-            for (int kk = 0; kk < BK; kk += 4) {
-                double a[4], bb[NJ];
+            for (int kk = 0; kk < BK; kk += 8) {
+                double a[2][4], bb[NJ][2];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = SA::at(as, kk + t, wm + 8 * i + g);
+                for (int I = 0; I < 2; ++I) {
+                    const int r = wm + 16 * I + g;
+                    a[I][0] = SA::at(as, kk + t, r);
+                    a[I][1] = SA::at(as, kk + t, r + 8);
+                    a[I][2] = SA::at(as, kk + t + 4, r);
+                    a[I][3] = SA::at(as, kk + t + 4, r + 8);
+                }
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) bb[j] = SB::at(bs, kk + t, wn + 8 * j + g);
+                for (int j = 0; j < NJ; ++j) {
+                    bb[j][0] = SB::at(bs, kk + t, wn + 8 * j + g);
+                    bb[j][1] = SB::at(bs, kk + t + 4, wn + 8 * j + g);
+                }
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int I = 0; I < 2; ++I)
 #pragma unroll
-                    for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+                    for (int j = 0; j < NJ; ++j)
+                        dmma1688(acc[2 * I][j][0], acc[2 * I][j][1], acc[2 * I + 1][j][0], acc[2 * I + 1][j][1],
+                                 a[I][0], a[I][1], a[I][2], a[I][3], bb[j][0], bb[j][1]);
             }
         } else if (fmask != 0 && k0 < kdiag + 8 * NJ) {
 #pragma unroll
