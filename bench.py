@@ -11,8 +11,11 @@ reconstruction (+ the NCCL gather of per-mesh results to all ranks when N > 1).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5|C2|C3|C4]
   python bench.py --impl reference ...     # CPU oracle (port) arm
 
-Chains shard across ranks with no data-path collective (strong scaling: the 64
-meshes are split over N GPUs).  Timing: W untimed warm-up steps, then K steps
+Chains shard across ranks with no data-path collective.  Default: weak
+scaling -- each GPU carries config 5's 64-mesh shard (mesh ids rank*64 ..
+rank*64+63, each its own seed), the job grows with N; `--strong` splits the 64
+meshes over the N GPUs instead.  The per-mesh reconstructions are all-gathered
+(NCCL over NVLink) at the end of every step.  Timing: W untimed warm-up steps, then K steps
 bracketed by barrier + synchronize, CUDA events on the launching device, max
 over ranks.  Inputs (0.9 GB for C5) exceed the 126 MB L2.
 """
@@ -52,7 +55,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
-    ap.add_argument("--meshes", type=int, default=0, help="override the mesh count (debug)")
+    ap.add_argument("--meshes", type=int, default=0, help="override the per-GPU mesh count (debug)")
+    ap.add_argument("--strong", action="store_true", help="split the config's meshes over the GPUs (strong scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tiles", type=int, default=8, help="tiles per chain in the CPU sample")
     return ap.parse_args()
@@ -222,7 +226,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    total_meshes = args.meshes or cfg["meshes"]
+    per_gpu = args.meshes or cfg["meshes"]
+    total_meshes = per_gpu if args.strong else per_gpu * world
     if cfg["meshes"] == 1:  # single-chain configs: replicas only
         ids = [rank]
         total_units = world
@@ -345,13 +350,16 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": value * (1 if cfg["meshes"] > 1 else 1), "unit": "vertices/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "strong" if cfg["meshes"] > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong" if (args.strong and cfg["meshes"] > 1) else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded sinusoid height-field grids + N(0,sigma^2) noise; no dataset exists)",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes": total_units, "tiles_per_mesh": K,
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes": total_units, "meshes_per_gpu": len(ids),
+                   "tiles_per_mesh": K,
                    "n_d": n, "c": c, "oi_iterations": t, "z": z, "shift_scale": PINNED["shift_scale"],
                    "weighting": PINNED["weighting"], "tile_order": "row-major",
-                   "parallelism": f"chains sharded over {world} GPU(s)" if cfg["meshes"] > 1 else "replicas",
+                   "parallelism": (f"chains sharded over {world} GPU(s), "
+                                   + (f"{total_meshes} meshes split (strong)" if args.strong
+                                      else f"{len(ids)} meshes per GPU (weak)")) if cfg["meshes"] > 1 else "replicas",
                    "l2": "inputs larger than L2 (%.0f MB per GPU)" % (job.h2d_bytes / 1e6)},
         "e2e": {"value": e2e_value, "unit": "vertices/s", "h2d_bytes_per_step": job.h2d_bytes,
                 "d2h_bytes_per_step": job.d2h_bytes},
@@ -426,7 +434,7 @@ def cpu_baseline(args, cfg, total_units):
 
 
 def reference_arm(args, cfg):
-    total_units = args.meshes or cfg["meshes"]
+    total_units = (args.meshes or cfg["meshes"]) * (1 if args.strong else max(1, args.gpus))
     vals = []
     for _ in range(max(1, args.steps)):
         cb = cpu_baseline(args, cfg, total_units)
@@ -436,7 +444,7 @@ def reference_arm(args, cfg):
     ms_step = total_units * n_mesh / cb["value"] * 1e3
     return {"metric": METRIC, "value": cb["value"], "unit": "vertices/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if cfg["meshes"] > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if (args.strong and cfg["meshes"] > 1) else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded sinusoid height-field grids + N(0,sigma^2) noise)",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes": total_units},
             "impl": "reference", "cpu_baseline": cb,
