@@ -173,8 +173,10 @@ class GpuJob:
         self.pcfg.shift_scale = PINNED["shift_scale"]
         self._abi = _abi
         self.views = {on: self._views(on) for on in (0, 1)}
-        self.h2d_bytes = sum(t.numel() * t.element_size() for xyz in self.h_xyz for t in xyz) + self.B * sum(
-            t.numel() * t.element_size() for t in self.h_conn.values())
+        # per-mesh coordinates + the shared topology once (the library stages host
+        # arrays that several chains pass by the same pointer only once)
+        self.h2d_bytes = sum(t.numel() * t.element_size() for xyz in self.h_xyz for t in xyz) + sum(
+            self.h_conn[k].numel() * self.h_conn[k].element_size() for k in ("offs", "cols", "members"))
         self.d2h_bytes = self.h_recon.numel() * 8 + self.h_coef.numel() * 8 + self.B * 5 * self.K * 8
 
     def _views(self, on_device):

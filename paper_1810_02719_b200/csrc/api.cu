@@ -29,11 +29,15 @@ struct MeshDev {
     int64_t nv = 0;
     const double *x = nullptr, *y = nullptr, *z = nullptr;
     const int32_t *offs = nullptr, *cols = nullptr;
+    const int32_t *hoffs = nullptr, *hcols = nullptr;  // host arrays a staged copy came from
     DBuf<double> bx, by, bz;
     DBuf<int32_t> boffs, bcols;
 };
 
-void stage_mesh(const smg_mesh* m, MeshDev& d, cudaStream_t st) {
+// `shared`: an already staged mesh whose host connectivity arrays are the same
+// ones (batched chains over one mesh topology): its device copy is reused, so
+// the topology crosses PCIe once per call instead of once per chain.
+void stage_mesh(const smg_mesh* m, MeshDev& d, cudaStream_t st, const MeshDev* shared = nullptr) {
     require(m != nullptr, "mesh view is null");
     require(m->vertex_count >= 0, "mesh vertex count is negative");
     d.nv = m->vertex_count;
@@ -53,14 +57,21 @@ void stage_mesh(const smg_mesh* m, MeshDev& d, cudaStream_t st) {
     up_d(d.bx, m->x);
     up_d(d.by, m->y);
     up_d(d.bz, m->z);
+    d.x = d.bx.get();
+    d.y = d.by.get();
+    d.z = d.bz.get();
+    d.hoffs = m->adj_offsets;
+    d.hcols = m->adj_cols;
+    if (shared) {
+        d.offs = shared->offs;
+        d.cols = shared->cols;
+        return;
+    }
     d.boffs.alloc(d.nv + 1, st);
     SMG_CUDA(cudaMemcpyAsync(d.boffs.get(), m->adj_offsets, sizeof(int32_t) * (d.nv + 1), cudaMemcpyHostToDevice, st));
     d.bcols.alloc(nadj, st);
     if (nadj)
         SMG_CUDA(cudaMemcpyAsync(d.bcols.get(), m->adj_cols, sizeof(int32_t) * nadj, cudaMemcpyHostToDevice, st));
-    d.x = d.bx.get();
-    d.y = d.by.get();
-    d.z = d.bz.get();
     d.offs = d.boffs.get();
     d.cols = d.bcols.get();
 }
@@ -69,10 +80,11 @@ struct SegDev {
     int k = 0, n_d = 0;
     std::vector<int32_t> offs_h, seq_h, pos_of;
     const int32_t* members = nullptr;
+    const int32_t* hmembers = nullptr;  // host array a staged copy came from
     DBuf<int32_t> bmembers;
 };
 
-void stage_seg(const smg_segmentation* s, SegDev& d, cudaStream_t st) {
+void stage_seg(const smg_segmentation* s, SegDev& d, cudaStream_t st, const SegDev* shared = nullptr) {
     require(s != nullptr, "segmentation view is null");
     require(s->submesh_count >= 1, "cannot process an empty submesh list");
     d.k = s->submesh_count;
@@ -90,9 +102,14 @@ void stage_seg(const smg_segmentation* s, SegDev& d, cudaStream_t st) {
         std::memcpy(d.offs_h.data(), s->member_offsets, sizeof(int32_t) * (d.k + 1));
         if (s->sequence_length) std::memcpy(d.seq_h.data(), s->sequence, sizeof(int32_t) * s->sequence_length);
         const int64_t tot = d.offs_h[d.k];
-        d.bmembers.alloc(tot, st);
-        SMG_CUDA(cudaMemcpyAsync(d.bmembers.get(), s->members, sizeof(int32_t) * tot, cudaMemcpyHostToDevice, st));
-        d.members = d.bmembers.get();
+        d.hmembers = s->members;
+        if (shared && shared->offs_h == d.offs_h) {
+            d.members = shared->members;
+        } else {
+            d.bmembers.alloc(tot, st);
+            SMG_CUDA(cudaMemcpyAsync(d.bmembers.get(), s->members, sizeof(int32_t) * tot, cudaMemcpyHostToDevice, st));
+            d.members = d.bmembers.get();
+        }
     }
     require((int)d.seq_h.size() == d.k, "the order sequence must be a permutation of the submesh ids");
     d.pos_of.assign(d.k, -1);
@@ -265,8 +282,17 @@ public:
         segs_.resize(B_);
         outs_.resize(B_);
         for (int b = 0; b < B_; ++b) {
-            stage_mesh(&meshes[b], meshes_[b], st_);
-            stage_seg(&segs[b], segs_[b], st_);
+            const MeshDev* msh = nullptr;
+            const SegDev* ssh = nullptr;
+            for (int q = 0; q < b && !(msh && ssh); ++q) {
+                const smg_mesh& m = meshes[b];
+                if (!msh && !m.on_device && meshes_[q].hoffs == m.adj_offsets && meshes_[q].hcols == m.adj_cols &&
+                    meshes_[q].nv == m.vertex_count)
+                    msh = &meshes_[q];
+                if (!ssh && !segs[b].on_device && segs_[q].hmembers == segs[b].members) ssh = &segs_[q];
+            }
+            stage_mesh(&meshes[b], meshes_[b], st_, msh);
+            stage_seg(&segs[b], segs_[b], st_, ssh);
             outs_[b].out = &outs[b];
         }
         K_ = segs_[0].k;
