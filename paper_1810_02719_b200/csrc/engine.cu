@@ -2,6 +2,7 @@
 #include <cstdio>
 
 #include <cstdlib>
+#include <string>
 
 #include "engine.h"
 #include "profiler.h"
@@ -102,10 +103,14 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
     };
     int wmax = widest(nullptr);
     use_perm = false;
+    // SMG_ORDERING=geometric|natural forces a candidate (tests exercise every path)
+    const char* force = std::getenv("SMG_ORDERING");
+    const bool force_geo = force && std::string(force) == "geometric";
+    const bool force_nat = force && std::string(force) == "natural";
     // A narrower W halves the solve's flops and shrinks its per-step slabs, but
     // doubles its sequential steps: worth it when many tiles keep the GPU
     // throughput-bound, not for a few latency-bound chains whose natural order works.
-    if (coords && (supported_width(wmax) < 0 || ntiles >= 2048)) {
+    if (coords && !force_nat && (supported_width(wmax) < 0 || ntiles >= 2048 || force_geo)) {
         DBuf<int32_t> ap;
         ap.alloc((size_t)ntiles * n, st);
         axis_order(coords, (int64_t)n * 3, ntiles, n, ap.get(), st);

@@ -97,3 +97,22 @@ def test_config4_doi_controller_properties(ctx):
     assert np.all(np.isfinite(bb.reconstruction))
     rel = np.linalg.norm(bb.reconstruction - w.mesh.vertices, axis=1).max() / np.abs(w.mesh.vertices).max()
     assert rel < 1e-2
+
+
+@pytest.mark.parametrize("name", ["C5", "C3"])
+def test_geometric_ordering_parity(ctx, monkeypatch, name):
+    """The factorisation's geometric ordering (sort along the tile's longest
+    axis; W = 32 for the 32x64 grid tiles) gives the oracle's chain too.  The
+    library picks it by itself for large batches; forced here on a prefix."""
+    monkeypatch.setenv("SMG_ORDERING", "geometric")
+    w = synth.config(name, mesh_index=7) if name == "C5" else synth.config(name)
+    T = 5 if name == "C5" else 12
+    seg = synth.Segmentation(w.seg.members[:T], np.arange(T, dtype=np.int32))
+    subs = O.build_submeshes(w.mesh.adj_offsets, w.mesh.adj_cols, seg.members)
+    cfg = G.PipelineConfig(weighting="binary", subspace_size=w.c, iterations=1, shift_scale=1e-3)
+    bb = G.run_chains([w.mesh], [seg], cfg, [w.c] * T, want_bases=True, want_recon=False, ctx=ctx)[0]
+    ocfg = O.PipelineConfig(weighting=O.BINARY, subspace_size=w.c, iterations=1, shift_scale=1e-3)
+    ob = O.compute_block_bases_fixed_sizes(w.mesh.vertices, subs, seg.sequence, ocfg, [w.c] * T)
+    for i in range(T):
+        assert O.max_principal_angle(bb.bases[i], ob.bases[i]) < 1e-8
+        assert abs(bb.stats[i].residual_rms - ob.stats[i].residual_rms) <= 1e-9 * ob.stats[i].residual_rms
