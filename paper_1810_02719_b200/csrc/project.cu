@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(PNT) partial_kernel(ProjParams p) {
         double best = -1.0, bval = 0.0;
         int bidx = 0;
         double px = 0.0, py = 0.0, pz = 0.0, ps = 0.0;
+#pragma unroll 8
         for (int i = r0; i < r1; ++i) {
             const double q = Q[(int64_t)i * p.ldq + j];
             const double mag = fabs(q);
@@ -91,11 +92,14 @@ __global__ void __launch_bounds__(PNT) reduce_kernel(ProjParams p) {
 // warp per row: x^_i = sum_j q_ij P_j ; e_i = s_i - sum_j q_ij Ps_j
 __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
     __shared__ double red[2][PNT / 32];
+    extern __shared__ __align__(16) double scoef[];  // c x 4, staged once per CTA
     const int b = blockIdx.y;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const double* Q = p.Q + (int64_t)b * p.strideQ;
     const double* X = p.X + (int64_t)b * p.strideX;
-    const double* coef = p.coeff + (int64_t)b * p.strideCoef;
+    for (int e = threadIdx.x; e < 4 * c; e += PNT) scoef[e] = p.coeff[(int64_t)b * p.strideCoef + e];
+    __syncthreads();
+    const double* coef = scoef;
     double* xhat = p.xhat ? p.xhat + (int64_t)b * p.strideXhat : nullptr;
     double* e_out = p.e_out ? p.e_out + (int64_t)b * p.strideE : nullptr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -105,6 +109,7 @@ __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
         const int i = blockIdx.x * rows_per_block + warp * p.rows_per_warp + rr;
         if (i >= p.n) break;
         double ax = 0.0, ay = 0.0, az = 0.0, as = 0.0;
+#pragma unroll 4
         for (int j = lane; j < c; j += 32) {
             const double q = Q[(int64_t)i * p.ldq + j];
             ax = fma(q, coef[4 * j + 0], ax);
@@ -175,7 +180,7 @@ void project(const ProjParams& p0, cudaStream_t st) {
     ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), PNT, 0, st>>>(p);
     ::smg::count_launch(), reduce_kernel<<<p.batch, PNT, 0, st>>>(p);
     const int nb = proj_recon_blocks(p.n, p.rows_per_warp);
-    ::smg::count_launch(), recon_kernel<<<dim3(nb, p.batch), PNT, 0, st>>>(p);
+    ::smg::count_launch(), recon_kernel<<<dim3(nb, p.batch), PNT, 4 * p.c_cap * sizeof(double), st>>>(p);
     ::smg::count_launch(), stats_kernel<<<(p.batch + 127) / 128, 128, 0, st>>>(p, nb);
 }
 
