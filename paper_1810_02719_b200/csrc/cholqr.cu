@@ -384,26 +384,10 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     SMG_CHOL_T(127);
 }
 
-// partial diag(Q^T V) over a chunk of rows, threads over columns (coalesced rows)
-constexpr int RC_ROWS = 32;
-__global__ void rank_partial_kernel(RankCheckParams p) {
-    const int b = blockIdx.y, chunk = blockIdx.x;
-    if (p.status[b] != kOk) return;
-    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
-    const int r0 = chunk * RC_ROWS, r1 = min(p.n, r0 + RC_ROWS);
-    const double* Q = p.Q + (int64_t)b * p.stride;
-    const double* V = p.V + (int64_t)b * p.stride;
-    for (int k = threadIdx.x; k < c; k += blockDim.x) {
-        double acc = 0.0;
-        for (int i = r0; i < r1; ++i) acc = fma(Q[(int64_t)i * p.ld + k], V[(int64_t)i * p.ld + k], acc);
-        p.partial[((int64_t)b * gridDim.x + chunk) * p.c_cap + k] = acc;
-    }
-}
-
-__global__ void rank_test_kernel(RankCheckParams p, int nchunks) {
+// The last chunk CTA of a chain (counter, threadfence reduction pattern) sums
+// the chunk partials in chunk order -- deterministic -- and runs the test.
+SMG_DEV void rank_test_block(const RankCheckParams& p, int b, int nchunks) {
     __shared__ int first;
-    const int b = blockIdx.x;
-    if (p.status[b] != kOk) return;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     if (threadIdx.x == 0) first = c;
     __syncthreads();
@@ -421,12 +405,36 @@ __global__ void rank_test_kernel(RankCheckParams p, int nchunks) {
     }
 }
 
+// partial diag(Q^T V) over a chunk of rows, threads over columns (coalesced rows)
+constexpr int RC_ROWS = 32;
+__global__ void rank_partial_kernel(RankCheckParams p) {
+    const int b = blockIdx.y, chunk = blockIdx.x;
+    if (p.status[b] != kOk) return;
+    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    const int r0 = chunk * RC_ROWS, r1 = min(p.n, r0 + RC_ROWS);
+    const double* Q = p.Q + (int64_t)b * p.stride;
+    const double* V = p.V + (int64_t)b * p.stride;
+    for (int k = threadIdx.x; k < c; k += blockDim.x) {
+        double acc = 0.0;
+        for (int i = r0; i < r1; ++i) acc = fma(Q[(int64_t)i * p.ld + k], V[(int64_t)i * p.ld + k], acc);
+        p.partial[((int64_t)b * gridDim.x + chunk) * p.c_cap + k] = acc;
+    }
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&p.counter[b], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    rank_test_block(p, b, gridDim.x);
+    if (threadIdx.x == 0) p.counter[b] = 0;
+}
+
 }  // namespace
 
 void rank_check(const RankCheckParams& p, cudaStream_t st) {
     const int chunks = (p.n + RC_ROWS - 1) / RC_ROWS;
     ::smg::count_launch(), rank_partial_kernel<<<dim3(chunks, p.batch), 256, 0, st>>>(p);
-    ::smg::count_launch(), rank_test_kernel<<<p.batch, 256, 0, st>>>(p, chunks);
 }
 
 int chol_smem_bytes(int c_cap) {

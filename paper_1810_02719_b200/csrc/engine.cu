@@ -218,6 +218,8 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     rdiag.alloc((size_t)B * ld, st);
     vnorm.alloc(B, st);
     rpart.alloc((size_t)B * ((npad + 31) / 32) * ld, st);  // rank_check chunks of 32 rows
+    counters.alloc((size_t)3 * B, st);  // last-CTA reductions: rank check | projection (2)
+    counters.zero();
     coeff.alloc((size_t)B * ld * 4, st);
     sign.alloc((size_t)B * ld, st);
     e.alloc((size_t)B * npad, st);
@@ -428,6 +430,7 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
         r.dimStride = 1;
         r.vnorm = ws.vnorm.get();
         r.partial = ws.rpart.get();
+        r.counter = ws.counters.get();
         r.status = ws.status.get();
         r.status_detail = ws.detail.get();
         r.errpos = ws.errpos.get();
@@ -464,6 +467,7 @@ void project_batch(const StepCtx& cx, Workspace& ws, const double* Q, int c, con
     p.stats = ws.stats.get();
     p.strideStats = 4;
     p.rows_per_warp = 2;
+    p.counter = ws.counters.get() + ws.B;
     project(p, cx.st);
     SMG_CUDA(cudaGetLastError());
 }

@@ -127,6 +127,7 @@ struct Workspace {
     int B = 0, n = 0, npad = 0, ld = 0, ccap = 0;
     int splits = 1;
     DBuf<double> U, V, T, R, G, Gws, Bm, work, rdiag, vnorm, rpart, coeff, sign, e, ppart, ppart2, stats;
+    DBuf<int> counters;
     DBuf<int> status, errpos, scratch_status;
     DBuf<int64_t> detail;
     DBuf<double> H, Hst, Vj, theta, theta_s, Wm, ritz_part, ritz;

@@ -163,6 +163,7 @@ struct RankCheckParams {
     int64_t* status_detail = nullptr;
     int* errpos = nullptr;
     int pos = 0;
+    int* counter = nullptr;  // per batch, zero: the last chunk CTA of a chain runs the test
 };
 void rank_check(const RankCheckParams& p, cudaStream_t st);
 
@@ -187,6 +188,7 @@ struct ProjParams {
     double* e_out = nullptr;
     int64_t strideE = 0;
     double* stats = nullptr;  // per batch: [0] residual_rms [1] ||e|| [2] ||X-X^||^2
+    int* counter = nullptr;   // 2 per batch, zero: last-CTA reductions of the partial / recon passes
     int64_t strideStats = 4;
 };
 int proj_chunks(int n);

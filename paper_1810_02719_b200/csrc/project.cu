@@ -24,6 +24,33 @@ namespace {
 
 constexpr int PNT = 256;
 
+SMG_DEV void reduce_block(const ProjParams& p, int b) {
+    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    const double* part = p.partial + (int64_t)b * p.nchunks * (int64_t)p.c_cap * 8;
+    double* coef = p.coeff + (int64_t)b * p.strideCoef;  // c x 4: Px Py Pz Ps (unsigned)
+    double* sign = p.sign + (int64_t)b * p.strideSign;
+    for (int j = threadIdx.x; j < c; j += PNT) {
+        double best = -1.0, bval = 0.0;
+        double px = 0.0, py = 0.0, pz = 0.0, ps = 0.0;
+        for (int ch = 0; ch < p.nchunks; ++ch) {
+            const double* o = part + ((int64_t)ch * p.c_cap + j) * 8;
+            if (o[0] > best) {  // chunks in row order: strict > keeps the first index
+                best = o[0];
+                bval = o[1];
+            }
+            px += o[3];
+            py += o[4];
+            pz += o[5];
+            ps += o[6];
+        }
+        sign[j] = bval < 0.0 ? -1.0 : 1.0;
+        coef[4 * j + 0] = px;
+        coef[4 * j + 1] = py;
+        coef[4 * j + 2] = pz;
+        coef[4 * j + 3] = ps;
+    }
+}
+
 __global__ void __launch_bounds__(PNT) partial_kernel(ProjParams p) {
     const int b = blockIdx.y, chunk = blockIdx.x;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
@@ -59,34 +86,29 @@ __global__ void __launch_bounds__(PNT) partial_kernel(ProjParams p) {
         o[5] = pz;
         o[6] = ps;
     }
+    // the last chunk CTA of a chain reduces the chunks in order (deterministic)
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&p.counter[2 * b], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    reduce_block(p, b);
+    if (threadIdx.x == 0) p.counter[2 * b] = 0;
 }
 
-__global__ void __launch_bounds__(PNT) reduce_kernel(ProjParams p) {
-    const int b = blockIdx.x;
-    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
-    const double* part = p.partial + (int64_t)b * p.nchunks * (int64_t)p.c_cap * 8;
-    double* coef = p.coeff + (int64_t)b * p.strideCoef;  // c x 4: Px Py Pz Ps (unsigned)
-    double* sign = p.sign + (int64_t)b * p.strideSign;
-    for (int j = threadIdx.x; j < c; j += PNT) {
-        double best = -1.0, bval = 0.0;
-        double px = 0.0, py = 0.0, pz = 0.0, ps = 0.0;
-        for (int ch = 0; ch < p.nchunks; ++ch) {
-            const double* o = part + ((int64_t)ch * p.c_cap + j) * 8;
-            if (o[0] > best) {  // chunks in row order: strict > keeps the first index
-                best = o[0];
-                bval = o[1];
-            }
-            px += o[3];
-            py += o[4];
-            pz += o[5];
-            ps += o[6];
-        }
-        sign[j] = bval < 0.0 ? -1.0 : 1.0;
-        coef[4 * j + 0] = px;
-        coef[4 * j + 1] = py;
-        coef[4 * j + 2] = pz;
-        coef[4 * j + 3] = ps;
+SMG_DEV void stats_block(const ProjParams& p, int b, int nblocks) {
+    double a = 0.0, e = 0.0;
+    const double* o = p.partial2 + (int64_t)b * nblocks * 2;
+    for (int k = 0; k < nblocks; ++k) {
+        a += o[2 * k];
+        e += o[2 * k + 1];
     }
+    double* s = p.stats + (int64_t)b * p.strideStats;
+    s[0] = sqrt(a / (3.0 * p.n));  // projection_residual_rms
+    s[1] = sqrt(e);                // ||e||
+    s[2] = a;
 }
 
 // warp per row: x^_i = sum_j q_ij P_j ; e_i = s_i - sum_j q_ij Ps_j
@@ -150,21 +172,15 @@ __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
         o[0] = a;
         o[1] = e;
     }
-}
-
-__global__ void stats_kernel(ProjParams p, int nblocks) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= p.batch) return;
-    double a = 0.0, e = 0.0;
-    const double* o = p.partial2 + (int64_t)b * nblocks * 2;
-    for (int k = 0; k < nblocks; ++k) {
-        a += o[2 * k];
-        e += o[2 * k + 1];
-    }
-    double* s = p.stats + (int64_t)b * p.strideStats;
-    s[0] = sqrt(a / (3.0 * p.n));  // projection_residual_rms
-    s[1] = sqrt(e);                // ||e||
-    s[2] = a;
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&p.counter[2 * b + 1], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    stats_block(p, b, gridDim.x);
+    p.counter[2 * b + 1] = 0;
 }
 
 }  // namespace
@@ -178,10 +194,8 @@ void project(const ProjParams& p0, cudaStream_t st) {
     p.nchunks = proj_chunks(p.n);
     if (p.rows_per_warp <= 0) p.rows_per_warp = 2;
     ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), PNT, 0, st>>>(p);
-    ::smg::count_launch(), reduce_kernel<<<p.batch, PNT, 0, st>>>(p);
     const int nb = proj_recon_blocks(p.n, p.rows_per_warp);
     ::smg::count_launch(), recon_kernel<<<dim3(nb, p.batch), PNT, 4 * p.c_cap * sizeof(double), st>>>(p);
-    ::smg::count_launch(), stats_kernel<<<(p.batch + 127) / 128, 128, 0, st>>>(p, nb);
 }
 
 }  // namespace smg
