@@ -14,6 +14,9 @@
 // (predicated) inner loop only runs where the tile crosses a row/column edge,
 // the Gram's diagonal or B's diagonal block.  Split-K partials are summed in a
 // fixed order by gemm_reduce (deterministic).
+#include <cstdint>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -64,6 +67,64 @@ struct Slab {
         }
     }
 };
+
+// DMMA products of one BK-deep slab pair (shared by the register-staged and the
+// producer-warp kernels).
+template <class SA, class SB, int NJ>
+SMG_DEV void slab_mma(const double* __restrict__ as, const double* __restrict__ bs, double (&acc)[4][NJ][2],
+                      unsigned fmask, unsigned kFull, int k0, int kdiag, int upperB, int wm, int wn, int g, int t) {
+    if (fmask == kFull && k0 + BK <= kdiag) {
+            // interior: every fragment active, no predication; m16n8k8 (4x the
+            // work per instruction of m8n8k4, same accumulator registers)
+#pragma unroll
+            for (int kk = 0; kk < BK; kk += 8) {
+                double a[2][4], bb[NJ][2];
+#pragma unroll
+                for (int I = 0; I < 2; ++I) {
+                    const int r = wm + 16 * I + g;
+                    a[I][0] = SA::at(as, kk + t, r);
+                    a[I][1] = SA::at(as, kk + t, r + 8);
+                    a[I][2] = SA::at(as, kk + t + 4, r);
+                    a[I][3] = SA::at(as, kk + t + 4, r + 8);
+                }
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    bb[j][0] = SB::at(bs, kk + t, wn + 8 * j + g);
+                    bb[j][1] = SB::at(bs, kk + t + 4, wn + 8 * j + g);
+                }
+#pragma unroll
+                for (int I = 0; I < 2; ++I)
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j)
+                        dmma1688(acc[2 * I][j][0], acc[2 * I][j][1], acc[2 * I + 1][j][0], acc[2 * I + 1][j][1],
+                                 a[I][0], a[I][1], a[I][2], a[I][3], bb[j][0], bb[j][1]);
+            }
+        } else if (fmask != 0 && k0 < kdiag + 8 * NJ) {
+#pragma unroll
+            for (int kk = 0; kk < BK; kk += 4) {
+                unsigned m = fmask;
+                if (upperB) {
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j)
+                        if (kdiag + 8 * j + 7 < k0 + kk) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) m &= ~(1u << (NJ * i + j));
+                        }
+                }
+                if (m == 0) continue;
+                double a[4], bb[NJ];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = SA::at(as, kk + t, wm + 8 * i + g);
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) bb[j] = SB::at(bs, kk + t, wn + 8 * j + g);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j)
+                        if (m & (1u << (NJ * i + j))) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+            }
+        }
+}
 
 template <bool TA, bool TB, int NJ>
 __global__ void __launch_bounds__(NT, 4) gemm_kernel(GemmParams p, int n_base, int n_end) {
@@ -139,63 +200,189 @@ __global__ void __launch_bounds__(NT, 4) gemm_kernel(GemmParams p, int n_base, i
         }
         const double* as = As[buf];
         const double* bs = Bs[buf];
-        if (fmask == kFull && k0 + BK <= kdiag) {
-            // interior: every fragment active, no predication; m16n8k8 (4x the
-            // work per instruction of m8n8k4, same accumulator registers)
-#pragma unroll
-            for (int kk = 0; kk < BK; kk += 8) {
-                double a[2][4], bb[NJ][2];
-#pragma unroll
-                for (int I = 0; I < 2; ++I) {
-                    const int r = wm + 16 * I + g;
-                    a[I][0] = SA::at(as, kk + t, r);
-                    a[I][1] = SA::at(as, kk + t, r + 8);
-                    a[I][2] = SA::at(as, kk + t + 4, r);
-                    a[I][3] = SA::at(as, kk + t + 4, r + 8);
-                }
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    bb[j][0] = SB::at(bs, kk + t, wn + 8 * j + g);
-                    bb[j][1] = SB::at(bs, kk + t + 4, wn + 8 * j + g);
-                }
-#pragma unroll
-                for (int I = 0; I < 2; ++I)
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j)
-                        dmma1688(acc[2 * I][j][0], acc[2 * I][j][1], acc[2 * I + 1][j][0], acc[2 * I + 1][j][1],
-                                 a[I][0], a[I][1], a[I][2], a[I][3], bb[j][0], bb[j][1]);
-            }
-        } else if (fmask != 0 && k0 < kdiag + 8 * NJ) {
-#pragma unroll
-            for (int kk = 0; kk < BK; kk += 4) {
-                unsigned m = fmask;
-                if (p.upperB) {
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j)
-                        if (kdiag + 8 * j + 7 < k0 + kk) {
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) m &= ~(1u << (NJ * i + j));
-                        }
-                }
-                if (m == 0) continue;
-                double a[4], bb[NJ];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = SA::at(as, kk + t, wm + 8 * i + g);
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) bb[j] = SB::at(bs, kk + t, wn + 8 * j + g);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j)
-                        if (m & (1u << (NJ * i + j))) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
-            }
-        }
+        slab_mma<SA, SB, NJ>(as, bs, acc, fmask, kFull, k0, kdiag, p.upperB, wm, wn, g, t);
         if (more) {
             la.store(As[buf ^ 1]);
             lb.store(Bs[buf ^ 1]);
         }
         __syncthreads();
         buf ^= 1;
+    }
+
+    double* C;
+    double alpha = p.alpha, beta = p.beta;
+    if (splits > 1) {
+        C = p.C + ((int64_t)b * splits + s) * p.strideP;
+        alpha = 1.0;
+        beta = 0.0;
+    } else {
+        C = p.C + (int64_t)b * p.strideC;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = m0 + wm + 8 * i + g;
+        if (row >= M) continue;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int col = n0 + wn + 8 * j + 2 * t + q;
+                if (col >= N) continue;
+                double* dst = C + (int64_t)row * p.ldc + col;
+                double v = alpha * acc[i][j][q];
+                if (beta != 0.0) v += beta * *dst;
+                *dst = v;
+            }
+        }
+    }
+}
+
+
+// ---- producer-warp pipeline: one warp moves the slabs with cp.async into a
+// PNS-stage ring (completion on mbarriers), the four DMMA warps never have
+// loads in flight (no register staging, no long-scoreboard coupling of their
+// fragment reads to outstanding LDGSTS) and never meet at a CTA barrier.
+constexpr int PNS = 3;
+constexpr int NT_P = NT + 32;
+
+SMG_DEV uint32_t g_smem_u32(const void* ptr) { return static_cast<uint32_t>(__cvta_generic_to_shared(ptr)); }
+SMG_DEV void g_mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(g_smem_u32(bar)), "r"(count) : "memory");
+}
+SMG_DEV void g_mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(g_smem_u32(bar)) : "memory");
+}
+SMG_DEV void g_mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n GWAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra GWAIT_%=;\n}\n" ::"r"(g_smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// cp.async of one BK x XW slab into the Slab<XW, KMAJOR> layout, 16-byte chunks
+// (zero-filled past kmax / xmax, partial chunks at odd edges)
+template <int XW, bool KMAJOR>
+SMG_DEV void issue_slab(double* sl, const double* __restrict__ ptr, int64_t ld, int k0, int x0, int kmax, int xmax,
+                        int lane) {
+    using SL = Slab<XW, KMAJOR>;
+    constexpr int CH = KMAJOR ? XW / 2 : BK / 2;  // chunks per smem row
+    constexpr int NCH = XW * BK / 2;
+    for (int c = lane; c < NCH; c += 32) {
+        int k, x;
+        if (KMAJOR) {
+            k = c / CH;
+            x = (c % CH) * 2;
+        } else {
+            x = c / CH;
+            k = (c % CH) * 2;
+        }
+        const int gk = k0 + k, gx = x0 + x;
+        int valid;
+        const double* src;
+        if (KMAJOR) {
+            valid = (gk < kmax) ? max(0, min(2, xmax - gx)) : 0;
+            src = ptr + (int64_t)gk * ld + gx;
+        } else {
+            valid = (gx < xmax) ? max(0, min(2, kmax - gk)) : 0;
+            src = ptr + (int64_t)gx * ld + gk;
+        }
+        if (valid == 0) src = ptr;
+        double* dst = KMAJOR ? sl + k * SL::S + x : sl + x * SL::S + k;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(g_smem_u32(dst)), "l"(src),
+                     "r"(valid * 8)
+                     : "memory");
+    }
+}
+
+template <bool TA, bool TB, int NJ>
+__global__ void __launch_bounds__(NT_P) gemm_pipe_kernel(GemmParams p, int n_base, int n_end) {
+    constexpr int BN = 16 * NJ;
+    using SA = Slab<BM, TA>;
+    using SB = Slab<BN, !TB>;
+    const int splits = p.splits > 0 ? p.splits : 1;
+    const int b = blockIdx.z / splits;
+    const int s = blockIdx.z % splits;
+    const int M = p.dimM ? p.dimM[(int64_t)b * p.dimStride] : p.M;
+    const int N = min(p.dimN ? p.dimN[(int64_t)b * p.dimStride] : p.N, n_end);
+    const int K = p.dimK ? p.dimK[(int64_t)b * p.dimStride] : p.K;
+    const int m0 = blockIdx.y * BM, n0 = n_base + blockIdx.x * BN;
+    if (m0 >= M || n0 >= N) return;
+    if (p.syrkUpper && (m0 >> 5) > ((n0 + BN - 1) >> 5)) return;
+
+    int kEnd = K;
+    if (p.upperB) kEnd = min(kEnd, n0 + BN);
+    const int kchunk = ((kEnd + splits - 1) / splits + BK - 1) / BK * BK;
+    const int kBeg = s * kchunk;
+    const int kStop = min(kEnd, kBeg + kchunk);
+    const int nsteps = kStop > kBeg ? (kStop - kBeg + BK - 1) / BK : 0;
+
+    const double* A = p.A + (int64_t)b * p.strideA;
+    const double* B = p.B + (int64_t)b * p.strideB;
+    extern __shared__ __align__(16) double gsm[];
+    double* As = gsm;
+    double* Bs = gsm + PNS * SA::ELEMS;
+    __shared__ __align__(8) uint64_t full[PNS], consumed[PNS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < PNS; ++i) {
+            g_mbar_init(&full[i], 1);
+            g_mbar_init(&consumed[i], NT / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NT / 32) {  // producer
+        uint32_t cph[PNS];
+        for (int i = 0; i < PNS; ++i) cph[i] = 0u;
+        for (int ks = 0; ks < nsteps; ++ks) {
+            const int st = ks % PNS, k0 = kBeg + ks * BK;
+            if (ks >= PNS) {
+                g_mbar_wait(&consumed[st], cph[st]);
+                cph[st] ^= 1u;
+            }
+            // op(A)(m, k) lives at A[k*lda + m] (TA, k-major) or A[m*lda + k]
+            issue_slab<BM, TA>(As + st * SA::ELEMS, A, p.lda, k0, m0, kStop, M, lane);
+            issue_slab<BN, !TB>(Bs + st * SB::ELEMS, B, p.ldb, k0, n0, kStop, N, lane);
+            asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(g_smem_u32(&full[st])) : "memory");
+            __syncwarp();
+            if (lane == 0) g_mbar_arrive(&full[st]);
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        return;
+    }
+
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * (8 * NJ);
+    double acc[4][NJ][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    constexpr unsigned kFull = (1u << (4 * NJ)) - 1u;
+    unsigned fmask = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int r = m0 + wm + 8 * i, cc = n0 + wn + 8 * j;
+            bool on = r < M && cc < N;
+            if (p.syrkUpper && (r >> 5) > ((cc + 7) >> 5)) on = false;
+            if (on) fmask |= 1u << (NJ * i + j);
+        }
+    const int kdiag = p.upperB ? n0 + wn : 1 << 30;
+    uint32_t fph[PNS];
+    for (int i = 0; i < PNS; ++i) fph[i] = 0u;
+    for (int ks = 0; ks < nsteps; ++ks) {
+        const int st = ks % PNS, k0 = kBeg + ks * BK;
+        g_mbar_wait(&full[st], fph[st]);
+        fph[st] ^= 1u;
+        slab_mma<SA, SB, NJ>(As + st * SA::ELEMS, Bs + st * SB::ELEMS, acc, fmask, kFull, k0, kdiag, p.upperB, wm, wn,
+                             g, t);
+        __syncwarp();
+        if (lane == 0) g_mbar_arrive(&consumed[st]);
     }
 
     double* C;
@@ -252,6 +439,23 @@ void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
     const int gm = (p.M + BM - 1) / BM, gn = (width + BN - 1) / BN;
     dim3 grid(gn, gm, p.batch * p.splits);
     ::smg::count_launch();
+    // the cp.async pipeline needs 16-byte aligned chunks: even leading
+    // dimensions, strides and tile origins
+    auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    const bool aligned = al(p.A) && al(p.B) && !(p.lda & 1) && !(p.ldb & 1) && !(p.strideA & 1) && !(p.strideB & 1) &&
+                         !(n_base & 1) && !std::getenv("SMG_GEMM_NOPIPE");
+    if (aligned) {
+        using SA = Slab<BM, TA>;
+        using SB = Slab<BN, !TB>;
+        const int bytes = PNS * (SA::ELEMS + SB::ELEMS) * 8;
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(gemm_pipe_kernel<TA, TB, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            configured = true;
+        }
+        gemm_pipe_kernel<TA, TB, NJ><<<grid, NT_P, bytes, st>>>(p, n_base, n_base + width);
+        return;
+    }
     gemm_kernel<TA, TB, NJ><<<grid, NT, 0, st>>>(p, n_base, n_base + width);
 }
 
