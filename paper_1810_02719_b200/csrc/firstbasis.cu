@@ -61,8 +61,10 @@ std::vector<double> gaussian_block_colmajor(int rows, int cols, uint64_t seed) {
     return out;
 }
 
-FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts, int tile0, int tstride, int c,
-                             const FirstBasisConfig& cfg, const FactorSet* op_factor) {
+namespace {
+FirstBasisReport first_basis_impl(const StepCtx& cx, Workspace& ws, const TileSet& ts, int tile0, int tstride, int c,
+                                  const FirstBasisConfig& cfg, const FactorSet* op_factor, bool allow_cheb,
+                                  bool* broke) {
     FirstBasisReport rep;
     const cudaStream_t st = cx.st;
     const int n = ts.n;
@@ -134,7 +136,8 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
         SMG_CUDA(cudaMemcpyAsync(&upper[b], ts.shift0.get() + ts.ntiles + tile0 + (int64_t)b * tstride,
                                  sizeof(double), cudaMemcpyDeviceToHost, st));
     SMG_CUDA(cudaStreamSynchronize(st));
-    const bool use_cheb = !(std::getenv("SMG_FIRST_BASIS") && std::string(std::getenv("SMG_FIRST_BASIS")) == "si");
+    const bool use_cheb =
+        allow_cheb && !(std::getenv("SMG_FIRST_BASIS") && std::string(std::getenv("SMG_FIRST_BASIS")) == "si");
     const int deg = 30;
     DBuf<double> dcoef;          // [deg][B] alpha | [deg][B] gamma | [B] shift
     int iters_next = (m == n) ? 0 : (use_cheb ? 4 : 6);
@@ -254,7 +257,10 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
         jp.sweeps = sweeps.get();
         // the bootstrap round only plans the Chebyshev filter (interval ends, rate);
         // the filter input needs the span, not converged Ritz vectors
-        if (round == 0 && use_cheb && c < m) jp.max_sweeps = 3;
+        if (round == 0 && use_cheb && c < m) {
+            jp.max_sweeps = 2;  // the Ritz values only plan the filter (interval ends, rate)
+            if (const char* e = std::getenv("SMG_FB_BOOT_SWEEPS")) jp.max_sweeps = std::max(1, std::atoi(e));
+        }
         const int jerr = jacobi_eigh(jp, pl, m, st);
         if (jerr != 0) SMG_CUDA((cudaError_t)jerr);
         if (std::getenv("SMG_DEBUG")) {
@@ -274,8 +280,17 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
         std::vector<double> th = download(ws.theta_s.get(), (size_t)ws.B * m, st);
         std::vector<double> rs = download(ws.ritz.get(), (size_t)ws.B * nres, st);
         std::vector<int> sts = download(ws.status.get(), ws.B, st);
-        for (int b = 0; b < ws.B; ++b)
-            if (sts[b] != 0) fail(3, "first-submesh basis: orthonormalization of the subspace iterate broke down");
+        bool bad = false;
+        for (int b = 0; b < ws.B; ++b) bad |= sts[b] != 0;
+        if (bad) {
+            // a filter planned from rough bootstrap Ritz values can over-amplify
+            // (single-pass CholeskyQR breaks down): the caller retries shift-invert only
+            if (use_cheb && broke) {
+                *broke = true;
+                return rep;
+            }
+            fail(3, "first-submesh basis: orthonormalization of the subspace iterate broke down");
+        }
         double bound = 0.0, worst_rate = 0.0;
         for (int b = 0; b < ws.B; ++b) {
             const double* tb = th.data() + (size_t)b * m;
@@ -351,6 +366,16 @@ FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts
                          cheb_apps, deg, cheb_apps ? 0 : iters_next);
     }
     return rep;
+}
+}  // namespace
+
+FirstBasisReport first_basis(const StepCtx& cx, Workspace& ws, const TileSet& ts, int tile0, int tstride, int c,
+                             const FirstBasisConfig& cfg, const FactorSet* op_factor) {
+    bool broke = false;
+    FirstBasisReport rep = first_basis_impl(cx, ws, ts, tile0, tstride, c, cfg, op_factor, true, &broke);
+    if (!broke) return rep;
+    ws.status.zero();
+    return first_basis_impl(cx, ws, ts, tile0, tstride, c, cfg, op_factor, false, nullptr);
 }
 
 }  // namespace smg
