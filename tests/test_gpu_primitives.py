@@ -252,3 +252,21 @@ def test_one_step_parity_sphere_chain(ctx, sphere):
         worst = max(worst, O.max_principal_angle(ug, uo))
         prev = uo
     assert worst < 1e-10
+
+
+@pytest.mark.parametrize("env", [{"SMG_FB_BOOT_SWEEPS": "1"}, {"SMG_FIRST_BASIS": "si"}])
+def test_first_basis_fallback_paths(ctx, grid, monkeypatch, env):
+    """A filter planned from one bootstrap Jacobi sweep over-amplifies at c = 400
+    of 1024 (the single-pass CholeskyQR breaks down) and the first basis retries
+    shift-invert only; SMG_FIRST_BASIS=si runs that path directly.  Both must
+    still give bottom_subspace(dense_eigendecomposition(L), c)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    mesh, seg, subs = grid
+    lap = O.build_laplacian(subs[2], mesh.vertices, "binary")
+    g, _ = _op(ctx, lap)
+    w, u = O.dense_eigendecomposition(lap)
+    c = 400
+    ug, ev = G.bottom_subspace(g, c, return_eigenvalues=True)
+    assert O.max_principal_angle(ug, u[:, :c]) < 1e-9
+    assert np.abs(ev - w[:c]).max() < 1e-10
