@@ -58,6 +58,14 @@ __global__ void __launch_bounds__(PNT) partial_kernel(ProjParams p) {
     const double* Q = p.Q + (int64_t)b * p.strideQ;
     const double* X = p.X + (int64_t)b * p.strideX;
     double* part = p.partial + ((int64_t)b * p.nchunks + chunk) * (int64_t)p.c_cap * 8;
+    // the chunk's coordinates (and s = (x + y) + z) once in shared memory: one
+    // broadcast 32-byte read per row instead of three global loads per element
+    __shared__ double4 sx[64];
+    for (int i = threadIdx.x; i < r1 - r0; i += PNT) {
+        const double x = X[3 * (r0 + i)], y = X[3 * (r0 + i) + 1], z = X[3 * (r0 + i) + 2];
+        sx[i] = make_double4(x, y, z, (x + y) + z);
+    }
+    __syncthreads();
     for (int j = threadIdx.x; j < c; j += PNT) {
         double best = -1.0, bval = 0.0;
         int bidx = 0;
@@ -71,11 +79,11 @@ __global__ void __launch_bounds__(PNT) partial_kernel(ProjParams p) {
                 bval = q;
                 bidx = i;
             }
-            const double x = X[3 * i], y = X[3 * i + 1], z = X[3 * i + 2];
-            px = fma(q, x, px);
-            py = fma(q, y, py);
-            pz = fma(q, z, pz);
-            ps = fma(q, (x + y) + z, ps);
+            const double4 v = sx[i - r0];
+            px = fma(q, v.x, px);
+            py = fma(q, v.y, py);
+            pz = fma(q, v.z, pz);
+            ps = fma(q, v.w, ps);
         }
         double* o = part + (int64_t)j * 8;
         o[0] = best;
