@@ -333,7 +333,8 @@ void trsm(Workspace& ws, const double* V, double* out, int c, const int* dimC, i
 // is faster (the back-substitution overlaps the other chain group's kernels).
 bool use_trsm(int c, int batch) {
     static const bool off = std::getenv("SMG_NO_TRSM") != nullptr;
-    return !off && batch <= 4 && trsm_supported(c);
+    static const int maxb = std::getenv("SMG_TRSM_MAXB") ? std::atoi(std::getenv("SMG_TRSM_MAXB")) : 4;
+    return !off && batch <= maxb && trsm_supported(c);
 }
 
 void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st) {
