@@ -42,6 +42,10 @@ CONFIGS = {
     # name: (W, H, tile_w, tile_h, c, t, meshes, sigma, seed0)
     "C5": dict(W=512, H=512, tw=64, th=32, c=200, t=1, meshes=64, sigma=0.01, seed0=5000,
                desc="64 x 512^2 grid meshes, 128 tiles of 32x64 (n_d=2048) each, c=200, t=1"),
+    # F3: denoise_dynamic of a frame sequence on config 5's grid and tiles
+    "F3": dict(W=512, H=512, tw=64, th=32, c=200, t=1, meshes=1, frames=64, sigma=0.01, seed0=7000,
+               desc="denoise_dynamic: 64 frames of a 512^2 grid sequence, 128 tiles of 32x64 (n_d=2048), "
+                    "bases from frame 0 (c=200, t=1), every frame projected + stitched"),
     "C2": dict(W=256, H=256, tw=32, th=32, c=100, t=1, meshes=1, sigma=0.005, seed0=202,
                desc="256^2 grid, 64 tiles of 32x32 (n_d=1024), c=100, t=1"),
 }
@@ -453,6 +457,192 @@ def reference_arm(args, cfg):
             "e2e": {"value": cb["value"], "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+# ----------------------------------------------------------------------- F3 arm
+
+def _frames_inputs(cfg, seed):
+    from paper_1810_02719_b200 import synth
+    topo = synth.grid_mesh(cfg["W"], cfg["H"], seed, cfg["sigma"])
+    seg = synth.grid_tiles(cfg["W"], cfg["H"], cfg["tw"], cfg["th"])
+    verts = synth.grid_sequence(cfg["W"], cfg["H"], cfg["frames"], seed, cfg["sigma"])
+    return topo, seg, verts
+
+
+def frames_arm(args, cfg, rank, world, local_rank):
+    """denoise_dynamic (denoise.hpp:258-291) through smg_denoise_dynamic: each rank
+    denoises its own sequence (frame sequences are independent: weak scaling,
+    no collective).  value = vertex-frames/s with device-resident frames; e2e =
+    host frames in, host frames out."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    import paper_1810_02719_b200 as G
+    from paper_1810_02719_b200 import _abi
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    ctx = G.Context(local_rank)
+    topo, seg, verts = _frames_inputs(cfg, cfg["seed0"] + rank)
+    F, n, K = cfg["frames"], topo.n, seg.count
+    offs, members = seg.flat()
+    seq = np.arange(K, dtype=np.int32)
+    d_xyz = [[torch.from_numpy(np.ascontiguousarray(v[:, a])).to(dev) for a in range(3)] for v in verts]
+    h_xyz = [[torch.from_numpy(np.ascontiguousarray(v[:, a])).pin_memory() for a in range(3)] for v in verts]
+    conn = dict(offs=topo.adj_offsets, cols=topo.adj_cols, moffs=offs, members=members, seq=seq)
+    d_conn = {k: torch.from_numpy(np.asarray(a, np.int32)).to(dev) for k, a in conn.items()}
+    h_conn = {k: torch.from_numpy(np.asarray(a, np.int32)).pin_memory() for k, a in conn.items()}
+    d_out = torch.empty((F, 3 * n), dtype=torch.float64, device=dev)
+    h_out = torch.empty((F, 3 * n), dtype=torch.float64).pin_memory()
+    pc = _abi.smg_pipeline_config()
+    ctx.lib.smg_default_config(pc)
+    pc.weighting = _abi.WEIGHTING[PINNED["weighting"]]
+    pc.subspace_size = cfg["c"]
+    pc.iterations = cfg["t"]
+    pc.power = PINNED["power"]
+    pc.shift_scale = PINNED["shift_scale"]
+    sizes = np.full(K, cfg["c"], np.int32)
+    nb = C.c_int32()
+    tms = np.zeros(3)
+
+    def views(on):
+        xyz, cn, out = (d_xyz, d_conn, d_out) if on else (h_xyz, h_conn, h_out)
+        ms = (_abi.smg_mesh * F)()
+        for f in range(F):
+            ms[f] = _abi.smg_mesh(n, xyz[f][0].data_ptr(), xyz[f][1].data_ptr(), xyz[f][2].data_ptr(),
+                                  cn["offs"].data_ptr(), cn["cols"].data_ptr(), on)
+        sv = _abi.smg_segmentation(K, cn["moffs"].data_ptr(), cn["members"].data_ptr(), K, cn["seq"].data_ptr(), on)
+        outp = (C.c_void_p * F)(*[out[f].data_ptr() for f in range(F)])
+        return ms, sv, outp
+
+    vw = {on: views(on) for on in (0, 1)}
+
+    def step(on):
+        ms, sv, outp = vw[on]
+        ctx.check(ctx.lib.smg_denoise_dynamic(ctx.handle, F, ms, C.byref(sv), C.byref(pc), sizes.ctypes.data, 1,
+                                              outp, on, C.byref(nb), tms.ctypes.data_as(_abi.c_double_p)))
+
+    def launches():
+        n_, t_ = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, b"launches", C.byref(n_), C.byref(t_))
+        return n_.value
+
+    def timed(on, steps):
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = launches()
+        ev0.record()
+        basis_s = frames_s = 0.0
+        for _ in range(steps):
+            step(on)
+            basis_s += tms[0]
+            frames_s += tms[1]
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, launches() - l0, basis_s / steps, frames_s / steps
+
+    for _ in range(args.warmup):
+        step(1)
+    ctx.lib.smg_profile_enable(ctx.handle, 1)
+    with ClockSampler(local_rank) as clk:
+        ms, nl, basis_s, frames_s = timed(1, args.steps)
+    stages = {}
+    for nm in ("frames", "frames_gemm", "solve", "orthonormalize", "project"):
+        n_, t_ = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, nm.encode(), C.byref(n_), C.byref(t_))
+        stages[nm] = {"launches": n_.value / args.steps, "ms": t_.value / args.steps}
+    ctx.lib.smg_profile_enable(ctx.handle, 0)
+    step(0)
+    ms_e2e, _, _, _ = timed(0, args.steps)
+    ms_step = ms / args.steps
+    units = world * F * n
+    c = cfg["c"]
+    n_d = seg.block_size
+    # frames-stage GEMMs: C = U^T X and X^ = U C, 2 * (2 n_d c 3F) flops per tile
+    gemm_flops = K * 2 * 2.0 * n_d * c * 3 * F
+    g = stages["frames_gemm"]
+    achieved = gemm_flops / (g["ms"] * 1e-3) / 1e12 if g["ms"] > 0 else None
+    out = {
+        "metric": METRIC + " [F3 denoise_dynamic: vertex-frames/s]", "value": units / (ms_step * 1e-3),
+        "unit": "vertex-frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded moving sinusoid height-field grid sequence + per-frame N(0,sigma^2) noise)",
+        "config": {"workload": f"F3: {cfg['desc']}", "frames": F, "n_vertices": n, "tiles": K, "n_d": n_d, "c": c,
+                   "parallelism": f"one sequence per GPU ({world} GPU(s))",
+                   "l2": "frames (%.0f MB) larger than L2" % (F * n * 24 / 1e6)},
+        "e2e": {"value": units / (ms_e2e / args.steps * 1e-3), "unit": "vertex-frames/s",
+                "h2d_bytes_per_step": F * n * 24 + (n + 1 + len(topo.adj_cols) + K * n_d + 2 * (K + 1)) * 4,
+                "d2h_bytes_per_step": F * n * 24},
+        "roofline": {"kernel": "frames-stage DMMA GEMMs (U^T X, U C over 3F frame columns)", "bound": "tensor",
+                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": None,
+                     "flops_per_step": gemm_flops, "gemm_ms_per_step": g["ms"], "launches_per_step": g["launches"]},
+        "split_ms": {"shared_basis": basis_s * 1e3, "frames": frames_s * 1e3},
+        "frames_stage_value": units / frames_s if frames_s > 0 else None,
+        "stages_ms_per_step": {k: round(v["ms"], 3) for k, v in stages.items()},
+        "clocks": clk.summary(), "gpu_launches": nl,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = frames_cpu_baseline(args, cfg)
+    if dist is not None:
+        dist.destroy_process_group()
+    ctx.close()
+    return out if rank == 0 else None
+
+
+def frames_cpu_baseline(args, cfg):
+    """The oracle's denoise_dynamic on a bounded sample: the chain over the first T
+    tiles, then all F frames projected onto those T bases, extrapolated to all
+    tiles (one core, BLAS 1 thread -- the reference's frames loop is parallel_for
+    over frames, so the frames share is divided by the host cores)."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import specmesh_oracle as O
+    cores = os.cpu_count() or 1
+    topo, seg, verts = _frames_inputs(cfg, cfg["seed0"])
+    T = min(seg.count, max(2, args.cpu_tiles))
+    subs = O.build_submeshes(topo.adj_offsets, topo.adj_cols, seg.members[:T])
+    ocfg = O.PipelineConfig(weighting=O.BINARY, subspace_size=cfg["c"], iterations=cfg["t"],
+                            shift_scale=PINNED["shift_scale"])
+    t0 = time.perf_counter()
+    bb = O.compute_block_bases_fixed_sizes(verts[0], subs, np.arange(T), ocfg, [cfg["c"]] * T)
+    t1 = time.perf_counter()
+    for v in verts:
+        O.project_blocks(bb, v)
+    t2 = time.perf_counter()
+    K, F, n = seg.count, cfg["frames"], topo.n
+    t_step = (t1 - t0) * K / T + (t2 - t1) * K / T / cores
+    return {"value": F * n / t_step, "unit": "vertex-frames/s", "cores": cores, "kind": "port",
+            "sample": f"chain over the first {T} of {K} tiles ({t1 - t0:.2f}s, 1 core) + {F} frames projected on "
+                      f"those tiles ({t2 - t1:.2f}s, 1 core; frames loop credited with {cores} cores), "
+                      f"extrapolated to {K} tiles"}
+
+
+def frames_reference_arm(args, cfg):
+    vals = []
+    for _ in range(max(1, args.steps)):
+        cb = frames_cpu_baseline(args, cfg)
+        vals.append(cb["value"])
+    cb["value"] = statistics.median(vals)
+    units = cfg["frames"] * cfg["W"] * cfg["H"]
+    return {"metric": METRIC + " [F3 denoise_dynamic: vertex-frames/s]", "value": cb["value"],
+            "unit": "vertex-frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": units / cb["value"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"F3: {cfg['desc']}"}, "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "vertex-frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
@@ -462,7 +652,14 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        print(json.dumps(reference_arm(args, cfg)), flush=True)
+        arm = frames_reference_arm if "frames" in cfg else reference_arm
+        print(json.dumps(arm(args, cfg)), flush=True)
+        return
+    if "frames" in cfg:
+        if args.impl == "ours":
+            out = frames_arm(args, cfg, rank, world, local_rank)
+            if out is not None:
+                print(json.dumps(out), flush=True)
         return
     out = gpu_arm(args, cfg, rank, world, local_rank)
     if out is not None:

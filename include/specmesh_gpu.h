@@ -149,6 +149,48 @@ smg_status smg_run_chains(smg_context* ctx, int32_t n_chains, const smg_mesh* me
                           const smg_segmentation* segs, const smg_pipeline_config* cfg,
                           const int32_t* sizes_in_order, smg_chain_output* outs);
 
+/* ------------------------------------------------------ F3 dynamic meshes */
+
+/* AverageMode (partition.hpp:53). */
+typedef enum { SMG_AVERAGE_SIMPLE = 0, SMG_AVERAGE_WEIGHTED = 1 } smg_average_mode;
+
+/* BlockBases.bases (pipeline.hpp:78-92) in the layout smg_chain_output writes:
+ * the basis of submesh id is n_d x subspace_size[id], column-major, at
+ * data + offsets[id].  subspace_size/offsets are host arrays. */
+typedef struct {
+    int32_t submesh_count;
+    const int32_t* subspace_size; /* [submesh_count] */
+    const int64_t* offsets;       /* [submesh_count + 1] */
+    const double* data;
+    int32_t on_device;
+} smg_bases;
+
+/* coarse_reconstruct_points(frame, bases, mode) (pipeline.hpp:300-305) for
+ * frame_count frames that share `topology`'s connectivity (its coordinates are
+ * not read; x/y/z may be NULL) -- the frames stage of denoise_dynamic
+ * (denoise.hpp:280-288).  frames_xyz: 3 * frame_count pointers x_0, y_0, z_0,
+ * x_1, ... of vertex_count doubles; out: frame_count pointers, each a SoA
+ * vertex_count x 3 result.  Uncovered vertices -> status 2 with the reference
+ * message (partition.hpp:347-353). */
+smg_status smg_coarse_reconstruct_frames(smg_context* ctx, const smg_mesh* topology,
+                                         const smg_segmentation* seg, const smg_bases* bases,
+                                         int32_t frame_count, const double* const* frames_xyz,
+                                         int32_t frames_on_device, int32_t average_mode,
+                                         double* const* out, int32_t out_on_device);
+
+/* denoise_dynamic (denoise.hpp:258-291) over an EXTERNAL segmentation: the
+ * bases of frames[0] (fixed sizes_in_order when given, else compute_block_bases
+ * by cfg->basis_mode), then every frame's coarse reconstruction.  Every frame
+ * must share frames[0]'s connectivity (status 2, "frame i does not share the
+ * sequence connectivity").  *basis_blocks_computed = number of bases (k).
+ * timings (optional, 3 doubles, device-event seconds): [0] shared_basis
+ * [1] frames [2] total. */
+smg_status smg_denoise_dynamic(smg_context* ctx, int32_t frame_count, const smg_mesh* frames,
+                               const smg_segmentation* seg, const smg_pipeline_config* cfg,
+                               const int32_t* sizes_in_order, int32_t average_mode,
+                               double* const* out, int32_t out_on_device,
+                               int32_t* basis_blocks_computed, double* timings);
+
 /* ------------------------------------------------------------ L3 primitives
  * Host pointers, column-major.  They run the same kernels as the chain. */
 

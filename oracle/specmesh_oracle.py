@@ -739,3 +739,18 @@ def reconstruct_weighted(submeshes: List[Submesh], local_results: List[np.ndarra
 def coarse_reconstruct_points(bb: BlockBases, vertices: np.ndarray, weighted: bool = True) -> np.ndarray:
     """pipeline.hpp:300-305"""
     return reconstruct_weighted(bb.submeshes, project_blocks(bb, vertices), vertices.shape[0], weighted)
+
+
+def denoise_dynamic(frames: List[np.ndarray], submeshes: List[Submesh], sequence, cfg: "PipelineConfig",
+                    sizes_in_order, weighted: bool = True):
+    """denoise.hpp:258-291 with an external segmentation: bases computed once
+    from the first frame (:276-277), then coarse_reconstruct_points of every frame
+    (:280-288).  Returns (frames, basis_blocks_computed, bases)."""
+    require(len(frames) > 0, "dynamic denoising needs at least one frame")
+    n = frames[0].shape[0]
+    for i in range(1, len(frames)):
+        if frames[i].shape[0] != n:
+            raise InvalidArgument(f"frame {i} does not share the sequence connectivity")
+    bb = compute_block_bases_fixed_sizes(frames[0], submeshes, sequence, cfg, sizes_in_order)
+    out = [coarse_reconstruct_points(bb, v, weighted) for v in frames]
+    return out, len(bb.bases), bb

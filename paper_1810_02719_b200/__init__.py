@@ -24,7 +24,8 @@ __all__ = [
     "SpecmeshError", "InvalidArgument", "Context", "PipelineConfig", "BlockBases", "default_context",
     "build_laplacian", "default_shift", "ShiftedInverseOperator", "orthonormalize", "orthogonal_iteration",
     "dynamic_oi", "bottom_subspace", "gft", "igft", "compute_block_bases_fixed_sizes", "compute_block_bases",
-    "run_chains", "coarse_reconstruct_points",
+    "run_chains", "coarse_reconstruct_points", "coarse_reconstruct_frames", "DynamicDenoiseResult",
+    "denoise_dynamic",
 ]
 
 
@@ -462,3 +463,88 @@ def coarse_reconstruct_points(bb: BlockBases) -> np.ndarray:
     if bb.reconstruction is None:
         raise InvalidArgument("the chain was run without want_recon")
     return bb.reconstruction
+
+
+# ------------------------------------------------------------------ F3 dynamic meshes
+
+def _frame_tables(frames, n: int, keep: list):
+    """x_0, y_0, z_0, x_1, ... host pointers of (n, 3) frame arrays + SoA outputs."""
+    xyz = (C.c_void_p * (3 * len(frames)))()
+    outs = []
+    outp = (C.c_void_p * len(frames))()
+    for f, v in enumerate(frames):
+        v = np.asarray(v, dtype=np.float64)
+        if v.shape != (n, 3):
+            raise InvalidArgument(f"frame {f} has shape {v.shape}, expected ({n}, 3)")
+        for a in range(3):
+            col = _f64(v[:, a])
+            keep.append(col)
+            xyz[3 * f + a] = col.ctypes.data
+        o = np.zeros(3 * n)
+        outs.append(o)
+        outp[f] = o.ctypes.data
+    return xyz, outp, outs
+
+
+def coarse_reconstruct_frames(mesh, seg, bb: BlockBases, frames, mode: str = "weighted",
+                              ctx: Optional[Context] = None) -> List[np.ndarray]:
+    """coarse_reconstruct_points(frame, bases, mode) (pipeline.hpp:300-305) for
+    every frame of a sequence sharing ``mesh``'s connectivity -- the frames stage
+    of denoise_dynamic (denoise.hpp:280-288), batched on the GPU."""
+    ctx = ctx or default_context()
+    if bb.bases is None:
+        raise InvalidArgument("the chain was run without want_bases")
+    if mode not in _abi.AVERAGE_MODE:
+        raise InvalidArgument(f"unknown average mode '{mode}' (expected simple|weighted)")
+    keep: list = []
+    mv, sv = _mesh_view(mesh, keep), _seg_view(seg, keep)
+    k = len(bb.bases)
+    sizes = _i32([b.shape[1] for b in bb.bases])
+    offs = np.zeros(k + 1, np.int64)
+    offs[1:] = np.cumsum([b.size for b in bb.bases])
+    data = np.concatenate([np.asarray(b, np.float64).ravel(order="F") for b in bb.bases])
+    bv = _abi.smg_bases(k, sizes.ctypes.data, offs.ctypes.data, data.ctypes.data, 0)
+    xyz, outp, outs = _frame_tables(frames, mesh.n, keep)
+    ctx.check(ctx.lib.smg_coarse_reconstruct_frames(ctx.handle, C.byref(mv), C.byref(sv), C.byref(bv), len(frames),
+                                                    xyz, 0, _abi.AVERAGE_MODE[mode], outp, 0))
+    return [o.reshape((3, mesh.n)).T.copy() for o in outs]
+
+
+@dataclasses.dataclass
+class DynamicDenoiseResult:
+    """DynamicDenoiseResult (denoise.hpp:251-256): per-frame vertices (the
+    connectivity is unchanged), basis computations (= k), stage seconds."""
+
+    frames: List[np.ndarray]
+    basis_blocks_computed: int
+    timings: dict
+
+
+def denoise_dynamic(frames, seg, cfg: PipelineConfig, sizes_in_order: Optional[Sequence[int]] = None,
+                    mode: str = "weighted", ctx: Optional[Context] = None) -> DynamicDenoiseResult:
+    """denoise_dynamic (denoise.hpp:258-291) over an external segmentation:
+    bases from frames[0], then every frame's coarse projection.  ``frames``
+    are meshes sharing one connectivity (``vertices``, ``adj_offsets``,
+    ``adj_cols``)."""
+    ctx = ctx or default_context()
+    if len(frames) == 0:
+        raise InvalidArgument("dynamic denoising needs at least one frame")
+    if mode not in _abi.AVERAGE_MODE:
+        raise InvalidArgument(f"unknown average mode '{mode}' (expected simple|weighted)")
+    keep: list = []
+    mvs = (_abi.smg_mesh * len(frames))(*[_mesh_view(m, keep) for m in frames])
+    sv = _seg_view(seg, keep)
+    sizes = None if sizes_in_order is None else _i32(sizes_in_order)
+    if sizes is not None and sizes.size != seg.count:
+        raise InvalidArgument("need one subspace size per block")
+    n = frames[0].n
+    outs = [np.zeros(3 * n) for _ in frames]
+    outp = (C.c_void_p * len(frames))(*[o.ctypes.data for o in outs])
+    nb = C.c_int32()
+    tm = np.zeros(3)
+    cc = cfg.to_c()
+    ctx.check(ctx.lib.smg_denoise_dynamic(ctx.handle, len(frames), mvs, C.byref(sv), C.byref(cc), _ptr(sizes),
+                                          _abi.AVERAGE_MODE[mode], outp, 0, C.byref(nb), tm.ctypes.data_as(
+                                              _abi.c_double_p)))
+    return DynamicDenoiseResult([o.reshape((3, n)).T.copy() for o in outs], int(nb.value),
+                                {"shared_basis": float(tm[0]), "frames": float(tm[1]), "total": float(tm[2])})

@@ -49,6 +49,13 @@ class smg_chain_output(C.Structure):
                 ("basis_offsets", C.c_void_p), ("on_device", C.c_int32), ("timings", C.c_double * 6)]
 
 
+class smg_bases(C.Structure):
+    _fields_ = [("submesh_count", C.c_int32), ("subspace_size", C.c_void_p), ("offsets", C.c_void_p),
+                ("data", C.c_void_p), ("on_device", C.c_int32)]
+
+
+AVERAGE_MODE = {"simple": 0, "weighted": 1}
+
 # every symbol include/specmesh_gpu.h declares (checked by the CPU test suite)
 EXPORTED = [
     "smg_abi_version", "smg_last_error", "smg_create", "smg_destroy", "smg_default_config",
@@ -56,6 +63,7 @@ EXPORTED = [
     "smg_build_laplacian", "smg_default_shift", "smg_operator_create", "smg_operator_destroy",
     "smg_operator_apply", "smg_operator_spmm", "smg_orthonormalize", "smg_orthogonal_iteration",
     "smg_dynamic_oi", "smg_bottom_subspace", "smg_gft", "smg_igft", "smg_profile_enable", "smg_profile_read",
+    "smg_coarse_reconstruct_frames", "smg_denoise_dynamic",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -99,6 +107,12 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_igft": ([vp, C.c_int32, C.c_int32, vp, vp, vp], C.c_int),
         "smg_profile_enable": ([vp, C.c_int32], C.c_int),
         "smg_profile_read": ([vp, C.c_char_p, c_int64_p, c_double_p], C.c_int),
+        "smg_coarse_reconstruct_frames": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
+                                           C.POINTER(smg_bases), C.c_int32, vp, C.c_int32, C.c_int32, vp,
+                                           C.c_int32], C.c_int),
+        "smg_denoise_dynamic": ([vp, C.c_int32, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
+                                 C.POINTER(smg_pipeline_config), vp, C.c_int32, vp, C.c_int32, c_int32_p,
+                                 c_double_p], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -3,6 +3,7 @@
 // primitives.  Exceptions never cross the boundary.
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -930,6 +931,187 @@ void ChainRunner::apply_signs(Workspace& ws, int b, int c, cudaStream_t st) {
         ws.U.get() + (int64_t)b * ws.mstride(), ws.ld, n_, c, ws.sign.get() + (int64_t)b * ws.ld);
 }
 
+// ---------------------------------------------------------------- F3 frames
+// adjacency only (the frames stage never reads the topology's coordinates)
+void stage_topology(const smg_mesh* m, MeshDev& d, cudaStream_t st) {
+    require(m != nullptr, "mesh view is null");
+    require(m->vertex_count >= 0, "mesh vertex count is negative");
+    d.nv = m->vertex_count;
+    if (m->on_device) {
+        d.offs = m->adj_offsets;
+        d.cols = m->adj_cols;
+        return;
+    }
+    const int64_t nadj = m->adj_offsets[d.nv];
+    d.boffs.upload(m->adj_offsets, d.nv + 1, st);
+    d.bcols.upload(m->adj_cols, nadj, st);
+    d.offs = d.boffs.get();
+    d.cols = d.bcols.get();
+}
+
+// reconstruct_weighted's coverage error (partition.hpp:347-353)
+void require_covered(const Stitcher& stt, int64_t nv, cudaStream_t st) {
+    int32_t missing = 0;
+    SMG_CUDA(cudaMemcpyAsync(&missing, stt.missing, 4, cudaMemcpyDeviceToHost, st));
+    SMG_CUDA(cudaStreamSynchronize(st));
+    if (missing == 0) return;
+    std::vector<int32_t> offs = download(stt.offs, nv + 1, st);
+    std::string msg = "reconstruction is missing " + std::to_string(missing) + " vertices:";
+    int shown = 0;
+    for (int64_t g = 0; g < nv && shown < 16; ++g)
+        if (offs[g + 1] == offs[g]) {
+            msg += " " + std::to_string(g);
+            ++shown;
+        }
+    if (missing > 16) msg += " ...";
+    fail(2, msg);
+}
+
+// coarse_reconstruct_points for F frames over device bases (uniform stride
+// strideU between ids; c per id in c_of_id); xyz/out are device pointers
+void run_frames(const MeshDev& topo, const SegDev& seg, const double* bases, int64_t strideU,
+                const std::vector<int>& c_of_id, int F, const std::vector<const double*>& xyz,
+                const std::vector<double*>& outp, int weighted, cudaStream_t st) {
+    const int k = seg.k, n_d = seg.n_d;
+    require((int)c_of_id.size() == k, "basis count does not match the submesh count");
+    int c_cap = 0;
+    for (int c : c_of_id) {
+        require(c >= 1 && c <= n_d, "basis subspace size out of range for block");
+        c_cap = std::max(c_cap, c);
+    }
+    for (int id = 0; id < k; ++id)
+        require(seg.offs_h[id] == seg.offs_h[0] + (int64_t)id * n_d, "submesh member lists must be stored in id order");
+    const int32_t* members = seg.members + seg.offs_h[0];
+    Stitcher stt;
+    stt.build(members, k, n_d, (int)topo.nv, st);
+    try {
+        require_covered(stt, topo.nv, st);
+    } catch (...) {
+        stt.release(st);
+        throw;
+    }
+    DBuf<int32_t> deg, dimc;
+    deg.alloc((size_t)k * n_d, st);
+    local_degrees(members, k, n_d, topo.offs, topo.cols, deg.get(), st);
+    dimc.upload(c_of_id.data(), k, st);
+    DBuf<const double*> txyz;
+    DBuf<double*> tout;
+    txyz.upload(xyz.data(), xyz.size(), st);
+    tout.upload(outp.data(), outp.size(), st);
+    FramesParams p;
+    p.n = (int)topo.nv;
+    p.k = k;
+    p.n_d = n_d;
+    p.members = members;
+    p.bases = bases;
+    p.strideU = strideU;
+    p.dimC = dimc.get();
+    p.c_cap = c_cap;
+    p.frames = F;
+    p.xyz = txyz.get();
+    p.out = tout.get();
+    p.weighted = weighted;
+    p.deg = deg.get();
+    p.owner_offs = stt.offs;
+    p.owner_slots = stt.slots;
+    FramesWork w;
+    w.batch_frames = frames_batch(p);
+    const int64_t ldx = (3 * w.batch_frames + 7) / 8 * 8;
+    const int smax = std::max(1, n_d / 256);
+    DBuf<double> X, Xh, C, Cws;
+    X.alloc((size_t)k * n_d * ldx, st);
+    Xh.alloc((size_t)k * n_d * ldx, st);
+    C.alloc((size_t)k * c_cap * ldx, st);
+    Cws.alloc((size_t)k * smax * c_cap * ldx, st);
+    w.X = X.get();
+    w.Xhat = Xh.get();
+    w.C = C.get();
+    w.Cws = Cws.get();
+    {
+        ProfScope ps("frames", st);
+        coarse_reconstruct_frames(p, w, st);
+    }
+    SMG_CUDA(cudaGetLastError());
+    stt.release(st);
+}
+
+// bases as given -> device, uniform stride (copied into a padded buffer when the
+// caller's offsets are not an arithmetic progression or live on the host)
+const double* stage_bases(const smg_bases* b, int n_d, DBuf<double>& buf, int64_t& strideU, std::vector<int>& cs,
+                          cudaStream_t st) {
+    require(b != nullptr && b->data != nullptr && b->subspace_size != nullptr && b->offsets != nullptr,
+            "bases view is null");
+    const int k = b->submesh_count;
+    cs.assign(b->subspace_size, b->subspace_size + k);
+    int cmax = 0;
+    for (int c : cs) cmax = std::max(cmax, c);
+    bool uniform = b->on_device && k >= 1;
+    const int64_t stride = k > 1 ? b->offsets[1] - b->offsets[0] : (int64_t)n_d * cmax;
+    for (int id = 0; id < k && uniform; ++id) uniform = b->offsets[id] == b->offsets[0] + id * stride;
+    uniform = uniform && stride >= (int64_t)n_d * cmax && !(stride & 1) && !(b->offsets[0] & 1);
+    if (uniform) {
+        strideU = stride;
+        return b->data + b->offsets[0];
+    }
+    strideU = (int64_t)n_d * cmax + ((int64_t)n_d * cmax & 1);
+    buf.alloc((size_t)k * strideU, st);
+    for (int id = 0; id < k; ++id) {
+        require(b->offsets[id + 1] - b->offsets[id] >= (int64_t)n_d * cs[id], "basis offsets too small for n_d x c");
+        SMG_CUDA(cudaMemcpyAsync(buf.get() + id * strideU, b->data + b->offsets[id], sizeof(double) * n_d * cs[id],
+                                 b->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    }
+    return buf.get();
+}
+
+bool same_connectivity(const smg_mesh& a, const smg_mesh& b) {
+    if (a.vertex_count != b.vertex_count) return false;
+    if (a.adj_offsets == b.adj_offsets && a.adj_cols == b.adj_cols && a.on_device == b.on_device) return true;
+    auto host = [&](const smg_mesh& m, std::vector<int32_t>& offs, std::vector<int32_t>& cols) {
+        offs.resize(m.vertex_count + 1);
+        if (m.on_device) SMG_CUDA(cudaMemcpy(offs.data(), m.adj_offsets, 4 * offs.size(), cudaMemcpyDeviceToHost));
+        else std::memcpy(offs.data(), m.adj_offsets, 4 * offs.size());
+        cols.resize(offs.back());
+        if (m.on_device) SMG_CUDA(cudaMemcpy(cols.data(), m.adj_cols, 4 * cols.size(), cudaMemcpyDeviceToHost));
+        else std::memcpy(cols.data(), m.adj_cols, 4 * cols.size());
+    };
+    std::vector<int32_t> oa, ca, ob, cb;
+    host(a, oa, ca);
+    host(b, ob, cb);
+    return oa == ob && ca == cb;
+}
+
+// device copies of host frames / device outputs for host destinations
+struct FrameIO {
+    std::vector<DBuf<double>> in, out;
+    std::vector<const double*> xyz;
+    std::vector<double*> outp;
+    void add_input(const double* a, int on_device, int64_t nv, cudaStream_t st) {
+        require(a != nullptr, "frame coordinate pointer is null");
+        if (on_device) {
+            xyz.push_back(a);
+            return;
+        }
+        in.emplace_back();
+        in.back().upload(a, nv, st);
+        xyz.push_back(in.back().get());
+    }
+    void add_output(double* o, int on_device, int64_t nv, cudaStream_t st) {
+        require(o != nullptr, "output pointer is null");
+        if (on_device) {
+            outp.push_back(o);
+            return;
+        }
+        out.emplace_back();
+        out.back().alloc((size_t)nv * 3, st);
+        outp.push_back(out.back().get());
+    }
+    void download_outputs(double* const* dst, int on_device, int64_t nv, cudaStream_t st) {
+        if (on_device) return;
+        for (size_t f = 0; f < outp.size(); ++f)
+            SMG_CUDA(cudaMemcpyAsync(dst[f], outp[f], sizeof(double) * nv * 3, cudaMemcpyDeviceToHost, st));
+    }
+};
+
 }  // namespace
 
 // ==================================================================== C ABI
@@ -1022,6 +1204,116 @@ smg_status smg_run_chains(smg_context* ctx, int32_t n_chains, const smg_mesh* me
         require(c.basis_mode == SMG_BASIS_OI, "batched chains run the fixed-size OI path");
         ChainRunner r(ctx, n_chains, meshes, segs, c, outs);
         r.run_fixed(sizes_in_order);
+    });
+}
+
+smg_status smg_coarse_reconstruct_frames(smg_context* ctx, const smg_mesh* topology, const smg_segmentation* seg,
+                                         const smg_bases* bases, int32_t frame_count, const double* const* frames_xyz,
+                                         int32_t frames_on_device, int32_t average_mode, double* const* out,
+                                         int32_t out_on_device) {
+    return guard(ctx, [&] {
+        require(frame_count >= 1, "need at least one frame");
+        require(frames_xyz != nullptr && out != nullptr, "frame / output tables are null");
+        require(average_mode == SMG_AVERAGE_SIMPLE || average_mode == SMG_AVERAGE_WEIGHTED, "unknown average mode");
+        cudaStream_t st = ctx->stream;
+        MeshDev topo;
+        stage_topology(topology, topo, st);
+        SegDev sd;
+        stage_seg(seg, sd, st);
+        require(bases && bases->submesh_count == sd.k, "basis count does not match the submesh count");
+        DBuf<double> bbuf;
+        int64_t strideU = 0;
+        std::vector<int> cs;
+        const double* U = stage_bases(bases, sd.n_d, bbuf, strideU, cs, st);
+        FrameIO io;
+        for (int i = 0; i < 3 * frame_count; ++i) io.add_input(frames_xyz[i], frames_on_device, topo.nv, st);
+        for (int f = 0; f < frame_count; ++f) io.add_output(out[f], out_on_device, topo.nv, st);
+        run_frames(topo, sd, U, strideU, cs, frame_count, io.xyz, io.outp, average_mode == SMG_AVERAGE_WEIGHTED, st);
+        io.download_outputs(out, out_on_device, topo.nv, st);
+        SMG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+smg_status smg_denoise_dynamic(smg_context* ctx, int32_t frame_count, const smg_mesh* frames,
+                               const smg_segmentation* seg, const smg_pipeline_config* cfg,
+                               const int32_t* sizes_in_order, int32_t average_mode, double* const* out,
+                               int32_t out_on_device, int32_t* basis_blocks_computed, double* timings) {
+    return guard(ctx, [&] {
+        require(frame_count >= 1 && frames != nullptr, "dynamic denoising needs at least one frame");
+        require(out != nullptr, "output table is null");
+        require(average_mode == SMG_AVERAGE_SIMPLE || average_mode == SMG_AVERAGE_WEIGHTED, "unknown average mode");
+        cudaStream_t st = ctx->stream;
+        for (int i = 1; i < frame_count; ++i)
+            if (!same_connectivity(frames[0], frames[i]))
+                fail(2, "frame " + std::to_string(i) + " does not share the sequence connectivity");
+        Cfg c = read_cfg(cfg);
+        require(seg != nullptr && seg->submesh_count >= 1, "cannot process an empty submesh list");
+        const int k = seg->submesh_count;
+        int32_t o2[2] = {0, 0};
+        if (seg->on_device) SMG_CUDA(cudaMemcpy(o2, seg->member_offsets, 8, cudaMemcpyDeviceToHost));
+        else std::memcpy(o2, seg->member_offsets, 8);
+        const int n_d = o2[1] - o2[0];
+        require(n_d >= 2, "submesh must have at least 2 vertices");
+        const int cmax = sizes_in_order ? *std::max_element(sizes_in_order, sizes_in_order + k)
+                                        : (c.basis_mode == SMG_BASIS_OI ? c.subspace_size : c.resolve_c_max(n_d));
+        require(cmax >= 1 && cmax <= n_d, "subspace size out of range for block");
+        cudaEvent_t ev[3];
+        for (auto& e : ev) SMG_CUDA(cudaEventCreate(&e));
+        SMG_CUDA(cudaEventRecord(ev[0], st));
+        // the shared bases, from the first frame (denoise.hpp:276-277)
+        DBuf<double> bases;
+        bases.alloc((size_t)k * n_d * cmax, st);
+        std::vector<int64_t> boff(k + 1, 0);
+        std::vector<int32_t> csz(k, 0);
+        smg_chain_output o;
+        std::memset(&o, 0, sizeof(o));
+        o.subspace_size = csz.data();
+        o.bases = bases.get();
+        o.bases_capacity = (int64_t)k * n_d * cmax;
+        o.basis_offsets = boff.data();
+        o.on_device = 1;
+        {
+            ChainRunner r(ctx, 1, &frames[0], seg, c, &o);
+            if (sizes_in_order) r.run_fixed(sizes_in_order);
+            else if (c.basis_mode == SMG_BASIS_OI) {
+                std::vector<int32_t> sizes(k, c.subspace_size);
+                r.run_fixed(sizes.data());
+            } else {
+                r.run_doi();
+            }
+        }
+        SMG_CUDA(cudaEventRecord(ev[1], st));
+        if (basis_blocks_computed) *basis_blocks_computed = k;
+        // every frame's coarse projection (denoise.hpp:280-288)
+        MeshDev topo;
+        stage_topology(&frames[0], topo, st);
+        SegDev sd;
+        stage_seg(seg, sd, st);
+        smg_bases bv{k, csz.data(), boff.data(), bases.get(), 1};
+        DBuf<double> bbuf;
+        int64_t strideU = 0;
+        std::vector<int> cs;
+        const double* U = stage_bases(&bv, n_d, bbuf, strideU, cs, st);
+        FrameIO io;
+        for (int f = 0; f < frame_count; ++f) {
+            io.add_input(frames[f].x, frames[f].on_device, topo.nv, st);
+            io.add_input(frames[f].y, frames[f].on_device, topo.nv, st);
+            io.add_input(frames[f].z, frames[f].on_device, topo.nv, st);
+            io.add_output(out[f], out_on_device, topo.nv, st);
+        }
+        run_frames(topo, sd, U, strideU, cs, frame_count, io.xyz, io.outp, average_mode == SMG_AVERAGE_WEIGHTED, st);
+        io.download_outputs(out, out_on_device, topo.nv, st);
+        SMG_CUDA(cudaEventRecord(ev[2], st));
+        SMG_CUDA(cudaStreamSynchronize(st));
+        if (timings) {
+            float a = 0.f, b = 0.f;
+            SMG_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+            SMG_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+            timings[0] = a * 1e-3;
+            timings[1] = b * 1e-3;
+            timings[2] = (a + b) * 1e-3;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
     });
 }
 

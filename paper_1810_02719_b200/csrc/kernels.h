@@ -272,4 +272,35 @@ struct StitchParams {
 };
 void stitch(const StitchParams& p, cudaStream_t st);
 
+// ------------------------------------------------------------------ frames (frames.cu)
+// coarse_reconstruct_points for many frames over one set of bases (F3,
+// denoise_dynamic's frames stage, denoise.hpp:280-288)
+struct FramesParams {
+    int n = 0;                 // mesh vertex count
+    int k = 0, n_d = 0;        // submeshes (ids 0..k-1), block size
+    const int32_t* members = nullptr;  // k * n_d, sorted per submesh
+    const double* bases = nullptr;     // per id n_d x c column-major, stride strideU
+    int64_t strideU = 0;
+    const int* dimC = nullptr;         // per id c (device)
+    int c_cap = 0;
+    int frames = 0;
+    const double* const* xyz = nullptr;  // device table: x_0 y_0 z_0 x_1 ... (3 * frames)
+    double* const* out = nullptr;        // device table: frames SoA n x 3 outputs
+    int weighted = 1;
+    const int32_t* deg = nullptr;        // k * n_d local degrees
+    const int32_t* owner_offs = nullptr; // Stitcher owners
+    const int64_t* owner_slots = nullptr;
+};
+struct FramesWork {
+    int batch_frames = 1;
+    double* X = nullptr;     // k * n_d * ldx
+    double* Xhat = nullptr;  // k * n_d * ldx
+    double* C = nullptr;     // k * c_cap * ldx
+    double* Cws = nullptr;   // split-K workspace k * splits * c_cap * ldx (splits <= n_d / 256)
+};
+int frames_batch(const FramesParams& p);
+void local_degrees(const int32_t* members, int k, int n_d, const int32_t* adj_offsets, const int32_t* adj_cols,
+                   int32_t* deg, cudaStream_t st);
+void coarse_reconstruct_frames(const FramesParams& p, const FramesWork& w, cudaStream_t st);
+
 }  // namespace smg

@@ -139,6 +139,28 @@ def grid_vertices(W: int, H: int, seed: int, sigma: float) -> np.ndarray:
     return np.stack([x, y, z], axis=1)
 
 
+def grid_sequence(W: int, H: int, frames: int, seed: int, sigma: float, drift: float = 0.05) -> List[np.ndarray]:
+    """A dynamic mesh (frames sharing the grid connectivity, denoise.hpp:248-256):
+    the seeded sinusoid surface with per-sinusoid phases advancing by ``drift``
+    times a seeded rate each frame, fresh N(0, sigma^2) noise per frame."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    fx = rng.uniform(1.0, 4.0, size=3)
+    fy = rng.uniform(1.0, 4.0, size=3)
+    phi = rng.uniform(0.0, 2.0 * math.pi, size=3)
+    rate = rng.uniform(-1.0, 1.0, size=3)
+    ids = np.arange(W * H)
+    x = (ids % W).astype(np.float64)
+    y = (ids // W).astype(np.float64)
+    out = []
+    for t in range(frames):
+        z = np.zeros(W * H)
+        for k in range(3):
+            z += np.sin(2.0 * math.pi * (fx[k] * x / (W - 1) + fy[k] * y / (H - 1)) + phi[k] + drift * rate[k] * t)
+        z += rng.normal(0.0, sigma, size=W * H)
+        out.append(np.stack([x, y, z], axis=1))
+    return out
+
+
 def grid_tiles(W: int, H: int, tw: int, th: int) -> Segmentation:
     """Row-major tiles of tw (x) by th (y) vertices; local order ascending id."""
     assert W % tw == 0 and H % th == 0
