@@ -36,7 +36,8 @@ extern "C" {
 
 #define SMG_ABI_VERSION 1
 
-typedef enum { SMG_OK = 0, SMG_INVALID_ARGUMENT = 2, SMG_ERROR = 3 } smg_status;
+/* 2 = InvalidArgument, 3 = Error, 4 = ParseError (core.hpp:18-34) */
+typedef enum { SMG_OK = 0, SMG_INVALID_ARGUMENT = 2, SMG_ERROR = 3, SMG_PARSE_ERROR = 4 } smg_status;
 
 /* spectral.hpp:22 Weighting */
 typedef enum { SMG_WEIGHTING_BINARY = 0, SMG_WEIGHTING_DISTANCE = 1 } smg_weighting;
@@ -190,6 +191,47 @@ smg_status smg_denoise_dynamic(smg_context* ctx, int32_t frame_count, const smg_
                                const int32_t* sizes_in_order, int32_t average_mode,
                                double* const* out, int32_t out_on_device,
                                int32_t* basis_blocks_computed, double* timings);
+
+/* ------------------------------------------------------------ F2 spectral codec */
+
+/* EncodedBlock (compress.hpp:17-25) of every block in SubmeshOrder sequence
+ * order, plus the block payloads exactly as serialize_encoded_mesh packs them
+ * (compress.hpp:415-423: non-constant axes' values, quant_bits each, MSB first,
+ * each block padded to a byte).  Host arrays. */
+typedef struct {
+    int32_t block_count;
+    int32_t quant_bits;
+    uint32_t* submesh_id;     /* [block_count] */
+    uint32_t* subspace_size;  /* [block_count] */
+    double* coeff_min;        /* [3 * block_count] */
+    double* coeff_max;        /* [3 * block_count] */
+    uint8_t* constant_axis;   /* [block_count]: bit a = axis a constant (the serialized flags byte) */
+    uint16_t* values;         /* optional [3 * sum c]: block i's 3c values (axis-major) at 3 * (sum of earlier c) */
+    uint8_t* payload;
+    int64_t payload_capacity; /* bytes; sum over blocks of ceil(3 c quant_bits / 8) always suffices */
+    int64_t* payload_offsets; /* [block_count + 1] */
+} smg_encoded_blocks;
+
+/* compress_mesh's basis and encode stages (compress.hpp:152-219) over an
+ * EXTERNAL segmentation: Binary weighting (forced, as the reference does);
+ * sizes_in_order (host, one c per position) when given, else cfg->basis_mode:
+ * OI -> subspace_size for every block, DOI -> the sizes a DOI probe chain picks
+ * (compress.hpp:162-166); then the fixed-size OI chain, gft and encode_block
+ * (compress.hpp:33-62) per block.  quant_bits in [1, 16]. */
+smg_status smg_compress_blocks(smg_context* ctx, const smg_mesh* mesh, const smg_segmentation* seg,
+                               const smg_pipeline_config* cfg, const int32_t* sizes_in_order,
+                               int32_t quant_bits, smg_encoded_blocks* out);
+
+/* decompress_mesh (compress.hpp:221-256) over an external segmentation: replays
+ * the chain from `topology`'s connectivity alone (coordinates not read; Binary
+ * weighting, the blocks' sizes), decodes every block (dequantize_block +
+ * igft, compress.hpp:64-89) and stitches with degree weights.  `in->payload`
+ * and the per-block headers are read; `in->values` may be NULL.  A block count
+ * or order that does not match the segmentation -> status 4 (ParseError) with
+ * the reference message.  out: SoA vertex_count x 3. */
+smg_status smg_decompress_blocks(smg_context* ctx, const smg_mesh* topology, const smg_segmentation* seg,
+                                 const smg_pipeline_config* cfg, const smg_encoded_blocks* in,
+                                 double* out, int32_t out_on_device);
 
 /* ------------------------------------------------------------ L3 primitives
  * Host pointers, column-major.  They run the same kernels as the chain. */

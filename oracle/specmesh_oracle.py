@@ -754,3 +754,283 @@ def denoise_dynamic(frames: List[np.ndarray], submeshes: List[Submesh], sequence
     bb = compute_block_bases_fixed_sizes(frames[0], submeshes, sequence, cfg, sizes_in_order)
     out = [coarse_reconstruct_points(bb, v, weighted) for v in frames]
     return out, len(bb.bases), bb
+
+
+# --------------------------------------------------------------------------
+# F2 spectral codec (compress.hpp)
+
+@dataclasses.dataclass
+class EncodedBlock:
+    """compress.hpp:17-25."""
+
+    submesh_id: int = 0
+    subspace_size: int = 0
+    coeff_min: List[float] = dataclasses.field(default_factory=lambda: [0.0, 0.0, 0.0])
+    coeff_max: List[float] = dataclasses.field(default_factory=lambda: [0.0, 0.0, 0.0])
+    constant_axis: List[int] = dataclasses.field(default_factory=lambda: [0, 0, 0])
+    values: List[int] = dataclasses.field(default_factory=list)  # axis-major: c x, c y, c z
+
+
+def bits_per_vertex(quant_bits: int, subspace_size: int, block_count: int, vertex_count: int) -> float:
+    """compress.hpp:28-31"""
+    require(quant_bits > 0 and subspace_size > 0 and block_count > 0 and vertex_count > 0,
+            "bits_per_vertex arguments must be positive")
+    return 3.0 * quant_bits * subspace_size * block_count / float(vertex_count)
+
+
+def encode_coefficients(coefficients: np.ndarray, quant_bits: int, submesh_id: int = 0) -> EncodedBlock:
+    """compress.hpp:36-62 after the gft (:40): per-axis range, step = (hi-lo)/2^q,
+    value = clamp(long((x - lo) / step), 0, 2^q - 1); constant axes send nothing.
+    Python floats are IEEE doubles without FMA contraction, int() truncates toward
+    zero like static_cast<long>."""
+    require(1 <= quant_bits <= 16, "quantization bits must be in [1,16]")
+    c = int(coefficients.shape[0])
+    levels = 1 << quant_bits
+    blk = EncodedBlock(submesh_id=submesh_id, subspace_size=c, values=[0] * (3 * c))
+    for axis in range(3):
+        col = [float(v) for v in coefficients[:, axis]]
+        lo, hi = min(col), max(col)
+        blk.coeff_min[axis] = lo
+        blk.coeff_max[axis] = hi
+        if not (hi > lo):
+            blk.constant_axis[axis] = 1
+            continue
+        step = (hi - lo) / levels
+        for i in range(c):
+            q = int((col[i] - lo) / step)
+            blk.values[axis * c + i] = min(max(q, 0), levels - 1)
+    return blk
+
+
+def encode_block(sub: Submesh, vertices: np.ndarray, basis: np.ndarray, quant_bits: int,
+                 submesh_id: int = 0) -> EncodedBlock:
+    """compress.hpp:33-62"""
+    require(1 <= quant_bits <= 16, "quantization bits must be in [1,16]")
+    require(basis.shape[0] == sub.size(), "basis does not match the submesh size")
+    return encode_coefficients(gft(basis, sub.local_coords(vertices)), quant_bits, submesh_id)
+
+
+def dequantize_block(block: EncodedBlock, quant_bits: int) -> np.ndarray:
+    """compress.hpp:64-80: lo + (q + 0.5) * step."""
+    c = block.subspace_size
+    levels = 1 << quant_bits
+    out = np.zeros((c, 3))
+    for axis in range(3):
+        if block.constant_axis[axis]:
+            out[:, axis] = block.coeff_min[axis]
+            continue
+        step = (block.coeff_max[axis] - block.coeff_min[axis]) / levels
+        for i in range(c):
+            out[i, axis] = block.coeff_min[axis] + (block.values[axis * c + i] + 0.5) * step
+    return out
+
+
+def decode_block(block: EncodedBlock, basis: np.ndarray, quant_bits: int) -> np.ndarray:
+    """compress.hpp:84-89"""
+    if basis.shape[1] != block.subspace_size:
+        raise Error("decode_block: basis subspace size does not match the block")
+    return igft(basis, dequantize_block(block, quant_bits))
+
+
+@dataclasses.dataclass
+class EncodedMesh:
+    """compress.hpp:100-150 (config echo + connectivity + blocks in order)."""
+
+    version: int = 1
+    basis_mode: int = 0  # BasisMode::OI
+    quant_bits: int = 12
+    part_count: int = 0
+    growth: float = 1.15
+    subspace_size: int = 0
+    eps_low: float = 0.0
+    eps_high: float = 0.0
+    c_min: int = 0
+    c_max: int = 0
+    power: int = 2
+    iterations: int = 2
+    initial_iterations: int = 60
+    seed: int = 1
+    dense_limit: int = 4096
+    shift_scale: float = 1e-8
+    vertex_count: int = 0
+    faces: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros((0, 3), np.int32))
+    blocks: List[EncodedBlock] = dataclasses.field(default_factory=list)
+
+    def total_bpv(self) -> float:
+        """compress.hpp:145-150"""
+        bits = sum(3 * self.quant_bits * b.subspace_size for b in self.blocks)
+        return bits / self.vertex_count
+
+
+def compress_mesh(vertices: np.ndarray, faces: np.ndarray, submeshes: List[Submesh], sequence,
+                  cfg: PipelineConfig, quant_bits: int, sizes_in_order=None, doi: bool = False):
+    """compress.hpp:152-219 with an external segmentation: Binary weighting
+    (:157); DOI only picks the sizes (:162-166); the transmitted bases are the
+    fixed-size OI chain (:168-174); blocks in order sequence (:208-212)."""
+    cfg = dataclasses.replace(cfg, weighting=BINARY)
+    k = len(submeshes)
+    if sizes_in_order is None:
+        if doi:
+            probe = compute_block_bases_doi(vertices, submeshes, sequence, cfg)
+            sizes_in_order = [probe.stats[i].subspace_size for i in sequence]
+        else:
+            sizes_in_order = [cfg.subspace_size] * k
+    bb = compute_block_bases_fixed_sizes(vertices, submeshes, sequence, cfg, sizes_in_order)
+    enc = EncodedMesh(basis_mode=1 if doi else 0, quant_bits=quant_bits, part_count=k,
+                      subspace_size=cfg.subspace_size, eps_low=cfg.eps_low, eps_high=cfg.eps_high,
+                      c_min=cfg.c_min, c_max=cfg.c_max, power=cfg.power, iterations=cfg.iterations,
+                      initial_iterations=cfg.initial_iterations, seed=cfg.seed, dense_limit=cfg.dense_limit,
+                      shift_scale=cfg.shift_scale, vertex_count=int(vertices.shape[0]),
+                      faces=np.asarray(faces, np.int32))
+    for sid in sequence:
+        enc.blocks.append(encode_block(submeshes[sid], vertices, bb.bases[sid], quant_bits, int(sid)))
+    return enc, bb
+
+
+def replay_config(enc: EncodedMesh) -> PipelineConfig:
+    """compress.hpp:125-143"""
+    return PipelineConfig(weighting=BINARY, subspace_size=enc.subspace_size, eps_low=enc.eps_low,
+                          eps_high=enc.eps_high, c_min=enc.c_min, c_max=enc.c_max, power=enc.power,
+                          iterations=enc.iterations, initial_iterations=enc.initial_iterations, seed=enc.seed,
+                          dense_limit=enc.dense_limit, shift_scale=enc.shift_scale)
+
+
+def decompress_mesh(enc: EncodedMesh, submeshes: List[Submesh], sequence):
+    """compress.hpp:221-256: replay the chain from connectivity alone (zero
+    coordinates, :224-226), decode every block, stitch Weighted."""
+    cfg = replay_config(enc)
+    zero = np.zeros((enc.vertex_count, 3))
+    sizes = [b.subspace_size for b in enc.blocks]
+    if len(enc.blocks) != len(sequence):
+        raise ParseError("encoded block count does not match the replayed segmentation")
+    bb = compute_block_bases_fixed_sizes(zero, submeshes, sequence, cfg, sizes)
+    locals_: List[Optional[np.ndarray]] = [None] * len(submeshes)
+    for pos, blk in enumerate(enc.blocks):
+        if blk.submesh_id >= len(locals_) or int(sequence[pos]) != blk.submesh_id:
+            raise ParseError("encoded block order does not match the replayed segmentation")
+        locals_[blk.submesh_id] = decode_block(blk, bb.bases[blk.submesh_id], enc.quant_bits)
+    return reconstruct_weighted(submeshes, locals_, enc.vertex_count, True)
+
+
+CODEC_MAGIC = b"SPECMSH1"
+
+
+class _BitPacker:
+    """compress.hpp:334-360: MSB first, pad_to_byte shifts the tail left."""
+
+    def __init__(self, out: bytearray):
+        self.out, self.buffer, self.filled = out, 0, 0
+
+    def put(self, value: int, bits: int) -> None:
+        for b in range(bits - 1, -1, -1):
+            self.buffer = ((self.buffer << 1) | ((value >> b) & 1)) & 0xFF
+            self.filled += 1
+            if self.filled == 8:
+                self._flush()
+
+    def pad_to_byte(self) -> None:
+        if self.filled > 0:
+            self.buffer = (self.buffer << (8 - self.filled)) & 0xFF
+            self._flush()
+
+    def _flush(self) -> None:
+        self.out.append(self.buffer)
+        self.buffer, self.filled = 0, 0
+
+
+def pack_block_values(block: EncodedBlock, quant_bits: int) -> bytes:
+    """The payload one block contributes (compress.hpp:415-423)."""
+    out = bytearray()
+    pk = _BitPacker(out)
+    c = block.subspace_size
+    for a in range(3):
+        if block.constant_axis[a]:
+            continue
+        for i in range(c):
+            pk.put(block.values[a * c + i], quant_bits)
+    pk.pad_to_byte()
+    return bytes(out)
+
+
+def serialize_encoded_mesh(enc: EncodedMesh) -> bytes:
+    """compress.hpp:392-426: little endian, coefficients bit-packed MSB first."""
+    o = bytearray(CODEC_MAGIC)
+    o += struct.pack("<IBBH", enc.version, enc.basis_mode, 0, enc.quant_bits)
+    o += struct.pack("<IdI", enc.part_count, enc.growth, enc.subspace_size)
+    o += struct.pack("<dd", enc.eps_low, enc.eps_high)
+    o += struct.pack("<IIIII", enc.c_min, enc.c_max, enc.power, enc.iterations, enc.initial_iterations)
+    o += struct.pack("<QId", enc.seed, enc.dense_limit, enc.shift_scale)
+    faces = np.asarray(enc.faces, np.int64).reshape(-1, 3)
+    o += struct.pack("<II", enc.vertex_count, faces.shape[0])
+    o += faces.astype("<u4").tobytes()
+    o += struct.pack("<I", len(enc.blocks))
+    for b in enc.blocks:
+        o += struct.pack("<IIB", b.submesh_id, b.subspace_size,
+                         b.constant_axis[0] | (b.constant_axis[1] << 1) | (b.constant_axis[2] << 2))
+        o += struct.pack("<3d", *b.coeff_min)
+        o += struct.pack("<3d", *b.coeff_max)
+        o += pack_block_values(b, enc.quant_bits)
+    return bytes(o)
+
+
+class _Reader:
+    """compress.hpp:294-332 (ByteReader) + :362-386 (BitUnpacker)."""
+
+    def __init__(self, data: bytes):
+        self.data, self.at = data, 0
+
+    def take(self, n: int) -> bytes:
+        if self.at + n > len(self.data):
+            raise ParseError("bitstream truncated")
+        v = self.data[self.at:self.at + n]
+        self.at += n
+        return v
+
+    def unpack(self, fmt: str):
+        return struct.unpack(fmt, self.take(struct.calcsize(fmt)))
+
+
+def parse_encoded_mesh(data: bytes) -> EncodedMesh:
+    """compress.hpp:428-474"""
+    r = _Reader(bytes(data))
+    if r.take(8) != CODEC_MAGIC:
+        raise ParseError("not a specmesh bitstream (bad magic)")
+    enc = EncodedMesh()
+    (enc.version,) = r.unpack("<I")
+    if enc.version != 1:
+        raise ParseError("unsupported bitstream version")
+    enc.basis_mode, _w, enc.quant_bits = r.unpack("<BBH")
+    if enc.quant_bits < 1 or enc.quant_bits > 16:
+        raise ParseError("bitstream has invalid quantization bits")
+    enc.part_count, enc.growth, enc.subspace_size = r.unpack("<IdI")
+    enc.eps_low, enc.eps_high = r.unpack("<dd")
+    enc.c_min, enc.c_max, enc.power, enc.iterations, enc.initial_iterations = r.unpack("<IIIII")
+    enc.seed, enc.dense_limit, enc.shift_scale = r.unpack("<QId")
+    enc.vertex_count, nf = r.unpack("<II")
+    enc.faces = np.frombuffer(r.take(12 * nf), "<u4").astype(np.int32).reshape(nf, 3)
+    (nb,) = r.unpack("<I")
+    q = enc.quant_bits
+    for _ in range(nb):
+        b = EncodedBlock()
+        b.submesh_id, b.subspace_size, flags = r.unpack("<IIB")
+        b.constant_axis = [(flags >> a) & 1 for a in range(3)]
+        b.coeff_min = list(r.unpack("<3d"))
+        b.coeff_max = list(r.unpack("<3d"))
+        b.values = [0] * (3 * b.subspace_size)
+        buf, filled = 0, 0
+        for a in range(3):
+            if b.constant_axis[a]:
+                continue
+            for i in range(b.subspace_size):
+                v = 0
+                for _bit in range(q):
+                    if filled == 0:
+                        buf = r.take(1)[0]
+                        filled = 8
+                    v = (v << 1) | ((buf >> (filled - 1)) & 1)
+                    filled -= 1
+                b.values[a * b.subspace_size + i] = v
+        enc.blocks.append(b)
+    if r.at != len(r.data):
+        raise ParseError("trailing bytes after bitstream payload")
+    return enc

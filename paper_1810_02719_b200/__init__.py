@@ -21,7 +21,7 @@ import numpy as np
 from . import _abi
 
 __all__ = [
-    "SpecmeshError", "InvalidArgument", "Context", "PipelineConfig", "BlockBases", "default_context",
+    "SpecmeshError", "InvalidArgument", "ParseError", "Context", "PipelineConfig", "BlockBases", "default_context",
     "build_laplacian", "default_shift", "ShiftedInverseOperator", "orthonormalize", "orthogonal_iteration",
     "dynamic_oi", "bottom_subspace", "gft", "igft", "compute_block_bases_fixed_sizes", "compute_block_bases",
     "run_chains", "coarse_reconstruct_points", "coarse_reconstruct_frames", "DynamicDenoiseResult",
@@ -35,6 +35,10 @@ class SpecmeshError(RuntimeError):
 
 class InvalidArgument(SpecmeshError):
     """specmesh::InvalidArgument (core.hpp:24-28)."""
+
+
+class ParseError(SpecmeshError):
+    """specmesh::ParseError (core.hpp:30-34)."""
 
 
 def _ptr(a: Optional[np.ndarray]):
@@ -72,6 +76,8 @@ class Context:
         msg = self.lib.smg_last_error(self.handle).decode()
         if status == _abi.SMG_INVALID_ARGUMENT:
             raise InvalidArgument(msg)
+        if status == _abi.SMG_PARSE_ERROR:
+            raise ParseError(msg)
         raise SpecmeshError(msg)
 
     def close(self) -> None:

@@ -14,7 +14,7 @@ from typing import Optional
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libspecmesh_b200.so")
 
-SMG_OK, SMG_INVALID_ARGUMENT, SMG_ERROR = 0, 2, 3
+SMG_OK, SMG_INVALID_ARGUMENT, SMG_ERROR, SMG_PARSE_ERROR = 0, 2, 3, 4
 WEIGHTING = {"binary": 0, "distance": 1}
 BASIS_MODE = {"oi": 0, "doi": 1}
 
@@ -54,6 +54,13 @@ class smg_bases(C.Structure):
                 ("data", C.c_void_p), ("on_device", C.c_int32)]
 
 
+class smg_encoded_blocks(C.Structure):
+    _fields_ = [("block_count", C.c_int32), ("quant_bits", C.c_int32), ("submesh_id", C.c_void_p),
+                ("subspace_size", C.c_void_p), ("coeff_min", C.c_void_p), ("coeff_max", C.c_void_p),
+                ("constant_axis", C.c_void_p), ("values", C.c_void_p), ("payload", C.c_void_p),
+                ("payload_capacity", C.c_int64), ("payload_offsets", C.c_void_p)]
+
+
 AVERAGE_MODE = {"simple": 0, "weighted": 1}
 
 # every symbol include/specmesh_gpu.h declares (checked by the CPU test suite)
@@ -63,7 +70,7 @@ EXPORTED = [
     "smg_build_laplacian", "smg_default_shift", "smg_operator_create", "smg_operator_destroy",
     "smg_operator_apply", "smg_operator_spmm", "smg_orthonormalize", "smg_orthogonal_iteration",
     "smg_dynamic_oi", "smg_bottom_subspace", "smg_gft", "smg_igft", "smg_profile_enable", "smg_profile_read",
-    "smg_coarse_reconstruct_frames", "smg_denoise_dynamic",
+    "smg_coarse_reconstruct_frames", "smg_denoise_dynamic", "smg_compress_blocks", "smg_decompress_blocks",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -110,6 +117,12 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_coarse_reconstruct_frames": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
                                            C.POINTER(smg_bases), C.c_int32, vp, C.c_int32, C.c_int32, vp,
                                            C.c_int32], C.c_int),
+        "smg_compress_blocks": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
+                                 C.POINTER(smg_pipeline_config), vp, C.c_int32, C.POINTER(smg_encoded_blocks)],
+                                C.c_int),
+        "smg_decompress_blocks": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
+                                   C.POINTER(smg_pipeline_config), C.POINTER(smg_encoded_blocks), vp, C.c_int32],
+                                  C.c_int),
         "smg_denoise_dynamic": ([vp, C.c_int32, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
                                  C.POINTER(smg_pipeline_config), vp, C.c_int32, vp, C.c_int32, c_int32_p,
                                  c_double_p], C.c_int),

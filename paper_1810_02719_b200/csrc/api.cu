@@ -132,6 +132,7 @@ struct Cfg {
     double eps_low, eps_high, shift_scale;
     uint64_t seed;
     int basis_mode;
+    bool topology_ordering = false;  // codec replay (TileSet::topology_ordering)
     int resolve_c_max(int n) const {
         const int cm = c_max > 0 ? c_max : std::max(64, 2 * subspace_size);
         return std::min(cm, n);
@@ -600,6 +601,7 @@ private:
                 t.y = meshes_[b].y;
                 t.z = meshes_[b].z;
             }
+        ts_.topology_ordering = cfg_.topology_ordering;
         ts_.build(refs, n_, cfg_.weighting, cfg_.shift_scale, st_);
         // tile index of (chain b, submesh id): pos_of[id] * B + b
         tile_of_.resize(B_);
@@ -1314,6 +1316,267 @@ smg_status smg_denoise_dynamic(smg_context* ctx, int32_t frame_count, const smg_
             timings[2] = (a + b) * 1e-3;
         }
         for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+smg_status smg_compress_blocks(smg_context* ctx, const smg_mesh* mesh, const smg_segmentation* seg,
+                               const smg_pipeline_config* cfg, const int32_t* sizes_in_order, int32_t quant_bits,
+                               smg_encoded_blocks* out) {
+    return guard(ctx, [&] {
+        require(quant_bits >= 1 && quant_bits <= 16, "quantization bits must be in [1,16]");
+        require(out != nullptr && out->submesh_id && out->subspace_size && out->coeff_min && out->coeff_max &&
+                    out->constant_axis && out->payload && out->payload_offsets,
+                "encoded block output is null");
+        require(seg != nullptr && seg->submesh_count >= 1, "cannot process an empty submesh list");
+        cudaStream_t st = ctx->stream;
+        Cfg c = read_cfg(cfg);
+        c.weighting = SMG_WEIGHTING_BINARY;  // compress.hpp:157: the decoder has no coordinates
+        c.topology_ordering = true;
+        const int k = seg->submesh_count;
+        require(out->block_count == k, "encoded block output must hold one block per submesh");
+        std::vector<int32_t> sizes(k);
+        if (sizes_in_order) {
+            sizes.assign(sizes_in_order, sizes_in_order + k);
+        } else if (c.basis_mode == SMG_BASIS_OI) {
+            sizes.assign(k, c.subspace_size);
+        } else {
+            // DOI probe picks each block's size (compress.hpp:162-166)
+            std::vector<int32_t> by_id(k, 0);
+            smg_chain_output po;
+            std::memset(&po, 0, sizeof(po));
+            po.subspace_size = by_id.data();
+            ChainRunner r(ctx, 1, mesh, seg, c, &po);
+            r.run_doi();
+            SegDev sd;
+            stage_seg(seg, sd, st);
+            for (int p = 0; p < k; ++p) sizes[p] = by_id[sd.seq_h[p]];
+        }
+        // the transmitted bases: the fixed-size OI chain (compress.hpp:168-174)
+        SegDev sd;
+        stage_seg(seg, sd, st);
+        int cmax = 0;
+        for (int v : sizes) cmax = std::max(cmax, v);
+        DBuf<double> coef;
+        coef.alloc((size_t)k * cmax * 3, st);
+        std::vector<int64_t> coff(k + 1, 0);
+        smg_chain_output o;
+        std::memset(&o, 0, sizeof(o));
+        o.coefficients = coef.get();
+        o.coefficients_capacity = (int64_t)k * cmax * 3;
+        o.coefficient_offsets = coff.data();
+        o.on_device = 1;
+        {
+            Cfg cf = c;
+            cf.basis_mode = SMG_BASIS_OI;
+            ChainRunner r(ctx, 1, mesh, seg, cf, &o);
+            r.run_fixed(sizes.data());
+        }
+        // encode_block per position (compress.hpp:208-212)
+        std::vector<const double*> cp(k);
+        std::vector<int64_t> voff(k + 1, 0);
+        for (int p = 0; p < k; ++p) {
+            const int id = sd.seq_h[p];
+            cp[p] = coef.get() + coff[id];
+            voff[p + 1] = voff[p] + 3 * (int64_t)sizes[p];
+            out->submesh_id[p] = (uint32_t)id;
+            out->subspace_size[p] = (uint32_t)sizes[p];
+        }
+        DBuf<const double*> dcp;
+        DBuf<int> dc;
+        DBuf<int64_t> dvoff, dbytes, dpoff;
+        DBuf<uint16_t> dvals;
+        DBuf<double> dlo, dhi;
+        DBuf<uint8_t> dflags, dpay;
+        dcp.upload(cp, st);
+        dc.upload(sizes.data(), k, st);
+        dvoff.upload(voff, st);
+        dvals.alloc(voff[k], st);
+        dlo.alloc(3 * (size_t)k, st);
+        dhi.alloc(3 * (size_t)k, st);
+        dflags.alloc(k, st);
+        dbytes.alloc(k, st);
+        CodecParams cp_;
+        cp_.blocks = k;
+        cp_.quant_bits = quant_bits;
+        cp_.c = dc.get();
+        cp_.coef = dcp.get();
+        cp_.values = dvals.get();
+        cp_.value_off = dvoff.get();
+        cp_.lo = dlo.get();
+        cp_.hi = dhi.get();
+        cp_.flags = dflags.get();
+        cp_.payload_bytes = dbytes.get();
+        {
+            ProfScope ps("encode", st);
+            codec_encode(cp_, st);
+        }
+        std::vector<int64_t> bytes = download(dbytes.get(), k, st);
+        std::vector<int64_t> poff(k + 1, 0);
+        for (int p = 0; p < k; ++p) poff[p + 1] = poff[p] + bytes[p];
+        require(out->payload_capacity >= poff[k], "payload buffer too small");
+        dpoff.upload(poff, st);
+        dpay.alloc(std::max<int64_t>(poff[k], 1), st);
+        cp_.payload = dpay.get();
+        cp_.payload_off = dpoff.get();
+        {
+            ProfScope ps("encode", st);
+            codec_pack(cp_, st);
+        }
+        SMG_CUDA(cudaGetLastError());
+        if (poff[k]) SMG_CUDA(cudaMemcpyAsync(out->payload, dpay.get(), poff[k], cudaMemcpyDeviceToHost, st));
+        SMG_CUDA(cudaMemcpyAsync(out->coeff_min, dlo.get(), 24 * (size_t)k, cudaMemcpyDeviceToHost, st));
+        SMG_CUDA(cudaMemcpyAsync(out->coeff_max, dhi.get(), 24 * (size_t)k, cudaMemcpyDeviceToHost, st));
+        SMG_CUDA(cudaMemcpyAsync(out->constant_axis, dflags.get(), k, cudaMemcpyDeviceToHost, st));
+        if (out->values)
+            SMG_CUDA(cudaMemcpyAsync(out->values, dvals.get(), 2 * voff[k], cudaMemcpyDeviceToHost, st));
+        std::memcpy(out->payload_offsets, poff.data(), sizeof(int64_t) * (k + 1));
+        out->quant_bits = quant_bits;
+        SMG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+smg_status smg_decompress_blocks(smg_context* ctx, const smg_mesh* topology, const smg_segmentation* seg,
+                                 const smg_pipeline_config* cfg, const smg_encoded_blocks* in, double* out,
+                                 int32_t out_on_device) {
+    return guard(ctx, [&] {
+        require(in != nullptr && in->submesh_id && in->subspace_size && in->coeff_min && in->coeff_max &&
+                    in->constant_axis && in->payload && in->payload_offsets,
+                "encoded block input is null");
+        require(out != nullptr, "output is null");
+        const int q = in->quant_bits;
+        if (q < 1 || q > 16) fail(4, "bitstream has invalid quantization bits");
+        cudaStream_t st = ctx->stream;
+        Cfg c = read_cfg(cfg);  // EncodedMesh::replay_config (compress.hpp:125-143)
+        c.weighting = SMG_WEIGHTING_BINARY;
+        c.basis_mode = SMG_BASIS_OI;
+        c.topology_ordering = true;
+        MeshDev topo;
+        stage_topology(topology, topo, st);
+        SegDev sd;
+        stage_seg(seg, sd, st);
+        const int k = sd.k, nb = in->block_count;
+        require(nb >= 0, "negative block count");
+        // sizes in order from the blocks (compress.hpp:237-241); an empty or short
+        // block list still replays the chain in the reference before the count check
+        if (nb != k) fail(4, "encoded block count does not match the replayed segmentation");
+        std::vector<int32_t> sizes(k);
+        for (int p = 0; p < k; ++p) {
+            sizes[p] = (int32_t)in->subspace_size[p];
+            require(sizes[p] >= 1 && sizes[p] <= sd.n_d, "subspace size out of range for block");
+        }
+        for (int p = 0; p < k; ++p)
+            if (in->submesh_id[p] >= (uint32_t)k || sd.seq_h[p] != (int)in->submesh_id[p])
+                fail(4, "encoded block order does not match the replayed segmentation");
+        // replay the chain from connectivity alone (zero coordinates, compress.hpp:224-226)
+        DBuf<double> zero;
+        zero.alloc(std::max<int64_t>(topo.nv, 1), st);
+        zero.zero();
+        smg_mesh zm{topo.nv, zero.get(), zero.get(), zero.get(), topo.offs, topo.cols, 1};
+        smg_segmentation zs = *seg;
+        int cmax = 0;
+        for (int v : sizes) cmax = std::max(cmax, v);
+        DBuf<double> bases;
+        bases.alloc((size_t)k * sd.n_d * cmax, st);
+        std::vector<int64_t> boff(k + 1, 0);
+        std::vector<int32_t> csz(k, 0);
+        smg_chain_output o;
+        std::memset(&o, 0, sizeof(o));
+        o.subspace_size = csz.data();
+        o.bases = bases.get();
+        o.bases_capacity = (int64_t)k * sd.n_d * cmax;
+        o.basis_offsets = boff.data();
+        o.on_device = 1;
+        {
+            ChainRunner r(ctx, 1, &zm, &zs, c, &o);
+            r.run_fixed(sizes.data());
+        }
+        smg_bases bv{k, csz.data(), boff.data(), bases.get(), 1};
+        DBuf<double> bbuf;
+        int64_t strideU = 0;
+        std::vector<int> cs;
+        const double* U = stage_bases(&bv, sd.n_d, bbuf, strideU, cs, st);
+        // dequantize (compress.hpp:64-80) straight from the payload, by submesh id
+        const int64_t pbytes = in->payload_offsets[k];
+        std::vector<int> dest(k);
+        for (int p = 0; p < k; ++p) dest[p] = (int)in->submesh_id[p];
+        DBuf<int> dc, ddest;
+        DBuf<int64_t> dpoff;
+        DBuf<double> dlo, dhi, C, Xh;
+        DBuf<uint8_t> dflags, dpay;
+        dc.upload(sizes.data(), k, st);
+        ddest.upload(dest, st);
+        dpoff.upload(in->payload_offsets, k + 1, st);
+        dlo.upload(in->coeff_min, 3 * (size_t)k, st);
+        dhi.upload(in->coeff_max, 3 * (size_t)k, st);
+        dflags.upload(in->constant_axis, k, st);
+        dpay.upload(in->payload, std::max<int64_t>(pbytes, 1), st);
+        const int ldc = 8;
+        C.alloc((size_t)k * cmax * ldc, st);
+        C.zero();
+        Xh.alloc((size_t)k * sd.n_d * ldc, st);
+        CodecParams cp_;
+        cp_.blocks = k;
+        cp_.quant_bits = q;
+        cp_.c = dc.get();
+        cp_.lo = dlo.get();
+        cp_.hi = dhi.get();
+        cp_.flags = dflags.get();
+        cp_.payload = dpay.get();
+        cp_.payload_off = dpoff.get();
+        cp_.dest = ddest.get();
+        cp_.C = C.get();
+        cp_.strideC = (int64_t)cmax * ldc;
+        cp_.ldc = ldc;
+        // igft per id + reconstruct_weighted (Weighted, compress.hpp:251-253)
+        for (int id = 0; id < k; ++id)
+            require(sd.offs_h[id] == sd.offs_h[0] + (int64_t)id * sd.n_d, "submesh member lists must be stored in id order");
+        const int32_t* members = sd.members + sd.offs_h[0];
+        Stitcher stt;
+        stt.build(members, k, sd.n_d, (int)topo.nv, st);
+        try {
+            require_covered(stt, topo.nv, st);
+        } catch (...) {
+            stt.release(st);
+            throw;
+        }
+        DBuf<int32_t> deg, dimc;
+        deg.alloc((size_t)k * sd.n_d, st);
+        local_degrees(members, k, sd.n_d, topo.offs, topo.cols, deg.get(), st);
+        dimc.upload(cs.data(), k, st);
+        DBuf<double> obuf;
+        double* dst = out;
+        if (!out_on_device) {
+            obuf.alloc((size_t)topo.nv * 3, st);
+            dst = obuf.get();
+        }
+        DBuf<double*> tout;
+        std::vector<double*> ov{dst};
+        tout.upload(ov, st);
+        FramesParams p;
+        p.n = (int)topo.nv;
+        p.k = k;
+        p.n_d = sd.n_d;
+        p.members = members;
+        p.bases = U;
+        p.strideU = strideU;
+        p.dimC = dimc.get();
+        p.c_cap = cmax;
+        p.frames = 1;
+        p.out = tout.get();
+        p.weighted = 1;
+        p.deg = deg.get();
+        p.owner_offs = stt.offs;
+        p.owner_slots = stt.slots;
+        {
+            ProfScope ps("decode", st);
+            codec_unpack(cp_, st);
+            reconstruct_from_coefficients(p, C.get(), ldc, Xh.get(), st);
+        }
+        SMG_CUDA(cudaGetLastError());
+        stt.release(st);
+        if (!out_on_device)
+            SMG_CUDA(cudaMemcpyAsync(out, dst, sizeof(double) * topo.nv * 3, cudaMemcpyDeviceToHost, st));
+        SMG_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -38,7 +38,7 @@ int guarded_call(smg_context* ctx, F&& f) {
         return 0;
     } catch (const Failure& e) {
         ctx->error = e.what();
-        return e.code == 2 ? 2 : 3;
+        return (e.code == 2 || e.code == 4) ? e.code : 3;
     } catch (const std::exception& e) {
         ctx->error = e.what();
         return 3;

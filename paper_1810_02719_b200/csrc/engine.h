@@ -86,6 +86,9 @@ struct TileSet {
     int W = 0, Kb = 0, npad = 0;
     int cpl = 16;  // bound on a row's couplings into the previous block (factor smem stride)
     bool use_perm = false;
+    // orderings from the connectivity alone (codec: the decoder has no coordinates,
+    // so encoder and decoder must factor identically)
+    bool topology_ordering = false;
     int64_t total_nnz = 0;
     DBuf<TileRef> refs;
     DBuf<int32_t> nnz, rowptr, cols, perm, bw, blockw;

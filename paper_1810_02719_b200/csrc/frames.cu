@@ -183,4 +183,26 @@ void coarse_reconstruct_frames(const FramesParams& p, const FramesWork& w, cudaS
     }
 }
 
+void reconstruct_from_coefficients(const FramesParams& p, const double* C, int ldc, double* Xhat, cudaStream_t st) {
+    GemmParams h;
+    h.M = p.n_d;
+    h.N = 3;
+    h.K = p.c_cap;
+    h.batch = p.k;
+    h.A = p.bases;
+    h.lda = p.n_d;
+    h.strideA = p.strideU;
+    h.B = C;
+    h.ldb = ldc;
+    h.strideB = (int64_t)p.c_cap * ldc;
+    h.C = Xhat;
+    h.ldc = ldc;
+    h.strideC = (int64_t)p.n_d * ldc;
+    h.dimK = p.dimC;
+    h.dimStride = 1;
+    gemm(h, true, false, st);
+    ::smg::count_launch(), stitch_frames_kernel<<<grid_for(p.n, 256, 4096), 256, 0, st>>>(
+        p.n, p.n_d, p.weighted, p.owner_offs, p.owner_slots, p.deg, Xhat, ldc, 0, 1, p.out);
+}
+
 }  // namespace smg

@@ -303,4 +303,30 @@ void local_degrees(const int32_t* members, int k, int n_d, const int32_t* adj_of
                    int32_t* deg, cudaStream_t st);
 void coarse_reconstruct_frames(const FramesParams& p, const FramesWork& w, cudaStream_t st);
 
+// ------------------------------------------------------------------ codec (codec.cu)
+// per block in SubmeshOrder position order (EncodedMesh.blocks, compress.hpp:108)
+struct CodecParams {
+    int blocks = 0, quant_bits = 12;
+    const int* c = nullptr;               // subspace size per position
+    const double* const* coef = nullptr;  // encode: c x 3 column-major coefficients per position
+    uint16_t* values = nullptr;           // 3c per position, axis-major (EncodedBlock.values)
+    const int64_t* value_off = nullptr;
+    double* lo = nullptr;                 // 3 per position (coeff_min)
+    double* hi = nullptr;                 // 3 per position (coeff_max)
+    uint8_t* flags = nullptr;             // constant_axis bits
+    int64_t* payload_bytes = nullptr;     // encode: packed bytes per position
+    uint8_t* payload = nullptr;
+    const int64_t* payload_off = nullptr;
+    const int* dest = nullptr;            // unpack: submesh id of the position
+    double* C = nullptr;                  // unpack: c x ldc row-major per submesh id
+    int64_t strideC = 0;
+    int ldc = 0;
+};
+void codec_encode(const CodecParams& p, cudaStream_t st);
+void codec_pack(const CodecParams& p, cudaStream_t st);
+void codec_unpack(const CodecParams& p, cudaStream_t st);
+// igft + stitch of given coefficients (decompress_mesh's decode + reconstruct_weighted)
+void reconstruct_from_coefficients(const FramesParams& p, const double* C, int ldc, double* Xhat,
+                                   cudaStream_t st);
+
 }  // namespace smg
