@@ -26,15 +26,35 @@ oracle/_ref/rng_ref: oracle/rng_ref.cpp
 	g++ -O2 -std=c++17 -o $@ $<
 
 # standalone kernel timing tools (not part of the library)
-tools: build/solve_bench build/solve_bench_noload build/solve_bench_nomma build/chol_bench
+tools: build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_ns5 build/solve_bench_nomma_ns5 build/chol_bench
 
 build/solve_bench: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -o $@ $<
 
-build/solve_bench_noload: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+build/solve_bench_norhs: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
-	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_LOAD -o $@ $<
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_RHS -o $@ $<
+
+build/solve_bench_noslab: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_SLAB -o $@ $<
+
+build/solve_bench_ns5: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NS_FORCE=5 -o $@ $<
+
+build/solve_bench_nomma_ns5: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NS_FORCE=5 -DSMG_SOLVE_NO_MMA -o $@ $<
+
+build/solve_bench_nomma_norhs: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_MMA -DSMG_SOLVE_NO_RHS -o $@ $<
+
+build/solve_bench_nomma_noslab: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_MMA -DSMG_SOLVE_NO_SLAB -o $@ $<
 
 build/solve_bench_nomma: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build

@@ -415,6 +415,12 @@ public:
                     SMG_CUDA(cudaMemcpy2DAsync(g.ws.U.get(), (size_t)g.ws.ld * 8,
                                                ws_.U.get() + (int64_t)g.b0 * ws_.mstride(), (size_t)ws_.ld * 8,
                                                (size_t)c * 8, (size_t)g.nb * ts_.npad, cudaMemcpyDeviceToDevice, st_));
+                // ... and its sign convention: a growth at position 1 re-signs the
+                // carried columns before appending (resize_basis grows the signed basis)
+                for (Group& g : grp)
+                    SMG_CUDA(cudaMemcpy2DAsync(g.ws.sign.get(), (size_t)g.ws.ld * 8,
+                                               ws_.sign.get() + (int64_t)g.b0 * ws_.ld, (size_t)ws_.ld * 8,
+                                               (size_t)c * 8, (size_t)g.nb, cudaMemcpyDeviceToDevice, st_));
                 tm.add(kStBasis, a, tm.mark());
                 fork();
                 t_basis0 = tm.mark();

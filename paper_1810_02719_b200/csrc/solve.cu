@@ -27,22 +27,37 @@ namespace {
 // (cp.async issued by the DMMA warps themselves serialised the next slab's
 // transfer with the current step's products).
 constexpr int kSolveWarps = 8;
-constexpr int kProdWarps = 2;
+constexpr int kRhsWarps = 2;                  // right-hand-side producers
+constexpr int kProdWarps = 1 + kRhsWarps;     // + one factor-slab producer
 constexpr int NT_MMA = kSolveWarps * 32;
 constexpr int NT = NT_MMA + kProdWarps * 32;
-constexpr int NT_PROD = kProdWarps * 32;
+constexpr int NT_RHS = kRhsWarps * 32;
 
+// Shared-memory plan: a ring of NSF factor slabs (2W x FS, one bulk copy each),
+// a deeper ring of NSR right-hand-side blocks (W x XS, cp.async rows) and a
+// double-buffered carry y_{k-1} (W x XS, written by the step epilogue).  The
+// rhs ring runs furthest ahead: its rows come from the previous sweep's output
+// in HBM (or the permuted input), the slabs mostly from L2.  Two CTAs per SM
+// when the plan fits, else one CTA with the deepest rings that fit.
 template <int W, int CS>
 struct SolveSmem {
     static constexpr int FS = W + 4;   // padded row of the transposed factor slab
     static constexpr int XS = CS + 4;  // padded row of the right-hand-side slab
     static constexpr int F_ELEMS = 2 * W * FS;
-    static constexpr int X_ELEMS = 2 * W * XS;
-    // pipeline depth: as many stages as fit two CTAs per SM (at least 2); a
-    // narrow W has short steps, so its loads need more than one step of lead
-    static constexpr int STAGE = (F_ELEMS + X_ELEMS) * 8;
-    static constexpr int NS = (4 * STAGE <= 113 * 1024) ? 4 : ((3 * STAGE <= 113 * 1024) ? 3 : 2);
-    static constexpr int BYTES = NS * STAGE;
+    static constexpr int R_ELEMS = W * XS;
+    static constexpr int FB = F_ELEMS * 8, RB = R_ELEMS * 8, YB = 2 * RB;
+    static constexpr int HALF = 113 * 1024, FULL = 226 * 1024;
+    static constexpr bool TWO = 2 * FB + 3 * RB + YB <= HALF;
+    static constexpr int BUDGET = TWO ? HALF : FULL;
+    static constexpr int NSF = (!TWO && 3 * FB + 3 * RB + YB <= FULL) ? 3 : 2;
+    static constexpr int NSR_FIT = (BUDGET - NSF * FB - YB) / RB;
+#ifdef SMG_SOLVE_NS_FORCE  // timing probe: rhs ring depth override
+    static constexpr int NSR = SMG_SOLVE_NS_FORCE;
+#else
+    static constexpr int NSR = NSR_FIT > 8 ? 8 : NSR_FIT;
+#endif
+    static_assert(NSR >= 2, "solve shared-memory plan");
+    static constexpr int BYTES = NSF * FB + NSR * RB + YB;
 };
 
 // zero-fill variant: src_bytes = 0 writes zeros
@@ -77,7 +92,7 @@ struct SolveTiling {
 };
 
 template <int W, int CS, bool FWD>
-SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ xs,
+SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ xs, const double* __restrict__ ys,
                       double (&acc)[SolveTiling<W, CS>::MT][SolveTiling<W, CS>::NT][2], int warp, int g, int t,
                       bool skip_second) {
     using TL = SolveTiling<W, CS>;
@@ -164,7 +179,7 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
     for (int kk = W; kk < 2 * W; kk += 4) {
         double a[MT], b[NT];
 #pragma unroll
-        for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
+        for (int j = 0; j < NT; ++j) b[j] = ys[(kk - W + t) * XS + 8 * (wn * NT + j) + g];
 #pragma unroll
         for (int i = 0; i < MT; ++i) a[i] = fs[(kk + t) * FS + 8 * TL::tile(wm, i) + g];
 #pragma unroll
@@ -243,26 +258,25 @@ SMG_DEV void cluster_sync_all() {
 SMG_DEV void mma_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT_MMA) : "memory"); }
 
 // Warp-specialised: the DMMA warps run the steps (named barrier among
-// themselves for the epilogue rows), the producer warps run one step ahead
-// and never meet them at a CTA barrier -- they wait for a buffer to be
-// released (consumed[buf], one arrive per DMMA warp) and fill it (full[buf]).
-// MC: the column-slice CTAs of one chain form a cluster; every CTA releases a
-// buffer by arriving on rank 0's empty[buf], and rank 0 multicasts the factor
-// slab (read from L2 once per cluster) into every CTA's buffer.
-template <int W, int CS, bool MC>
+// themselves for the carry rows); one producer warp streams the factor slabs
+// (fullF/consumedF ring), two stream the right-hand-side rows (fullR/consumedR
+// ring, deeper).  Producers never meet the DMMA warps at a CTA barrier.  Ring
+// slot s of step gs is gs % N, the phase parity of that step (gs / N) & 1.
+template <int W, int CS>
 __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     using S = SolveSmem<W, CS>;
     using TL = SolveTiling<W, CS>;
     constexpr int FS = S::FS, XS = S::XS;
+    constexpr int NSF = S::NSF, NSR = S::NSR;
     extern __shared__ __align__(16) double smem[];
-    constexpr int NS = S::NS;
     auto Fs = [&](int i) { return smem + i * S::F_ELEMS; };
-    auto Xs = [&](int i) { return smem + NS * S::F_ELEMS + i * S::X_ELEMS; };
+    auto Rs = [&](int i) { return smem + NSF * S::F_ELEMS + i * S::R_ELEMS; };
+    auto Ys = [&](int i) { return smem + NSF * S::F_ELEMS + NSR * S::R_ELEMS + i * S::R_ELEMS; };
 
     const int b = blockIdx.y;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const int col0 = blockIdx.x * CS;
-    if (!MC && col0 >= c) return;  // (MC launches only with every slice in range)
+    if (col0 >= c) return;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -278,87 +292,90 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     const int sweeps = p.once ? 2 : 2 * p.z;
     const int total = sweeps * Kb;
 
-    const bool producer = tid >= NT_MMA;
-    const int ptid = tid - NT_MMA;
-    __shared__ __align__(8) uint64_t full[NS], consumed[NS], empty[NS];
-    uint32_t csz = 1, crank = 0;
-    if (MC) {
-        csz = cluster_size();
-        crank = cluster_rank();
-    }
+    __shared__ __align__(8) uint64_t fullF[NSF], consF[NSF], fullR[NSR], consR[NSR];
     if (tid == 0) {
-        for (int i = 0; i < NS; ++i) {
-            mbar_init(&full[i], kProdWarps);        // one arrive per producer warp (+ tx bytes, cp.async)
-            mbar_init(&consumed[i], kSolveWarps);  // one arrive per DMMA warp
-            mbar_init(&empty[i], (int)csz);        // rank 0 (MC): one arrive per cluster CTA
+        for (int i = 0; i < NSF; ++i) {
+            mbar_init(&fullF[i], 1);            // the slab producer's arrive (+ tx bytes)
+            mbar_init(&consF[i], kSolveWarps);  // one arrive per DMMA warp
+        }
+        for (int i = 0; i < NSR; ++i) {
+            mbar_init(&fullR[i], kRhsWarps);    // one arrive per rhs warp (+ its lanes' cp.async)
+            mbar_init(&consR[i], kSolveWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    if (MC) cluster_sync_all();  // every CTA's barriers exist before the first remote arrive
 
     auto block_of = [&](int gs) {
         const int sweep = gs / Kb, step = gs % Kb;
         return (sweep & 1) ? Kb - 1 - step : step;
     };
 
-    if (producer) {
-        uint32_t cph[NS], eph[NS];
-        for (int i = 0; i < NS; ++i) cph[i] = eph[i] = 0u;
+    if (warp == kSolveWarps) {
+        // ---- factor slabs: one bulk copy (TMA engine) per step
+        if (lane == 0) {
+            for (int gs = 0; gs < total; ++gs) {
+                const int sweep = gs / Kb, k = block_of(gs), sl = gs % NSF;
+                if (gs >= NSF) mbar_wait(&consF[sl], ((gs - NSF) / NSF) & 1);
+                const double* F = ((sweep & 1) ? Fbwd : Ffwd) + (int64_t)k * slab;
+                mbar_arrive_expect_tx(&fullF[sl], (uint32_t)(2 * W * FS * 8));
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                bulk_g2s(Fs(sl), F, 2 * W * FS * 8, &fullF[sl]);
+            }
+        }
+    } else if (warp > kSolveWarps) {
+        // ---- right-hand-side rows: cp.async, NSR steps ahead; sweep 0 gathers
+        // the permuted input rows, later sweeps read the previous sweep's output
+        const int rt = tid - NT_MMA - 32;
+        constexpr int CCH = CS / 2;                              // 16-byte chunks per row
+        constexpr int PER = (W * CCH + NT_RHS - 1) / NT_RHS;     // chunks per thread per step
+        int pn[PER];                                             // next step's source rows (perm prefetch)
+        auto src_rows = [&](int gs, int (&rows)[PER]) {
+            const int k = block_of(gs), sweep = gs / Kb;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = rt + i * NT_RHS, r = e / CCH, prow = k * W + r;
+                rows[i] = (e < W * CCH && prow < n && sweep == 0 && perm) ? __ldg(perm + prow) : prow;
+            }
+        };
+        src_rows(0, pn);
         for (int gs = 0; gs < total; ++gs) {
-            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), buf = gs % NS;
-            // the buffer's previous contents (step gs-NS) are consumed; at a sweep's
-            // first step the previous sweep (its tmp rows) is complete
-            if (gs >= NS) {
-                mbar_wait(&consumed[buf], cph[buf]);
-                cph[buf] ^= 1u;
+            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), sl = gs % NSR;
+            int rows[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) rows[i] = pn[i];
+            if (gs + 1 < total) src_rows(gs + 1, pn);  // overlaps the waits below
+            if (gs >= NSR) mbar_wait(&consR[sl], ((gs - NSR) / NSR) & 1);
+            if (step == 0 && gs > 0) {
+                // this sweep reads the previous sweep's rows: all of its steps are done
+                mbar_wait(&consR[(gs - 1) % NSR], ((gs - 1) / NSR) & 1);
             }
-            if (step == 0 && gs > 0) {  // step gs-1 (the sweep's end) is consumed; the regular
-                const int pb = (gs - 1) % NS;  // wait of step gs-1+NS re-checks this phase
-                mbar_wait(&consumed[pb], cph[pb]);
-            }
-            const double* F = ((sweep & 1) ? Fbwd : Ffwd) + (int64_t)k * slab;
-            double* fs = Fs(buf);
-            double* xs = Xs(buf);
-            const int nvalid = max(0, min(W, n - k * W));  // rhs rows of the block inside the tile
-            constexpr int CCH = CS / 2;
-            for (int e = ptid; e < W * CCH; e += NT_PROD) {
+            double* xs = Rs(sl);
+            const int nvalid = max(0, min(W, n - k * W));
+#ifndef SMG_SOLVE_NO_RHS
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = rt + i * NT_RHS;
+                if (e >= W * CCH) break;
                 const int r = e / CCH, ch = e % CCH;
-                const int prow = k * W + r;
                 if (r < nvalid) {
-                    const double* src = (sweep == 0) ? in + (int64_t)(perm ? perm[prow] : prow) * p.ldin + col0
-                                                     : tmp + (int64_t)prow * p.ldt + col0;
+                    const double* src = (sweep == 0) ? in + (int64_t)rows[i] * p.ldin + col0
+                                                     : tmp + (int64_t)rows[i] * p.ldt + col0;
                     cp_async16(xs + r * XS + 2 * ch, src + 2 * ch);
                 } else {
                     cp_async16_zfill(xs + r * XS + 2 * ch, in, false);  // padded rows past n
                 }
             }
-            asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[buf])) : "memory");
+#endif
+            asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&fullR[sl])) : "memory");
             __syncwarp();
-            if (ptid == 0) {
-                mbar_arrive_expect_tx(&full[buf], (uint32_t)(2 * W * FS * 8));
-                if constexpr (MC) {
-                    mbar_arrive_remote(&empty[buf], 0);  // this CTA's buffer is free and armed
-                    if (crank == 0) {
-                        mbar_wait_cluster(&empty[buf], eph[buf]);
-                        eph[buf] ^= 1u;
-                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                        bulk_multicast(fs, F, 2 * W * FS * 8, &full[buf], (uint16_t)((1u << csz) - 1u));
-                    }
-                } else {
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    bulk_g2s(fs, F, 2 * W * FS * 8, &full[buf]);
-                }
-            } else if (lane == 0) {
-                mbar_arrive_local(&full[buf]);
-            }
+            if (lane == 0) mbar_arrive_local(&fullR[sl]);
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
     } else {
-        uint32_t fph[NS];
-        for (int i = 0; i < NS; ++i) fph[i] = 0u;
         for (int gs = 0; gs < total; ++gs) {
-            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), buf = gs % NS;
+            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs);
+            const int sf = gs % NSF, sr = gs % NSR;
             const bool fwd = (sweep & 1) == 0;
             const bool last = sweep == sweeps - 1;
             // output rows of the last sweep go through the permutation: fetch them
@@ -372,19 +389,27 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                     lrow[i] = (last && perm && prow < n) ? __ldg(perm + prow) : prow;
                 }
             }
-            mbar_wait(&full[buf], fph[buf]);
-            fph[buf] ^= 1u;
+            mbar_wait(&fullR[sr], (gs / NSR) & 1);
+            mbar_wait(&fullF[sf], (gs / NSF) & 1);
             double acc[TL::MT][TL::NT][2];
             const bool skip2 = step == 0;  // previous-block rows of a sweep's first step are zero
+            double* ycur = Ys(gs & 1);             // this step's output = next step's carry
+            const double* yprev = Ys((gs + 1) & 1);
 #ifndef SMG_SOLVE_NO_MMA
-            if (fwd) mma_step<W, CS, true>(Fs(buf), Xs(buf), acc, warp, g, t, skip2);
-            else mma_step<W, CS, false>(Fs(buf), Xs(buf), acc, warp, g, t, skip2);
+            if (fwd) mma_step<W, CS, true>(Fs(sf), Rs(sr), yprev, acc, warp, g, t, skip2);
+            else mma_step<W, CS, false>(Fs(sf), Rs(sr), yprev, acc, warp, g, t, skip2);
 #else
+            (void)fwd;
+            (void)skip2;
             for (int i = 0; i < TL::MT; ++i)
-                for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Xs(buf)[tid];
+                for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Rs(sr)[tid] + yprev[tid];
 #endif
-            // epilogue: result is the "previous block" of the next step and goes to dst
-            double* xnext = Xs((gs + 1) % NS) + W * XS;
+            // the slab and rhs block are read: release them before the epilogue
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive_local(&consF[sf]);
+                if (step + 1 != Kb) mbar_arrive_local(&consR[sr]);
+            }
             if (warp < TL::ACTIVE) {
                 const int wm = warp % TL::WM, wn = warp / TL::WM;
 #pragma unroll
@@ -392,8 +417,8 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
 #pragma unroll
                     for (int j = 0; j < TL::NT; ++j) {
                         const int r = 8 * TL::tile(wm, i) + g, cc = 8 * (wn * TL::NT + j) + 2 * t;
-                        xnext[r * XS + cc] = acc[i][j][0];
-                        xnext[r * XS + cc + 1] = acc[i][j][1];
+                        ycur[r * XS + cc] = acc[i][j][0];
+                        ycur[r * XS + cc + 1] = acc[i][j][1];
                         const int prow = k * W + r;
                         if (last) {
                             if (prow < n && col0 + cc < c) {
@@ -407,17 +432,15 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                     }
             }
             if (step + 1 == Kb) {
-                // the next sweep's rhs rows (read by the producers) are this sweep's tmp rows
+                // the next sweep's rhs rows (read by the producers) are this sweep's
+                // output rows: visible to the async proxy before the release
                 __threadfence_block();
                 asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_local(&consR[sr]);
             }
-            mma_bar();  // xnext complete before the next step reads it; buf fully read
-            if (lane == 0) mbar_arrive_local(&consumed[buf]);
+            mma_bar();  // ycur complete before the next step reads it; yprev free for reuse
         }
-    }
-    if (MC) {
-        __syncthreads();
-        cluster_sync_all();  // no CTA leaves while cluster peers may still address its barriers
     }
 }
 
@@ -425,42 +448,13 @@ template <int W, int CS>
 void launch(const SolveParams& p, cudaStream_t st) {
     const int bytes = SolveSmem<W, CS>::BYTES;
     const int slices = (p.c_cap + CS - 1) / CS;
-    int csz = 0;  // cluster size: largest divisor of the slice count in [2, 8]
-    // opt-in (SMG_SOLVE_MC=1): with two slab buffers the per-step cross-CTA
-    // release/multicast round trip sits on the critical path and the cluster
-    // runs slower than independent CTAs (1.48 ms vs 0.83 ms per C5 launch)
-    if (p.dimC == nullptr && std::getenv("SMG_SOLVE_MC"))
-        for (int d = 8; d >= 2; --d)
-            if (slices % d == 0) {
-                csz = d;
-                break;
-            }
-    static bool configured[2] = {false, false};
-    const bool mc = csz >= 2;
-    if (!configured[mc]) {
-        if (mc) cudaFuncSetAttribute(solve_kernel<W, CS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        else cudaFuncSetAttribute(solve_kernel<W, CS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        configured[mc] = true;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(solve_kernel<W, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        configured = true;
     }
     dim3 grid(slices, p.batch);
-    ::smg::count_launch();
-    if (!mc) {
-        solve_kernel<W, CS, false><<<grid, NT, bytes, st>>>(p);
-        return;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = bytes;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = csz;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, solve_kernel<W, CS, true>, p);
+    ::smg::count_launch(), solve_kernel<W, CS><<<grid, NT, bytes, st>>>(p);
 }
 
 }  // namespace

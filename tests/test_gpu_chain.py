@@ -120,6 +120,20 @@ def test_chain_variable_sizes_shrink_and_grow(ctx):
     check_parity(mesh, bb, ob)
 
 
+def test_chain_grows_at_position_one(ctx):
+    """Growth right after the first basis: the appended columns follow the
+    first block's sign-fixed basis (resize_basis, pipeline.hpp:97-109)."""
+    mesh = synth.small_grid(64, 64, 32, 32, seed=8, flip=1)
+    seg = synth.grid_tiles(64, 64, 32, 32)
+    subs = O.build_submeshes(mesh.adj_offsets, mesh.adj_cols, seg.members)
+    sizes = [30, 36, 30, 24]
+    cfg = G.PipelineConfig(weighting="binary", iterations=1, shift_scale=1e-3)
+    ocfg = O.PipelineConfig(weighting=O.BINARY, iterations=1, shift_scale=1e-3)
+    bb = G.compute_block_bases_fixed_sizes(mesh, seg, cfg, sizes, want_bases=True, ctx=ctx)
+    ob = O.compute_block_bases_fixed_sizes(mesh.vertices, subs, seg.sequence, ocfg, sizes)
+    check_parity(mesh, bb, ob)
+
+
 def test_doi_chain_decisions_match(ctx):
     """DOI chain with a band each block meets in a few steps: per-block c,
     iteration count and convergence flags equal the oracle's."""
