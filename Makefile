@@ -26,7 +26,7 @@ oracle/_ref/rng_ref: oracle/rng_ref.cpp
 	g++ -O2 -std=c++17 -o $@ $<
 
 # standalone kernel timing tools (not part of the library)
-tools: build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_ns5 build/solve_bench_nomma_ns5 build/chol_bench
+tools: build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_f3r4 build/solve_bench_nomma_ns5 build/chol_bench
 
 build/solve_bench: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
@@ -40,13 +40,13 @@ build/solve_bench_noslab: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_SLAB -o $@ $<
 
-build/solve_bench_ns5: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+build/solve_bench_f3r4: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
-	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NS_FORCE=5 -o $@ $<
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NSF_FORCE=3 -DSMG_SOLVE_NS_FORCE=4 -o $@ $<
 
 build/solve_bench_nomma_ns5: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
-	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NS_FORCE=5 -DSMG_SOLVE_NO_MMA -o $@ $<
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NSF_FORCE=3 -DSMG_SOLVE_NS_FORCE=4 -DSMG_SOLVE_NO_MMA -o $@ $<
 
 build/solve_bench_nomma_norhs: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build

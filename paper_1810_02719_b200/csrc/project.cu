@@ -22,26 +22,45 @@ namespace smg {
 
 namespace {
 
-constexpr int PNT = 256;
+constexpr int PNT = 256;   // recon CTA: 8 column parts x 32 row groups of RPT rows
+constexpr int QNT = 128;   // partial CTA: two adjacent columns per thread
+constexpr int RPC = 32;    // rows per partial chunk
+constexpr int RPT = 4;     // rows per recon thread (coefficients reused across them)
+constexpr int RROWS = (PNT / 8) * RPT;  // rows per recon CTA
 
+// partial record per (chunk, column): best |q|, its q, Px, Py, Pz, Ps (8 doubles, 64 B)
 SMG_DEV void reduce_block(const ProjParams& p, int b) {
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const double* part = p.partial + (int64_t)b * p.nchunks * (int64_t)p.c_cap * 8;
     double* coef = p.coeff + (int64_t)b * p.strideCoef;  // c x 4: Px Py Pz Ps (unsigned)
     double* sign = p.sign + (int64_t)b * p.strideSign;
-    for (int j = threadIdx.x; j < c; j += PNT) {
+    for (int j = threadIdx.x; j < c; j += QNT) {
         double best = -1.0, bval = 0.0;
         double px = 0.0, py = 0.0, pz = 0.0, ps = 0.0;
-        for (int ch = 0; ch < p.nchunks; ++ch) {
-            const double* o = part + ((int64_t)ch * p.c_cap + j) * 8;
-            if (o[0] > best) {  // chunks in row order: strict > keeps the first index
-                best = o[0];
-                bval = o[1];
+        // chunks in row order: strict > keeps the first index; loads of 4 chunks
+        // are issued before they are combined
+        for (int ch0 = 0; ch0 < p.nchunks; ch0 += 4) {
+            double4 h[4], d[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (ch0 + u < p.nchunks) {
+                    const double4* o = reinterpret_cast<const double4*>(part + ((int64_t)(ch0 + u) * p.c_cap + j) * 8);
+                    h[u] = o[0];
+                    d[u] = o[1];
+                }
             }
-            px += o[3];
-            py += o[4];
-            pz += o[5];
-            ps += o[6];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (ch0 + u >= p.nchunks) break;
+                if (h[u].x > best) {
+                    best = h[u].x;
+                    bval = h[u].y;
+                }
+                px += h[u].z;
+                py += h[u].w;
+                pz += d[u].x;
+                ps += d[u].y;
+            }
         }
         sign[j] = bval < 0.0 ? -1.0 : 1.0;
         coef[4 * j + 0] = px;
@@ -51,48 +70,52 @@ SMG_DEV void reduce_block(const ProjParams& p, int b) {
     }
 }
 
-__global__ void __launch_bounds__(PNT) partial_kernel(ProjParams p) {
+// one double2 (two adjacent columns) per thread and row: a warp reads 512
+// contiguous bytes of a row; 32-row chunks give every chain (n / 32) CTAs
+__global__ void __launch_bounds__(QNT) partial_kernel(ProjParams p) {
     const int b = blockIdx.y, chunk = blockIdx.x;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
-    const int r0 = chunk * p.rows_per_chunk, r1 = min(p.n, r0 + p.rows_per_chunk);
+    const int r0 = chunk * RPC, r1 = min(p.n, r0 + RPC);
     const double* Q = p.Q + (int64_t)b * p.strideQ;
     const double* X = p.X + (int64_t)b * p.strideX;
     double* part = p.partial + ((int64_t)b * p.nchunks + chunk) * (int64_t)p.c_cap * 8;
-    // the chunk's coordinates (and s = (x + y) + z) once in shared memory: one
-    // broadcast 32-byte read per row instead of three global loads per element
-    __shared__ double4 sx[64];
-    for (int i = threadIdx.x; i < r1 - r0; i += PNT) {
+    // the chunk's coordinates (and s = (x + y) + z) once in shared memory
+    __shared__ double4 sx[RPC];
+    for (int i = threadIdx.x; i < r1 - r0; i += QNT) {
         const double x = X[3 * (r0 + i)], y = X[3 * (r0 + i) + 1], z = X[3 * (r0 + i) + 2];
         sx[i] = make_double4(x, y, z, (x + y) + z);
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < c; j += PNT) {
-        double best = -1.0, bval = 0.0;
-        int bidx = 0;
-        double px = 0.0, py = 0.0, pz = 0.0, ps = 0.0;
+    for (int j0 = 2 * threadIdx.x; j0 < c; j0 += 2 * QNT) {
+        double best0 = -1.0, bval0 = 0.0, best1 = -1.0, bval1 = 0.0;
+        double px0 = 0.0, py0 = 0.0, pz0 = 0.0, ps0 = 0.0, px1 = 0.0, py1 = 0.0, pz1 = 0.0, ps1 = 0.0;
+        const double* q0 = Q + (int64_t)r0 * p.ldq + j0;
 #pragma unroll 8
-        for (int i = r0; i < r1; ++i) {
-            const double q = Q[(int64_t)i * p.ldq + j];
-            const double mag = fabs(q);
-            if (mag > best) {
-                best = mag;
-                bval = q;
-                bidx = i;
-            }
-            const double4 v = sx[i - r0];
-            px = fma(q, v.x, px);
-            py = fma(q, v.y, py);
-            pz = fma(q, v.z, pz);
-            ps = fma(q, v.w, ps);
+        for (int i = 0; i < r1 - r0; ++i) {
+            const double2 q = __ldg(reinterpret_cast<const double2*>(q0 + (int64_t)i * p.ldq));
+            const double m0 = fabs(q.x), m1 = fabs(q.y);
+            const bool u0 = m0 > best0, u1 = m1 > best1;  // rows in order: first index wins
+            best0 = u0 ? m0 : best0;
+            bval0 = u0 ? q.x : bval0;
+            best1 = u1 ? m1 : best1;
+            bval1 = u1 ? q.y : bval1;
+            const double4 v = sx[i];
+            px0 = fma(q.x, v.x, px0);
+            py0 = fma(q.x, v.y, py0);
+            pz0 = fma(q.x, v.z, pz0);
+            ps0 = fma(q.x, v.w, ps0);
+            px1 = fma(q.y, v.x, px1);
+            py1 = fma(q.y, v.y, py1);
+            pz1 = fma(q.y, v.z, pz1);
+            ps1 = fma(q.y, v.w, ps1);
         }
-        double* o = part + (int64_t)j * 8;
-        o[0] = best;
-        o[1] = bval;
-        o[2] = (double)bidx;
-        o[3] = px;
-        o[4] = py;
-        o[5] = pz;
-        o[6] = ps;
+        double4* o = reinterpret_cast<double4*>(part + (int64_t)j0 * 8);
+        o[0] = make_double4(best0, bval0, px0, py0);
+        o[1] = make_double4(pz0, ps0, 0.0, 0.0);
+        if (j0 + 1 < c) {
+            o[2] = make_double4(best1, bval1, px1, py1);
+            o[3] = make_double4(pz1, ps1, 0.0, 0.0);
+        }
     }
     // the last chunk CTA of a chain reduces the chunks in order (deterministic)
     __shared__ bool last;
@@ -119,7 +142,10 @@ SMG_DEV void stats_block(const ProjParams& p, int b, int nblocks) {
     s[2] = a;
 }
 
-// warp per row: x^_i = sum_j q_ij P_j ; e_i = s_i - sum_j q_ij Ps_j
+// x^_i = sum_j q_ij P_j ; e_i = s_i - sum_j q_ij Ps_j.  Thread = (column part,
+// group of RPT rows): per column pair it loads the coefficients once from smem
+// and RPT double2 of Q (8 lanes of a part group cover 128 contiguous bytes of a
+// row); the 8 parts of a row group are 8 consecutive lanes, summed by shuffles.
 __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
     __shared__ double red[2][PNT / 32];
     extern __shared__ __align__(16) double scoef[];  // c x 4, staged once per CTA
@@ -128,43 +154,69 @@ __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
     const double* Q = p.Q + (int64_t)b * p.strideQ;
     const double* X = p.X + (int64_t)b * p.strideX;
     for (int e = threadIdx.x; e < 4 * c; e += PNT) scoef[e] = p.coeff[(int64_t)b * p.strideCoef + e];
+    for (int e = 4 * c + threadIdx.x; e < 4 * (c + 1); e += PNT) scoef[e] = 0.0;  // odd c: the pair's tail
     __syncthreads();
-    const double* coef = scoef;
     double* xhat = p.xhat ? p.xhat + (int64_t)b * p.strideXhat : nullptr;
     double* e_out = p.e_out ? p.e_out + (int64_t)b * p.strideE : nullptr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int rows_per_block = PNT / 32 * p.rows_per_warp;
-    double res2 = 0.0, e2 = 0.0;
-    for (int rr = 0; rr < p.rows_per_warp; ++rr) {
-        const int i = blockIdx.x * rows_per_block + warp * p.rows_per_warp + rr;
-        if (i >= p.n) break;
-        double ax = 0.0, ay = 0.0, az = 0.0, as = 0.0;
-#pragma unroll 4
-        for (int j = lane; j < c; j += 32) {
-            const double q = Q[(int64_t)i * p.ldq + j];
-            ax = fma(q, coef[4 * j + 0], ax);
-            ay = fma(q, coef[4 * j + 1], ay);
-            az = fma(q, coef[4 * j + 2], az);
-            as = fma(q, coef[4 * j + 3], as);
+    const int part = threadIdx.x & 7, rg = threadIdx.x >> 3;
+    const int i0 = blockIdx.x * RROWS + rg * RPT;
+    double acc[RPT][4];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
+    const double4* cf = reinterpret_cast<const double4*>(scoef);
+#pragma unroll 2
+    for (int j = 2 * part; j < c; j += 16) {
+        const double4 ca = cf[j], cb = cf[j + 1];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            if (i0 + r >= p.n) break;
+            double2 q = __ldg(reinterpret_cast<const double2*>(Q + (int64_t)(i0 + r) * p.ldq + j));
+            if (j + 1 >= c) q.y = 0.0;  // odd c: the padding column is not part of the basis
+            acc[r][0] = fma(q.x, ca.x, acc[r][0]);
+            acc[r][1] = fma(q.x, ca.y, acc[r][1]);
+            acc[r][2] = fma(q.x, ca.z, acc[r][2]);
+            acc[r][3] = fma(q.x, ca.w, acc[r][3]);
+            acc[r][0] = fma(q.y, cb.x, acc[r][0]);
+            acc[r][1] = fma(q.y, cb.y, acc[r][1]);
+            acc[r][2] = fma(q.y, cb.z, acc[r][2]);
+            acc[r][3] = fma(q.y, cb.w, acc[r][3]);
         }
-        ax = warp_sum(ax);
-        ay = warp_sum(ay);
-        az = warp_sum(az);
-        as = warp_sum(as);
-        if (lane == 0) {
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            double v = acc[r][a];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            acc[r][a] = v;
+        }
+    double res2 = 0.0, e2 = 0.0;
+    if (part == 0) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int i = i0 + r;
+            if (i >= p.n) break;
             const double x = X[3 * i], y = X[3 * i + 1], z = X[3 * i + 2];
             if (xhat) {
-                xhat[3 * i] = ax;
-                xhat[3 * i + 1] = ay;
-                xhat[3 * i + 2] = az;
+                xhat[3 * i] = acc[r][0];
+                xhat[3 * i + 1] = acc[r][1];
+                xhat[3 * i + 2] = acc[r][2];
             }
-            const double dx = x - ax, dy = y - ay, dz = z - az;
+            const double dx = x - acc[r][0], dy = y - acc[r][1], dz = z - acc[r][2];
             res2 += dx * dx + dy * dy + dz * dz;
-            const double e = ((x + y) + z) - as;
+            const double e = ((x + y) + z) - acc[r][3];
             if (e_out) e_out[i] = e;
             e2 += e * e;
         }
     }
+    // fixed-order block sum (lanes 0, 8, 16, 24 hold the row groups' sums)
+    res2 += __shfl_xor_sync(0xffffffffu, res2, 8);
+    e2 += __shfl_xor_sync(0xffffffffu, e2, 8);
+    res2 += __shfl_xor_sync(0xffffffffu, res2, 16);
+    e2 += __shfl_xor_sync(0xffffffffu, e2, 16);
     if (lane == 0) {
         red[0][warp] = res2;
         red[1][warp] = e2;
@@ -193,17 +245,16 @@ __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
 
 }  // namespace
 
-int proj_chunks(int n) { return (n + 63) / 64; }
-int proj_recon_blocks(int n, int rows_per_warp) { return (n + (PNT / 32) * rows_per_warp - 1) / ((PNT / 32) * rows_per_warp); }
+int proj_chunks(int n) { return (n + RPC - 1) / RPC; }
+int proj_recon_blocks(int n, int /*rows_per_warp*/) { return (n + RROWS - 1) / RROWS; }
 
 void project(const ProjParams& p0, cudaStream_t st) {
     ProjParams p = p0;
-    p.rows_per_chunk = 64;
+    p.rows_per_chunk = RPC;
     p.nchunks = proj_chunks(p.n);
-    if (p.rows_per_warp <= 0) p.rows_per_warp = 2;
-    ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), PNT, 0, st>>>(p);
-    const int nb = proj_recon_blocks(p.n, p.rows_per_warp);
-    ::smg::count_launch(), recon_kernel<<<dim3(nb, p.batch), PNT, 4 * p.c_cap * sizeof(double), st>>>(p);
+    ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), QNT, 0, st>>>(p);
+    const int nb = proj_recon_blocks(p.n, 0);
+    ::smg::count_launch(), recon_kernel<<<dim3(nb, p.batch), PNT, 4 * (p.c_cap + 1) * sizeof(double), st>>>(p);
 }
 
 }  // namespace smg

@@ -49,7 +49,11 @@ struct SolveSmem {
     static constexpr int HALF = 113 * 1024, FULL = 226 * 1024;
     static constexpr bool TWO = 2 * FB + 3 * RB + YB <= HALF;
     static constexpr int BUDGET = TWO ? HALF : FULL;
+#ifdef SMG_SOLVE_NSF_FORCE  // timing probe: slab ring depth override
+    static constexpr int NSF = SMG_SOLVE_NSF_FORCE;
+#else
     static constexpr int NSF = (!TWO && 3 * FB + 3 * RB + YB <= FULL) ? 3 : 2;
+#endif
     static constexpr int NSR_FIT = (BUDGET - NSF * FB - YB) / RB;
 #ifdef SMG_SOLVE_NS_FORCE  // timing probe: rhs ring depth override
     static constexpr int NSR = SMG_SOLVE_NS_FORCE;
@@ -94,17 +98,21 @@ struct SolveTiling {
 template <int W, int CS, bool FWD>
 SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ xs, const double* __restrict__ ys,
                       double (&acc)[SolveTiling<W, CS>::MT][SolveTiling<W, CS>::NT][2], int warp, int g, int t,
-                      bool skip_second) {
+                      int part) {
+    // part 1: acc = triangular block x b_k (independent of the carry: computed
+    // ahead, while other warps finish the previous step); part 2: acc += the
+    // coupling block x y_{k-1} (the step's critical path)
     using TL = SolveTiling<W, CS>;
     constexpr int MT = TL::MT, NT = TL::NT;
     constexpr int FS = SolveSmem<W, CS>::FS;
     constexpr int XS = SolveSmem<W, CS>::XS;
     const int wm = warp % TL::WM, wn = warp / TL::WM;
+    if (warp >= TL::ACTIVE) return;
+    if (part == 2) goto second;
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    if (warp >= TL::ACTIVE) return;
     // first half: triangular block (Linv_k lower for FWD, Linv_k^T Sigma upper for BWD)
     if constexpr (TL::PAIRED) {
         // row tiles lo = wm and hi = MT_ALL-1-wm; the k ranges where a tile's
@@ -174,7 +182,8 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
         }
     }
     }
-    if (skip_second) return;
+    return;
+second:
 #pragma unroll 2
     for (int kk = W; kk < 2 * W; kk += 4) {
         double a[MT], b[NT];
@@ -373,13 +382,26 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
     } else {
+        double acc[TL::MT][TL::NT][2];
+        // the independent half of step gs (waits for the step's slab and rhs block)
+        auto first = [&](int gs) {
+            mbar_wait(&fullR[gs % NSR], (gs / NSR) & 1);
+            mbar_wait(&fullF[gs % NSF], (gs / NSF) & 1);
+#ifndef SMG_SOLVE_NO_MMA
+            if (((gs / Kb) & 1) == 0) mma_step<W, CS, true>(Fs(gs % NSF), Rs(gs % NSR), nullptr, acc, warp, g, t, 1);
+            else mma_step<W, CS, false>(Fs(gs % NSF), Rs(gs % NSR), nullptr, acc, warp, g, t, 1);
+#else
+            for (int i = 0; i < TL::MT; ++i)
+                for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Rs(gs % NSR)[tid];
+#endif
+        };
+        first(0);
         for (int gs = 0; gs < total; ++gs) {
             const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs);
             const int sf = gs % NSF, sr = gs % NSR;
-            const bool fwd = (sweep & 1) == 0;
             const bool last = sweep == sweeps - 1;
             // output rows of the last sweep go through the permutation: fetch them
-            // before the wait so the loads overlap it and the products
+            // before the products so the loads overlap them
             int lrow[TL::MT];
             {
                 const int wm = warp % TL::WM;
@@ -389,20 +411,18 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                     lrow[i] = (last && perm && prow < n) ? __ldg(perm + prow) : prow;
                 }
             }
-            mbar_wait(&fullR[sr], (gs / NSR) & 1);
-            mbar_wait(&fullF[sf], (gs / NSF) & 1);
-            double acc[TL::MT][TL::NT][2];
-            const bool skip2 = step == 0;  // previous-block rows of a sweep's first step are zero
-            double* ycur = Ys(gs & 1);             // this step's output = next step's carry
+            double* ycur = Ys(gs & 1);  // this step's output = next step's carry
             const double* yprev = Ys((gs + 1) & 1);
+            // the carry of a sweep's first step is zero
 #ifndef SMG_SOLVE_NO_MMA
-            if (fwd) mma_step<W, CS, true>(Fs(sf), Rs(sr), yprev, acc, warp, g, t, skip2);
-            else mma_step<W, CS, false>(Fs(sf), Rs(sr), yprev, acc, warp, g, t, skip2);
+            if (step != 0) {
+                if ((sweep & 1) == 0) mma_step<W, CS, true>(Fs(sf), nullptr, yprev, acc, warp, g, t, 2);
+                else mma_step<W, CS, false>(Fs(sf), nullptr, yprev, acc, warp, g, t, 2);
+            }
 #else
-            (void)fwd;
-            (void)skip2;
-            for (int i = 0; i < TL::MT; ++i)
-                for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Rs(sr)[tid] + yprev[tid];
+            if (step != 0)
+                for (int i = 0; i < TL::MT; ++i)
+                    for (int j = 0; j < TL::NT; ++j) acc[i][j][0] += yprev[tid];
 #endif
             // the slab and rhs block are read: release them before the epilogue
             __syncwarp();
@@ -439,6 +459,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive_local(&consR[sr]);
             }
+            if (gs + 1 < total) first(gs + 1);  // off the critical path: before the barrier
             mma_bar();  // ycur complete before the next step reads it; yprev free for reuse
         }
     }
