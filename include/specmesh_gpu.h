@@ -233,6 +233,31 @@ smg_status smg_decompress_blocks(smg_context* ctx, const smg_mesh* topology, con
                                  const smg_pipeline_config* cfg, const smg_encoded_blocks* in,
                                  double* out, int32_t out_on_device);
 
+/* ------------------------------------------------------ F4 fine denoising */
+
+/* BilateralParams (denoise.hpp:11-24). */
+typedef struct {
+    double sigma_spatial;       /* 0: mean adjacent-centroid distance (default_sigma_spatial) */
+    double sigma_range;         /* (0.35) */
+    int32_t normal_iterations;  /* (5) */
+    int32_t vertex_iterations;  /* (10) */
+    int32_t ring_depth;         /* (1) */
+} smg_bilateral_params;
+
+void smg_default_bilateral_params(smg_bilateral_params* params);
+
+/* fine_denoise (denoise.hpp:172-178): face_geometry (mesh.hpp:94-116),
+ * face_ring_adjacency (denoise.hpp:39-65), bilateral_normals (:87-127) and
+ * update_vertices (:133-165).  Vertices SoA (x, y, z: vertex_count each),
+ * faces face_count x 3 row-major; out: SoA vertex_count x 3; normals_out
+ * (optional): the filtered face normals, SoA face_count x 3.  All pointers
+ * host (on_device = 0) or device.  The reference's validate() and
+ * "mesh has no adjacent face pairs" errors -> status 2. */
+smg_status smg_fine_denoise(smg_context* ctx, int64_t vertex_count, const double* x, const double* y,
+                            const double* z, int64_t face_count, const int32_t* faces,
+                            const smg_bilateral_params* params, double* out, double* normals_out,
+                            int32_t on_device);
+
 /* ------------------------------------------------------------ L3 primitives
  * Host pointers, column-major.  They run the same kernels as the chain. */
 

@@ -1034,3 +1034,167 @@ def parse_encoded_mesh(data: bytes) -> EncodedMesh:
     if r.at != len(r.data):
         raise ParseError("trailing bytes after bitstream payload")
     return enc
+
+
+# --------------------------------------------------------------------------
+# F4 fine denoising (denoise.hpp:11-180, mesh.hpp:87-116)
+
+@dataclasses.dataclass
+class BilateralParams:
+    """denoise.hpp:11-24"""
+
+    sigma_spatial: float = 0.0
+    sigma_range: float = 0.35
+    normal_iterations: int = 5
+    vertex_iterations: int = 10
+    ring_depth: int = 1
+
+    def validate(self) -> None:
+        require(self.sigma_spatial >= 0.0, "sigma_spatial must be positive (or 0 for automatic)")
+        require(self.sigma_range > 0.0, "sigma_range must be positive")
+        require(self.normal_iterations > 0 and self.vertex_iterations > 0 and self.ring_depth > 0,
+                "iteration counts and ring depth must be positive")
+
+
+def _sq3(dx, dy, dz):
+    """squaredNorm of a 3-vector, (x*x + y*y) + z*z."""
+    return (dx * dx + dy * dy) + dz * dz
+
+
+def face_geometry(vertices: np.ndarray, faces: np.ndarray):
+    """mesh.hpp:94-116: centroids ((a+b)+c)/3, unit normals of (b-a)x(c-a), areas
+    0.5|cross|, degenerate faces (zero cross) get a zero normal.  Component-wise
+    scalar arithmetic in the reference's order."""
+    f = np.asarray(faces, np.int64)
+    a, b, c = vertices[f[:, 0]], vertices[f[:, 1]], vertices[f[:, 2]]
+    cen = ((a + b) + c) / 3.0
+    u, v = b - a, c - a
+    cx = u[:, 1] * v[:, 2] - u[:, 2] * v[:, 1]
+    cy = u[:, 2] * v[:, 0] - u[:, 0] * v[:, 2]
+    cz = u[:, 0] * v[:, 1] - u[:, 1] * v[:, 0]
+    norm = np.sqrt(_sq3(cx, cy, cz))
+    areas = 0.5 * norm
+    nrm = np.zeros((f.shape[0], 3))
+    ok = norm > 0.0
+    nrm[ok, 0] = cx[ok] / norm[ok]
+    nrm[ok, 1] = cy[ok] / norm[ok]
+    nrm[ok, 2] = cz[ok] / norm[ok]
+    return cen, nrm, areas, np.nonzero(~ok)[0]
+
+
+def faces_of_vertex(faces: np.ndarray, n: int) -> List[np.ndarray]:
+    """denoise.hpp:43-45 / :152-154: incident faces per vertex, ascending."""
+    out: List[list] = [[] for _ in range(n)]
+    for fi, fv in enumerate(np.asarray(faces)):
+        for k in range(3):
+            out[int(fv[k])].append(fi)
+    return [np.asarray(l, np.int64) for l in out]
+
+
+def face_ring_adjacency(faces: np.ndarray, n: int, depth: int = 1) -> List[np.ndarray]:
+    """denoise.hpp:39-65: faces sharing >= 1 vertex (self included), sorted unique;
+    `depth` repeats the expansion."""
+    require(depth >= 1, "ring depth must be at least 1")
+    fov = faces_of_vertex(faces, n)
+    f = np.asarray(faces)
+    ring = [np.unique(np.concatenate([fov[int(f[i, 0])], fov[int(f[i, 1])], fov[int(f[i, 2])]]))
+            for i in range(f.shape[0])]
+    for _ in range(1, depth):
+        ring = [np.unique(np.concatenate([ring[g] for g in ring[i]])) for i in range(f.shape[0])]
+    return ring
+
+
+def _padded(lists: List[np.ndarray]):
+    width = max(len(l) for l in lists) if lists else 0
+    idx = np.zeros((len(lists), width), np.int64)
+    valid = np.zeros((len(lists), width), bool)
+    for i, l in enumerate(lists):
+        idx[i, :len(l)] = l
+        valid[i, :len(l)] = True
+    return idx, valid
+
+
+def default_sigma_spatial(centroids: np.ndarray, ring: List[np.ndarray]) -> float:
+    """denoise.hpp:67-83: mean centroid distance over adjacent pairs g > f,
+    summed in (f, g) order."""
+    total, count = 0.0, 0
+    for fi, lst in enumerate(ring):
+        g = lst[lst > fi]
+        if g.size == 0:
+            continue
+        d = centroids[g] - centroids[fi]
+        dist = np.sqrt(_sq3(d[:, 0], d[:, 1], d[:, 2]))
+        for v in dist:
+            total += float(v)
+        count += int(g.size)
+    require(count > 0, "mesh has no adjacent face pairs")
+    return total / count
+
+
+def bilateral_normals(centroids, normals, areas, degenerate, ring, params: BilateralParams) -> np.ndarray:
+    """denoise.hpp:87-127: Jacobi sweeps; per face acc += ((A_g * ks) * kr) * n_g
+    over its ring in ascending order (zero-area faces skipped), normalised when
+    nonzero; degenerate faces are not updated."""
+    params.validate()
+    sigma_s = params.sigma_spatial if params.sigma_spatial > 0.0 else default_sigma_spatial(centroids, ring)
+    idx, valid = _padded(ring)
+    nf = normals.shape[0]
+    deg = np.zeros(nf, bool)
+    deg[np.asarray(degenerate, np.int64)] = True
+    cur = normals.copy()
+    two_s = 2.0 * sigma_s * sigma_s
+    two_r = 2.0 * params.sigma_range * params.sigma_range
+    for _ in range(params.normal_iterations):
+        acc = np.zeros((nf, 3))
+        for r in range(idx.shape[1]):
+            g = idx[:, r]
+            use = valid[:, r] & (areas[g] > 0.0)
+            dc = centroids - centroids[g]
+            ks = np.exp(-_sq3(dc[:, 0], dc[:, 1], dc[:, 2]) / two_s)
+            dn = cur - cur[g]
+            kr = np.exp(-_sq3(dn[:, 0], dn[:, 1], dn[:, 2]) / two_r)
+            w = (areas[g] * ks) * kr
+            contrib = w[:, None] * cur[g]
+            acc[use] += contrib[use]
+        norm = np.sqrt(_sq3(acc[:, 0], acc[:, 1], acc[:, 2]))
+        nxt = cur.copy()
+        upd = (~deg) & (norm > 0.0)
+        nxt[upd] = acc[upd] / norm[upd][:, None]
+        cur = nxt
+    return cur
+
+
+def update_vertices(vertices: np.ndarray, faces: np.ndarray, target_normals: np.ndarray,
+                    vertex_iterations: int) -> np.ndarray:
+    """denoise.hpp:133-165: per pass, centroids from the current vertices, then
+    v += (1/|F_v|) sum_{f in F_v, ascending} n_f (n_f . (m_f - v))."""
+    f = np.asarray(faces, np.int64)
+    require(target_normals.shape[0] == f.shape[0], "one target normal per face required")
+    require(vertex_iterations >= 0, "vertex iterations must be nonnegative")
+    fov = faces_of_vertex(faces, vertices.shape[0])
+    idx, valid = _padded(fov)
+    cnt = valid.sum(axis=1)
+    out = vertices.copy()
+    for _ in range(vertex_iterations):
+        cen = ((out[f[:, 0]] + out[f[:, 1]]) + out[f[:, 2]]) / 3.0
+        delta = np.zeros_like(out)
+        for r in range(idx.shape[1]):
+            fi = idx[:, r]
+            use = valid[:, r]
+            nrm = target_normals[fi]
+            d = cen[fi] - out
+            dot = (nrm[:, 0] * d[:, 0] + nrm[:, 1] * d[:, 1]) + nrm[:, 2] * d[:, 2]
+            delta[use] += (nrm * dot[:, None])[use]
+        has = cnt > 0
+        nxt = out.copy()
+        nxt[has] = out[has] + delta[has] / cnt[has][:, None].astype(np.float64)
+        out = nxt
+    return out
+
+
+def fine_denoise(vertices: np.ndarray, faces: np.ndarray, params: BilateralParams):
+    """denoise.hpp:172-178; returns (vertices, filtered normals)."""
+    cen, nrm, areas, degenerate = face_geometry(vertices, faces)
+    ring = face_ring_adjacency(faces, vertices.shape[0], params.ring_depth)
+    filtered = bilateral_normals(cen, nrm, areas, degenerate, ring, params)
+    return update_vertices(vertices, faces, filtered, params.vertex_iterations), filtered

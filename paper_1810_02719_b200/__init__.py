@@ -25,7 +25,7 @@ __all__ = [
     "build_laplacian", "default_shift", "ShiftedInverseOperator", "orthonormalize", "orthogonal_iteration",
     "dynamic_oi", "bottom_subspace", "gft", "igft", "compute_block_bases_fixed_sizes", "compute_block_bases",
     "run_chains", "coarse_reconstruct_points", "coarse_reconstruct_frames", "DynamicDenoiseResult",
-    "denoise_dynamic",
+    "denoise_dynamic", "BilateralParams", "fine_denoise",
 ]
 
 
@@ -554,3 +554,39 @@ def denoise_dynamic(frames, seg, cfg: PipelineConfig, sizes_in_order: Optional[S
                                               _abi.c_double_p)))
     return DynamicDenoiseResult([o.reshape((3, n)).T.copy() for o in outs], int(nb.value),
                                 {"shared_basis": float(tm[0]), "frames": float(tm[1]), "total": float(tm[2])})
+
+
+# ------------------------------------------------------------------ F4 fine denoising
+
+@dataclasses.dataclass
+class BilateralParams:
+    """BilateralParams (denoise.hpp:11-24), reference defaults."""
+
+    sigma_spatial: float = 0.0
+    sigma_range: float = 0.35
+    normal_iterations: int = 5
+    vertex_iterations: int = 10
+    ring_depth: int = 1
+
+
+def fine_denoise(vertices, faces, params: Optional[BilateralParams] = None, return_normals: bool = False,
+                 ctx: Optional[Context] = None):
+    """fine_denoise (denoise.hpp:172-178) on the GPU: bilateral filtering of
+    the face normals over face rings, then vertex repositioning.  Returns the
+    n x 3 vertices (and the filtered face normals when ``return_normals``)."""
+    ctx = ctx or default_context()
+    params = params or BilateralParams()
+    v = np.asarray(vertices, dtype=np.float64)
+    f = _i32(np.asarray(faces).reshape(-1, 3))
+    n, nf = v.shape[0], f.shape[0]
+    xs = [_f64(v[:, a]) for a in range(3)]
+    out = np.zeros(3 * n)
+    nrm = np.zeros(3 * nf) if return_normals else None
+    bp = _abi.smg_bilateral_params(params.sigma_spatial, params.sigma_range, params.normal_iterations,
+                                   params.vertex_iterations, params.ring_depth)
+    ctx.check(ctx.lib.smg_fine_denoise(ctx.handle, n, _ptr(xs[0]), _ptr(xs[1]), _ptr(xs[2]), nf, _ptr(f),
+                                       C.byref(bp), _ptr(out), _ptr(nrm), 0))
+    res = out.reshape((3, n)).T.copy()
+    if return_normals:
+        return res, nrm.reshape((3, nf)).T.copy()
+    return res

@@ -61,6 +61,11 @@ class smg_encoded_blocks(C.Structure):
                 ("payload_capacity", C.c_int64), ("payload_offsets", C.c_void_p)]
 
 
+class smg_bilateral_params(C.Structure):
+    _fields_ = [("sigma_spatial", C.c_double), ("sigma_range", C.c_double), ("normal_iterations", C.c_int32),
+                ("vertex_iterations", C.c_int32), ("ring_depth", C.c_int32)]
+
+
 AVERAGE_MODE = {"simple": 0, "weighted": 1}
 
 # every symbol include/specmesh_gpu.h declares (checked by the CPU test suite)
@@ -71,6 +76,7 @@ EXPORTED = [
     "smg_operator_apply", "smg_operator_spmm", "smg_orthonormalize", "smg_orthogonal_iteration",
     "smg_dynamic_oi", "smg_bottom_subspace", "smg_gft", "smg_igft", "smg_profile_enable", "smg_profile_read",
     "smg_coarse_reconstruct_frames", "smg_denoise_dynamic", "smg_compress_blocks", "smg_decompress_blocks",
+    "smg_default_bilateral_params", "smg_fine_denoise",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -123,6 +129,9 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_decompress_blocks": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
                                    C.POINTER(smg_pipeline_config), C.POINTER(smg_encoded_blocks), vp, C.c_int32],
                                   C.c_int),
+        "smg_default_bilateral_params": ([C.POINTER(smg_bilateral_params)], None),
+        "smg_fine_denoise": ([vp, C.c_int64, vp, vp, vp, C.c_int64, vp, C.POINTER(smg_bilateral_params), vp, vp,
+                              C.c_int32], C.c_int),
         "smg_denoise_dynamic": ([vp, C.c_int32, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
                                  C.POINTER(smg_pipeline_config), vp, C.c_int32, vp, C.c_int32, c_int32_p,
                                  c_double_p], C.c_int),

@@ -1586,6 +1586,72 @@ smg_status smg_decompress_blocks(smg_context* ctx, const smg_mesh* topology, con
     });
 }
 
+void smg_default_bilateral_params(smg_bilateral_params* p) {
+    if (!p) return;
+    p->sigma_spatial = 0.0;
+    p->sigma_range = 0.35;
+    p->normal_iterations = 5;
+    p->vertex_iterations = 10;
+    p->ring_depth = 1;
+}
+
+smg_status smg_fine_denoise(smg_context* ctx, int64_t vertex_count, const double* x, const double* y,
+                            const double* z, int64_t face_count, const int32_t* faces,
+                            const smg_bilateral_params* params, double* out, double* normals_out,
+                            int32_t on_device) {
+    return guard(ctx, [&] {
+        require(params != nullptr, "bilateral params are null");
+        // BilateralParams::validate (denoise.hpp:18-23)
+        require(params->sigma_spatial >= 0.0, "sigma_spatial must be positive (or 0 for automatic)");
+        require(params->sigma_range > 0.0, "sigma_range must be positive");
+        require(params->normal_iterations > 0 && params->vertex_iterations > 0 && params->ring_depth > 0,
+                "iteration counts and ring depth must be positive");
+        require(vertex_count >= 0 && face_count >= 0, "mesh sizes must be nonnegative");
+        require(out != nullptr && (vertex_count == 0 || (x && y && z)) && (face_count == 0 || faces),
+                "mesh / output pointers are null");
+        cudaStream_t st = ctx->stream;
+        const int64_t n = vertex_count, nf = face_count;
+        DBuf<double> bx, by, bz, bo, bn;
+        DBuf<int32_t> bf;
+        FineParams p;
+        p.n = n;
+        p.nf = nf;
+        if (on_device) {
+            p.x = x;
+            p.y = y;
+            p.z = z;
+            p.faces = faces;
+            p.out = out;
+            p.normals_out = normals_out;
+        } else {
+            bx.upload(x, n, st);
+            by.upload(y, n, st);
+            bz.upload(z, n, st);
+            bf.upload(faces, 3 * nf, st);
+            bo.alloc((size_t)std::max<int64_t>(3 * n, 1), st);
+            if (normals_out) bn.alloc((size_t)std::max<int64_t>(3 * nf, 1), st);
+            p.x = bx.get();
+            p.y = by.get();
+            p.z = bz.get();
+            p.faces = bf.get();
+            p.out = bo.get();
+            p.normals_out = normals_out ? bn.get() : nullptr;
+        }
+        p.sigma_spatial = params->sigma_spatial;
+        p.sigma_range = params->sigma_range;
+        p.normal_iterations = params->normal_iterations;
+        p.vertex_iterations = params->vertex_iterations;
+        p.ring_depth = params->ring_depth;
+        fine_denoise(p, st);
+        if (!on_device) {
+            if (n) SMG_CUDA(cudaMemcpyAsync(out, bo.get(), sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+            if (normals_out && nf)
+                SMG_CUDA(cudaMemcpyAsync(normals_out, bn.get(), sizeof(double) * 3 * nf, cudaMemcpyDeviceToHost, st));
+        }
+        SMG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 smg_status smg_profile_enable(smg_context* ctx, int32_t on) {
     if (!ctx) return SMG_INVALID_ARGUMENT;
     ctx->profiling = on != 0;

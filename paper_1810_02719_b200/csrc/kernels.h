@@ -329,4 +329,20 @@ void codec_unpack(const CodecParams& p, cudaStream_t st);
 void reconstruct_from_coefficients(const FramesParams& p, const double* C, int ldc, double* Xhat,
                                    cudaStream_t st);
 
+// ------------------------------------------------------------------ fine denoising (fine.cu)
+// fine_denoise (denoise.hpp:172-178): face_geometry, face_ring_adjacency,
+// bilateral_normals, update_vertices; device pointers
+struct FineParams {
+    int64_t n = 0, nf = 0;
+    const double* x = nullptr;  // SoA vertices
+    const double* y = nullptr;
+    const double* z = nullptr;
+    const int32_t* faces = nullptr;  // nf x 3 row-major
+    double sigma_spatial = 0.0, sigma_range = 0.35;
+    int normal_iterations = 5, vertex_iterations = 10, ring_depth = 1;
+    double* out = nullptr;          // SoA n x 3
+    double* normals_out = nullptr;  // optional SoA nf x 3 (filtered normals)
+};
+void fine_denoise(const FineParams& p, cudaStream_t st);
+
 }  // namespace smg
