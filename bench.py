@@ -46,6 +46,10 @@ CONFIGS = {
     "F3": dict(W=512, H=512, tw=64, th=32, c=200, t=1, meshes=1, frames=64, sigma=0.01, seed0=7000,
                desc="denoise_dynamic: 64 frames of a 512^2 grid sequence, 128 tiles of 32x64 (n_d=2048), "
                     "bases from frame 0 (c=200, t=1), every frame projected + stitched"),
+    # F4: fine_denoise of config 4's 1024^2 noisy grid (2 M faces)
+    "F4": dict(W=1024, H=1024, tw=64, th=64, c=0, t=0, meshes=1, fine=True, sigma=0.01, seed0=404,
+               desc="fine_denoise (bilateral normals x5 over 1-rings + 10 vertex passes) of the 1024^2 noisy grid "
+                    "(1 048 576 vertices, 2 093 058 faces), reference default BilateralParams"),
     "C2": dict(W=256, H=256, tw=32, th=32, c=100, t=1, meshes=1, sigma=0.005, seed0=202,
                desc="256^2 grid, 64 tiles of 32x32 (n_d=1024), c=100, t=1"),
 }
@@ -643,6 +647,153 @@ def frames_reference_arm(args, cfg):
                     "d2h_bytes_per_step": 0}}
 
 
+# ----------------------------------------------------------------------- F4 arm
+
+def _fine_inputs(cfg, seed):
+    from paper_1810_02719_b200 import synth
+    return synth.grid_mesh(cfg["W"], cfg["H"], seed, cfg["sigma"])
+
+
+def fine_arm(args, cfg, rank, world, local_rank):
+    """fine_denoise (denoise.hpp:172-178) through smg_fine_denoise; one mesh per
+    rank (independent meshes: weak scaling, no collective)."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    import paper_1810_02719_b200 as G
+    from paper_1810_02719_b200 import _abi
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    ctx = G.Context(local_rank)
+    m = _fine_inputs(cfg, cfg["seed0"] + rank)
+    n, nf = m.n, m.faces.shape[0]
+    d_xyz = [torch.from_numpy(np.ascontiguousarray(m.vertices[:, a])).to(dev) for a in range(3)]
+    h_xyz = [torch.from_numpy(np.ascontiguousarray(m.vertices[:, a])).pin_memory() for a in range(3)]
+    d_f = torch.from_numpy(np.ascontiguousarray(m.faces, dtype=np.int32)).to(dev)
+    h_f = torch.from_numpy(np.ascontiguousarray(m.faces, dtype=np.int32)).pin_memory()
+    d_out = torch.empty(3 * n, dtype=torch.float64, device=dev)
+    h_out = torch.empty(3 * n, dtype=torch.float64).pin_memory()
+    bp = _abi.smg_bilateral_params()
+    ctx.lib.smg_default_bilateral_params(C.byref(bp))
+
+    def step(on):
+        xyz, f, out = (d_xyz, d_f, d_out) if on else (h_xyz, h_f, h_out)
+        ctx.check(ctx.lib.smg_fine_denoise(ctx.handle, n, xyz[0].data_ptr(), xyz[1].data_ptr(), xyz[2].data_ptr(), nf,
+                                           f.data_ptr(), C.byref(bp), out.data_ptr(), None, on))
+
+    def launches():
+        n_, t_ = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, b"launches", C.byref(n_), C.byref(t_))
+        return n_.value
+
+    def timed(on, steps):
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = launches()
+        ev0.record()
+        for _ in range(steps):
+            step(on)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, launches() - l0
+
+    for _ in range(args.warmup):
+        step(1)
+    ctx.lib.smg_profile_enable(ctx.handle, 1)
+    with ClockSampler(local_rank) as clk:
+        ms, nl = timed(1, args.steps)
+    stages = {}
+    for nm in ("fine_geometry", "fine_rings", "fine_sigma", "fine_normals", "fine_vertices"):
+        n_, t_ = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, nm.encode(), C.byref(n_), C.byref(t_))
+        stages[nm] = t_.value / args.steps
+    ctx.lib.smg_profile_enable(ctx.handle, 0)
+    step(0)
+    ms_e2e, _ = timed(0, args.steps)
+    ms_step = ms / args.steps
+    units = world * n
+    # dominant kernel: the bilateral sweep; algorithmic bytes per face and sweep =
+    # its {centroid, area} + normal read (2 x 32 B) + normal write (32 B) + ring
+    # offsets (4 B) + ring ids (4 B per member, 13 on this grid: 52 B) = 152 B
+    ring_ids = 13
+    bytes_face = 32 + 32 + 32 + 4 + 4 * ring_ids
+    sweeps = bp.normal_iterations
+    t_sweep = stages["fine_normals"] / sweeps if stages["fine_normals"] > 0 else None
+    achieved = bytes_face * nf / (t_sweep * 1e-3) / 1e9 if t_sweep else None
+    peak = 6550.7
+    try:
+        with open(PEAKS) as fh:
+            peak = float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        pass
+    out = {
+        "metric": METRIC + " [F4 fine_denoise: vertices/s]", "value": units / (ms_step * 1e-3), "unit": "vertices/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded sinusoid height-field grid + N(0, 0.01^2) noise)",
+        "config": {"workload": f"F4: {cfg['desc']}", "vertices": n, "faces": nf,
+                   "params": {"sigma_spatial": "auto", "sigma_range": bp.sigma_range,
+                              "normal_iterations": bp.normal_iterations,
+                              "vertex_iterations": bp.vertex_iterations, "ring_depth": bp.ring_depth},
+                   "parallelism": f"one mesh per GPU ({world} GPU(s))",
+                   "l2": "face data (%.0f MB) larger than L2" % (nf * 64 / 1e6)},
+        "e2e": {"value": units / (ms_e2e / args.steps * 1e-3), "unit": "vertices/s",
+                "h2d_bytes_per_step": 3 * n * 8 + nf * 12, "d2h_bytes_per_step": 3 * n * 8},
+        "roofline": {"kernel": "bilateral_kernel (one Jacobi sweep of the normal filter)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "bytes_per_face": bytes_face, "sweep_ms": t_sweep,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "stages_ms_per_step": {k: round(v, 3) for k, v in stages.items()},
+        "clocks": clk.summary(), "gpu_launches": nl,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = fine_cpu_baseline(cfg)
+    if dist is not None:
+        dist.destroy_process_group()
+    ctx.close()
+    return out if rank == 0 else None
+
+
+def fine_cpu_baseline(cfg, rows=128):
+    """The oracle's fine_denoise on a bounded sample: the first `rows` grid rows
+    (a W x rows strip, same connectivity pattern), one core, scaled per vertex."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import specmesh_oracle as O
+    from paper_1810_02719_b200 import synth
+    m = synth.grid_mesh(cfg["W"], rows, cfg["seed0"], cfg["sigma"])
+    t0 = time.perf_counter()
+    O.fine_denoise(m.vertices, m.faces, O.BilateralParams())
+    dt = time.perf_counter() - t0
+    return {"value": m.n / dt, "unit": "vertices/s", "cores": 1, "kind": "port",
+            "sample": f"oracle fine_denoise of a {cfg['W']} x {rows} strip of the grid ({m.n} vertices, "
+                      f"{dt:.2f}s, numpy vectorised over faces, 1 core)"}
+
+
+def fine_reference_arm(args, cfg):
+    vals = [fine_cpu_baseline(cfg)["value"] for _ in range(max(1, args.steps))]
+    cb = fine_cpu_baseline(cfg)
+    cb["value"] = statistics.median(vals)
+    units = cfg["W"] * cfg["H"]
+    return {"metric": METRIC + " [F4 fine_denoise: vertices/s]", "value": cb["value"], "unit": "vertices/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": units / cb["value"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": {"workload": f"F4: {cfg['desc']}"},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
@@ -652,8 +803,14 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        arm = frames_reference_arm if "frames" in cfg else reference_arm
+        arm = frames_reference_arm if "frames" in cfg else (fine_reference_arm if "fine" in cfg else reference_arm)
         print(json.dumps(arm(args, cfg)), flush=True)
+        return
+    if "fine" in cfg:
+        if args.impl == "ours":
+            out = fine_arm(args, cfg, rank, world, local_rank)
+            if out is not None:
+                print(json.dumps(out), flush=True)
         return
     if "frames" in cfg:
         if args.impl == "ours":
