@@ -7,7 +7,9 @@
 //   T   = V[:, p] D_p^-1 - sum_{s<p} Q[:, s] R~_{s,p}
 //   Q_p = T X_pp,   X_pp = R~_pp^-1 (written by the Cholesky's diagonal phase)
 // with the CTA's finished panels kept in shared memory and each panel's column
-// of R~ staged once.  This replaces the explicit block back-substitution for
+// of R~ staged once (64-row CTAs), or -- when a 64-row block of finished panels
+// and the whole column would not fit (c > ~280) -- 32-row CTAs that stream the
+// column of R~ through shared memory in 64-row chunks.  This replaces the explicit block back-substitution for
 // R~^-1 -- a serial single-CTA phase of the Cholesky -- by row-parallel work.
 #include "common.cuh"
 #include "kernels.h"
@@ -16,25 +18,34 @@ namespace smg {
 
 namespace {
 
-constexpr int TNT = 256;  // 8 warps: 4 (16 rows) x 2 (16 columns) over the 64 x 32 panel
-constexpr int TRB = 64;   // rows per CTA
+constexpr int TNT = 256;  // 8 warps: 4 (8 MI rows) x 2 (16 columns) over the (32 MI) x 32 panel
 constexpr int PS36 = 36;  // 32-wide block stride (% 16 == 4)
+constexpr int KC = 64;    // streamed R~ rows per chunk
 
-struct TrsmSmem {
+// MI = 2: 64-row CTAs, whole R~ column staged; MI = 1 (CHUNK): 32-row CTAs,
+// R~ column streamed in KC-row chunks
+template <int MI, bool CHUNK>
+struct TrsmCfg {
+    static constexpr int TRB = 32 * MI;
     __host__ __device__ static int qs(int cp) { return cp + 4; }
-    static int bytes(int cp) { return (TRB * qs(cp) + cp * PS36 + 32 * PS36 + TRB * PS36) * 8; }
+    static int bytes(int cp) { return (TRB * qs(cp) + (CHUNK ? KC : cp) * PS36 + 32 * PS36 + TRB * PS36) * 8; }
 };
+using TrsmFull = TrsmCfg<2, false>;
+using TrsmStream = TrsmCfg<1, true>;
 
+template <int MI, bool CHUNK>
 __global__ void __launch_bounds__(TNT) trsm_kernel(TrsmParams p) {
+    using TC = TrsmCfg<MI, CHUNK>;
+    constexpr int TRB = TC::TRB;
     extern __shared__ __align__(16) double sm[];
     const int b = blockIdx.y;
     if (p.status && p.status[b] != kOk) return;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const int P = (c + 31) / 32, cp = (p.c_cap + 31) / 32 * 32;
-    const int QS = TrsmSmem::qs(cp);
-    double* Qs = sm;                  // TRB x QS: finished panels of this row block
-    double* Rc = Qs + TRB * QS;       // cp x 36: column panel p of R~ (rows < p0)
-    double* Xp = Rc + cp * PS36;      // 32 x 36: X_pp
+    const int QS = TC::qs(cp);
+    double* Qs = sm;                         // TRB x QS: finished panels of this row block
+    double* Rc = Qs + TRB * QS;              // (cp | KC) x 36: column panel p of R~ (rows < p0)
+    double* Xp = Rc + (CHUNK ? KC : cp) * PS36;  // 32 x 36: X_pp
     double* Tp = Xp + 32 * PS36;      // TRB x 36: T
     const int r0 = blockIdx.x * TRB;
     const double* V = p.V + (int64_t)b * p.strideV;
@@ -44,74 +55,87 @@ __global__ void __launch_bounds__(TNT) trsm_kernel(TrsmParams p) {
     const double* d = p.dscale + (int64_t)b * p.strideD;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm = warp & 3, wn = warp >> 2;  // rows 16 wm .., columns 16 wn ..
+    const int wm = warp & 3, wn = warp >> 2;  // rows 8 MI wm .., columns 16 wn ..
 
     for (int pb = 0; pb < P; ++pb) {
         const int p0 = pb * 32;
-        // stage R~[0:p0, p0:p0+32] and X_pp = d_row * B_pp
-        for (int e = tid; e < p0 * 32; e += TNT) {
-            const int r = e >> 5, k = e & 31;
-            Rc[r * PS36 + k] = A[(int64_t)r * p.ldr + p0 + k];
-        }
+        // stage R~[0:p0, p0:p0+32] (whole panel) and X_pp = d_row * B_pp
+        if (!CHUNK)
+            for (int e = tid; e < p0 * 32; e += TNT) {
+                const int r = e >> 5, k = e & 31;
+                Rc[r * PS36 + k] = A[(int64_t)r * p.ldr + p0 + k];
+            }
         for (int e = tid; e < 32 * 32; e += TNT) {
             const int r = e >> 5, k = e & 31;
             Xp[r * PS36 + k] = Bo[(int64_t)(p0 + r) * p.ldb + p0 + k] * d[p0 + r];
         }
         // T starts as V[:, p] D^-1 (accumulator fragments)
-        double acc[2][2][2];
+        double acc[MI][2][2];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    const int row = r0 + 16 * wm + 8 * i + g, col = p0 + 16 * wn + 8 * j + 2 * t + q;
+                    const int row = r0 + 8 * MI * wm + 8 * i + g, col = p0 + 16 * wn + 8 * j + 2 * t + q;
                     acc[i][j][q] = (row < p.n) ? V[(int64_t)row * p.ldv + col] / d[col] : 0.0;
                 }
         __syncthreads();
         // T -= Q[:, <p] R~[<p, p]
-        for (int kk = 0; kk < p0; kk += 4) {
-            double a[2], bb[2];
+        for (int k0 = 0; k0 < p0; k0 += (CHUNK ? KC : p0)) {
+            const int k1 = CHUNK ? min(p0, k0 + KC) : p0;
+            if (CHUNK) {
+                if (k0 > 0) __syncthreads();  // the previous chunk is consumed
+                for (int e = tid; e < (k1 - k0) * 32; e += TNT) {
+                    const int r = e >> 5, k = e & 31;
+                    Rc[r * PS36 + k] = A[(int64_t)(k0 + r) * p.ldr + p0 + k];
+                }
+                __syncthreads();
+            }
+            for (int kk = k0; kk < k1; kk += 4) {
+                const int kr = CHUNK ? kk - k0 : kk;
+                double a[MI], bb[2];
 #pragma unroll
-            for (int i = 0; i < 2; ++i) a[i] = Qs[(16 * wm + 8 * i + g) * QS + kk + t];
+                for (int i = 0; i < MI; ++i) a[i] = Qs[(8 * MI * wm + 8 * i + g) * QS + kk + t];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) bb[j] = -Rc[(kk + t) * PS36 + 16 * wn + 8 * j + g];
+                for (int j = 0; j < 2; ++j) bb[j] = -Rc[(kr + t) * PS36 + 16 * wn + 8 * j + g];
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < MI; ++i)
 #pragma unroll
-                for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+                    for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+            }
         }
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const int r = 16 * wm + 8 * i + g, cc = 16 * wn + 8 * j + 2 * t;
+                const int r = 8 * MI * wm + 8 * i + g, cc = 16 * wn + 8 * j + 2 * t;
                 Tp[r * PS36 + cc] = acc[i][j][0];
                 Tp[r * PS36 + cc + 1] = acc[i][j][1];
             }
         __syncthreads();
         // Q_p = T X_pp
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
         for (int kk = 0; kk < 32; kk += 4) {
-            double a[2], bb[2];
+            double a[MI], bb[2];
 #pragma unroll
-            for (int i = 0; i < 2; ++i) a[i] = Tp[(16 * wm + 8 * i + g) * PS36 + kk + t];
+            for (int i = 0; i < MI; ++i) a[i] = Tp[(8 * MI * wm + 8 * i + g) * PS36 + kk + t];
 #pragma unroll
             for (int j = 0; j < 2; ++j) bb[j] = Xp[(kk + t) * PS36 + 16 * wn + 8 * j + g];
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < MI; ++i)
 #pragma unroll
                 for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
         }
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const int r = 16 * wm + 8 * i + g, cc = 16 * wn + 8 * j + 2 * t;
+                const int r = 8 * MI * wm + 8 * i + g, cc = 16 * wn + 8 * j + 2 * t;
                 Qs[r * QS + p0 + cc] = acc[i][j][0];
                 Qs[r * QS + p0 + cc + 1] = acc[i][j][1];
                 const int row = r0 + r, col = p0 + cc;
@@ -126,19 +150,31 @@ __global__ void __launch_bounds__(TNT) trsm_kernel(TrsmParams p) {
 
 }  // namespace
 
-int trsm_smem_bytes(int c_cap) { return TrsmSmem::bytes((c_cap + 31) / 32 * 32); }
+int trsm_smem_bytes(int c_cap) {
+    const int cp = (c_cap + 31) / 32 * 32;
+    const int full = TrsmFull::bytes(cp);
+    return full <= 227 * 1024 ? full : TrsmStream::bytes(cp);
+}
 
 bool trsm_supported(int c_cap) { return trsm_smem_bytes(c_cap) <= 227 * 1024; }
 
 void trsm_right_upper(const TrsmParams& p, cudaStream_t st) {
+    const int cp = (p.c_cap + 31) / 32 * 32;
+    const bool full = TrsmFull::bytes(cp) <= 227 * 1024;
     const int bytes = trsm_smem_bytes(p.c_cap);
-    static int configured = 0;
-    if (bytes > configured) {
-        cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        configured = bytes;
+    static int configured[2] = {0, 0};
+    if (bytes > configured[full]) {
+        if (full) cudaFuncSetAttribute(trsm_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        else cudaFuncSetAttribute(trsm_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        configured[full] = bytes;
     }
-    dim3 grid((p.n + TRB - 1) / TRB, p.batch);
-    ::smg::count_launch(), trsm_kernel<<<grid, TNT, bytes, st>>>(p);
+    if (full) {
+        dim3 grid((p.n + TrsmFull::TRB - 1) / TrsmFull::TRB, p.batch);
+        ::smg::count_launch(), trsm_kernel<2, false><<<grid, TNT, bytes, st>>>(p);
+    } else {
+        dim3 grid((p.n + TrsmStream::TRB - 1) / TrsmStream::TRB, p.batch);
+        ::smg::count_launch(), trsm_kernel<1, true><<<grid, TNT, bytes, st>>>(p);
+    }
 }
 
 }  // namespace smg
