@@ -437,8 +437,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
 #pragma unroll
                     for (int j = 0; j < TL::NT; ++j) {
                         const int r = 8 * TL::tile(wm, i) + g, cc = 8 * (wn * TL::NT + j) + 2 * t;
-                        ycur[r * XS + cc] = acc[i][j][0];
-                        ycur[r * XS + cc + 1] = acc[i][j][1];
+                        *reinterpret_cast<double2*>(ycur + r * XS + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
                         const int prow = k * W + r;
                         if (last) {
                             if (prow < n && col0 + cc < c) {
