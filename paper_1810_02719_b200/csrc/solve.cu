@@ -224,44 +224,8 @@ SMG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
         : "memory");
 }
 
-SMG_DEV void bulk_multicast(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
-        "%4;\n" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
-        : "memory");
-}
 SMG_DEV void mbar_arrive_local(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-// arrive on the mbarrier at the same offset in cluster CTA `rank`
-SMG_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
-    asm volatile(
-        "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, %1;\n"
-        " mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(smem_u32(bar)),
-        "r"(rank)
-        : "memory");
-}
-SMG_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAITC_%=:\n"
-        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-SMG_DEV uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-SMG_DEV uint32_t cluster_size() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
-    return r;
-}
-SMG_DEV void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 // named barrier over the DMMA warps only (the producers run ahead on mbarriers)
 SMG_DEV void mma_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT_MMA) : "memory"); }
