@@ -65,3 +65,26 @@ def test_fine_denoise_errors(ctx):
     bad[3, 1] = v.shape[0]
     with pytest.raises(G.InvalidArgument, match="face 3 references a vertex out of range"):
         G.fine_denoise(v, bad, G.BilateralParams())
+
+
+def test_fine_denoise_device_pointers(ctx):
+    """on_device = 1: device-resident inputs and outputs give the host path's result."""
+    import ctypes as C
+
+    import torch
+    from paper_1810_02719_b200 import _abi
+    v, f = noisy_grid(24, 20, seed=4)
+    want, wn = G.fine_denoise(v, f, G.BilateralParams(), return_normals=True, ctx=ctx)
+    dev = torch.device("cuda", 0)
+    xyz = [torch.from_numpy(np.ascontiguousarray(v[:, a])).to(dev) for a in range(3)]
+    df = torch.from_numpy(np.ascontiguousarray(f, dtype=np.int32)).to(dev)
+    out = torch.empty(3 * v.shape[0], dtype=torch.float64, device=dev)
+    nrm = torch.empty(3 * f.shape[0], dtype=torch.float64, device=dev)
+    bp = _abi.smg_bilateral_params()
+    ctx.lib.smg_default_bilateral_params(C.byref(bp))
+    ctx.check(ctx.lib.smg_fine_denoise(ctx.handle, v.shape[0], xyz[0].data_ptr(), xyz[1].data_ptr(),
+                                       xyz[2].data_ptr(), f.shape[0], df.data_ptr(), C.byref(bp), out.data_ptr(),
+                                       nrm.data_ptr(), 1))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().reshape(3, -1).T, want)
+    assert np.array_equal(nrm.cpu().numpy().reshape(3, -1).T, wn)

@@ -122,3 +122,34 @@ def test_frames_stage_uncovered_vertices(ctx):
     bb = G.BlockBases(part.sequence, [], ob.bases, None, None, {}, part.block_size)
     with pytest.raises(G.InvalidArgument, match="reconstruction is missing 1024 vertices: 2080 2081"):
         G.coarse_reconstruct_frames(topo, part, bb, [frames[0].vertices], ctx=ctx)
+
+
+def test_frames_stage_device_pointers(ctx):
+    """smg_coarse_reconstruct_frames with device bases, frames and outputs equals
+    the host-pointer call bit for bit."""
+    import ctypes as C
+
+    import torch
+    from paper_1810_02719_b200 import _abi
+    topo, frames = sequence(64, 64, 3, seed=17)
+    seg = synth.grid_tiles(64, 64, 32, 32)
+    cfg = G.PipelineConfig(weighting="binary", subspace_size=24, iterations=1, shift_scale=1e-3)
+    bb = G.compute_block_bases_fixed_sizes(frames[0], seg, cfg, [24] * seg.count, want_bases=True, ctx=ctx)
+    want = G.coarse_reconstruct_frames(topo, seg, bb, [f.vertices for f in frames], ctx=ctx)
+    dev = torch.device("cuda", 0)
+    keep = []
+    mv, sv = G._mesh_view(topo, keep), G._seg_view(seg, keep)
+    k = seg.count
+    sizes = np.full(k, 24, np.int32)
+    offs = (np.arange(k + 1) * 24 * seg.block_size).astype(np.int64)
+    data = torch.from_numpy(np.concatenate([b.ravel(order="F") for b in bb.bases])).to(dev)
+    bv = _abi.smg_bases(k, sizes.ctypes.data, offs.ctypes.data, data.data_ptr(), 1)
+    cols = [torch.from_numpy(np.ascontiguousarray(f.vertices[:, a])).to(dev) for f in frames for a in range(3)]
+    xyz = (C.c_void_p * len(cols))(*[t.data_ptr() for t in cols])
+    outs = [torch.empty(3 * topo.n, dtype=torch.float64, device=dev) for _ in frames]
+    outp = (C.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
+    ctx.check(ctx.lib.smg_coarse_reconstruct_frames(ctx.handle, C.byref(mv), C.byref(sv), C.byref(bv), len(frames),
+                                                    xyz, 1, 1, outp, 1))
+    torch.cuda.synchronize()
+    for o, w in zip(outs, want):
+        assert np.array_equal(o.cpu().numpy().reshape(3, -1).T, w)

@@ -41,6 +41,15 @@ def main():
             def run():
                 return G.compute_block_bases_fixed_sizes(w.mesh, w.seg, cfg, [w.c] * w.seg.count, ctx=ctx)
         run()
+        import ctypes as C
+        ctx.lib.smg_profile_enable(ctx.handle, 1)
+        run()
+        stages = {}
+        for nm in ("assemble", "factor", "first_basis", "solve", "orthonormalize", "gram", "chol", "trmm", "project"):
+            n_, t_ = C.c_int64(), C.c_double()
+            ctx.lib.smg_profile_read(ctx.handle, nm.encode(), C.byref(n_), C.byref(t_))
+            stages[nm] = {"launches": n_.value, "ms": round(t_.value, 3)}
+        ctx.lib.smg_profile_enable(ctx.handle, 0)
         best_dev, best_wall, bb = 1e30, 1e30, None
         for _ in range(args.reps):
             t0 = time.perf_counter()
@@ -54,7 +63,7 @@ def main():
                "c": w.c if not w.doi else {"min": min(sizes), "max": max(sizes), "mean": sum(sizes) / len(sizes)},
                "device_s": best_dev, "wall_s": best_wall, "vertices_per_s_device": n / best_dev,
                "vertices_per_s_e2e": n / best_wall,
-               "timings": {k: round(v, 6) for k, v in bb.timings.items()}}
+               "timings": {k: round(v, 6) for k, v in bb.timings.items()}, "stages_ms": stages}
         if w.doi:
             out["doi_steps"] = int(sum(s.oi_iterations for s in bb.stats))
             out["converged_blocks"] = int(sum(s.converged for s in bb.stats))
