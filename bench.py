@@ -296,7 +296,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     clocks = clk.summary()
     stages = {}
     import ctypes as C
-    for nm in ("assemble", "factor", "first_basis", "fb_iterate", "fb_rayleigh_ritz", "solve", "orthonormalize",
+    for nm in ("assemble", "factor", "first_basis", "fb_iterate", "fb_filter", "fb_rayleigh_ritz", "solve", "orthonormalize",
                "gram", "chol", "trmm", "project"):
         n, t = C.c_int64(), C.c_double()
         ctx.lib.smg_profile_read(ctx.handle, nm.encode(), C.byref(n), C.byref(t))

@@ -27,6 +27,7 @@ void TileSet::build(const std::vector<TileRef>& tiles, int n_, int weighting, do
     ProfScope prof("assemble", st);
     ntiles = (int)tiles.size();
     n = n_;
+    this->weighting = weighting;
     require(n >= 2, "submesh must have at least 2 vertices");
     require(n <= 4096, "submesh size exceeds the GPU limit of 4096 vertices");
     refs.upload(tiles, st);

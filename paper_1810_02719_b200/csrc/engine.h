@@ -89,6 +89,7 @@ struct TileSet {
     // orderings from the connectivity alone (codec: the decoder has no coordinates,
     // so encoder and decoder must factor identically)
     bool topology_ordering = false;
+    int weighting = -1;  // smg_weighting of the assembled tiles (-1: external CSR)
     int64_t total_nnz = 0;
     DBuf<TileRef> refs;
     DBuf<int32_t> nnz, rowptr, cols, perm, bw, blockw;

@@ -150,7 +150,46 @@ FirstBasisReport first_basis_impl(const StepCtx& cx, Workspace& ws, const TileSe
             // Chebyshev-filtered subspace iteration on L (SpMM only): p_d damps
             // [a, b] = [theta_m, Gershgorin bound] and keeps the bottom of the spectrum
             double* bufs[3] = {ws.U.get(), ws.V.get(), ws.T.get()};
-            for (int app = 0; app < cheb_apps; ++app) {
+            // binary-weight tiles whose pattern fits shared memory run the fused filter
+            int max_nnz = 0;
+            bool fused = ts.weighting == 0 && !std::getenv("SMG_CHEB_UNFUSED");
+            if (fused) {
+                std::vector<int32_t> nz = download(ts.nnz.get(), (size_t)ts.ntiles, st);
+                for (int b = 0; b < ws.B; ++b) max_nnz = std::max(max_nnz, nz[(size_t)tile0 + (size_t)b * tstride]);
+                fused = cheb_filter_supported(n, max_nnz);
+            }
+            for (int app = 0; app < cheb_apps && fused; ++app) {
+                // all deg steps in one launch, iterates in shared memory (bit-identical
+                // to the per-step SpMM path below)
+                ChebParams cp;
+                cp.n = n;
+                cp.c = m;
+                cp.batch = ws.B;
+                cp.deg = deg;
+                cp.rowptr = ts.rowptr.get() + (int64_t)tile0 * (n + 1);
+                cp.strideRowptr = (int64_t)tstride * (n + 1);
+                cp.csr_offsets = ts.off.get() + tile0;
+                cp.offStride = tstride;
+                cp.cols = ts.cols.get();
+                cp.vals = ts.vals.get();
+                cp.coef = dcoef.get();
+                cp.X = ws.U.get();
+                cp.ldx = ws.ld;
+                cp.strideX = ws.mstride();
+                cp.Y = ws.V.get();
+                cp.ldy = ws.ld;
+                cp.strideY = ws.mstride();
+                {
+                    ProfScope ps("fb_filter", st);
+                    cheb_filter(cp, max_nnz, st);
+                }
+                // same CholeskyQR passes as the per-step path, whose iterate lands back
+                // in U (in place: full CholeskyQR2) when deg % 3 == 0
+                const bool last = app + 1 == cheb_apps;
+                orth_batch(cx, ws, ws.V.get(), ws.U.get(), m, nullptr, false, 0, (last || deg % 3 == 0) ? 2 : 1);
+                rep.iterations += deg;
+            }
+            for (int app = 0; app < cheb_apps && !fused; ++app) {
                 int x = 0, y = 1;
                 for (int i = 1; i <= deg; ++i) {
                     const int z = (i == 1) ? 1 : 3 - x - y;

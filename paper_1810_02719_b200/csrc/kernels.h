@@ -253,6 +253,27 @@ struct SpmmParams {
 };
 void spmm(const SpmmParams& p, cudaStream_t st);
 
+// The whole Chebyshev filter of one application (deg steps of the three-term
+// recurrence X_i = alpha_i (L + s I) X_{i-1} + gamma_i X_{i-2}) for binary-weight
+// Laplacians, with the CSR pattern and the iterates of a column slice held in
+// shared memory: the same per-element arithmetic as deg spmm() calls.
+struct ChebParams {
+    int n = 0, c = 0, batch = 1, deg = 0;
+    const int32_t* rowptr = nullptr;
+    int64_t strideRowptr = 0;
+    const int64_t* csr_offsets = nullptr;
+    int64_t offStride = 1;
+    const int32_t* cols = nullptr;
+    const double* vals = nullptr;
+    const double* coef = nullptr;  // [deg][batch] alpha | [deg][batch] gamma | [batch] shift
+    const double* X = nullptr;     // X_0
+    int64_t ldx = 0, strideX = 0;
+    double* Y = nullptr;           // X_deg
+    int64_t ldy = 0, strideY = 0;
+};
+bool cheb_filter_supported(int n, int max_nnz);
+void cheb_filter(const ChebParams& p, int max_nnz, cudaStream_t st);
+
 struct Stitcher {
     int n = 0, n_d = 0;
     int32_t* offs = nullptr;

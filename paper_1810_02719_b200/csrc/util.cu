@@ -284,6 +284,92 @@ void spmm(const SpmmParams& p, cudaStream_t st) {
     ::smg::count_launch(), spmm_kernel<<<dim3((p.n + SPMM_ROWS - 1) / SPMM_ROWS, p.batch), SPMM_NT, 0, st>>>(p);
 }
 
+// ---- fused Chebyshev filter for binary-weight Laplacians (off-diagonal entries
+// exactly -1, diagonal = degree): one CTA per (chain, CSL-column slice) holds
+// the tile's CSR pattern, its shifted diagonal and two iterates in shared
+// memory and runs all deg steps of X_i = alpha_i (L + s I) X_{i-1} + gamma_i
+// X_{i-2} there (X_{i-2} is overwritten in place by the thread that owns its
+// row).  The per-element arithmetic is spmm_kernel's: v = vals[q] (+ s on the
+// diagonal), acc = fma(v, x, acc) in CSR order, acc * alpha, fma(gamma, z, .).
+template <int CSL>
+__global__ void __launch_bounds__(1024) cheb_bin_kernel(ChebParams p) {
+    extern __shared__ __align__(16) double cbuf[];
+    const int b = blockIdx.y, col0 = blockIdx.x * CSL, n = p.n;
+    const int64_t half = (int64_t)n * CSL;
+    double* dg = cbuf + 2 * half;                           // vals[diag] + shift per row
+    int32_t* rp = reinterpret_cast<int32_t*>(dg + n);       // n + 1
+    int32_t* cl = rp + n + 1;                               // nnz
+    const int32_t* rowptr = p.rowptr + (int64_t)b * p.strideRowptr;
+    const int64_t base = p.csr_offsets ? p.csr_offsets[(int64_t)b * p.offStride] : 0;
+    const int32_t* cols = p.cols + base;
+    const double* vals = p.vals + base;
+    const double shift = p.coef[(int64_t)2 * p.deg * p.batch + b];
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) rp[i] = rowptr[i];
+    __syncthreads();
+    const int nnz = rp[n];
+    for (int q = threadIdx.x; q < nnz; q += blockDim.x) {
+        const int col = cols[q];
+        cl[q] = col;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int q = rp[i]; q < rp[i + 1]; ++q)
+            if (cols[q] == i) dg[i] = vals[q] + shift;
+    const double* X = p.X + (int64_t)b * p.strideX;
+    for (int e = threadIdx.x; e < n * CSL; e += blockDim.x) {
+        const int i = e / CSL, j = col0 + e % CSL;
+        cbuf[e] = j < p.c ? X[(int64_t)i * p.ldx + j] : 0.0;
+    }
+    __syncthreads();
+    for (int step = 1; step <= p.deg; ++step) {
+        const double alpha = p.coef[(int64_t)(step - 1) * p.batch + b];
+        const double gam = step > 1 ? p.coef[(int64_t)p.deg * p.batch + (int64_t)(step - 1) * p.batch + b] : 0.0;
+        const double* xc = cbuf + ((step - 1) & 1) * half;
+        double* xo = cbuf + (step & 1) * half;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            double acc[CSL];
+#pragma unroll
+            for (int u = 0; u < CSL; ++u) acc[u] = 0.0;
+            const double di = dg[i];
+            for (int q = rp[i]; q < rp[i + 1]; ++q) {
+                const int col = cl[q];
+                const double v = col == i ? di : -1.0;
+                const double* xr = xc + (int64_t)col * CSL;
+#pragma unroll
+                for (int u = 0; u < CSL; ++u) acc[u] = fma(v, xr[u], acc[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < CSL; ++u) {
+                double a = acc[u] * alpha;
+                if (step > 1) a = fma(gam, xo[(int64_t)i * CSL + u], a);
+                xo[(int64_t)i * CSL + u] = a;
+            }
+        }
+        __syncthreads();
+    }
+    const double* res = cbuf + (p.deg & 1) * half;
+    double* Y = p.Y + (int64_t)b * p.strideY;
+    for (int e = threadIdx.x; e < n * CSL; e += blockDim.x) {
+        const int i = e / CSL, j = col0 + e % CSL;
+        if (j < p.c) Y[(int64_t)i * p.ldy + j] = res[e];
+    }
+}
+
+int cheb_bin_bytes(int n, int max_nnz, int csl) {
+    return 2 * n * csl * 8 + n * 8 + ((n + 1 + max_nnz + 1) / 2) * 8;
+}
+
+bool cheb_filter_supported(int n, int max_nnz) { return cheb_bin_bytes(n, max_nnz, 2) <= 227 * 1024; }
+
+void cheb_filter(const ChebParams& p, int max_nnz, cudaStream_t st) {
+    auto go = [&](auto kernel, int csl) {
+        const int bytes = cheb_bin_bytes(p.n, max_nnz, csl);
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        ::smg::count_launch(), kernel<<<dim3((p.c + csl - 1) / csl, p.batch), 1024, bytes, st>>>(p);
+    };
+    if (cheb_bin_bytes(p.n, max_nnz, 4) <= 227 * 1024) go(cheb_bin_kernel<4>, 4);
+    else go(cheb_bin_kernel<2>, 2);
+}
+
 void Stitcher::build(const int32_t* members, int nsub, int n_d, int n, cudaStream_t st) {
     this->n = n;
     this->n_d = n_d;

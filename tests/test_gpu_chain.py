@@ -166,3 +166,17 @@ def test_batched_chains_equal_single_chains(ctx):
         assert np.linalg.norm(b.reconstruction - r, axis=1).max() <= 1e-10 * np.linalg.norm(r, axis=1).max()
         for i in range(seg.count):
             assert abs(single.stats[i].residual_rms - b.stats[i].residual_rms) <= 1e-10 * single.stats[i].residual_rms
+
+
+def test_fused_chebyshev_filter_bit_identical(ctx, monkeypatch):
+    """The fused first-basis filter (all degree steps in one launch, iterates in
+    shared memory) performs the per-step SpMM path's arithmetic exactly."""
+    mesh = synth.small_grid(64, 64, 32, 32, seed=6, flip=2)
+    seg = synth.grid_tiles(64, 64, 32, 32)
+    cfg = G.PipelineConfig(weighting="binary", subspace_size=40, iterations=1, shift_scale=1e-3)
+    fused = G.compute_block_bases_fixed_sizes(mesh, seg, cfg, [40] * seg.count, want_bases=True, ctx=ctx)
+    monkeypatch.setenv("SMG_CHEB_UNFUSED", "1")
+    plain = G.compute_block_bases_fixed_sizes(mesh, seg, cfg, [40] * seg.count, want_bases=True, ctx=ctx)
+    for a, b in zip(fused.bases, plain.bases):
+        assert np.array_equal(a, b)
+    assert np.array_equal(fused.reconstruction, plain.reconstruction)
