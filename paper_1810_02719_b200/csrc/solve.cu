@@ -279,18 +279,27 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     }
     __syncthreads();
 
-    auto block_of = [&](int gs) {
-        const int sweep = gs / Kb, step = gs % Kb;
-        return (sweep & 1) ? Kb - 1 - step : step;
+    // step cursor: (sweep, step) of global step gs, advanced incrementally (no
+    // division by the runtime block count in the loops)
+    struct Cursor {
+        int gs, sweep, step, Kb;
+        SMG_DEV int k() const { return (sweep & 1) ? Kb - 1 - step : step; }
+        SMG_DEV void next() {
+            ++gs;
+            if (++step == Kb) {
+                step = 0;
+                ++sweep;
+            }
+        }
     };
 
     if (warp == kSolveWarps) {
         // ---- factor slabs: one bulk copy (TMA engine) per step
         if (lane == 0) {
-            for (int gs = 0; gs < total; ++gs) {
-                const int sweep = gs / Kb, k = block_of(gs), sl = gs % NSF;
+            for (Cursor cu{0, 0, 0, Kb}; cu.gs < total; cu.next()) {
+                const int gs = cu.gs, sl = gs % NSF;
                 if (gs >= NSF) mbar_wait(&consF[sl], ((gs - NSF) / NSF) & 1);
-                const double* F = ((sweep & 1) ? Fbwd : Ffwd) + (int64_t)k * slab;
+                const double* F = ((cu.sweep & 1) ? Fbwd : Ffwd) + (int64_t)cu.k() * slab;
                 mbar_arrive_expect_tx(&fullF[sl], (uint32_t)(2 * W * FS * 8));
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 bulk_g2s(Fs(sl), F, 2 * W * FS * 8, &fullF[sl]);
@@ -303,21 +312,23 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
         constexpr int CCH = CS / 2;                              // 16-byte chunks per row
         constexpr int PER = (W * CCH + NT_RHS - 1) / NT_RHS;     // chunks per thread per step
         int pn[PER];                                             // next step's source rows (perm prefetch)
-        auto src_rows = [&](int gs, int (&rows)[PER]) {
-            const int k = block_of(gs), sweep = gs / Kb;
+        auto src_rows = [&](const Cursor& c, int (&rows)[PER]) {
+            const int k = c.k(), sweep = c.sweep;
 #pragma unroll
             for (int i = 0; i < PER; ++i) {
                 const int e = rt + i * NT_RHS, r = e / CCH, prow = k * W + r;
                 rows[i] = (e < W * CCH && prow < n && sweep == 0 && perm) ? __ldg(perm + prow) : prow;
             }
         };
-        src_rows(0, pn);
-        for (int gs = 0; gs < total; ++gs) {
-            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs), sl = gs % NSR;
+        Cursor nx{0, 0, 0, Kb};
+        src_rows(nx, pn);
+        for (Cursor cu{0, 0, 0, Kb}; cu.gs < total; cu.next()) {
+            const int gs = cu.gs, sweep = cu.sweep, step = cu.step, k = cu.k(), sl = gs % NSR;
             int rows[PER];
 #pragma unroll
             for (int i = 0; i < PER; ++i) rows[i] = pn[i];
-            if (gs + 1 < total) src_rows(gs + 1, pn);  // overlaps the waits below
+            nx.next();
+            if (nx.gs < total) src_rows(nx, pn);  // overlaps the waits below
             if (gs >= NSR) mbar_wait(&consR[sl], ((gs - NSR) / NSR) & 1);
             if (step == 0 && gs > 0) {
                 // this sweep reads the previous sweep's rows: all of its steps are done
@@ -348,20 +359,22 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     } else {
         double acc[TL::MT][TL::NT][2];
         // the independent half of step gs (waits for the step's slab and rhs block)
-        auto first = [&](int gs) {
+        auto first = [&](int gs, int sweep) {
             mbar_wait(&fullR[gs % NSR], (gs / NSR) & 1);
             mbar_wait(&fullF[gs % NSF], (gs / NSF) & 1);
 #ifndef SMG_SOLVE_NO_MMA
-            if (((gs / Kb) & 1) == 0) mma_step<W, CS, true>(Fs(gs % NSF), Rs(gs % NSR), nullptr, acc, warp, g, t, 1);
+            if ((sweep & 1) == 0) mma_step<W, CS, true>(Fs(gs % NSF), Rs(gs % NSR), nullptr, acc, warp, g, t, 1);
             else mma_step<W, CS, false>(Fs(gs % NSF), Rs(gs % NSR), nullptr, acc, warp, g, t, 1);
 #else
             for (int i = 0; i < TL::MT; ++i)
                 for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Rs(gs % NSR)[tid];
 #endif
         };
-        first(0);
-        for (int gs = 0; gs < total; ++gs) {
-            const int sweep = gs / Kb, step = gs % Kb, k = block_of(gs);
+        first(0, 0);
+        Cursor nx{0, 0, 0, Kb};
+        for (Cursor cu{0, 0, 0, Kb}; cu.gs < total; cu.next()) {
+            const int gs = cu.gs, sweep = cu.sweep, step = cu.step, k = cu.k();
+            nx.next();
             const int sf = gs % NSF, sr = gs % NSR;
             const bool last = sweep == sweeps - 1;
             // output rows of the last sweep go through the permutation: fetch them
@@ -422,7 +435,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive_local(&consR[sr]);
             }
-            if (gs + 1 < total) first(gs + 1);  // off the critical path: before the barrier
+            if (nx.gs < total) first(nx.gs, nx.sweep);  // off the critical path: before the barrier
             mma_bar();  // ycur complete before the next step reads it; yprev free for reuse
         }
     }

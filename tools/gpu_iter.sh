@@ -6,7 +6,7 @@ T=${1:-x}
 make -s all tools >/dev/null 2>&1 || { echo build failed; exit 1; }
 {
 for W in 32 64; do
-  for v in solve_bench solve_bench_nomma solve_bench_norhs solve_bench_f3r4 solve_bench_nomma_ns5; do
+  for v in solve_bench solve_bench_nomma; do
     echo -n "$v: "; build/$v 32 200 20 $W 1
   done
 done
