@@ -184,7 +184,7 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
     }
     return;
 second:
-#pragma unroll 2
+#pragma unroll
     for (int kk = W; kk < 2 * W; kk += 4) {
         double a[MT], b[NT];
 #pragma unroll
