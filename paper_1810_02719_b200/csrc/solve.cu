@@ -156,8 +156,11 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
         // one row tile: its nonzero k range is a loop bound
         const int r = TL::tile(wm, 0);
         const int k0 = FWD ? 0 : 8 * r, k1 = FWD ? 8 * r + 8 : W;
-#pragma unroll 2
-        for (int kk = k0; kk < k1; kk += 4) {
+        // fully unrolled over the block; the tile's zero k range is branched
+        // around (no DMMA issued), not predicated
+#pragma unroll
+        for (int kk = 0; kk < W; kk += 4) {
+            if (kk < k0 || kk >= k1) continue;
             double b[NT];
 #pragma unroll
             for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
