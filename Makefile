@@ -1,7 +1,7 @@
 # Builds libspecmesh_b200.so (sm_100a) in-tree and the oracle's C++ helpers.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr $(EXTRA)
 SRC_DIR := paper_1810_02719_b200/csrc
 OBJ_DIR := build/obj
 LIB := paper_1810_02719_b200/lib/libspecmesh_b200.so

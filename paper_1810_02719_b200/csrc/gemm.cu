@@ -30,11 +30,12 @@ constexpr int SPX = BK + 4;  // x-major slab row (k contiguous): 20 % 16 == 4, c
 // Shared-memory slab of one operand: BK x XW (k, x).  k-major operands (x
 // contiguous in global memory) are stored [k][x], x-major ones [x][k]; both
 // strides are 4 mod 16 doubles so fragment reads and stores avoid bank conflicts.
-template <int XW, bool KMAJOR>
+template <int XW, bool KMAJOR, int KB = BK>
 struct Slab {
-    static constexpr int S = KMAJOR ? XW + 4 : SPX;
-    static constexpr int ELEMS = KMAJOR ? BK * (XW + 4) : XW * SPX;
-    static constexpr int PER = XW * BK / NT;  // elements per thread
+    static constexpr int DEPTH = KB;
+    static constexpr int S = KMAJOR ? XW + 4 : KB + 4;
+    static constexpr int ELEMS = KMAJOR ? KB * (XW + 4) : XW * (KB + 4);
+    static constexpr int PER = XW * KB / NT;  // elements per thread
     double r[PER];
     SMG_DEV static double at(const double* s, int k, int x) { return KMAJOR ? s[k * S + x] : s[x * S + k]; }
     SMG_DEV static void coords(int e, int& k, int& x) {
@@ -42,8 +43,8 @@ struct Slab {
             k = e / XW;
             x = e % XW;
         } else {
-            k = e % BK;
-            x = e / BK;
+            k = e % KB;
+            x = e / KB;
         }
     }
     // element (k, x) lives at ptr[k*ld + x] (KMAJOR) or ptr[x*ld + k]
@@ -73,11 +74,12 @@ struct Slab {
 template <class SA, class SB, int NJ>
 SMG_DEV void slab_mma(const double* __restrict__ as, const double* __restrict__ bs, double (&acc)[4][NJ][2],
                       unsigned fmask, unsigned kFull, int k0, int kdiag, int upperB, int wm, int wn, int g, int t) {
-    if (fmask == kFull && k0 + BK <= kdiag) {
+    constexpr int KD = SA::DEPTH;
+    if (fmask == kFull && k0 + KD <= kdiag) {
             // interior: every fragment active, no predication; m16n8k8 (4x the
             // work per instruction of m8n8k4, same accumulator registers)
 #pragma unroll
-            for (int kk = 0; kk < BK; kk += 8) {
+            for (int kk = 0; kk < KD; kk += 8) {
                 double a[2][4], bb[NJ][2];
 #pragma unroll
                 for (int I = 0; I < 2; ++I) {
@@ -101,7 +103,7 @@ SMG_DEV void slab_mma(const double* __restrict__ as, const double* __restrict__ 
             }
         } else if (fmask != 0 && k0 < kdiag + 8 * NJ) {
 #pragma unroll
-            for (int kk = 0; kk < BK; kk += 4) {
+            for (int kk = 0; kk < KD; kk += 4) {
                 unsigned m = fmask;
                 if (upperB) {
 #pragma unroll
@@ -242,7 +244,16 @@ __global__ void __launch_bounds__(NT, 4) gemm_kernel(GemmParams p, int n_base, i
 // PNS-stage ring (completion on mbarriers), the four DMMA warps never have
 // loads in flight (no register staging, no long-scoreboard coupling of their
 // fragment reads to outstanding LDGSTS) and never meet at a CTA barrier.
+#ifndef SMG_GEMM_PNS
 constexpr int PNS = 3;
+#else
+constexpr int PNS = SMG_GEMM_PNS;
+#endif
+#ifndef SMG_GEMM_BKP
+constexpr int BKP = 16;  // k depth of a pipeline stage
+#else
+constexpr int BKP = SMG_GEMM_BKP;
+#endif
 constexpr int NT_P = NT + 32;
 
 SMG_DEV uint32_t g_smem_u32(const void* ptr) { return static_cast<uint32_t>(__cvta_generic_to_shared(ptr)); }
@@ -266,9 +277,9 @@ SMG_DEV void g_mbar_wait(uint64_t* bar, uint32_t parity) {
 template <int XW, bool KMAJOR>
 SMG_DEV void issue_slab(double* sl, const double* __restrict__ ptr, int64_t ld, int k0, int x0, int kmax, int xmax,
                         int lane) {
-    using SL = Slab<XW, KMAJOR>;
-    constexpr int CH = KMAJOR ? XW / 2 : BK / 2;  // chunks per smem row
-    constexpr int NCH = XW * BK / 2;
+    using SL = Slab<XW, KMAJOR, BKP>;
+    constexpr int CH = KMAJOR ? XW / 2 : BKP / 2;  // chunks per smem row
+    constexpr int NCH = XW * BKP / 2;
     for (int c = lane; c < NCH; c += 32) {
         int k, x;
         if (KMAJOR) {
@@ -299,8 +310,8 @@ SMG_DEV void issue_slab(double* sl, const double* __restrict__ ptr, int64_t ld, 
 template <bool TA, bool TB, int NJ>
 __global__ void __launch_bounds__(NT_P) gemm_pipe_kernel(GemmParams p, int n_base, int n_end) {
     constexpr int BN = 16 * NJ;
-    using SA = Slab<BM, TA>;
-    using SB = Slab<BN, !TB>;
+    using SA = Slab<BM, TA, BKP>;
+    using SB = Slab<BN, !TB, BKP>;
     const int splits = p.splits > 0 ? p.splits : 1;
     const int b = blockIdx.z / splits;
     const int s = blockIdx.z % splits;
@@ -313,10 +324,10 @@ __global__ void __launch_bounds__(NT_P) gemm_pipe_kernel(GemmParams p, int n_bas
 
     int kEnd = K;
     if (p.upperB) kEnd = min(kEnd, n0 + BN);
-    const int kchunk = ((kEnd + splits - 1) / splits + BK - 1) / BK * BK;
+    const int kchunk = ((kEnd + splits - 1) / splits + BKP - 1) / BKP * BKP;
     const int kBeg = s * kchunk;
     const int kStop = min(kEnd, kBeg + kchunk);
-    const int nsteps = kStop > kBeg ? (kStop - kBeg + BK - 1) / BK : 0;
+    const int nsteps = kStop > kBeg ? (kStop - kBeg + BKP - 1) / BKP : 0;
 
     const double* A = p.A + (int64_t)b * p.strideA;
     const double* B = p.B + (int64_t)b * p.strideB;
@@ -338,7 +349,7 @@ __global__ void __launch_bounds__(NT_P) gemm_pipe_kernel(GemmParams p, int n_bas
         uint32_t cph[PNS];
         for (int i = 0; i < PNS; ++i) cph[i] = 0u;
         for (int ks = 0; ks < nsteps; ++ks) {
-            const int st = ks % PNS, k0 = kBeg + ks * BK;
+            const int st = ks % PNS, k0 = kBeg + ks * BKP;
             if (ks >= PNS) {
                 g_mbar_wait(&consumed[st], cph[st]);
                 cph[st] ^= 1u;
@@ -376,7 +387,7 @@ __global__ void __launch_bounds__(NT_P) gemm_pipe_kernel(GemmParams p, int n_bas
     uint32_t fph[PNS];
     for (int i = 0; i < PNS; ++i) fph[i] = 0u;
     for (int ks = 0; ks < nsteps; ++ks) {
-        const int st = ks % PNS, k0 = kBeg + ks * BK;
+        const int st = ks % PNS, k0 = kBeg + ks * BKP;
         g_mbar_wait(&full[st], fph[st]);
         fph[st] ^= 1u;
         slab_mma<SA, SB, NJ>(As + st * SA::ELEMS, Bs + st * SB::ELEMS, acc, fmask, kFull, k0, kdiag, p.upperB, wm, wn,
@@ -445,8 +456,8 @@ void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
     const bool aligned = al(p.A) && al(p.B) && !(p.lda & 1) && !(p.ldb & 1) && !(p.strideA & 1) && !(p.strideB & 1) &&
                          !(n_base & 1) && !std::getenv("SMG_GEMM_NOPIPE");
     if (aligned) {
-        using SA = Slab<BM, TA>;
-        using SB = Slab<BN, !TB>;
+        using SA = Slab<BM, TA, BKP>;
+        using SB = Slab<BN, !TB, BKP>;
         const int bytes = PNS * (SA::ELEMS + SB::ELEMS) * 8;
         static bool configured = false;
         if (!configured) {
