@@ -315,8 +315,11 @@ __global__ void __launch_bounds__(1024) cheb_bin_kernel(ChebParams p) {
         for (int q = rp[i]; q < rp[i + 1]; ++q)
             if (cols[q] == i) dg[i] = vals[q] + shift;
     const double* X = p.X + (int64_t)b * p.strideX;
+    // iterates column-major within the slice ([u][row]): the q-th neighbours of
+    // consecutive rows are consecutive rows on a structured tile, so a warp's
+    // reads of one column hit consecutive banks
     for (int e = threadIdx.x; e < n * CSL; e += blockDim.x) {
-        const int i = e / CSL, j = col0 + e % CSL;
+        const int u = e / n, i = e % n, j = col0 + u;
         cbuf[e] = j < p.c ? X[(int64_t)i * p.ldx + j] : 0.0;
     }
     __syncthreads();
@@ -333,15 +336,14 @@ __global__ void __launch_bounds__(1024) cheb_bin_kernel(ChebParams p) {
             for (int q = rp[i]; q < rp[i + 1]; ++q) {
                 const int col = cl[q];
                 const double v = col == i ? di : -1.0;
-                const double* xr = xc + (int64_t)col * CSL;
 #pragma unroll
-                for (int u = 0; u < CSL; ++u) acc[u] = fma(v, xr[u], acc[u]);
+                for (int u = 0; u < CSL; ++u) acc[u] = fma(v, xc[u * n + col], acc[u]);
             }
 #pragma unroll
             for (int u = 0; u < CSL; ++u) {
                 double a = acc[u] * alpha;
-                if (step > 1) a = fma(gam, xo[(int64_t)i * CSL + u], a);
-                xo[(int64_t)i * CSL + u] = a;
+                if (step > 1) a = fma(gam, xo[u * n + i], a);
+                xo[u * n + i] = a;
             }
         }
         __syncthreads();
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(1024) cheb_bin_kernel(ChebParams p) {
     const double* res = cbuf + (p.deg & 1) * half;
     double* Y = p.Y + (int64_t)b * p.strideY;
     for (int e = threadIdx.x; e < n * CSL; e += blockDim.x) {
-        const int i = e / CSL, j = col0 + e % CSL;
+        const int u = e / n, i = e % n, j = col0 + u;
         if (j < p.c) Y[(int64_t)i * p.ldy + j] = res[e];
     }
 }
