@@ -33,7 +33,7 @@ struct FactorSmem {
     static constexpr int LD = W + 4;  // LD % 16 == 4: conflict-free DMMA fragment reads
     static constexpr int MAT = W * LD;
     static int bytes(int n, int cpl, bool permuted) {
-        return (3 * MAT + 4 * W + 32) * 8 + (permuted ? ((n + 1) & ~1) * 4 : 0) + W * cpl * (8 + 4) + W * 4;
+        return (3 * MAT + 5 * W + 32) * 8 + (permuted ? ((n + 1) & ~1) * 4 : 0) + W * cpl * (8 + 4) + W * 4;
     }
 };
 
@@ -84,9 +84,10 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
     double* sigp = sig + W;      // Sigma_{k-1}
     double* piv = sigp + W;      // pivots of the current block
     double* rsc = piv + W;       // 1 / (l_jj sigma_j)
-    int* flag = reinterpret_cast<int*>(rsc + W);
+    double* rdv = rsc + W;       // pivot reciprocals, published by the diagonal's owner
+    int* flag = reinterpret_cast<int*>(rdv + W);
     const int CPL = p.cpl;
-    int* ipos = reinterpret_cast<int*>(rsc + W + 32);                                  // RCM only
+    int* ipos = reinterpret_cast<int*>(rdv + W + 32);                                  // RCM only
     double* cval = reinterpret_cast<double*>(ipos + (p.perm ? ((p.n + 1) & ~1) : 0));  // [W][CPL]
     int* cidx = reinterpret_cast<int*>(cval + W * CPL);                                // [W][CPL]
     int* ccnt = cidx + W * CPL;                                                        // [W]
@@ -214,17 +215,24 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
         // ---- signed Cholesky S = L Sigma L^T, right-looking in LDL^T form on the
         // upper triangle (row j is read contiguously): every thread updates the
         // elements it owns, one barrier per column; pivots kept, rows scaled at the end
+        // 1 / d of column j + 1 is computed once, by the owner of that diagonal
+        // element right after its last update, and read by everyone after the
+        // barrier (a double division per thread per column dominated the loop)
+        const double rd0 = 1.0 / S[0];
         for (int j = 0; j < W; ++j) {
             const double d = S[j * LD + j];
             if (tid == 0) {
                 if (!(d != 0.0) || !isfinite(d)) flag[0] = 1;
                 piv[j] = d;
             }
-            const double rd = 1.0 / d;
+            const double rd = j == 0 ? rd0 : rdv[j];
 #pragma unroll
             for (int q = 0; q < NOWN; ++q) {
                 const int a = own_a[q], b = own_b[q];
-                if (q < nown && a > j) S[a * LD + b] = fma(-S[j * LD + a] * rd, S[j * LD + b], S[a * LD + b]);
+                if (q < nown && a > j) {
+                    S[a * LD + b] = fma(-S[j * LD + a] * rd, S[j * LD + b], S[a * LD + b]);
+                    if (a == j + 1 && b == a) rdv[a] = 1.0 / S[a * LD + a];
+                }
             }
             __syncthreads();
         }
@@ -235,8 +243,12 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
             const int a = own_a[q], b = own_b[q];
             const double d = piv[a];
             const double la = sqrt(fabs(d));
-            if (a == b) S[a * LD + a] = la;
-            else S[b * LD + a] = S[a * LD + b] / (la * (d < 0.0 ? -1.0 : 1.0));
+            if (a == b) {
+                S[a * LD + a] = la;
+                rdv[a] = 1.0 / la;  // 1 / l_aa for the inverse below (after the next barrier)
+            } else {
+                S[b * LD + a] = S[a * LD + b] / (la * (d < 0.0 ? -1.0 : 1.0));
+            }
         }
         for (int e = tid; e < W; e += NT) {
             sig[e] = piv[e] < 0.0 ? -1.0 : 1.0;
@@ -250,7 +262,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
 #pragma unroll
             for (int q = 0; q < NOWN; ++q) xacc[q] = (q < nown && own_a[q] == own_b[q]) ? 1.0 : 0.0;
             for (int i = 0; i < W; ++i) {
-                const double rii = 1.0 / S[i * LD + i];
+                const double rii = rdv[i];
 #pragma unroll
                 for (int q = 0; q < NOWN; ++q)
                     if (q < nown && own_b[q] == i) Lc[i * LD + own_a[q]] = xacc[q] * rii;
