@@ -308,7 +308,7 @@ SMG_DEV void issue_slab(double* sl, const double* __restrict__ ptr, int64_t ld, 
 }
 
 template <bool TA, bool TB, int NJ>
-__global__ void __launch_bounds__(NT_P) gemm_pipe_kernel(GemmParams p, int n_base, int n_end) {
+__global__ void __launch_bounds__(NT_P, 4) gemm_pipe_kernel(GemmParams p, int n_base, int n_end) {
     constexpr int BN = 16 * NJ;
     using SA = Slab<BM, TA, BKP>;
     using SB = Slab<BN, !TB, BKP>;
