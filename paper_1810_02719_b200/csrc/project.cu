@@ -11,10 +11,11 @@
 //    X^ = Q~ (Q~^T X), rms = sqrt(||X - X^||_F^2 / (3 n)).
 //  * projection_residual (spectral.hpp:216-220): e = s - Q~ (Q~^T s), s = x+y+z,
 //    the DOI control signal, and ||e||.
-// Pass 1 (per row chunk, threads over columns, coalesced rows of Q) produces
-// partial column maxima and partial Q^T [X | s]; pass 2 reduces them in chunk
-// order (deterministic); pass 3 (warp per row) rebuilds X^ and e; pass 4 sums
-// the per-CTA residual partials in a fixed order.
+// Pass 1 (per row chunk, threads over column pairs, coalesced rows of Q)
+// produces partial column maxima and partial Q^T [X | s]; pass 2 reduces them
+// in a fixed order (32 columns x 8 contiguous chunk ranges per CTA); pass 3
+// (thread = column part x 4 rows) rebuilds X^ and e and the chain's last CTA
+// sums the residual partials in block order.  Deterministic.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -29,47 +30,6 @@ constexpr int RPT = 4;     // rows per recon thread (coefficients reused across 
 constexpr int RROWS = (PNT / 8) * RPT;  // rows per recon CTA
 
 // partial record per (chunk, column): best |q|, its q, Px, Py, Pz, Ps (8 doubles, 64 B)
-SMG_DEV void reduce_block(const ProjParams& p, int b) {
-    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
-    const double* part = p.partial + (int64_t)b * p.nchunks * (int64_t)p.c_cap * 8;
-    double* coef = p.coeff + (int64_t)b * p.strideCoef;  // c x 4: Px Py Pz Ps (unsigned)
-    double* sign = p.sign + (int64_t)b * p.strideSign;
-    for (int j = threadIdx.x; j < c; j += QNT) {
-        double best = -1.0, bval = 0.0;
-        double px = 0.0, py = 0.0, pz = 0.0, ps = 0.0;
-        // chunks in row order: strict > keeps the first index; loads of 4 chunks
-        // are issued before they are combined
-        for (int ch0 = 0; ch0 < p.nchunks; ch0 += 4) {
-            double4 h[4], d[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (ch0 + u < p.nchunks) {
-                    const double4* o = reinterpret_cast<const double4*>(part + ((int64_t)(ch0 + u) * p.c_cap + j) * 8);
-                    h[u] = o[0];
-                    d[u] = o[1];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (ch0 + u >= p.nchunks) break;
-                if (h[u].x > best) {
-                    best = h[u].x;
-                    bval = h[u].y;
-                }
-                px += h[u].z;
-                py += h[u].w;
-                pz += d[u].x;
-                ps += d[u].y;
-            }
-        }
-        sign[j] = bval < 0.0 ? -1.0 : 1.0;
-        coef[4 * j + 0] = px;
-        coef[4 * j + 1] = py;
-        coef[4 * j + 2] = pz;
-        coef[4 * j + 3] = ps;
-    }
-}
-
 // one double2 (two adjacent columns) per thread and row: a warp reads 512
 // contiguous bytes of a row; 32-row chunks give every chain (n / 32) CTAs
 __global__ void __launch_bounds__(QNT) partial_kernel(ProjParams p) {
@@ -117,16 +77,70 @@ __global__ void __launch_bounds__(QNT) partial_kernel(ProjParams p) {
             o[3] = make_double4(pz1, ps1, 0.0, 0.0);
         }
     }
-    // the last chunk CTA of a chain reduces the chunks in order (deterministic)
-    __shared__ bool last;
-    __threadfence();
+}
+
+// chunk records -> coefficients and signs: CTA = 32 columns x 8 parts; part q
+// combines a contiguous range of chunks in order, then part 0 combines the 8
+// part results in order (the first index still wins the argmax; fixed order,
+// deterministic).  Replaces one last-arriving CTA reducing every column of a
+// chain, which serialised ~nchunks * c records through a single SM.
+constexpr int RCOL = 32, RPART = 8;
+__global__ void __launch_bounds__(RCOL * RPART) chunk_reduce_kernel(ProjParams p) {
+    __shared__ double4 ph[RPART][RCOL], pd[RPART][RCOL];
+    const int b = blockIdx.y;
+    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    const int jj = threadIdx.x % RCOL, part = threadIdx.x / RCOL;
+    const int j = blockIdx.x * RCOL + jj;
+    const int n0 = (int)((int64_t)p.nchunks * part / RPART), n1 = (int)((int64_t)p.nchunks * (part + 1) / RPART);
+    double best = -1.0, bval = 0.0, px = 0.0, py = 0.0, pz = 0.0, ps = 0.0;
+    if (j < c) {
+        const double* part_b = p.partial + (int64_t)b * p.nchunks * (int64_t)p.c_cap * 8;
+        for (int ch0 = n0; ch0 < n1; ch0 += 4) {
+            double4 h[4], d[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ch0 + u < n1) {
+                    const double4* o = reinterpret_cast<const double4*>(part_b + ((int64_t)(ch0 + u) * p.c_cap + j) * 8);
+                    h[u] = o[0];
+                    d[u] = o[1];
+                }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (ch0 + u >= n1) break;
+                if (h[u].x > best) {
+                    best = h[u].x;
+                    bval = h[u].y;
+                }
+                px += h[u].z;
+                py += h[u].w;
+                pz += d[u].x;
+                ps += d[u].y;
+            }
+        }
+    }
+    ph[part][jj] = make_double4(best, bval, px, py);
+    pd[part][jj] = make_double4(pz, ps, 0.0, 0.0);
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&p.counter[2 * b], 1) == (int)gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    reduce_block(p, b);
-    if (threadIdx.x == 0) p.counter[2 * b] = 0;
+    if (part != 0 || j >= c) return;
+    best = -1.0;
+    bval = px = py = pz = ps = 0.0;
+    for (int q = 0; q < RPART; ++q) {
+        const double4 h = ph[q][jj], d = pd[q][jj];
+        if (h.x > best) {
+            best = h.x;
+            bval = h.y;
+        }
+        px += h.z;
+        py += h.w;
+        pz += d.x;
+        ps += d.y;
+    }
+    double* coef = p.coeff + (int64_t)b * p.strideCoef;
+    p.sign[(int64_t)b * p.strideSign + j] = bval < 0.0 ? -1.0 : 1.0;
+    coef[4 * j + 0] = px;
+    coef[4 * j + 1] = py;
+    coef[4 * j + 2] = pz;
+    coef[4 * j + 3] = ps;
 }
 
 SMG_DEV void stats_block(const ProjParams& p, int b, int nblocks) {
@@ -253,6 +267,7 @@ void project(const ProjParams& p0, cudaStream_t st) {
     p.rows_per_chunk = RPC;
     p.nchunks = proj_chunks(p.n);
     ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), QNT, 0, st>>>(p);
+    ::smg::count_launch(), chunk_reduce_kernel<<<dim3((p.c_cap + RCOL - 1) / RCOL, p.batch), RCOL * RPART, 0, st>>>(p);
     const int nb = proj_recon_blocks(p.n, 0);
     ::smg::count_launch(), recon_kernel<<<dim3(nb, p.batch), PNT, 4 * (p.c_cap + 1) * sizeof(double), st>>>(p);
 }
