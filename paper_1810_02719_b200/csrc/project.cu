@@ -26,8 +26,8 @@ namespace {
 constexpr int PNT = 256;   // recon CTA: 8 column parts x 32 row groups of RPT rows
 constexpr int QNT = 128;   // partial CTA: two adjacent columns per thread
 constexpr int RPC = 32;    // rows per partial chunk
-constexpr int RPT = 4;     // rows per recon thread (coefficients reused across them)
-constexpr int RROWS = (PNT / 8) * RPT;  // rows per recon CTA
+// rows per recon thread: 4 (coefficients reused across them) when the batch
+// fills the GPU, 1 for a single chain (4x the CTAs)
 
 // partial record per (chunk, column): best |q|, its q, Px, Py, Pz, Ps (8 doubles, 64 B)
 // one double2 (two adjacent columns) per thread and row: a warp reads 512
@@ -160,7 +160,9 @@ SMG_DEV void stats_block(const ProjParams& p, int b, int nblocks) {
 // group of RPT rows): per column pair it loads the coefficients once from smem
 // and RPT double2 of Q (8 lanes of a part group cover 128 contiguous bytes of a
 // row); the 8 parts of a row group are 8 consecutive lanes, summed by shuffles.
+template <int RPT>
 __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
+    constexpr int RROWS = (PNT / 8) * RPT;
     __shared__ double red[2][PNT / 32];
     extern __shared__ __align__(16) double scoef[];  // c x 4, staged once per CTA
     const int b = blockIdx.y;
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
 }  // namespace
 
 int proj_chunks(int n) { return (n + RPC - 1) / RPC; }
-int proj_recon_blocks(int n, int /*rows_per_warp*/) { return (n + RROWS - 1) / RROWS; }
+int proj_recon_blocks(int n, int /*rows_per_warp*/) { return (n + PNT / 8 - 1) / (PNT / 8); }  // upper bound
 
 void project(const ProjParams& p0, cudaStream_t st) {
     ProjParams p = p0;
@@ -268,8 +270,14 @@ void project(const ProjParams& p0, cudaStream_t st) {
     p.nchunks = proj_chunks(p.n);
     ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), QNT, 0, st>>>(p);
     ::smg::count_launch(), chunk_reduce_kernel<<<dim3((p.c_cap + RCOL - 1) / RCOL, p.batch), RCOL * RPART, 0, st>>>(p);
-    const int nb = proj_recon_blocks(p.n, 0);
-    ::smg::count_launch(), recon_kernel<<<dim3(nb, p.batch), PNT, 4 * (p.c_cap + 1) * sizeof(double), st>>>(p);
+    const int smem = 4 * (p.c_cap + 1) * sizeof(double);
+    const int nb4 = (p.n + 4 * (PNT / 8) - 1) / (4 * (PNT / 8));
+    if ((int64_t)nb4 * p.batch >= 2 * 148) {
+        ::smg::count_launch(), recon_kernel<4><<<dim3(nb4, p.batch), PNT, smem, st>>>(p);
+    } else {
+        const int nb1 = (p.n + PNT / 8 - 1) / (PNT / 8);
+        ::smg::count_launch(), recon_kernel<1><<<dim3(nb1, p.batch), PNT, smem, st>>>(p);
+    }
 }
 
 }  // namespace smg
