@@ -150,3 +150,14 @@ def test_decode_errors(ctx):
         K.decompress_mesh(short, seg, ctx=ctx)
     with pytest.raises(G.InvalidArgument, match="quantization bits must be in"):
         K.compress_mesh(mesh, seg, K.CompressionConfig(gc, 17), ctx=ctx)
+
+
+def test_compression_forces_binary_weighting(ctx):
+    """compress_mesh always uses the binary Laplacian (compress.hpp:155-157): a
+    distance-weighted config gives the same stream."""
+    mesh, seg, _ = problem(seed=13, flip=4)
+    gb = G.PipelineConfig(weighting="binary", subspace_size=24, iterations=1, shift_scale=1e-3)
+    gd = G.PipelineConfig(weighting="distance", subspace_size=24, iterations=1, shift_scale=1e-3)
+    a = K.serialize_encoded_mesh(K.compress_mesh(mesh, seg, K.CompressionConfig(gb, 10), ctx=ctx))
+    b = K.serialize_encoded_mesh(K.compress_mesh(mesh, seg, K.CompressionConfig(gd, 10), ctx=ctx))
+    assert a == b

@@ -153,3 +153,19 @@ def test_frames_stage_device_pointers(ctx):
     torch.cuda.synchronize()
     for o, w in zip(outs, want):
         assert np.array_equal(o.cpu().numpy().reshape(3, -1).T, w)
+
+
+def test_denoise_dynamic_doi_bases(ctx):
+    """DOI-chosen per-block sizes (cfg.basis_mode = doi, no sizes): the frames
+    stage runs on the variable-c bases and equals the per-frame projection of
+    those bases."""
+    topo, frames = sequence(64, 64, 3, seed=19, flip=2)
+    seg = synth.grid_tiles(64, 64, 32, 32)
+    cfg = G.PipelineConfig(weighting="binary", basis_mode="doi", subspace_size=8, c_min=4, c_max=48,
+                           eps_low=2e-3, eps_high=2e-2, shift_scale=1e-3)
+    res = G.denoise_dynamic(frames, seg, cfg, ctx=ctx)
+    bb = G.compute_block_bases(frames[0], seg, cfg, want_bases=True, ctx=ctx)
+    want = G.coarse_reconstruct_frames(topo, seg, bb, [f.vertices for f in frames], ctx=ctx)
+    for got, w in zip(res.frames, want):
+        assert rel_err(got, w) < 1e-12
+    assert len({b.shape[1] for b in bb.bases}) >= 1
