@@ -101,8 +101,15 @@ __global__ void __launch_bounds__(JNT) jacobi_kernel(JacobiParams p, JacobiShape
             blkV[h][e] = (r == col) ? 1.0 : 0.0;
         }
     }
+    // max |H_rr| by a block reduction (max is order independent: same value as
+    // the serial loop every thread used to run)
+    double nm = 0.0;
+    for (int r = threadIdx.x; r < m; r += JNT) nm = fmax(nm, fabs(H[(int64_t)r * p.ldh + r]));
+    nm = warp_max(nm);
+    if (lane == 0) wmax[warp] = nm;
+    __syncthreads();
     double normmax = 0.0;
-    for (int r = 0; r < m; ++r) normmax = fmax(normmax, fabs(H[(int64_t)r * p.ldh + r]));
+    for (int w = 0; w < JWARPS; ++w) normmax = fmax(normmax, wmax[w]);
     const double tiny2 = (1e-15 * normmax) * (1e-15 * normmax) + 1e-300;
     __syncthreads();
 
