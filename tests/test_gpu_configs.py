@@ -30,9 +30,14 @@ def test_config_end_to_end(ctx, name):
     check_parity(w.mesh, bb, ob)
 
 
-def test_config5_shard_prefix_matches_oracle(ctx):
+@pytest.mark.parametrize("env", [{}, {"SMG_SOLVE_CS": "32", "SMG_ORDERING": "geometric"}])
+def test_config5_shard_prefix_matches_oracle(ctx, monkeypatch, env):
     """First 6 tiles of two C5 meshes (n_d = 2048, c = 200, first basis from the
-    GPU subspace iteration) against the oracle's dense-eigendecomposition chain."""
+    GPU subspace iteration) against the oracle's dense-eigendecomposition chain.
+    The second variant forces the kernels the 64-mesh benchmark runs (geometric
+    ordering: W = 32; 32-column solve slices)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     T = 6
     ws = [synth.config("C5", mesh_index=i) for i in (0, 1)]
     seg = synth.Segmentation(ws[0].seg.members[:T], np.arange(T, dtype=np.int32))
