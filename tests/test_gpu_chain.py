@@ -151,17 +151,21 @@ def test_doi_chain_decisions_match(ctx):
         assert abs(g.doi_residual - o.doi_residual) <= 1e-6 * o.doi_residual
 
 
-def test_batched_chains_equal_single_chains(ctx):
+@pytest.mark.parametrize("nchains,sizes", [(3, None), (5, [60, 80, 80, 70])])
+def test_batched_chains_equal_single_chains(ctx, nchains, sizes):
     """smg_run_chains (config 5's per-GPU shard) matches running each chain
     alone.  Chains are independent and every reduction has a fixed order; the
     first-submesh subspace iteration runs as many rounds as the slowest chain of
-    the batch needs, so agreement is to the first-basis tolerance, not bitwise."""
-    meshes = [synth.small_grid(128, 64, 64, 32, seed=s, flip=s) for s in (1, 2, 3)]
+    the batch needs, so agreement is to the first-basis tolerance, not bitwise.
+    Five chains run as two chain groups on their own streams (with a growth at
+    position 1: each group re-signs its share of the first basis)."""
+    meshes = [synth.small_grid(128, 64, 64, 32, seed=s, flip=s) for s in range(1, nchains + 1)]
     seg = synth.grid_tiles(128, 64, 64, 32)
+    sizes = sizes or [80] * seg.count
     cfg = G.PipelineConfig(weighting="binary", subspace_size=80, iterations=1, shift_scale=1e-3)
-    batch = G.run_chains(meshes, [seg] * 3, cfg, [80] * seg.count, ctx=ctx)
+    batch = G.run_chains(meshes, [seg] * nchains, cfg, sizes, ctx=ctx)
     for m, b in zip(meshes, batch):
-        single = G.compute_block_bases_fixed_sizes(m, seg, cfg, [80] * seg.count, ctx=ctx)
+        single = G.compute_block_bases_fixed_sizes(m, seg, cfg, sizes, ctx=ctx)
         r = single.reconstruction
         assert np.linalg.norm(b.reconstruction - r, axis=1).max() <= 1e-10 * np.linalg.norm(r, axis=1).max()
         for i in range(seg.count):
