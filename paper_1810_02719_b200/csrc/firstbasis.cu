@@ -296,7 +296,7 @@ FirstBasisReport first_basis_impl(const StepCtx& cx, Workspace& ws, const TileSe
         jp.sweeps = sweeps.get();
         // the bootstrap round only plans the Chebyshev filter (interval ends, rate);
         // the filter input needs the span, not converged Ritz vectors
-        if (round == 0 && use_cheb && c < m) {
+        if (round == 0 && use_cheb && c < m && m < n) {  // (m == n: this Rayleigh-Ritz is exact and final)
             jp.max_sweeps = 2;  // the Ritz values only plan the filter (interval ends, rate)
             if (const char* e = std::getenv("SMG_FB_BOOT_SWEEPS")) jp.max_sweeps = std::max(1, std::atoi(e));
         }

@@ -184,3 +184,23 @@ def test_fused_chebyshev_filter_bit_identical(ctx, monkeypatch):
     for a, b in zip(fused.bases, plain.bases):
         assert np.array_equal(a, b)
     assert np.array_equal(fused.reconstruction, plain.reconstruction)
+
+
+@pytest.mark.parametrize("tw,th,c", [(4, 4, 16), (4, 4, 1), (4, 4, 4), (8, 4, 5), (2, 2, 2), (2, 2, 4)])
+def test_tiny_tiles_and_full_bases(ctx, tw, th, c):
+    """Edge sizes: 4- and 16-vertex tiles, c = 1 and c = n_d (the basis spans
+    the whole block, so the reconstruction is exact).  When the first-basis
+    subspace is the whole block its single Rayleigh-Ritz is final (not a
+    2-sweep bootstrap).  (A 2x2 tile has eigenvalues 0, 2, 4, 4: c = 3 would cut
+    a degenerate pair, where no basis is determined.)"""
+    W, H = 4 * tw, 2 * th
+    mesh = synth.small_grid(W, H, tw, th, seed=5, flip=3)
+    seg = synth.grid_tiles(W, H, tw, th)
+    bb, ob = run_both(ctx, mesh, seg, c)
+    if c < tw * th:
+        check_parity(mesh, bb, ob)
+        return
+    for i in range(seg.count):
+        assert O.max_principal_angle(bb.bases[i], ob.bases[i]) < 1e-8
+        assert bb.stats[i].residual_rms <= 1e-12 * np.abs(mesh.vertices).max()
+    assert np.abs(bb.reconstruction - mesh.vertices).max() <= 1e-11 * np.abs(mesh.vertices).max()
