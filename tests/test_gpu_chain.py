@@ -186,7 +186,8 @@ def test_fused_chebyshev_filter_bit_identical(ctx, monkeypatch):
     assert np.array_equal(fused.reconstruction, plain.reconstruction)
 
 
-@pytest.mark.parametrize("tw,th,c", [(4, 4, 16), (4, 4, 1), (4, 4, 4), (8, 4, 5), (2, 2, 2), (2, 2, 4)])
+@pytest.mark.parametrize("tw,th,c", [(4, 4, 16), (4, 4, 1), (4, 4, 4), (8, 4, 5), (2, 2, 2), (2, 2, 4), (5, 5, 7),
+                                     (40, 4, 20), (6, 8, 48), (48, 8, 64)])
 def test_tiny_tiles_and_full_bases(ctx, tw, th, c):
     """Edge sizes: 4- and 16-vertex tiles, c = 1 and c = n_d (the basis spans
     the whole block, so the reconstruction is exact).  When the first-basis
@@ -204,3 +205,17 @@ def test_tiny_tiles_and_full_bases(ctx, tw, th, c):
         assert O.max_principal_angle(bb.bases[i], ob.bases[i]) < 1e-8
         assert bb.stats[i].residual_rms <= 1e-12 * np.abs(mesh.vertices).max()
     assert np.abs(bb.reconstruction - mesh.vertices).max() <= 1e-11 * np.abs(mesh.vertices).max()
+
+
+def test_chain_distance_weighting(ctx):
+    """The reference's default weighting (1 / |v_i - v_j|^2 off the diagonal,
+    spectral.hpp:48-59): chain parity against the oracle (first basis through
+    the per-step SpMM filter, not the binary-pattern fused one)."""
+    mesh = synth.small_grid(64, 64, 32, 32, seed=9, flip=6)
+    seg = synth.grid_tiles(64, 64, 32, 32)
+    subs = O.build_submeshes(mesh.adj_offsets, mesh.adj_cols, seg.members)
+    cfg = G.PipelineConfig(weighting="distance", subspace_size=40, iterations=1, shift_scale=1e-3)
+    ocfg = O.PipelineConfig(weighting=O.DISTANCE, subspace_size=40, iterations=1, shift_scale=1e-3)
+    bb = G.compute_block_bases_fixed_sizes(mesh, seg, cfg, [40] * seg.count, want_bases=True, ctx=ctx)
+    ob = O.compute_block_bases_fixed_sizes(mesh.vertices, subs, seg.sequence, ocfg, [40] * seg.count)
+    check_parity(mesh, bb, ob)
