@@ -30,6 +30,7 @@ def check(v, f, gp, op, tol=1e-12):
 
 
 @pytest.mark.parametrize("kw", [{}, {"sigma_spatial": 1.5}, {"ring_depth": 2, "normal_iterations": 3},
+                                {"ring_depth": 3, "normal_iterations": 2, "vertex_iterations": 3},
                                 {"sigma_range": 0.2, "vertex_iterations": 4}])
 def test_fine_denoise_grid(ctx, kw):
     v, f = noisy_grid()

@@ -169,3 +169,13 @@ def test_denoise_dynamic_doi_bases(ctx):
     for got, w in zip(res.frames, want):
         assert rel_err(got, w) < 1e-12
     assert len({b.shape[1] for b in bb.bases}) >= 1
+
+
+def test_denoise_dynamic_single_frame_equals_chain(ctx):
+    """One frame: denoise_dynamic is the coarse pass of that frame."""
+    topo, frames = sequence(64, 64, 1, seed=23, flip=5)
+    seg = synth.grid_tiles(64, 64, 32, 32)
+    cfg = G.PipelineConfig(weighting="binary", subspace_size=30, iterations=1, shift_scale=1e-3)
+    res = G.denoise_dynamic(frames, seg, cfg, [30] * seg.count, ctx=ctx)
+    bb = G.compute_block_bases_fixed_sizes(frames[0], seg, cfg, [30] * seg.count, ctx=ctx)
+    assert rel_err(res.frames[0], bb.reconstruction) < 1e-12
