@@ -134,13 +134,19 @@ def test_chain_grows_at_position_one(ctx):
     check_parity(mesh, bb, ob)
 
 
-def test_doi_chain_decisions_match(ctx):
+@pytest.mark.parametrize("kw", [
+    dict(subspace_size=60, c_min=10, c_max=200, eps_low=2e-3, eps_high=2e-2, shift_scale=1e-3),
+    # c pinned (c_min = c_max): no adjustment possible, blocks above the band end unconverged
+    dict(subspace_size=30, c_min=30, c_max=30, eps_low=1e-4, eps_high=1e-3, shift_scale=1e-3),
+    # a band above every residual: every block shrinks towards c_min
+    dict(subspace_size=40, c_min=20, c_max=60, eps_low=0.5, eps_high=0.9, shift_scale=1e-3),
+])
+def test_doi_chain_decisions_match(ctx, kw):
     """DOI chain with a band each block meets in a few steps: per-block c,
     iteration count and convergence flags equal the oracle's."""
     mesh = synth.small_grid(128, 64, 32, 32, seed=4, flip=8)
     seg = synth.grid_tiles(128, 64, 32, 32)
     subs = O.build_submeshes(mesh.adj_offsets, mesh.adj_cols, seg.members)
-    kw = dict(subspace_size=60, c_min=10, c_max=200, eps_low=2e-3, eps_high=2e-2, shift_scale=1e-3)
     cfg = G.PipelineConfig(weighting="binary", basis_mode="doi", **kw)
     ocfg = O.PipelineConfig(weighting=O.BINARY, **kw)
     bb = G.compute_block_bases(mesh, seg, cfg, want_bases=True, ctx=ctx)
