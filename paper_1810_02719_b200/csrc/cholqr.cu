@@ -18,6 +18,8 @@
 // the trailing SYRK are 32x32x32 DMMA blocks on all warps; finally the block
 // upper-triangular inverse X = R~^-1 is formed by block back-substitution
 // (DMMA) and stored row-scaled as B = D^-1 X.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -60,6 +62,21 @@ SMG_DEV void warp_block_mma(double (&acc)[4][4][2], FA a, FB b, int g, int t) {
     }
 }
 
+// cluster helpers (a launch without clusters is a cluster of one CTA)
+SMG_DEV unsigned cl_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+SMG_DEV unsigned cl_size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
+    return r;
+}
+SMG_DEV void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 SMG_DEV void zero_acc(double (&acc)[4][4][2]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -97,7 +114,11 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     __shared__ double rinvd[32];  // 1 / r_ii of the current diagonal block
     __shared__ int fail;
     extern __shared__ __align__(16) double psm[];
-    const int b = blockIdx.x;
+    // single chains run on a cluster of CL CTAs: every CTA repeats the serial
+    // diagonal-block phases (identical results), the panel row and the trailing
+    // update -- the c^3 work -- are split over the cluster through global A
+    const int CL = (int)cl_size(), rank = (int)cl_rank();
+    const int b = blockIdx.x / CL;
     if (p.status[b] != kOk) return;  // sticky first error of this chain
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const int P = (c + 31) / 32, cp = P * 32;
@@ -187,12 +208,13 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     DiagOwn own;
     own.init(tid);
     __syncthreads();
+    if (CL > 1) cl_sync();  // every CTA's copy of A is written before any update
     SMG_CHOL_T(1);
 
     for (int pb = 0; pb < P; ++pb) {
         const int p0 = pb * 32;
         for (int r = warp; r < 32; r += CW)
-            for (int k = p0 + lane; k < cp; k += 32) Ps[r * PS + k] = A[(int64_t)(p0 + r) * lda + k];
+            for (int k = p0 + lane; k < cp; k += 32) Ps[r * PS + k] = __ldcg(A + (int64_t)(p0 + r) * lda + k);
         __syncthreads();
         SMG_CHOL_T(2 + pb * 5);
         // ---- (a) factor the diagonal block with all threads (right-looking, LDL^T
@@ -266,7 +288,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         __syncthreads();
         SMG_CHOL_T(4 + pb * 5);
         // ---- (b) panel row R_{p,q} = X^T A_{p,q}, q > p (smem operands, written back to smem and L2)
-        for (int q = pb + 1 + warp; q < P; q += CW) {
+        for (int q = pb + 1 + rank + CL * warp; q < P; q += CL * CW) {
             const int q0 = q * 32;
             double acc[4][4][2];
             zero_acc(acc);
@@ -292,11 +314,21 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             for (int k = lane; k < p0; k += 32) Bo[(int64_t)(p0 + r) * ldb + k] = 0.0;
         }
         __syncthreads();
+        if (CL > 1 && pb + 1 < P) {
+            // the panel row blocks the other CTAs computed, through L2
+            cl_sync();
+            for (int q = pb + 1; q < P; ++q) {
+                if ((q - pb - 1) % CL == rank) continue;
+                for (int r = warp; r < 32; r += CW)
+                    Ps[r * PS + q * 32 + lane] = __ldcg(A + (int64_t)(p0 + r) * lda + q * 32 + lane);
+            }
+            __syncthreads();
+        }
         SMG_CHOL_T(5 + pb * 5);
         // ---- (c) trailing update A_{q,r} -= R_{p,q}^T R_{p,r}, p < q <= r
         const int rem = P - pb - 1;
         const int nblk = rem * (rem + 1) / 2;
-        for (int e = warp; e < nblk; e += CW) {
+        for (int e = rank + CL * warp; e < nblk; e += CL * CW) {
             int q = 0, rowlen = rem, acc_e = e;
             while (acc_e >= rowlen) {
                 acc_e -= rowlen;
@@ -310,7 +342,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             for (int i = 0; i < 4; ++i)  // the block's current values load while the product runs
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const double2 o = *reinterpret_cast<const double2*>(A + (int64_t)(q0 + 8 * i + g) * lda + r0 + 8 * j + 2 * t);
+                    const double2 o = __ldcg(reinterpret_cast<const double2*>(A + (int64_t)(q0 + 8 * i + g) * lda + r0 + 8 * j + 2 * t));
                     old[i][j][0] = o.x;
                     old[i][j][1] = o.y;
                 }
@@ -327,9 +359,10 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                 }
         }
         __syncthreads();
+        if (CL > 1) cl_sync();  // the trailing blocks of every CTA are in A before the next panel
         SMG_CHOL_T(6 + pb * 5);
     }
-    if (p.skip_inverse) return;
+    if (p.skip_inverse || rank != 0) return;
     // ---- (d) X = R~^-1 by block back-substitution: X_pq = -X_pp sum_{s=p+1..q} R_ps X_sq.
     // B holds D^-1 X, so X_sq = d_row * B_sq on read.  R's panel row and X_pp sit
     // in shared memory; each X_sq block is staged into the warp's buffer with
@@ -449,7 +482,28 @@ void chol_factor(const CholParams& p, cudaStream_t st) {
         cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         configured = bytes;
     }
-    ::smg::count_launch(), chol_kernel<<<p.batch, CNT, bytes, st>>>(p);
+    // a few chains with c > 224: a cluster of 4 CTAs per chain splits the panel
+    // rows and trailing updates (single-chain configs are bound by this kernel)
+    const int P = (p.c_cap + 31) / 32;
+    const bool cluster = p.batch <= 4 && P >= 8 && !std::getenv("SMG_CHOL_NOCLUSTER");
+    if (!cluster) {
+        ::smg::count_launch(), chol_kernel<<<p.batch, CNT, bytes, st>>>(p);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.batch * 4);
+    cfg.blockDim = dim3(CNT);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ::smg::count_launch();
+    cudaLaunchKernelEx(&cfg, chol_kernel, p);
 }
 
 }  // namespace smg
