@@ -210,10 +210,11 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     G.alloc(cc, st);
     Bm.alloc(cc, st);
     work.alloc(cc, st);
-    // split-K over the n rows for the Gram: aim at ~2 waves of CTAs
+    // split-K over the n rows for the Gram: ~8 waves of CTAs (4 splits at C5,
+    // measured best), splits of >= 64 rows, at most 16 (single chains are
+    // latency-bound: 16 splits took C2 27.4 -> 24.2 ms)
     const int tiles = ((ld + 63) / 64) * ((ld + 63) / 64 + 1) / 2;
-    // ~8 waves of CTAs, each split at least 256 rows deep (measured best at C5)
-    splits = std::max(1, std::min(npad / 256, (1184 + tiles * B - 1) / std::max(1, tiles * B)));
+    splits = std::max(1, std::min(std::min(npad / 64, 16), (1184 + tiles * B - 1) / std::max(1, tiles * B)));
     if (const char* e = std::getenv("SMG_GRAM_SPLITS")) splits = std::max(1, std::min(npad / 64, std::atoi(e)));
     Gws.alloc((size_t)B * splits * ld * ld, st);
     rdiag.alloc((size_t)B * ld, st);
