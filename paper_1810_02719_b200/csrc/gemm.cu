@@ -307,9 +307,18 @@ SMG_DEV void issue_slab(double* sl, const double* __restrict__ ptr, int64_t ld, 
     }
 }
 
-template <bool TA, bool TB, int NJ>
-__global__ void __launch_bounds__(NT_P, 4) gemm_pipe_kernel(GemmParams p, int n_base, int n_end) {
+// MW warps along M: 2 -> 64-row tiles (4 DMMA warps); 1 -> 32-row tiles (2 DMMA
+// warps) for launches too small to fill the GPU (single chains)
+template <int MW>
+struct PipeShape {
+    static constexpr int BMv = 32 * MW, NDW = 2 * MW, THREADS = 32 * NDW + 32, MINB = 4;
+};
+
+template <bool TA, bool TB, int NJ, int MW = 2>
+__global__ void __launch_bounds__(PipeShape<MW>::THREADS, PipeShape<MW>::MINB)
+    gemm_pipe_kernel(GemmParams p, int n_base, int n_end) {
     constexpr int BN = 16 * NJ;
+    constexpr int BM = PipeShape<MW>::BMv, NDW = PipeShape<MW>::NDW;
     using SA = Slab<BM, TA, BKP>;
     using SB = Slab<BN, !TB, BKP>;
     const int splits = p.splits > 0 ? p.splits : 1;
@@ -339,13 +348,13 @@ __global__ void __launch_bounds__(NT_P, 4) gemm_pipe_kernel(GemmParams p, int n_
     if (threadIdx.x == 0) {
         for (int i = 0; i < PNS; ++i) {
             g_mbar_init(&full[i], 1);
-            g_mbar_init(&consumed[i], NT / 32);
+            g_mbar_init(&consumed[i], NDW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == NT / 32) {  // producer
+    if (warp == NDW) {  // producer
         uint32_t cph[PNS];
         for (int i = 0; i < PNS; ++i) cph[i] = 0u;
         for (int ks = 0; ks < nsteps; ++ks) {
@@ -366,7 +375,7 @@ __global__ void __launch_bounds__(NT_P, 4) gemm_pipe_kernel(GemmParams p, int n_
     }
 
     const int g = lane >> 2, t = lane & 3;
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * (8 * NJ);
+    const int wm = (warp % MW) * 32, wn = (warp / MW) * (8 * NJ);
     double acc[4][NJ][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -456,6 +465,21 @@ void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
     const bool aligned = al(p.A) && al(p.B) && !(p.lda & 1) && !(p.ldb & 1) && !(p.strideA & 1) && !(p.strideB & 1) &&
                          !(n_base & 1) && !std::getenv("SMG_GEMM_NOPIPE");
     if (aligned) {
+        // a launch that cannot fill the GPU runs 32-row tiles (twice the CTAs)
+        const bool small = (int64_t)gm * gn * p.batch * p.splits < 148 && !std::getenv("SMG_GEMM_NOSMALL");
+        if (small) {
+            using SA = Slab<32, TA, BKP>;
+            using SB = Slab<BN, !TB, BKP>;
+            const int bytes = PNS * (SA::ELEMS + SB::ELEMS) * 8;
+            static bool configured = false;
+            if (!configured) {
+                cudaFuncSetAttribute(gemm_pipe_kernel<TA, TB, NJ, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+                configured = true;
+            }
+            dim3 g2(gn, (p.M + 31) / 32, p.batch * p.splits);
+            gemm_pipe_kernel<TA, TB, NJ, 1><<<g2, PipeShape<1>::THREADS, bytes, st>>>(p, n_base, n_base + width);
+            return;
+        }
         using SA = Slab<BM, TA, BKP>;
         using SB = Slab<BN, !TB, BKP>;
         const int bytes = PNS * (SA::ELEMS + SB::ELEMS) * 8;
