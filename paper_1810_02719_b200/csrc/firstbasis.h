@@ -1,6 +1,8 @@
 // First-submesh basis (K9), see firstbasis.cu.
 #pragma once
 
+#include <cstdlib>
+
 #include <stdint.h>
 
 #include <algorithm>
@@ -31,7 +33,8 @@ struct FirstBasisReport {
 // capped at the 480-column limit of the cluster Jacobi (16 CTAs x 2 blocks of 15).
 constexpr int kFirstBasisMaxCols = 480;
 inline int first_basis_width(int n, int c) {
-    const int want = round_up(c + std::max(16, c / 4), 8);
+    static const int div = std::getenv("SMG_FB_GUARD") ? std::max(1, std::atoi(std::getenv("SMG_FB_GUARD"))) : 6;
+    const int want = round_up(c + std::max(16, c / div), 8);
     return std::min(n, std::max(c, std::min(kFirstBasisMaxCols, want)));
 }
 
