@@ -138,7 +138,7 @@ FirstBasisReport first_basis_impl(const StepCtx& cx, Workspace& ws, const TileSe
     SMG_CUDA(cudaStreamSynchronize(st));
     const bool use_cheb =
         allow_cheb && !(std::getenv("SMG_FIRST_BASIS") && std::string(std::getenv("SMG_FIRST_BASIS")) == "si");
-    const int deg = 30;
+    const int deg = std::getenv("SMG_FB_DEG") ? std::max(2, std::atoi(std::getenv("SMG_FB_DEG"))) : 40;
     DBuf<double> dcoef;          // [deg][B] alpha | [deg][B] gamma | [B] shift
     int iters_next = (m == n) ? 0 : (use_cheb ? 4 : 6);
     if (const char* e = std::getenv("SMG_FB_BOOT")) iters_next = std::max(1, std::atoi(e));
