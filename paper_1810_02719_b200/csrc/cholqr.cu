@@ -449,7 +449,17 @@ __global__ void rank_partial_kernel(RankCheckParams p) {
     const double* V = p.V + (int64_t)b * p.stride;
     for (int k = threadIdx.x; k < c; k += blockDim.x) {
         double acc = 0.0;
-        for (int i = r0; i < r1; ++i) acc = fma(Q[(int64_t)i * p.ld + k], V[(int64_t)i * p.ld + k], acc);
+        if (r1 - r0 == RC_ROWS) {
+            // full chunk: constant trip count so the loads are hoisted ahead of
+            // the (unchanged, row-ordered) FMA chain -- latency, not bandwidth,
+            // bound this kernel
+            const double* q = Q + (int64_t)r0 * p.ld + k;
+            const double* v = V + (int64_t)r0 * p.ld + k;
+#pragma unroll 16
+            for (int i = 0; i < RC_ROWS; ++i) acc = fma(q[(int64_t)i * p.ld], v[(int64_t)i * p.ld], acc);
+        } else {
+            for (int i = r0; i < r1; ++i) acc = fma(Q[(int64_t)i * p.ld + k], V[(int64_t)i * p.ld + k], acc);
+        }
         p.partial[((int64_t)b * gridDim.x + chunk) * p.c_cap + k] = acc;
     }
     __shared__ bool last;
@@ -467,7 +477,9 @@ __global__ void rank_partial_kernel(RankCheckParams p) {
 
 void rank_check(const RankCheckParams& p, cudaStream_t st) {
     const int chunks = (p.n + RC_ROWS - 1) / RC_ROWS;
-    ::smg::count_launch(), rank_partial_kernel<<<dim3(chunks, p.batch), 256, 0, st>>>(p);
+    // threads over columns: no idle warps at c = 200 (224 threads)
+    const int threads = std::min(256, std::max(32, (p.c_cap + 31) / 32 * 32));
+    ::smg::count_launch(), rank_partial_kernel<<<dim3(chunks, p.batch), threads, 0, st>>>(p);
 }
 
 int chol_smem_bytes(int c_cap) {
