@@ -26,6 +26,10 @@ namespace {
 constexpr int PNT = 256;   // recon CTA: 8 column parts x 32 row groups of RPT rows
 constexpr int QNT = 128;   // partial CTA: two adjacent columns per thread
 constexpr int RPC = 32;    // rows per partial chunk
+#ifndef SMG_RECON_UNROLL
+#define SMG_RECON_UNROLL 1
+#endif
+constexpr int kReconUnroll = SMG_RECON_UNROLL;  // column-pair steps unrolled in recon
 // rows per recon thread: 4 (coefficients reused across them) when the batch
 // fills the GPU, 1 for a single chain (4x the CTAs)
 
@@ -164,13 +168,26 @@ template <int RPT>
 __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
     constexpr int RROWS = (PNT / 8) * RPT;
     __shared__ double red[2][PNT / 32];
-    extern __shared__ __align__(16) double scoef[];  // c x 4, staged once per CTA
+    // coefficients staged once per CTA, swizzled so that the 8 column parts'
+    // reads of one 16-byte quarter are 128 contiguous bytes (one wavefront):
+    // double2 index ((g * 4 + quarter) * 8 + part) for column pair g * 8 + part,
+    // quarters {P_j.xy, P_j.zw, P_j+1.xy, P_j+1.zw}
+    extern __shared__ __align__(16) double scoef[];
     const int b = blockIdx.y;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const double* Q = p.Q + (int64_t)b * p.strideQ;
     const double* X = p.X + (int64_t)b * p.strideX;
-    for (int e = threadIdx.x; e < 4 * c; e += PNT) scoef[e] = p.coeff[(int64_t)b * p.strideCoef + e];
-    for (int e = 4 * c + threadIdx.x; e < 4 * (c + 1); e += PNT) scoef[e] = 0.0;  // odd c: the pair's tail
+    {
+        const double2* src = reinterpret_cast<const double2*>(p.coeff + (int64_t)b * p.strideCoef);
+        double2* dst = reinterpret_cast<double2*>(scoef);
+        const int npairs = (c + 1) / 2;
+        for (int e = threadIdx.x; e < 4 * npairs; e += PNT) {
+            const int pi = e >> 2, quarter = e & 3;
+            const int j = 2 * pi + (quarter >> 1);
+            const double2 v = j < c ? src[2 * j + (quarter & 1)] : make_double2(0.0, 0.0);  // odd c: the pair's tail
+            dst[((pi >> 3) * 4 + quarter) * 8 + (pi & 7)] = v;
+        }
+    }
     __syncthreads();
     double* xhat = p.xhat ? p.xhat + (int64_t)b * p.strideXhat : nullptr;
     double* e_out = p.e_out ? p.e_out + (int64_t)b * p.strideE : nullptr;
@@ -180,10 +197,11 @@ __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
     double acc[RPT][4];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
-    const double4* cf = reinterpret_cast<const double4*>(scoef);
-#pragma unroll 2
-    for (int j = 2 * part; j < c; j += 16) {
-        const double4 ca = cf[j], cb = cf[j + 1];
+    const double2* cf = reinterpret_cast<const double2*>(scoef) + part;
+#pragma unroll kReconUnroll
+    for (int j = 2 * part; j < c; j += 16, cf += 32) {
+        const double2 c0 = cf[0], c1 = cf[8], c2 = cf[16], c3 = cf[24];
+        const double4 ca = make_double4(c0.x, c0.y, c1.x, c1.y), cb = make_double4(c2.x, c2.y, c3.x, c3.y);
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
             if (i0 + r >= p.n) break;
@@ -270,7 +288,7 @@ void project(const ProjParams& p0, cudaStream_t st) {
     p.nchunks = proj_chunks(p.n);
     ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), QNT, 0, st>>>(p);
     ::smg::count_launch(), chunk_reduce_kernel<<<dim3((p.c_cap + RCOL - 1) / RCOL, p.batch), RCOL * RPART, 0, st>>>(p);
-    const int smem = 4 * (p.c_cap + 1) * sizeof(double);
+    const int smem = ((p.c_cap + 1) / 2 + 7) / 8 * 32 * (int)sizeof(double2);
     const int nb4 = (p.n + 4 * (PNT / 8) - 1) / (4 * (PNT / 8));
     if ((int64_t)nb4 * p.batch >= 2 * 148) {
         ::smg::count_launch(), recon_kernel<4><<<dim3(nb4, p.batch), PNT, smem, st>>>(p);
