@@ -18,6 +18,7 @@
 // the trailing SYRK are 32x32x32 DMMA blocks on all warps; finally the block
 // upper-triangular inverse X = R~^-1 is formed by block back-substitution
 // (DMMA) and stored row-scaled as B = D^-1 X.
+#include <cstdint>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -39,6 +40,9 @@ __device__ long long g_chol_t[128];
 
 namespace {
 
+#ifndef SMG_CHOL_SINGLE_BUFFER
+#define SMG_CHOL_SINGLE_BUFFER 0
+#endif
 constexpr int CNT = 256;
 constexpr int CW = CNT / 32;
 constexpr int XS = 36;
@@ -60,6 +64,12 @@ SMG_DEV void warp_block_mma(double (&acc)[4][4][2], FA a, FB b, int g, int t) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
     }
+}
+
+// back-substitution staging double-buffered when both per-warp buffers fit
+__host__ __device__ constexpr bool chol_double_buffered(int c_cap) {
+    return (32 * ((c_cap + 31) / 32 * 32 + 4) + 32 * XS + 2 * CW * 32 * XS + 2 * ((c_cap + 31) / 32 * 32)) * 8 <= 227 * 1024 &&
+           !SMG_CHOL_SINGLE_BUFFER;
 }
 
 // cluster helpers (a launch without clusters is a cluster of one CTA)
@@ -368,6 +378,12 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     // in shared memory; each X_sq block is staged into the warp's buffer with
     // one coalesced burst before its DMMA block product.
     double* Tw = Ts + warp * 32 * XS;
+    // when shared memory allows, a second per-warp buffer lets the next X_sq
+    // block stream in (cp.async) under the current block product; the d_row
+    // scaling then happens on the operand read (same rounding as staging it)
+    const bool dbl = chol_double_buffered(p.c_cap) && ((reinterpret_cast<uintptr_t>(p.Binv) & 15) == 0) &&
+                     (ldb % 2 == 0) && (p.strideB % 2 == 0);
+    double* Tw2 = rds + cp + warp * 32 * XS;
     for (int pb = P - 2; pb >= 0; --pb) {
         const int p0 = pb * 32;
         for (int r = warp; r < 32; r += CW) {
@@ -379,15 +395,44 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             const int q0 = q * 32;
             double acc[4][4][2];
             zero_acc(acc);
-            for (int s = pb + 1; s <= q; ++s) {
-                const int s0 = s * 32;
-                __syncwarp();
+            if (dbl) {
+                // 16-byte copies: lane -> row (lane >> 4) of a row pair, columns 2 (lane & 15) +{0,1}
+                auto stage = [&](double* buf, int s0) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) Tw[k * XS + lane] = Bo[(int64_t)(s0 + k) * ldb + q0 + lane] * ds[s0 + k];
-                __syncwarp();
-                warp_block_mma(
-                    acc, [&](int m, int k) { return Ps[m * PS + s0 + k]; }, [&](int k, int n) { return Tw[k * XS + n]; },
-                    g, t);
+                    for (int k = 0; k < 32; k += 2) {
+                        const int r = k + (lane >> 4), cc = 2 * (lane & 15);
+                        cp_async16(buf + r * XS + cc, Bo + (int64_t)(s0 + r) * ldb + q0 + cc);
+                    }
+                    cp_async_commit();
+                };
+                stage(Tw, (pb + 1) * 32);
+                for (int s = pb + 1; s <= q; ++s) {
+                    const int s0 = s * 32;
+                    double* cur = ((s - pb - 1) & 1) ? Tw2 : Tw;
+                    double* nxt = ((s - pb - 1) & 1) ? Tw : Tw2;
+                    __syncwarp();  // every lane is done reading nxt (the previous block)
+                    if (s < q) {
+                        stage(nxt, s0 + 32);
+                        cp_async_wait<1>();
+                    } else {
+                        cp_async_wait<0>();
+                    }
+                    __syncwarp();
+                    warp_block_mma(
+                        acc, [&](int m, int k) { return Ps[m * PS + s0 + k]; },
+                        [&](int k, int n) { return cur[k * XS + n] * ds[s0 + k]; }, g, t);
+                }
+            } else {
+                for (int s = pb + 1; s <= q; ++s) {
+                    const int s0 = s * 32;
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) Tw[k * XS + lane] = Bo[(int64_t)(s0 + k) * ldb + q0 + lane] * ds[s0 + k];
+                    __syncwarp();
+                    warp_block_mma(
+                        acc, [&](int m, int k) { return Ps[m * PS + s0 + k]; }, [&](int k, int n) { return Tw[k * XS + n]; },
+                        g, t);
+                }
             }
             __syncwarp();
 #pragma unroll
@@ -484,7 +529,7 @@ void rank_check(const RankCheckParams& p, cudaStream_t st) {
 
 int chol_smem_bytes(int c_cap) {
     const int cp = (c_cap + 31) / 32 * 32;
-    return (32 * (cp + 4) + 32 * XS + CW * 32 * XS + 2 * cp) * 8;
+    return (32 * (cp + 4) + 32 * XS + (chol_double_buffered(c_cap) ? 2 : 1) * CW * 32 * XS + 2 * cp) * 8;
 }
 
 void chol_factor(const CholParams& p, cudaStream_t st) {
