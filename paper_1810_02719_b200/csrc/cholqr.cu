@@ -372,7 +372,10 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         if (CL > 1) cl_sync();  // the trailing blocks of every CTA are in A before the next panel
         SMG_CHOL_T(6 + pb * 5);
     }
-    if (p.skip_inverse || rank != 0) return;
+    if (p.skip_inverse) return;
+    // block columns of X are independent: on a cluster each CTA back-substitutes
+    // the columns q = rank (mod CL), no exchange needed (the diagonal blocks X_pp
+    // every CTA wrote identically in (b))
     // ---- (d) X = R~^-1 by block back-substitution: X_pq = -X_pp sum_{s=p+1..q} R_ps X_sq.
     // B holds D^-1 X, so X_sq = d_row * B_sq on read.  R's panel row and X_pp sit
     // in shared memory; each X_sq block is staged into the warp's buffer with
@@ -391,7 +394,8 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
             Xs[r * XS + lane] = Bo[(int64_t)(p0 + r) * ldb + p0 + lane] * ds[p0 + r];
         }
         __syncthreads();
-        for (int q = pb + 1 + warp; q < P; q += CW) {
+        const int qfirst = pb + 1 + ((rank - (pb + 1)) % CL + CL) % CL;
+        for (int q = qfirst + CL * warp; q < P; q += CL * CW) {
             const int q0 = q * 32;
             double acc[4][4][2];
             zero_acc(acc);
