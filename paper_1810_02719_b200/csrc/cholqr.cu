@@ -395,10 +395,14 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         }
         __syncthreads();
         const int qfirst = pb + 1 + ((rank - (pb + 1)) % CL + CL) % CL;
-        for (int q = qfirst + CL * warp; q < P; q += CL * CW) {
-            const int q0 = q * 32;
-            double acc[4][4][2];
-            zero_acc(acc);
+        const int nown = qfirst < P ? (P - qfirst + CL - 1) / CL : 0;
+        // cluster (few long chains, latency-bound): each column's s-sum is split
+        // over S warps (s strided by S) and the part-0 warp adds the partials in
+        // part order (deterministic).  Measured: c = 400 592 -> 516 us, c = 320
+        // 384 -> 336 us; on one CTA at c = 200 the extra barrier costs more (222 -> 226 us)
+        const int S = (CL > 1 && nown > 0 && nown <= CW / 2) ? min(CW / nown, 4) : 1;
+        auto accumulate = [&](double(&acc)[4][4][2], int q0, int sb, int q) {
+            if (sb > q) return;
             if (dbl) {
                 // 16-byte copies: lane -> row (lane >> 4) of a row pair, columns 2 (lane & 15) +{0,1}
                 auto stage = [&](double* buf, int s0) {
@@ -409,14 +413,15 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                     }
                     cp_async_commit();
                 };
-                stage(Tw, (pb + 1) * 32);
-                for (int s = pb + 1; s <= q; ++s) {
+                stage(Tw, sb * 32);
+                int it = 0;
+                for (int s = sb; s <= q; s += S, ++it) {
                     const int s0 = s * 32;
-                    double* cur = ((s - pb - 1) & 1) ? Tw2 : Tw;
-                    double* nxt = ((s - pb - 1) & 1) ? Tw : Tw2;
+                    double* cur = (it & 1) ? Tw2 : Tw;
+                    double* nxt = (it & 1) ? Tw : Tw2;
                     __syncwarp();  // every lane is done reading nxt (the previous block)
-                    if (s < q) {
-                        stage(nxt, s0 + 32);
+                    if (s + S <= q) {
+                        stage(nxt, s0 + 32 * S);
                         cp_async_wait<1>();
                     } else {
                         cp_async_wait<0>();
@@ -427,7 +432,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                         [&](int k, int n) { return cur[k * XS + n] * ds[s0 + k]; }, g, t);
                 }
             } else {
-                for (int s = pb + 1; s <= q; ++s) {
+                for (int s = sb; s <= q; s += S) {
                     const int s0 = s * 32;
                     __syncwarp();
 #pragma unroll
@@ -438,7 +443,8 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                         g, t);
                 }
             }
-            __syncwarp();
+        };
+        auto put = [&](const double(&acc)[4][4][2]) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -446,6 +452,11 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                     Tw[(8 * i + g) * XS + 8 * j + 2 * t] = acc[i][j][0];
                     Tw[(8 * i + g) * XS + 8 * j + 2 * t + 1] = acc[i][j][1];
                 }
+        };
+        // X_pq = -X_pp (sum) scaled to B rows
+        auto finish = [&](double(&acc)[4][4][2], int q0) {
+            __syncwarp();
+            put(acc);
             __syncwarp();
             zero_acc(acc);
             warp_block_mma(
@@ -460,6 +471,37 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
                     dst[1] = -acc[i][j][1] * rds[r];
                 }
             __syncwarp();
+        };
+        if (S == 1) {
+            for (int q = qfirst + CL * warp; q < P; q += CL * CW) {
+                double acc[4][4][2];
+                zero_acc(acc);
+                accumulate(acc, q * 32, pb + 1, q);
+                finish(acc, q * 32);
+            }
+        } else {
+            const int qi = warp % nown, part = warp / nown;
+            const bool active = part < S;
+            const int q = qfirst + CL * qi;
+            double acc[4][4][2];
+            zero_acc(acc);
+            if (active) accumulate(acc, q * 32, pb + 1 + part, q);
+            __syncwarp();
+            if (active && part > 0) put(acc);
+            __syncthreads();
+            if (active && part == 0) {
+                for (int pp = 1; pp < S; ++pp) {
+                    const double* Tp = Ts + (qi + pp * nown) * 32 * XS;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            acc[i][j][0] += Tp[(8 * i + g) * XS + 8 * j + 2 * t];
+                            acc[i][j][1] += Tp[(8 * i + g) * XS + 8 * j + 2 * t + 1];
+                        }
+                }
+                finish(acc, q * 32);
+            }
         }
         __syncthreads();
     }

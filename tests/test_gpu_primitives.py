@@ -133,6 +133,21 @@ def test_orthonormalize_wide_blocks(ctx, c):
     assert np.abs(q - O.orthonormalize(b)).max() < 1e-10
 
 
+@pytest.mark.parametrize("c", [200, 256, 320, 400])
+def test_orthonormalize_ill_conditioned_second_pass(ctx, c):
+    """Conditioning that column scaling cannot remove (kappa = 1e5 spread over
+    mixed columns): the second CholeskyQR pass is not near-identity, so its
+    Cholesky forms the full inverse -- on one CTA (c <= 224) or split over a
+    4-CTA cluster with strided s-sums (c > 224, one chain)."""
+    rng = np.random.default_rng(100 + c)
+    u, _ = np.linalg.qr(rng.standard_normal((2048, c)))
+    w, _ = np.linalg.qr(rng.standard_normal((c, c)))
+    b = (u * np.logspace(0, -5, c)) @ w.T
+    q = G.orthonormalize(b, ctx=ctx)
+    assert np.abs(q.T @ q - np.eye(c)).max() < 1e-12
+    assert np.abs(q - O.orthonormalize(b)).max() < 1e-8
+
+
 def test_orthonormalize_errors(ctx):
     with pytest.raises(G.SpecmeshError, match=r"rank deficient \(all zero\)"):
         G.orthonormalize(np.zeros((5, 2)), ctx=ctx)
