@@ -411,11 +411,7 @@ void axis_order(const double* X, int64_t strideX, int ntiles, int n, int32_t* pe
     int N2 = 1;
     while (N2 < n) N2 <<= 1;
     const int bytes = N2 * (8 + 8 + 4);
-    static int configured = 0;
-    if (bytes > configured) {
-        cudaFuncSetAttribute(axis_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        configured = bytes;
-    }
+    ensure_smem((const void*)axis_order_kernel, bytes);
     if (ntiles) ::smg::count_launch(), axis_order_kernel<<<ntiles, 512, bytes, st>>>(X, strideX, n, perm);
 }
 

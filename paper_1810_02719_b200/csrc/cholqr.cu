@@ -83,6 +83,8 @@ SMG_DEV unsigned cl_size() {
     asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
     return r;
 }
+SMG_DEV void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+SMG_DEV void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 SMG_DEV void cl_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
@@ -226,6 +228,11 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         for (int r = warp; r < 32; r += CW)
             for (int k = p0 + lane; k < cp; k += 32) Ps[r * PS + k] = __ldcg(A + (int64_t)(p0 + r) * lda + k);
         __syncthreads();
+        // cluster: this CTA's panel-row load is done; no CTA may overwrite the
+        // panel row in A (diagonal block, panel-row blocks) before every CTA has
+        // loaded it -- the matching wait sits just before the first store, so the
+        // diagonal factor below hides the barrier
+        if (CL > 1) cl_arrive();
         SMG_CHOL_T(2 + pb * 5);
         // ---- (a) factor the diagonal block with all threads (right-looking, LDL^T
         // form: the pivots are kept and the rows scaled at the end), then invert it.
@@ -264,6 +271,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         __syncthreads();
         if (fail) return;
         SMG_CHOL_T(3 + pb * 5);
+        if (CL > 1) cl_wait();
         // rows scaled: R[i][k] = D[i][k] / sqrt(piv_i); X = R^-1 accumulators
         double xacc[3];
 #pragma unroll
@@ -580,11 +588,7 @@ int chol_smem_bytes(int c_cap) {
 
 void chol_factor(const CholParams& p, cudaStream_t st) {
     const int bytes = chol_smem_bytes(p.c_cap);
-    static int configured = 0;
-    if (bytes > configured) {
-        cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        configured = bytes;
-    }
+    ensure_smem((const void*)chol_kernel, bytes);
     // a few chains with c > 224: a cluster of 4 CTAs per chain splits the panel
     // rows and trailing updates (single-chain configs are bound by this kernel)
     const int P = (p.c_cap + 31) / 32;

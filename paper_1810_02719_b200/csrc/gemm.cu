@@ -471,11 +471,7 @@ void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
             using SA = Slab<32, TA, BKP>;
             using SB = Slab<BN, !TB, BKP>;
             const int bytes = PNS * (SA::ELEMS + SB::ELEMS) * 8;
-            static bool configured = false;
-            if (!configured) {
-                cudaFuncSetAttribute(gemm_pipe_kernel<TA, TB, NJ, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-                configured = true;
-            }
+            ensure_smem((const void*)gemm_pipe_kernel<TA, TB, NJ, 1>, bytes);
             dim3 g2(gn, (p.M + 31) / 32, p.batch * p.splits);
             gemm_pipe_kernel<TA, TB, NJ, 1><<<g2, PipeShape<1>::THREADS, bytes, st>>>(p, n_base, n_base + width);
             return;
@@ -483,11 +479,7 @@ void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
         using SA = Slab<BM, TA, BKP>;
         using SB = Slab<BN, !TB, BKP>;
         const int bytes = PNS * (SA::ELEMS + SB::ELEMS) * 8;
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(gemm_pipe_kernel<TA, TB, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-            configured = true;
-        }
+        ensure_smem((const void*)gemm_pipe_kernel<TA, TB, NJ>, bytes);
         gemm_pipe_kernel<TA, TB, NJ><<<grid, NT_P, bytes, st>>>(p, n_base, n_base + width);
         return;
     }

@@ -12,6 +12,8 @@ namespace smg {
 // diagnostics API as the "launches" stage.
 int count_launch();
 int64_t launch_count();
+// raise a kernel's dynamic shared-memory limit on the current device (cached per device)
+void ensure_smem(const void* func, int bytes);
 
 // ------------------------------------------------------------------ GEMM (gemm.cu)
 struct GemmParams {

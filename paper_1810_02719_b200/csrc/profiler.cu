@@ -1,4 +1,7 @@
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "kernels.h"
 #include "profiler.h"
@@ -15,6 +18,22 @@ int count_launch() {
 }
 
 int64_t launch_count() { return g_launches.load(); }
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device: cache the largest
+// value set per (kernel, device) under a lock, so contexts on several devices
+// (or host threads) each get their own call
+void ensure_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> have;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    int& cur = have[{func, dev}];
+    if (bytes > cur) {
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cur = bytes;
+    }
+}
 
 Profiler*& active_profiler() {
     thread_local Profiler* p = nullptr;

@@ -448,11 +448,7 @@ template <int W, int CS>
 void launch(const SolveParams& p, cudaStream_t st) {
     const int bytes = SolveSmem<W, CS>::BYTES;
     const int slices = (p.c_cap + CS - 1) / CS;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(solve_kernel<W, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        configured = true;
-    }
+    ensure_smem((const void*)solve_kernel<W, CS>, bytes);
     dim3 grid(slices, p.batch);
     ::smg::count_launch(), solve_kernel<W, CS><<<grid, NT, bytes, st>>>(p);
 }

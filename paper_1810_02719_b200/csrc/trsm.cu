@@ -162,12 +162,8 @@ void trsm_right_upper(const TrsmParams& p, cudaStream_t st) {
     const int cp = (p.c_cap + 31) / 32 * 32;
     const bool full = TrsmFull::bytes(cp) <= 227 * 1024;
     const int bytes = trsm_smem_bytes(p.c_cap);
-    static int configured[2] = {0, 0};
-    if (bytes > configured[full]) {
-        if (full) cudaFuncSetAttribute(trsm_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        else cudaFuncSetAttribute(trsm_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        configured[full] = bytes;
-    }
+    if (full) ensure_smem((const void*)trsm_kernel<2, false>, bytes);
+    else ensure_smem((const void*)trsm_kernel<1, true>, bytes);
     if (full) {
         dim3 grid((p.n + TrsmFull::TRB - 1) / TrsmFull::TRB, p.batch);
         ::smg::count_launch(), trsm_kernel<2, false><<<grid, TNT, bytes, st>>>(p);
