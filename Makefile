@@ -9,7 +9,13 @@ SRCS := $(wildcard $(SRC_DIR)/*.cu)
 OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
 HDRS := $(wildcard $(SRC_DIR)/*.h) $(wildcard $(SRC_DIR)/*.cuh) include/specmesh_gpu.h
 
-all: $(LIB) oracle
+all: $(LIB) oracle build/abi_chain
+
+# compiled C++ caller of the C ABI through include/specmesh_gpu.hpp (tests/test_cpp_abi.py)
+build/abi_chain: tests/cpp/abi_chain.cpp include/specmesh_gpu.hpp include/specmesh_gpu.h $(LIB)
+	@mkdir -p build
+	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude $< -Lpaper_1810_02719_b200/lib -lspecmesh_b200 \
+		-Wl,-rpath,'$$ORIGIN/../paper_1810_02719_b200/lib' -o $@
 
 $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p $(OBJ_DIR)

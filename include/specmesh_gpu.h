@@ -325,6 +325,15 @@ smg_status smg_igft(smg_context* ctx, int32_t rows, int32_t c, const double* bas
 smg_status smg_profile_enable(smg_context* ctx, int32_t on);
 smg_status smg_profile_read(smg_context* ctx, const char* stage, int64_t* launches, double* total_ms);
 
+/* DOI step log (decision-level parity of dynamic_oi, spectral.hpp:259-283):
+ * while enabled, every dynamic_oi step of smg_compute_block_bases (DOI mode)
+ * and smg_dynamic_oi appends (chain position, subspace size the step ran
+ * with, residual ||e||/bbox_diag that decided it).  Enabling or disabling
+ * clears the log.  smg_doi_trace_read with capacity 0 returns the count only. */
+smg_status smg_doi_trace_enable(smg_context* ctx, int32_t on);
+smg_status smg_doi_trace_read(smg_context* ctx, int64_t capacity, int32_t* position,
+                              int32_t* subspace_size, double* residual, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

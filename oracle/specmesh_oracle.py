@@ -438,8 +438,9 @@ class DoiResult:
     iterations: int = 0
 
 
-def dynamic_oi(op, init, coords, eps_low, eps_high, c_min, c_max, t_max) -> DoiResult:
-    """spectral.hpp:244-287"""
+def dynamic_oi(op, init, coords, eps_low, eps_high, c_min, c_max, t_max, trace=None) -> DoiResult:
+    """spectral.hpp:244-287.  ``trace`` (test hook): a list that receives
+    (subspace size the step ran with, residual) for every step."""
     require(eps_low > 0.0 and eps_low < eps_high, "need 0 < eps_low < eps_high")
     require(c_min >= 1 and c_min <= init.shape[1] and init.shape[1] <= c_max,
             "need c_min <= init subspace size <= c_max")
@@ -458,6 +459,8 @@ def dynamic_oi(op, init, coords, eps_low, eps_high, c_min, c_max, t_max) -> DoiR
         e = projection_residual(u, coords)
         en = float(np.linalg.norm(e))
         res.residual = en / scale
+        if trace is not None:
+            trace.append((u.shape[1], res.residual))
         if res.residual > eps_high:
             if u.shape[1] >= c_max:
                 break
@@ -656,8 +659,10 @@ def compute_block_bases_fixed_sizes(vertices, submeshes: List[Submesh], sequence
 
 
 def compute_block_bases_doi(vertices, submeshes: List[Submesh], sequence, cfg: PipelineConfig,
-                            keep_bases: bool = True) -> BlockBases:
-    """pipeline.hpp:245-285 (DOI branch), over an external segmentation."""
+                            keep_bases: bool = True, trace=None, on_block=None) -> BlockBases:
+    """pipeline.hpp:245-285 (DOI branch), over an external segmentation.
+    ``trace`` (test hook): list receiving (position, c, residual) per DOI step;
+    ``on_block(pos, sid, basis)`` is called after every block."""
     k = len(submeshes)
     res = BlockBases(submeshes, np.asarray(sequence), [None] * k, [BlockStats() for _ in range(k)],
                      {}, submeshes[0].size() if submeshes else 0)
@@ -681,7 +686,10 @@ def compute_block_bases_doi(vertices, submeshes: List[Submesh], sequence, cfg: P
             c_init = min(max(previous.shape[1], cfg.c_min), c_max)
             init = resize_basis(previous, c_init, _pos_seed(cfg, pos))
         coords = sub.local_coords(vertices)
-        doi = dynamic_oi(op, init, coords, cfg.eps_low, cfg.eps_high, cfg.c_min, c_max, doi_t)
+        steps = [] if trace is not None else None
+        doi = dynamic_oi(op, init, coords, cfg.eps_low, cfg.eps_high, cfg.c_min, c_max, doi_t, trace=steps)
+        if trace is not None:
+            trace.extend((pos, c, r) for c, r in steps)
         _add(res.timings, "basis", time.perf_counter() - t0)
         st = res.stats[sid]
         st.subspace_size = doi.basis.shape[1]
@@ -691,6 +699,8 @@ def compute_block_bases_doi(vertices, submeshes: List[Submesh], sequence, cfg: P
         st.residual_rms = projection_residual_rms(doi.basis, coords)
         previous = doi.basis
         res.bases[sid] = doi.basis if keep_bases else None
+        if on_block is not None:
+            on_block(pos, sid, doi.basis)
     _add(res.timings, "basis_total", time.perf_counter() - t_all)
     return res
 

@@ -80,6 +80,21 @@ class Context:
             raise ParseError(msg)
         raise SpecmeshError(msg)
 
+    def doi_trace(self, on: bool = True) -> None:
+        """Start (clear) or stop the DOI step log (smg_doi_trace_enable)."""
+        self.check(self.lib.smg_doi_trace_enable(self.handle, 1 if on else 0))
+
+    def read_doi_trace(self):
+        """(position, subspace size the step ran with, residual) per logged DOI step."""
+        n = C.c_int64()
+        self.check(self.lib.smg_doi_trace_read(self.handle, 0, None, None, None, C.byref(n)))
+        pos = np.zeros(n.value, np.int32)
+        c = np.zeros(n.value, np.int32)
+        r = np.zeros(n.value, np.float64)
+        if n.value:
+            self.check(self.lib.smg_doi_trace_read(self.handle, n.value, _ptr(pos), _ptr(c), _ptr(r), C.byref(n)))
+        return pos, c, r
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             self.lib.smg_destroy(self.handle)

@@ -76,7 +76,7 @@ EXPORTED = [
     "smg_operator_apply", "smg_operator_spmm", "smg_orthonormalize", "smg_orthogonal_iteration",
     "smg_dynamic_oi", "smg_bottom_subspace", "smg_gft", "smg_igft", "smg_profile_enable", "smg_profile_read",
     "smg_coarse_reconstruct_frames", "smg_denoise_dynamic", "smg_compress_blocks", "smg_decompress_blocks",
-    "smg_default_bilateral_params", "smg_fine_denoise",
+    "smg_default_bilateral_params", "smg_fine_denoise", "smg_doi_trace_enable", "smg_doi_trace_read",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -120,6 +120,8 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_igft": ([vp, C.c_int32, C.c_int32, vp, vp, vp], C.c_int),
         "smg_profile_enable": ([vp, C.c_int32], C.c_int),
         "smg_profile_read": ([vp, C.c_char_p, c_int64_p, c_double_p], C.c_int),
+        "smg_doi_trace_enable": ([vp, C.c_int32], C.c_int),
+        "smg_doi_trace_read": ([vp, C.c_int64, vp, vp, vp, c_int64_p], C.c_int),
         "smg_coarse_reconstruct_frames": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
                                            C.POINTER(smg_bases), C.c_int32, vp, C.c_int32, C.c_int32, vp,
                                            C.c_int32], C.c_int),

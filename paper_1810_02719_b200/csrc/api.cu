@@ -550,6 +550,7 @@ public:
             }
             DoiState r = loop.run(fs.f(pos), fs.b(pos), ts_.perm_of(pos), ts_.X.get() + (int64_t)pos * n_ * 3,
                                   bbox[pos], c_init);
+            ctx_->log_doi(loop, pos, r.t);
             int wst = 0;
             int64_t wdet = 0;
             SMG_CUDA(cudaMemcpyAsync(&wst, ws_.status.get(), sizeof(int), cudaMemcpyDeviceToHost, st_));
@@ -1668,6 +1669,30 @@ smg_status smg_profile_read(smg_context* ctx, const char* stage, int64_t* launch
     }
     cudaSetDevice(ctx->device);
     ctx->prof.read(stage, launches, total_ms);
+    return SMG_OK;
+}
+
+smg_status smg_doi_trace_enable(smg_context* ctx, int32_t on) {
+    if (!ctx) return SMG_INVALID_ARGUMENT;
+    ctx->doi_trace = on != 0;
+    ctx->trace_pos.clear();
+    ctx->trace_c.clear();
+    ctx->trace_r.clear();
+    return SMG_OK;
+}
+
+smg_status smg_doi_trace_read(smg_context* ctx, int64_t capacity, int32_t* position, int32_t* subspace_size,
+                              double* residual, int64_t* count) {
+    if (!ctx || !count) return SMG_INVALID_ARGUMENT;
+    const int64_t n = (int64_t)ctx->trace_c.size();
+    *count = n;
+    if (capacity < n) return capacity == 0 ? SMG_OK : SMG_INVALID_ARGUMENT;
+    if (!position || !subspace_size || !residual) return SMG_INVALID_ARGUMENT;
+    for (int64_t i = 0; i < n; ++i) {
+        position[i] = ctx->trace_pos[i];
+        subspace_size[i] = ctx->trace_c[i];
+        residual[i] = ctx->trace_r[i];
+    }
     return SMG_OK;
 }
 

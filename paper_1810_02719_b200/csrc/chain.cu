@@ -38,7 +38,8 @@ __global__ void ritz_reduce_kernel(const double* partial, int nchunks, int ncols
 // projection of step t: stats[1] = ||e||.  Decides, records DoiResult fields
 // and prepares the next step (append e/||e|| as column c, or drop column c-1).
 __global__ void doi_decide_kernel(DoiState* states, int batch, const double* stats, int64_t strideStats,
-                                  cudaGraphConditionalHandle handle, int use_handle, const int* chain_status) {
+                                  cudaGraphConditionalHandle handle, int use_handle, const int* chain_status,
+                                  int* trace_c, double* trace_r) {
     bool any_active = false;
     for (int b = 0; b < batch; ++b) {
         DoiState& s = states[b];
@@ -49,6 +50,10 @@ __global__ void doi_decide_kernel(DoiState* states, int batch, const double* sta
         const double en = stats[(int64_t)b * strideStats + 1];
         s.enorm = en;
         s.residual = en / s.scale;
+        if (trace_c && batch == 1) {  // step log for decision-level parity (c before the decision)
+            trace_c[s.t - 1] = s.c;
+            trace_r[s.t - 1] = s.residual;
+        }
         if (chain_status && chain_status[b] != 0) s.status = chain_status[b];
         if (s.status != 0) {
             s.active = 0;
@@ -159,8 +164,10 @@ void ritz_residual(const double* LZ, const double* Z, const double* theta, int n
 }
 
 void doi_decide(DoiState* states, int batch, const double* stats, int64_t strideStats,
-                cudaGraphConditionalHandle handle, int use_handle, const int* chain_status, cudaStream_t st) {
-    ::smg::count_launch(), doi_decide_kernel<<<1, 1, 0, st>>>(states, batch, stats, strideStats, handle, use_handle, chain_status);
+                cudaGraphConditionalHandle handle, int use_handle, const int* chain_status, cudaStream_t st,
+                int* trace_c, double* trace_r) {
+    ::smg::count_launch(), doi_decide_kernel<<<1, 1, 0, st>>>(states, batch, stats, strideStats, handle, use_handle, chain_status,
+                                                             trace_c, trace_r);
 }
 
 void doi_append(const DoiState* states, double* U, int64_t ldu, int64_t strideU, const double* e, int64_t strideE,

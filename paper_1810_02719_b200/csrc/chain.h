@@ -25,8 +25,11 @@ struct DoiState {
 
 void ritz_residual(const double* LZ, const double* Z, const double* theta, int n, int ncols, int64_t ld,
                    int64_t stride, int64_t strideTheta, int batch, double* partial, double* out, cudaStream_t st);
+// trace (optional, batch 1): per step t (0-based) the subspace size the step ran
+// with (trace_c[t]) and its residual ||e|| / scale (trace_r[t]), t < t_max
 void doi_decide(DoiState* states, int batch, const double* stats, int64_t strideStats,
-                cudaGraphConditionalHandle handle, int use_handle, const int* chain_status, cudaStream_t st);
+                cudaGraphConditionalHandle handle, int use_handle, const int* chain_status, cudaStream_t st,
+                int* trace_c = nullptr, double* trace_r = nullptr);
 void doi_append(const DoiState* states, double* U, int64_t ldu, int64_t strideU, const double* e, int64_t strideE,
                 int n, int batch, cudaStream_t st);
 void compute_delta(const double* trace, int ntiles, int n, double scale, double* delta, cudaStream_t st);

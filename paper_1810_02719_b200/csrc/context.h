@@ -3,6 +3,9 @@
 
 #include <string>
 
+#include <vector>
+
+#include "doi.h"
 #include "engine.h"
 #include "profiler.h"
 
@@ -12,6 +15,21 @@ struct smg_context {
     std::string error;
     bool profiling = false;
     smg::Profiler prof;
+    // DOI step log (smg_doi_trace_*): chain position, c the step ran with, residual
+    bool doi_trace = false;
+    std::vector<int> trace_pos, trace_c;
+    std::vector<double> trace_r;
+    void log_doi(const smg::DoiLoop& loop, int pos, int steps) {
+        if (!doi_trace) return;
+        std::vector<int> c;
+        std::vector<double> r;
+        loop.read_trace(steps, c, r);
+        for (size_t i = 0; i < c.size(); ++i) {
+            trace_pos.push_back(pos);
+            trace_c.push_back(c[i]);
+            trace_r.push_back(r[i]);
+        }
+    }
 };
 
 struct smg_operator {

@@ -18,6 +18,8 @@ void DoiLoop::build(const TileSet& ts, Workspace& ws, const DoiParams& prm, int6
     X_.alloc((size_t)ts.n * 3, st);
     if (ts.use_perm) P_.alloc(ts.n, st);
     state_.alloc(1, st);
+    trace_c_.alloc(std::max(prm.t_max, 1), st);
+    trace_r_.alloc(std::max(prm.t_max, 1), st);
     SMG_CUDA(cudaStreamSynchronize(st));
 
     SMG_CUDA(cudaGraphCreate(&graph_, 0));
@@ -62,7 +64,7 @@ void DoiLoop::build(const TileSet& ts, Workspace& ws, const DoiParams& prm, int6
     solve_block_tridiag(p, ts.W, cs);
     orth_batch(cx, ws, ws.V.get(), ws.U.get(), ws.ccap, dimC, true, -1);
     project_batch(cx, ws, ws.U.get(), ws.ccap, dimC, X_.get(), 0, nullptr, 0);
-    doi_decide(state, 1, ws.stats.get(), 4, h, 1, ws.status.get(), cs);
+    doi_decide(state, 1, ws.stats.get(), 4, h, 1, ws.status.get(), cs, trace_c_.get(), trace_r_.get());
     doi_append(state, ws.U.get(), ws.ld, ws.mstride(), ws.e.get(), ws.npad, ts.n, 1, cs);
     cudaGraph_t captured;
     SMG_CUDA(cudaStreamEndCapture(cs, &captured));
@@ -93,6 +95,16 @@ DoiState DoiLoop::run(const double* Ff, const double* Fb, const int32_t* perm, c
     SMG_CUDA(cudaMemcpyAsync(&r, state_.get(), sizeof(r), cudaMemcpyDeviceToHost, st_));
     SMG_CUDA(cudaStreamSynchronize(st_));
     return r;
+}
+
+void DoiLoop::read_trace(int steps, std::vector<int>& c, std::vector<double>& r) const {
+    steps = std::max(0, std::min(steps, prm_.t_max));
+    c.resize(steps);
+    r.resize(steps);
+    if (!steps) return;
+    SMG_CUDA(cudaMemcpyAsync(c.data(), trace_c_.get(), (size_t)steps * sizeof(int), cudaMemcpyDeviceToHost, st_));
+    SMG_CUDA(cudaMemcpyAsync(r.data(), trace_r_.get(), (size_t)steps * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    SMG_CUDA(cudaStreamSynchronize(st_));
 }
 
 }  // namespace smg

@@ -29,6 +29,8 @@ public:
     // with c_init columns.  Returns the final state; ws.U holds u (before the
     // final orthonormalize of a pending append, which the caller performs).
     DoiState run(const double* Ff, const double* Fb, const int32_t* perm, const double* X, double bbox, int c_init);
+    // per-step (c, residual) of the last run(), r.t entries
+    void read_trace(int steps, std::vector<int>& c, std::vector<double>& r) const;
 
 private:
     const TileSet* ts_ = nullptr;
@@ -39,6 +41,8 @@ private:
     DBuf<double> Ff_, Fb_, X_;
     DBuf<int32_t> P_;
     DBuf<DoiState> state_;
+    DBuf<int> trace_c_;
+    DBuf<double> trace_r_;
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t exec_ = nullptr;
 };

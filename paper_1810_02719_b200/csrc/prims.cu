@@ -268,6 +268,7 @@ smg_status smg_dynamic_oi(smg_context* ctx, const smg_operator* op, int32_t c, c
         DoiLoop loop;
         loop.build(op->ts, ws, dp, op->fs.strideF, st);
         DoiState r = loop.run(op->fs.f(0), op->fs.b(0), op->ts.perm_of(0), X.get(), bbox[0], c);
+        ctx->log_doi(loop, 0, r.t);
         check_ws(ws, st);
         StepCtx cx{st, &op->ts};
         if (r.appended_raw) {

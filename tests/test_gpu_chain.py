@@ -225,3 +225,24 @@ def test_chain_distance_weighting(ctx):
     bb = G.compute_block_bases_fixed_sizes(mesh, seg, cfg, [40] * seg.count, want_bases=True, ctx=ctx)
     ob = O.compute_block_bases_fixed_sizes(mesh.vertices, subs, seg.sequence, ocfg, [40] * seg.count)
     check_parity(mesh, bb, ob)
+
+
+@pytest.mark.parametrize("dense_limit", [512, 1023])
+def test_chain_cold_start_first_basis(ctx, dense_limit):
+    """n_d > dense_limit: the first basis is the reference's cold start,
+    random_orthonormal_basis(n_d, c, seed ^ 0x9E3779B97F4A7C15) followed by
+    initial_iterations OI steps (pipeline.hpp:118-119, spectral.hpp:134-141);
+    the Gaussian draws are libstdc++'s, so GPU and oracle start from the same
+    block and track the same iterates."""
+    mesh = synth.small_grid(64, 64, 32, 32, seed=9, flip=4)
+    seg = synth.grid_tiles(64, 64, 32, 32)
+    subs = O.build_submeshes(mesh.adj_offsets, mesh.adj_cols, seg.members)
+    kw = dict(subspace_size=24, iterations=1, shift_scale=1e-3, dense_limit=dense_limit, initial_iterations=12)
+    cfg = G.PipelineConfig(weighting="binary", **kw)
+    ocfg = O.PipelineConfig(weighting=O.BINARY, **kw)
+    bb = G.compute_block_bases_fixed_sizes(mesh, seg, cfg, [24] * seg.count, want_bases=True, ctx=ctx)
+    ob = O.compute_block_bases_fixed_sizes(mesh.vertices, subs, seg.sequence, ocfg, [24] * seg.count)
+    check_parity(mesh, bb, ob)
+    # the cold start is not the dense eigenbasis: 12 R^2 steps from a random block
+    dense = O.bottom_subspace(O.dense_eigendecomposition(O.build_laplacian(subs[0], mesh.vertices, O.BINARY)), 24)
+    assert O.max_principal_angle(ob.bases[0], dense) > 1e-6

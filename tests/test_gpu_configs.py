@@ -23,11 +23,81 @@ G = pytest.importorskip("paper_1810_02719_b200")
 from test_gpu_chain import check_parity, run_both  # noqa: E402
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C2", "C3"])
 def test_config_end_to_end(ctx, name):
     w = synth.config(name)
     bb, ob = run_both(ctx, w.mesh, w.seg, w.c, t=w.iterations)
     check_parity(w.mesh, bb, ob)
+
+
+def aligned_coefficients_close(ub, uo, cg, co, tol=1e-8):
+    """gft coefficients agree once the columns whose sign convention is a
+    rounding tie (two equal largest magnitudes) are aligned"""
+    s = np.sign(np.sum(ub * uo, axis=0))
+    mags = np.sort(np.abs(uo), axis=0)
+    tie = (mags[-1] - mags[-2]) <= 1e-9 * mags[-1]
+    assert np.all((s > 0) | tie), "sign convention differs on a column without a magnitude tie"
+    assert np.abs(cg * s[:, None] - co).max() <= tol * np.abs(co).max()
+
+
+def test_config1_as_configured(ctx):
+    """C1 as BASELINE.json states it: one 32x32 grid submesh,
+    build_laplacian -> ShiftedInverseOperator -> bottom_subspace(40) ->
+    orthogonal_iteration(op, init, 10) (spectral.hpp:204-211) -> gft / igft,
+    composed from the C-ABI primitives exactly as the reference composes its
+    functions.  Unlike compute_block_bases_fixed_sizes (position 0 never runs
+    OI, pipeline.hpp:177-178) the 10 R^2 + QR steps run here."""
+    w = synth.config("C1")
+    mem = w.seg.members[0]
+    rp, cols, vals, tr = G.build_laplacian(w.mesh, mem, weighting="binary", ctx=ctx)
+    op = G.ShiftedInverseOperator(rp, cols, vals, G.default_shift(tr, mem.size, 1e-3), 2, ctx=ctx)
+    init = G.bottom_subspace(op, w.c)
+    u = G.orthogonal_iteration(op, init, w.iterations)
+    x = w.mesh.vertices[np.sort(mem)]
+    cg = G.gft(u, x, ctx=ctx)
+    xh = G.igft(u, cg, ctx=ctx)
+
+    sub = O.build_submeshes(w.mesh.adj_offsets, w.mesh.adj_cols, [mem])[0]
+    lap = O.build_laplacian(sub, w.mesh.vertices, O.BINARY)
+    assert tr == lap.trace()
+    oop = O.ShiftedInverseOperator(lap, O.default_shift(lap, 1e-3), 2)
+    oinit = O.bottom_subspace(O.dense_eigendecomposition(lap), w.c)
+    uo = O.orthogonal_iteration(oop, oinit, w.iterations)
+    co = O.gft(uo, sub.local_coords(w.mesh.vertices))
+    xo = O.igft(uo, co)
+    assert O.max_principal_angle(init, oinit) < 1e-9
+    assert O.max_principal_angle(u, uo) < 1e-8
+    assert np.abs(u.T @ u - np.eye(w.c)).max() < 1e-12
+    aligned_coefficients_close(u, uo, cg, co)
+    assert np.abs(xh - xo).max() <= 1e-9 * np.abs(xo).max()
+    # OI from the exact eigenbasis is a fixed point (SPEC.md:264)
+    assert O.max_principal_angle(u, init) < 1e-9
+
+
+def test_config5_full_workload_two_chains_match_oracle(ctx):
+    """The full C5 workload (64 meshes, 128 tiles each, c = 200) through the
+    same batched call the benchmark makes -- so the kernels and orderings the
+    bench measures are the ones checked -- with meshes 0 and 63 compared to
+    the oracle on every tile: subspace angle, residual_rms, gft coefficients
+    and the stitched reconstruction."""
+    ws = [synth.config("C5", mesh_index=i) for i in range(64)]
+    cfg = G.PipelineConfig(weighting="binary", subspace_size=200, iterations=1, shift_scale=1e-3)
+    sizes = [200] * ws[0].seg.count
+    out = G.run_chains([w.mesh for w in ws], [w.seg for w in ws], cfg, sizes, want_bases=False, ctx=ctx)
+    ocfg = O.PipelineConfig(weighting=O.BINARY, subspace_size=200, iterations=1, shift_scale=1e-3)
+    for i in (0, 63):
+        w = ws[i]
+        subs = O.build_submeshes(w.mesh.adj_offsets, w.mesh.adj_cols, w.seg.members)
+        ob = O.compute_block_bases_fixed_sizes(w.mesh.vertices, subs, w.seg.sequence, ocfg, sizes)
+        rec = O.coarse_reconstruct_points(ob, w.mesh.vertices)
+        err = np.linalg.norm(out[i].reconstruction - rec, axis=1).max() / np.linalg.norm(rec, axis=1).max()
+        assert err < 1e-9, (i, err)
+        for t in range(w.seg.count):
+            ro, rg = ob.stats[t].residual_rms, out[i].stats[t].residual_rms
+            assert abs(rg - ro) <= 1e-9 * ro, (i, t, rg, ro)
+            co = O.gft(ob.bases[t], subs[t].local_coords(w.mesh.vertices))
+            # subspace-invariant: |C| row norms are sign free; the projection is exact
+            assert np.abs(np.abs(out[i].coefficients[t]) - np.abs(co)).max() <= 1e-8 * np.abs(co).max(), (i, t)
 
 
 @pytest.mark.parametrize("env", [{}, {"SMG_SOLVE_CS": "32", "SMG_ORDERING": "geometric"}])
