@@ -8,14 +8,16 @@ the batched configuration the metric's multi-GPU scaling is quoted on.  One
 assembly, factorisation, first-submesh basis, OI tracking, projection, stitched
 reconstruction (+ the NCCL gather of per-mesh results to all ranks when N > 1).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5|C2|C3|C4]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1|C2|C3|C4|C5|F3|F4]
   python bench.py --impl reference ...     # CPU oracle (port) arm
 
-Chains shard across ranks with no data-path collective.  Default: weak
-scaling -- each GPU carries config 5's 64-mesh shard (mesh ids rank*64 ..
-rank*64+63, each its own seed), the job grows with N; `--strong` splits the 64
-meshes over the N GPUs instead.  The per-mesh reconstructions are all-gathered
-(NCCL over NVLink) at the end of every step.  Timing: W untimed warm-up steps, then K steps
+`--gpus N` (N > 1) re-launches itself under torch.distributed.run with N
+ranks.  Chains shard across ranks with no data-path collective.  Default: the
+literal config 5 -- its 64 meshes split over the N GPUs (strong scaling);
+at N > 1 the same run also measures weak scaling (every GPU a 64-mesh shard,
+mesh ids rank*64 .., each its own seed) as `weak_scaling`; `--weak` makes that
+the headline.  The per-mesh reconstructions are all-gathered (NCCL over
+NVLink) at the end of every step.  Timing: W untimed warm-up steps, then K steps
 bracketed by barrier + synchronize, CUDA events on the launching device, max
 over ranks.  Inputs (0.9 GB for C5) exceed the 126 MB L2.
 """
@@ -52,8 +54,18 @@ CONFIGS = {
                     "(1 048 576 vertices, 2 093 058 faces), reference default BilateralParams"),
     "C2": dict(W=256, H=256, tw=32, th=32, c=100, t=1, meshes=1, sigma=0.005, seed0=202,
                desc="256^2 grid, 64 tiles of 32x32 (n_d=1024), c=100, t=1"),
+    # single chains (replicas only across GPUs)
+    "C1": dict(W=32, H=32, tw=32, th=32, c=40, t=10, meshes=1, single=True, seed0=101,
+               desc="one 32x32 grid submesh (n_d=1024): bottom_subspace(40) + orthogonal_iteration(op, init, 10) + "
+                    "gft/igft, composed from the C-ABI primitives (SURVEY.md §3.3)"),
+    "C3": dict(W=0, H=0, tw=0, th=0, c=60, t=1, meshes=1, synth="C3", seed0=303,
+               desc="icosphere level 7 (163 842 vertices), 160 polar-band blocks (n_d=1026), c=60, t=1, "
+                    "low-pass reconstruction"),
+    "C4": dict(W=1024, H=1024, tw=64, th=64, c=20, t=0, meshes=1, synth="C4", doi=True, seed0=404,
+               desc="1024^2 grid, 256 tiles of 64x64 (n_d=4096), DOI c in [20, 400], band 1e-5/1e-4"),
 }
 PINNED = dict(weighting="binary", power=2, shift_scale=1e-3, dense_limit=4096)
+DOI = dict(c_min=20, c_max=400, eps_low=1e-5, eps_high=1e-4)  # C4
 
 
 def parse():
@@ -64,7 +76,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--meshes", type=int, default=0, help="override the per-GPU mesh count (debug)")
-    ap.add_argument("--strong", action="store_true", help="split the config's meshes over the GPUs (strong scaling)")
+    ap.add_argument("--strong", action="store_true",
+                    help="(default) split the config's 64 meshes over the GPUs: the literal C5 (strong scaling)")
+    ap.add_argument("--weak", action="store_true",
+                    help="every GPU carries the config's full mesh count (weak scaling); at N > 1 the default "
+                         "run also reports this as `weak_scaling`")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tiles", type=int, default=8, help="tiles per chain in the CPU sample")
     return ap.parse_args()
@@ -73,11 +89,18 @@ def parse():
 # ----------------------------------------------------------------------- inputs
 
 def build_inputs(cfg, mesh_ids):
+    """(topology mesh, segmentation, per-chain vertices, member offsets, members).
+    Grid configs share one topology (each mesh its own seeded surface);
+    C3 / C4 come from synth.config (the parity tests' inputs)."""
     import numpy as np
     from paper_1810_02719_b200 import synth
-    base = synth.grid_mesh(cfg["W"], cfg["H"], cfg["seed0"], cfg["sigma"])
-    seg = synth.grid_tiles(cfg["W"], cfg["H"], cfg["tw"], cfg["th"])
-    verts = [synth.grid_vertices(cfg["W"], cfg["H"], cfg["seed0"] + i, cfg["sigma"]) for i in mesh_ids]
+    if "synth" in cfg:
+        w = synth.config(cfg["synth"])
+        base, seg, verts = w.mesh, w.seg, [w.mesh.vertices for _ in mesh_ids]
+    else:
+        base = synth.grid_mesh(cfg["W"], cfg["H"], cfg["seed0"], cfg["sigma"])
+        seg = synth.grid_tiles(cfg["W"], cfg["H"], cfg["tw"], cfg["th"])
+        verts = [synth.grid_vertices(cfg["W"], cfg["H"], cfg["seed0"] + i, cfg["sigma"]) for i in mesh_ids]
     offs, members = seg.flat()
     return base, seg, verts, np.asarray(offs, np.int32), np.asarray(members, np.int32)
 
@@ -153,7 +176,8 @@ class GpuJob:
         self.K = seg.count
         self.nd = seg.block_size
         self.B = len(mesh_ids)
-        c = cfg["c"]
+        self.doi = bool(cfg.get("doi"))
+        c = cfg["c"] if not self.doi else min(DOI["c_max"], self.nd)  # coefficient capacity
         dev = torch.device("cuda", device)
         self.torch, self.dev = torch, dev
         seq = np.arange(self.K, dtype=np.int32)
@@ -170,6 +194,8 @@ class GpuJob:
         self.h_recon = torch.empty((self.B, 3 * self.n), dtype=torch.float64).pin_memory()
         self.h_coef = torch.empty((self.B, self.ncoef), dtype=torch.float64).pin_memory()
         self.stats = [np.zeros((5, self.K)) for _ in range(self.B)]
+        self.sizes_out = [np.zeros(self.K, np.int32) for _ in range(self.B)]
+        self.iters_out = [np.zeros(self.K, np.int32) for _ in range(self.B)]
         self.coef_off = [np.zeros(self.K + 1, np.int64) for _ in range(self.B)]
         self.sizes = np.full(self.K, c, np.int32)
         self.pcfg = _abi.smg_pipeline_config()
@@ -179,6 +205,11 @@ class GpuJob:
         self.pcfg.iterations = cfg["t"]
         self.pcfg.power = PINNED["power"]
         self.pcfg.shift_scale = PINNED["shift_scale"]
+        if self.doi:
+            self.pcfg.subspace_size = cfg["c"]
+            self.pcfg.basis_mode = _abi.BASIS_MODE["doi"]
+            self.pcfg.c_min, self.pcfg.c_max = DOI["c_min"], DOI["c_max"]
+            self.pcfg.eps_low, self.pcfg.eps_high = DOI["eps_low"], DOI["eps_high"]
         self._abi = _abi
         self.views = {on: self._views(on) for on in (0, 1)}
         # per-mesh coordinates + the shared topology once (the library stages host
@@ -207,11 +238,11 @@ class GpuJob:
             s.sequence_length, s.sequence, s.on_device = self.K, conn["seq"].data_ptr(), on_device
             o = outs[b]
             st = self.stats[b]
-            o.subspace_size = None
+            o.subspace_size = self.sizes_out[b].ctypes.data
             o.residual_rms = st[1].ctypes.data
             o.doi_residual = st[2].ctypes.data
             o.converged = None
-            o.oi_iterations = None
+            o.oi_iterations = self.iters_out[b].ctypes.data
             o.reconstruction = recon[b].data_ptr()
             o.coefficients = coef[b].data_ptr()
             o.coefficients_capacity = self.ncoef
@@ -221,9 +252,29 @@ class GpuJob:
 
     def run(self, on_device):
         meshes, segs, outs = self.views[on_device]
-        st = self.ctx.lib.smg_run_chains(self.ctx.handle, self.B, meshes, segs, self.pcfg,
-                                         self.sizes.ctypes.data, outs)
+        if self.doi:  # compute_block_bases, DOI branch (one chain)
+            st = self.ctx.lib.smg_compute_block_bases(self.ctx.handle, meshes, segs, self.pcfg, outs)
+        else:
+            st = self.ctx.lib.smg_run_chains(self.ctx.handle, self.B, meshes, segs, self.pcfg,
+                                             self.sizes.ctypes.data, outs)
         self.ctx.check(st)
+
+
+def _solve_flops(cfg, job, trajectory, W_used):
+    """Algorithmic and executed flops of one step's solve
+    launches: z*4*n_d*b*c per tile and OI step with b the natural-order
+    half-bandwidth, + the first basis's shift-invert bootstrap (4 iterations on
+    m columns, the first with z = 1).  The executed count is the block solve's
+    own, 3*n*W*cols per triangular sweep (2z sweeps per step) at the block
+    width the library chose.  `trajectory`: per chain, the c of every OI step."""
+    n, z = job.nd, PINNED["power"]
+    b_half = (cfg["tw"] + 1) if cfg["tw"] else 33  # C3: 33 nominal (SURVEY.md §8(d))
+    c0 = cfg["c"]
+    m_fb = min(n, max(c0, min(480, -(-(c0 + max(16, c0 // 6)) // 8) * 8)))
+    cols = sum(sum(tr) for tr in trajectory)
+    alg = z * 4.0 * n * b_half * cols + job.B * (1 + 3 * z) * 4.0 * n * b_half * m_fb
+    hw = 3.0 * n * W_used * (2 * z * cols + job.B * (2 + 3 * 2 * z) * m_fb)
+    return alg, hw, b_half
 
 
 def gpu_arm(args, cfg, rank, world, local_rank):
@@ -236,15 +287,34 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    ctx = G.Context(local_rank)
+    out = measure_job(args, cfg, rank, world, local_rank, ctx, dist, weak=args.weak)
+    if out is not None and world > 1 and cfg["meshes"] > 1 and not args.weak:
+        # the second scaling mode on the same ranks: every GPU carries a full
+        # 64-mesh shard (weak scaling); the headline stays the literal config
+        w = measure_job(args, cfg, rank, world, local_rank, ctx, dist, weak=True, brief=True)
+        if w is not None:
+            out["weak_scaling"] = w
+    elif world > 1 and cfg["meshes"] > 1 and not args.weak:
+        measure_job(args, cfg, rank, world, local_rank, ctx, dist, weak=True, brief=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    ctx.close()
+    return out if rank == 0 else None
+
+
+def measure_job(args, cfg, rank, world, local_rank, ctx, dist, weak=False, brief=False):
+    import numpy as np
+    import torch
+    from paper_1810_02719_b200 import shard
     per_gpu = args.meshes or cfg["meshes"]
-    total_meshes = per_gpu if args.strong else per_gpu * world
+    total_meshes = per_gpu * world if weak else per_gpu
     if cfg["meshes"] == 1:  # single-chain configs: replicas only
         ids = [rank]
         total_units = world
     else:
         ids = shard.shard_meshes(total_meshes, world, rank)
         total_units = total_meshes
-    ctx = G.Context(local_rank)
     job = GpuJob(cfg, ids, local_rank, ctx)
     verts_per_unit = job.n
     gather = dist is not None and cfg["meshes"] > 1
@@ -260,6 +330,12 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def launches():
+        import ctypes as C
+        n, t = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, b"launches", C.byref(n), C.byref(t))
+        return n.value
 
     def timed(on_device, steps, profile=False):
         lib = ctx.lib
@@ -283,21 +359,26 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             ms = float(t.item())
         return ms, nl
 
-    def launches():
-        import ctypes as C
-        n, t = C.c_int64(), C.c_double()
-        ctx.lib.smg_profile_read(ctx.handle, b"launches", C.byref(n), C.byref(t))
-        return n.value
-
-    for _ in range(args.warmup):
+    # untimed: the run's choices and (DOI) the c of every step
+    if job.doi:
+        ctx.doi_trace(True)
+        job.run(True)
+        _, c_steps, _ = ctx.read_doi_trace()
+        ctx.doi_trace(False)
+        trajectory = [list(map(int, c_steps))]
+    else:
+        job.run(True)
+        trajectory = [[cfg["c"]] * ((job.K - 1) * cfg["t"])] * job.B
+    info = ctx.last_run_info()
+    for _ in range(max(0, args.warmup - 1)):
         step(True)
     with ClockSampler(local_rank) as clk:
         ms, nl = timed(True, args.steps, profile=True)
     clocks = clk.summary()
     stages = {}
     import ctypes as C
-    for nm in ("assemble", "factor", "first_basis", "fb_iterate", "fb_filter", "fb_rayleigh_ritz", "solve", "orthonormalize",
-               "gram", "chol", "trmm", "project"):
+    for nm in ("assemble", "factor", "first_basis", "fb_iterate", "fb_filter", "fb_rayleigh_ritz", "solve",
+               "orthonormalize", "gram", "chol", "trmm", "project"):
         n, t = C.c_int64(), C.c_double()
         ctx.lib.smg_profile_read(ctx.handle, nm.encode(), C.byref(n), C.byref(t))
         stages[nm] = {"launches": n.value, "ms": t.value / args.steps}
@@ -310,155 +391,306 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     units = total_units * verts_per_unit
     value = units / (ms_step / 1e3)
     e2e_value = units / (ms_e2e / args.steps / 1e3)
+    scaling = "weak" if (weak or cfg["meshes"] == 1) else "strong"
+    if brief:
+        return {"value": value, "unit": "vertices/s", "ms_per_step": ms_step, "scaling": scaling,
+                "meshes": total_units, "meshes_per_gpu": len(ids),
+                "e2e": {"value": e2e_value, "unit": "vertices/s"}, "clocks": clocks}
 
     # roofline of the dominant kernel (solve: the block-tridiagonal R^z sweeps).
-    # Algorithmic flops: z*4*n_d*b*c per tile and OI iteration,
-    # b = half-bandwidth in the natural order; the "solve" stage also holds the
-    # first basis's shift-invert bootstrap (4 iterations on m columns, the first
-    # with z = 1).  Launch durations are CUDA-event spans on the launching
-    # stream inside the timed region; two chain groups share the GPU, so a
-    # launch's span includes time the other group's kernels occupy SMs.
-    c, n, B, K, t = cfg["c"], job.nd, job.B, job.K, cfg["t"]
-    b_half = cfg["tw"] + 1
-    z = PINNED["power"]
-    m_fb = min(n, max(c, min(480, -(-(c + max(16, c // 2)) // 8) * 8)))
+    # Launch durations are CUDA-event spans on the launching stream inside the
+    # timed region; with two chain groups a launch's span includes time the
+    # other group's kernels occupy SMs.
+    W_used = info["block_width"]
+    alg, hw, b_half = _solve_flops(cfg, job, trajectory, W_used)
     solve = stages["solve"]
-    solve_launches_per_step = solve["launches"] / args.steps if solve["launches"] else 0
-    solve_flops_step = B * ((K - 1) * t * z * 4.0 * n * b_half * c + (1 + 3 * z) * 4.0 * n * b_half * m_fb)
-    flops_per_launch = solve_flops_step / max(solve_launches_per_step, 1e-9)
-    avg_ms = solve["ms"] / max(solve_launches_per_step, 1e-9)
-    achieved = solve_flops_step / (solve["ms"] * 1e-3) / 1e12 if solve["ms"] > 0 else None
+    spl = solve["launches"] / args.steps if solve["launches"] else 0
+    achieved = alg / (solve["ms"] * 1e-3) / 1e12 if solve["ms"] > 0 else None
     traffic = None
     try:  # dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "solve_traffic_r01.json")) as f:
-            traffic = json.load(f)["dram_bytes_per_launch"]
+            traffic = json.load(f)["dram_bytes_per_launch"] if args.config == "C5" else None
     except (OSError, KeyError, ValueError):
         pass
-    # the factorisation's ordering picks the block width: the geometric order gives
-    # 32x64 grid tiles W = 32 (band 33) where the natural order has 65, so the
-    # DMMA work done is below the SURVEY's algorithmic figure (kept as the
-    # contract's numerator); hw_flops_per_launch is the block solve's own count
-    W_used = 32 if B * K >= 2048 else 64
-    # per triangular sweep 3*n*W*cols flops (triangular half + full coupling half);
-    # an OI step is 2z sweeps, the bootstrap 2 + 3*2z sweeps on m columns
-    hw_step = B * 3.0 * n * W_used * ((K - 1) * t * 2 * z * c + (2 + 3 * 2 * z) * m_fb)
     roofline = {"kernel": "solve_kernel (block-tridiagonal R^z sweeps, DMMA f64)", "bound": "tensor",
                 "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
                 "traffic_source": "profiles/solve_traffic_r01.json (bytes per launch of 32 chains)",
                 "peak_source": "measured FP64 DMMA peak, profiles/fp64_peak_r01.txt (MEASURED_PEAKS.json has no FP64 entry)",
-                "flops_per_launch": flops_per_launch, "avg_launch_ms": avg_ms,
-                "b_algorithmic": b_half, "block_width_used": W_used,
-                "hw_flops_per_launch": hw_step / max(solve_launches_per_step, 1e-9),
-                "hw_frac": (hw_step / (solve["ms"] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS) if solve["ms"] > 0 else None,
-                "launches_per_step": solve_launches_per_step,
+                "flops_per_launch": alg / max(spl, 1e-9), "avg_launch_ms": solve["ms"] / max(spl, 1e-9),
+                "b_algorithmic": b_half, "block_width_used": W_used, "ordering": info["ordering"],
+                "hw_flops_per_launch": hw / max(spl, 1e-9),
+                "hw_frac": (hw / (solve["ms"] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS) if solve["ms"] > 0 else None,
+                "launches_per_step": spl,
                 "step_share": solve["ms"] / ms_step if ms_step else None}
     # whole-step algorithmic FP64 work (SURVEY.md §8(d) formulas, per GPU)
-    per_tile = z * 4.0 * n * b_half * c * t + (4.0 * n * c * c) * t + n * b_half ** 2 + 12.0 * n * c + 3 * n
-    first = (4.0 / 3.0) * n ** 3 + 2.0 * n * n * c
-    step_flops = B * ((K - 1) * per_tile + first)
+    # z*4*n*b*c + 4*n*c^2 per OI step, n*b^2 + 12*n*c + 3*n per tile, (4/3)n^3 + 2n^2c first tile
+    n, z, c = job.nd, PINNED["power"], cfg["c"]
+    oi = sum(z * 4.0 * n * b_half * cc + 4.0 * n * cc * cc for tr in trajectory for cc in tr)
+    c_tiles = sum(int(v) for s in job.sizes_out for v in s) if job.doi else job.B * job.K * c
+    tiles = job.B * job.K * (n * b_half ** 2 + 3.0 * n) + 12.0 * n * c_tiles
+    first = job.B * ((4.0 / 3.0) * n ** 3 + 2.0 * n * n * c)
+    step_flops = oi + tiles + first
+    # steady state: the chain without its first-submesh basis
+    fb_ms = stages["first_basis"]["ms"]
+    steady = units * (job.K - 1) / job.K / ((ms_step - fb_ms) / 1e3) if ms_step > fb_ms > 0 else None
     out = {
         "metric": METRIC, "value": value, "unit": "vertices/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "strong" if (args.strong and cfg["meshes"] > 1) else "weak",
+        "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded sinusoid height-field grids + N(0,sigma^2) noise; no dataset exists)",
+        "data": "synthetic (seeded sinusoid height-field grids / icosphere + noise; no dataset exists)",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes": total_units, "meshes_per_gpu": len(ids),
-                   "tiles_per_mesh": K,
-                   "n_d": n, "c": c, "oi_iterations": t, "z": z, "shift_scale": PINNED["shift_scale"],
-                   "weighting": PINNED["weighting"], "tile_order": "row-major",
+                   "tiles_per_mesh": job.K, "n_d": n, "c": c if not job.doi else "DOI [20, 400]",
+                   "oi_iterations": cfg["t"], "z": z, "shift_scale": PINNED["shift_scale"],
+                   "weighting": PINNED["weighting"], "tile_order": "row-major" if cfg["tw"] else "partition order",
                    "parallelism": (f"chains sharded over {world} GPU(s), "
-                                   + (f"{total_meshes} meshes split (strong)" if args.strong
-                                      else f"{len(ids)} meshes per GPU (weak)")) if cfg["meshes"] > 1 else "replicas",
+                                   + (f"{len(ids)} meshes per GPU (weak)" if weak
+                                      else f"{total_meshes} meshes split (strong)")) if cfg["meshes"] > 1
+                   else "replicas",
                    "l2": "inputs larger than L2 (%.0f MB per GPU)" % (job.h2d_bytes / 1e6)},
         "e2e": {"value": e2e_value, "unit": "vertices/s", "h2d_bytes_per_step": job.h2d_bytes,
                 "d2h_bytes_per_step": job.d2h_bytes},
         "roofline": roofline,
+        "steady_state": {"value": steady, "unit": "vertices/s",
+                         "note": "chain without the first-submesh basis (its device time subtracted)"},
         "fp64_step_efficiency": {"algorithmic_tflop_per_step": step_flops / 1e12,
                                  "achieved_tflops": step_flops / (ms_step * 1e-3) / 1e12,
                                  "frac_of_peak": step_flops / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
         "stages_ms_per_step": {k: round(v["ms"], 3) for k, v in stages.items()},
+        "run_info": info,
         "clocks": clocks,
         "gpu_launches": nl,
     }
+    if job.doi:
+        out["config"]["doi_steps"] = len(trajectory[0])
+        out["config"]["c_final"] = {"min": int(job.sizes_out[0].min()), "max": int(job.sizes_out[0].max())}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, cfg, total_units)
-    if dist is not None:
-        dist.destroy_process_group()
+    return out if rank == 0 else None
+
+
+def single_arm(args, cfg, rank, world, local_rank):
+    """C1: the reference has no single-call entry; the path is
+    the composition build_laplacian -> ShiftedInverseOperator ->
+    bottom_subspace(c) -> orthogonal_iteration(op, init, 10) -> gft / igft,
+    here through the C-ABI primitives (host pointers: every call copies its
+    inputs in and its results out, so `value` already includes the copies and
+    equals `e2e`).  Replicas only across GPUs."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    import paper_1810_02719_b200 as G
+    from paper_1810_02719_b200 import synth
+    torch.cuda.set_device(local_rank)
+    ctx = G.Context(local_rank)
+    w = synth.config(args.config)
+    mem = np.sort(w.seg.members[0])
+    x = w.mesh.vertices[mem]
+    n = int(mem.size)
+
+    def step():
+        rp, cols, vals, tr = G.build_laplacian(w.mesh, mem, weighting="binary", ctx=ctx)
+        op = G.ShiftedInverseOperator(rp, cols, vals, G.default_shift(tr, n, PINNED["shift_scale"]), PINNED["power"],
+                                      ctx=ctx)
+        u = G.orthogonal_iteration(op, G.bottom_subspace(op, cfg["c"]), cfg["t"])
+        return G.igft(u, G.gft(u, x, ctx=ctx), ctx=ctx)
+
+    def launches():
+        nn, t = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, b"launches", C.byref(nn), C.byref(t))
+        return nn.value
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    ctx.lib.smg_profile_enable(ctx.handle, 1)
+    l0 = launches()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms_step = ev0.elapsed_time(ev1) / args.steps
+    nl = launches() - l0
+    stages = {}
+    for nm in ("assemble", "factor", "first_basis", "solve", "orthonormalize", "gram", "chol", "trmm", "project"):
+        nn, t = C.c_int64(), C.c_double()
+        ctx.lib.smg_profile_read(ctx.handle, nm.encode(), C.byref(nn), C.byref(t))
+        stages[nm] = round(t.value / args.steps, 3)
+    ctx.lib.smg_profile_enable(ctx.handle, 0)
     ctx.close()
+    z, c, t = PINNED["power"], cfg["c"], cfg["t"]
+    b_half = cfg["tw"] + 1
+    oi_flops = t * (z * 4.0 * n * b_half * c + 4.0 * n * c * c)
+    value = world * n / (ms_step / 1e3)
+    h2d = x.nbytes + mem.nbytes + w.mesh.adj_offsets.nbytes + w.mesh.adj_cols.nbytes + w.mesh.vertices.nbytes
+    out = {"metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded sinusoid height-field grid)",
+           "config": {"workload": f"{args.config}: {cfg['desc']}", "n_d": n, "c": c, "oi_iterations": t, "z": z,
+                      "shift_scale": PINNED["shift_scale"], "parallelism": "replicas",
+                      "l2": "tiny single submesh (latency-bound)"},
+           "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(n * 3 * 8 * 2 + c * 3 * 8)},
+           "roofline": {"kernel": "the 10 OI steps (solve + CholeskyQR2)", "bound": "tensor",
+                        "achieved": oi_flops / ((stages["solve"] + stages["orthonormalize"]) * 1e-3) / 1e12
+                        if stages["solve"] > 0 else None,
+                        "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                        "frac": oi_flops / ((stages["solve"] + stages["orthonormalize"]) * 1e-3) / 1e12
+                        / FP64_PEAK_TFLOPS if stages["solve"] > 0 else None, "traffic": None,
+                        "note": "one 1024 x 40 block: latency-bound (a few CTAs); frac of the whole GPU's peak"},
+           "stages_ms_per_step": stages, "clocks": clk.summary(), "gpu_launches": nl}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, cfg, 1)
     return out if rank == 0 else None
 
 
 # ----------------------------------------------------------------------- CPU arm
 
-def _cpu_chain(task):
-    """One chain of the oracle over the first T tiles: (t_first, t_rest) seconds."""
-    cfgname, mesh_id, T = task
+_CPU_STATE = {}
+
+
+def _cpu_prepare(task):
+    """Untimed: build one chain's inputs in the worker (mesh, submeshes)."""
+    cfgname, mesh_id = task
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
     import specmesh_oracle as O
     from paper_1810_02719_b200 import synth
     cfg = CONFIGS[cfgname]
-    base = synth.grid_mesh(cfg["W"], cfg["H"], cfg["seed0"] + mesh_id, cfg["sigma"])
-    seg = synth.grid_tiles(cfg["W"], cfg["H"], cfg["tw"], cfg["th"])
-    subs = O.build_submeshes(base.adj_offsets, base.adj_cols, seg.members[:T])
-    ocfg = O.PipelineConfig(weighting=O.BINARY, subspace_size=cfg["c"], iterations=cfg["t"],
-                            shift_scale=PINNED["shift_scale"])
+    if "synth" in cfg or cfg.get("single"):
+        w = synth.config(cfgname)
+        base, seg = w.mesh, w.seg
+    else:
+        base = synth.grid_mesh(cfg["W"], cfg["H"], cfg["seed0"] + mesh_id, cfg["sigma"])
+        seg = synth.grid_tiles(cfg["W"], cfg["H"], cfg["tw"], cfg["th"])
+    subs = O.build_submeshes(base.adj_offsets, base.adj_cols, seg.members)
+    _CPU_STATE[task] = (base, seg, subs)
+    return os.getpid()
+
+
+def _cpu_chain(task):
+    """One whole chain of the oracle port, timed like the reference's
+    StageTimings (core.hpp:57-68): track + project + reconstruct.  Returns
+    (chain seconds, first-basis seconds, vertices)."""
+    import numpy as np
+    import specmesh_oracle as O
+    O.ShiftedInverseOperator.rcm_above = 0  # bandwidth-minimising order, as the GPU's geometric ordering
+    cfgname, mesh_id = task
+    if task not in _CPU_STATE:
+        _cpu_prepare(task)
+    base, seg, subs = _CPU_STATE[task]
+    cfg = CONFIGS[cfgname]
+    if cfg.get("single"):
+        # C1 (SURVEY.md §3.3): build_laplacian -> operator -> dense eig + bottom_subspace
+        # -> orthogonal_iteration(op, init, t) -> gft / igft
+        t0 = time.perf_counter()
+        lap = O.build_laplacian(subs[0], base.vertices, O.BINARY)
+        op = O.ShiftedInverseOperator(lap, O.default_shift(lap, PINNED["shift_scale"]), PINNED["power"])
+        init = O.bottom_subspace(O.dense_eigendecomposition(lap), cfg["c"])
+        t1 = time.perf_counter()
+        u = O.orthogonal_iteration(op, init, cfg["t"])
+        O.igft(u, O.gft(u, subs[0].local_coords(base.vertices)))
+        t2 = time.perf_counter()
+        return t2 - t0, t1 - t0, base.n
     t0 = time.perf_counter()
-    bb1 = O.compute_block_bases_fixed_sizes(base.vertices, subs[:1], np.arange(1), ocfg, [cfg["c"]])
-    O.project_blocks(bb1, base.vertices)
+    if cfg.get("doi"):
+        ocfg = O.PipelineConfig(weighting=O.BINARY, subspace_size=cfg["c"], shift_scale=PINNED["shift_scale"], **DOI)
+        bb = O.compute_block_bases_doi(base.vertices, subs, seg.sequence, ocfg)
+        fb = 0.0
+    else:
+        ocfg = O.PipelineConfig(weighting=O.BINARY, subspace_size=cfg["c"], iterations=cfg["t"],
+                                shift_scale=PINNED["shift_scale"])
+        bb = O.compute_block_bases_fixed_sizes(base.vertices, subs, seg.sequence, ocfg, [cfg["c"]] * seg.count)
+        fb = bb.timings.get("first_basis", 0.0)
+    O.reconstruct_weighted(subs, O.project_blocks(bb, base.vertices), base.n)
     t1 = time.perf_counter()
-    bb = O.compute_block_bases_fixed_sizes(base.vertices, subs, np.arange(T), ocfg, [cfg["c"]] * T)
-    locals_ = O.project_blocks(bb, base.vertices)
-    t2 = time.perf_counter()
-    return t1 - t0, (t2 - t1) - (t1 - t0)
+    return t1 - t0, fb, base.n
+
+
+class CpuArm:
+    """The oracle port on the host cores: one whole chain per core (BLAS 1
+    thread), the reference's only concurrency (detail::parallel_for,
+    core.hpp:84-100).  A step = P whole chains; its time = the slowest chain."""
+
+    def __init__(self, cfgname, P, first_mesh=0):
+        import multiprocessing as mp
+        for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[k] = "1"
+        self.cfgname, self.P = cfgname, P
+        self.tasks = [(cfgname, first_mesh + i) for i in range(P)]
+        self.pool = mp.get_context("fork").Pool(P, maxtasksperchild=None)
+        # pin one task per worker: prepare all inputs (untimed)
+        self.pool.map(_cpu_prepare, self.tasks, chunksize=1)
+
+    def step(self):
+        res = self.pool.map(_cpu_chain, self.tasks, chunksize=1)
+        return max(r[0] for r in res), sum(r[2] for r in res), statistics.mean(r[1] for r in res)
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
 
 
 def cpu_baseline(args, cfg, total_units):
-    """The oracle restatement timed on the host cores (one chain per core, BLAS 1 thread),
-    on a bounded sample: the first T tiles of P chains, extrapolated per chain to all tiles."""
-    import multiprocessing as mp
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    os.environ["OMP_NUM_THREADS"] = "1"
-    os.environ["MKL_NUM_THREADS"] = "1"
+    """Rank 0, N=1: one step of the CPU arm (bounded: P whole chains on P cores)."""
     cores = os.cpu_count() or 1
-    P = min(cores, max(1, total_units if cfg["meshes"] > 1 else 1))
-    T = max(2, args.cpu_tiles)
-    K = (cfg["W"] // cfg["tw"]) * (cfg["H"] // cfg["th"])
-    T = min(T, K)
-    ctxm = mp.get_context("spawn")
-    t0 = time.perf_counter()
-    with ctxm.Pool(P) as pool:
-        res = pool.map(_cpu_chain, [(args.config, i, T) for i in range(P)])
-    wall = time.perf_counter() - t0
-    t_first = sum(r[0] for r in res) / P
-    t_rest = sum(r[1] for r in res) / P / max(T - 1, 1)
-    t_chain = t_first + (K - 1) * t_rest
-    n_mesh = cfg["W"] * cfg["H"]
-    rounds = math.ceil(total_units / P)
-    value = total_units * n_mesh / (rounds * t_chain)
-    return {"value": value, "unit": "vertices/s", "cores": P, "kind": "port",
-            "sample": f"{P} chains in parallel (1 per core, BLAS 1 thread) x first {T} of {K} tiles "
-                      f"(numpy/LAPACK oracle, oracle/specmesh_oracle.py); per chain t_first={t_first:.2f}s "
-                      f"+ {K - 1} x t_tile={t_rest:.3f}s extrapolated; sample wall {wall:.1f}s"}
+    P = min(cores, max(1, total_units))
+    arm = CpuArm(args.config, P)
+    try:
+        t, verts, tfb = arm.step()
+    finally:
+        arm.close()
+    return {"value": verts / t, "unit": "vertices/s", "cores": P, "kind": "port",
+            "steady_state_value": verts / (t - tfb) if t > tfb else None,
+            "sample": f"{P} whole chains ({cfg['desc']}) in parallel, 1 per core, BLAS 1 thread; numpy/LAPACK "
+                      f"restatement oracle/specmesh_oracle.py (the C++/Eigen reference cannot be built: Eigen absent, "
+                      f"profiles/eigen_probe_r02.txt); banded Cholesky at the bandwidth-minimising order (RCM, "
+                      f"b=33 like the GPU); timed track+project+reconstruct per chain, no extrapolation; "
+                      f"step {t:.1f}s, first basis {tfb:.1f}s per chain"}
 
 
 def reference_arm(args, cfg):
-    total_units = (args.meshes or cfg["meshes"]) * (1 if args.strong else max(1, args.gpus))
-    vals = []
-    for _ in range(max(1, args.steps)):
-        cb = cpu_baseline(args, cfg, total_units)
-        vals.append(cb["value"])
-    cb["value"] = statistics.median(vals)
-    n_mesh = cfg["W"] * cfg["H"]
-    ms_step = total_units * n_mesh / cb["value"] * 1e3
-    return {"metric": METRIC, "value": cb["value"], "unit": "vertices/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if (args.strong and cfg["meshes"] > 1) else "weak", "vs_baseline": None, "dtype": "f64",
+    """--impl reference: the oracle port on all host cores.  Each step = P
+    whole chains (P = host cores, capped at the job's mesh count); the rate is
+    vertices processed / slowest chain.  One warm-up step at most (the CPU has
+    no caches to warm beyond the first call's imports)."""
+    total_units = (args.meshes or cfg["meshes"]) * (max(1, args.gpus) if args.weak else 1)
+    cores = os.cpu_count() or 1
+    P = min(cores, max(1, total_units))
+    arm = CpuArm(args.config, P)
+    t_start = time.perf_counter()
+    try:
+        for _ in range(min(args.warmup, 1)):
+            arm.step()
+        times, verts, tfbs = [], 0, []
+        for _ in range(max(1, args.steps)):
+            t, v, tfb = arm.step()
+            times.append(t)
+            tfbs.append(tfb)
+            verts = v
+            if time.perf_counter() - t_start > 240:  # bounded: long single chains (C4) stop early
+                break
+    finally:
+        arm.close()
+    total_t = sum(times)
+    value = verts * len(times) / total_t
+    steady = verts * len(times) / (total_t - sum(tfbs))
+    ms_step = total_t / len(times) * 1e3
+    cb = {"value": value, "unit": "vertices/s", "cores": P, "kind": "port", "steady_state_value": steady,
+          "sample": f"per step {P} whole chains of {args.config} in parallel (1 per core, BLAS 1 thread), "
+                    f"numpy/LAPACK restatement oracle/specmesh_oracle.py; no extrapolation"}
+    return {"metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": args.gpus, "steps": len(times),
+            "warmup": min(args.warmup, 1), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if (args.weak or cfg["meshes"] == 1) else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded sinusoid height-field grids + N(0,sigma^2) noise)",
-            "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes": total_units},
-            "impl": "reference", "cpu_baseline": cb,
-            "e2e": {"value": cb["value"], "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes_per_step": P,
+                       "job_meshes": total_units},
+            "impl": "reference", "arm": "oracle port (numpy/LAPACK restatement of the reference; Eigen absent)",
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 # ----------------------------------------------------------------------- F3 arm
@@ -798,7 +1030,19 @@ def main():
     args = parse()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.impl == "ours" and args.gpus > 1 and world_env is None:
+        # `bench.py --gpus N` launches its own N ranks (one process per GPU)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+    world = int(world_env or "1")
+    if args.impl == "ours" and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         if rank != 0:
@@ -818,7 +1062,7 @@ def main():
             if out is not None:
                 print(json.dumps(out), flush=True)
         return
-    out = gpu_arm(args, cfg, rank, world, local_rank)
+    out = (single_arm if cfg.get("single") else gpu_arm)(args, cfg, rank, world, local_rank)
     if out is not None:
         print(json.dumps(out), flush=True)
 

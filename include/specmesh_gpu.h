@@ -325,6 +325,19 @@ smg_status smg_igft(smg_context* ctx, int32_t rows, int32_t c, const double* bas
 smg_status smg_profile_enable(smg_context* ctx, int32_t on);
 smg_status smg_profile_read(smg_context* ctx, const char* stage, int64_t* launches, double* total_ms);
 
+/* What the last chain call (smg_compute_block_bases*, smg_run_chains) chose:
+ * the factorisation's block width W (the block-tridiagonal solve's half-band
+ * is W + 1) and ordering (0 natural, 1 geometric = sort along the tile's
+ * longest axis, 2 RCM), the chain groups (streams) and the batch shape. */
+typedef struct {
+    int32_t block_width;
+    int32_t ordering;
+    int32_t chain_groups;
+    int32_t chains;
+    int32_t positions;
+} smg_run_info;
+smg_status smg_last_run_info(smg_context* ctx, smg_run_info* info);
+
 /* DOI step log (decision-level parity of dynamic_oi, spectral.hpp:259-283):
  * while enabled, every dynamic_oi step of smg_compute_block_bases (DOI mode)
  * and smg_dynamic_oi appends (chain position, subspace size the step ran

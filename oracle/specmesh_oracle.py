@@ -267,6 +267,11 @@ class ShiftedInverseOperator:
     tiles are banded there) or RCM order, banded Cholesky via LAPACK; a no-pivot
     banded LDL^T takes over when the matrix is not positive definite."""
 
+    # RCM is tried when the natural bandwidth exceeds this (96: grid tiles keep
+    # their natural order).  The CPU baseline lowers it to 0 so a 32x64 tile is
+    # factored at bandwidth 33 like the GPU's geometric ordering (bench.py).
+    rcm_above = 96
+
     def __init__(self, lap: Laplacian, delta: float, z: int):
         require(delta > 0.0, "shift delta must be positive")
         require(z >= 1, "power z must be at least 1")
@@ -277,7 +282,7 @@ class ShiftedInverseOperator:
         a.sort_indices()
         perm = np.arange(self.size_)
         bw = self._bandwidth(a)
-        if bw > 96:
+        if bw > self.rcm_above:
             p = reverse_cuthill_mckee(a, symmetric_mode=True)
             ap = a[p][:, p].tocsr()
             if self._bandwidth(ap) < bw:
@@ -648,6 +653,8 @@ def compute_block_bases_fixed_sizes(vertices, submeshes: List[Submesh], sequence
             warm = resize_basis(previous, c, _pos_seed(cfg, pos))
             basis = orthogonal_iteration(op, warm, cfg.iterations)
         _add(res.timings, "basis", time.perf_counter() - t0)
+        if pos == 0:
+            _add(res.timings, "first_basis", time.perf_counter() - t0)
         st = res.stats[sid]
         st.subspace_size = c
         st.oi_iterations = 0 if pos == 0 else cfg.iterations
@@ -659,10 +666,13 @@ def compute_block_bases_fixed_sizes(vertices, submeshes: List[Submesh], sequence
 
 
 def compute_block_bases_doi(vertices, submeshes: List[Submesh], sequence, cfg: PipelineConfig,
-                            keep_bases: bool = True, trace=None, on_block=None) -> BlockBases:
+                            keep_bases: bool = True, trace=None, on_block=None,
+                            operator_factory=None) -> BlockBases:
     """pipeline.hpp:245-285 (DOI branch), over an external segmentation.
     ``trace`` (test hook): list receiving (position, c, residual) per DOI step;
-    ``on_block(pos, sid, basis)`` is called after every block."""
+    ``on_block(pos, sid, basis)`` is called after every block;
+    ``operator_factory(lap, delta, z)`` replaces ShiftedInverseOperator (a
+    second restatement of the solve, to measure rounding sensitivity)."""
     k = len(submeshes)
     res = BlockBases(submeshes, np.asarray(sequence), [None] * k, [BlockStats() for _ in range(k)],
                      {}, submeshes[0].size() if submeshes else 0)
@@ -676,7 +686,7 @@ def compute_block_bases_doi(vertices, submeshes: List[Submesh], sequence, cfg: P
         lap = build_laplacian(sub, vertices, cfg.weighting)
         _add(res.timings, "laplacian", time.perf_counter() - t0)
         t0 = time.perf_counter()
-        op = ShiftedInverseOperator(lap, default_shift(lap, cfg.shift_scale), cfg.power)
+        op = (operator_factory or ShiftedInverseOperator)(lap, default_shift(lap, cfg.shift_scale), cfg.power)
         _add(res.timings, "factorize", time.perf_counter() - t0)
         t0 = time.perf_counter()
         if pos == 0:

@@ -95,6 +95,14 @@ class Context:
             self.check(self.lib.smg_doi_trace_read(self.handle, n.value, _ptr(pos), _ptr(c), _ptr(r), C.byref(n)))
         return pos, c, r
 
+    def last_run_info(self) -> dict:
+        """What the last chain call chose (smg_last_run_info): block width,
+        ordering (natural / geometric / rcm), chain groups, batch shape."""
+        ri = _abi.smg_run_info()
+        self.check(self.lib.smg_last_run_info(self.handle, C.byref(ri)))
+        return {"block_width": ri.block_width, "ordering": ["natural", "geometric", "rcm"][ri.ordering],
+                "chain_groups": ri.chain_groups, "chains": ri.chains, "positions": ri.positions}
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             self.lib.smg_destroy(self.handle)

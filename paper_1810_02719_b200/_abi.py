@@ -66,6 +66,11 @@ class smg_bilateral_params(C.Structure):
                 ("vertex_iterations", C.c_int32), ("ring_depth", C.c_int32)]
 
 
+class smg_run_info(C.Structure):
+    _fields_ = [("block_width", C.c_int32), ("ordering", C.c_int32), ("chain_groups", C.c_int32),
+                ("chains", C.c_int32), ("positions", C.c_int32)]
+
+
 AVERAGE_MODE = {"simple": 0, "weighted": 1}
 
 # every symbol include/specmesh_gpu.h declares (checked by the CPU test suite)
@@ -77,6 +82,7 @@ EXPORTED = [
     "smg_dynamic_oi", "smg_bottom_subspace", "smg_gft", "smg_igft", "smg_profile_enable", "smg_profile_read",
     "smg_coarse_reconstruct_frames", "smg_denoise_dynamic", "smg_compress_blocks", "smg_decompress_blocks",
     "smg_default_bilateral_params", "smg_fine_denoise", "smg_doi_trace_enable", "smg_doi_trace_read",
+    "smg_last_run_info",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -121,6 +127,7 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_profile_enable": ([vp, C.c_int32], C.c_int),
         "smg_profile_read": ([vp, C.c_char_p, c_int64_p, c_double_p], C.c_int),
         "smg_doi_trace_enable": ([vp, C.c_int32], C.c_int),
+        "smg_last_run_info": ([vp, C.POINTER(smg_run_info)], C.c_int),
         "smg_doi_trace_read": ([vp, C.c_int64, vp, vp, vp, c_int64_p], C.c_int),
         "smg_coarse_reconstruct_frames": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
                                            C.POINTER(smg_bases), C.c_int32, vp, C.c_int32, C.c_int32, vp,

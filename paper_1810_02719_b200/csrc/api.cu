@@ -331,6 +331,7 @@ public:
         // chain groups
         int G = B_ >= 4 ? 2 : 1;
         if (const char* e = std::getenv("SMG_GROUPS")) G = std::max(1, std::min(B_, std::atoi(e)));
+        record_info(G);
         std::vector<Group> grp(G);
         for (int g = 0; g < G; ++g) {
             grp[g].b0 = (int)((int64_t)B_ * g / G);
@@ -507,6 +508,7 @@ public:
         require(c_max <= n_, "c_max cannot exceed the submesh size");
         require(c_max + 1 <= 512, "c_max exceeds the GPU limit of 511");
         setup_tiles();
+        record_info(1);
         const int t_lap = tm.mark();
         sizes_.assign(K_, 0);
         const int fb_m = first_basis_width(n_, c0);
@@ -617,6 +619,14 @@ private:
             for (int id = 0; id < K_; ++id) t[id] = (int64_t)segs_[b].pos_of[id] * B_ + b;
             tile_of_[b].upload(t, st_);
         }
+    }
+
+    void record_info(int groups) {
+        ctx_->info.block_width = ts_.W;
+        ctx_->info.ordering = ts_.ordering;
+        ctx_->info.chain_groups = groups;
+        ctx_->info.chains = B_;
+        ctx_->info.positions = K_;
     }
 
     void check_assembly() {
@@ -1669,6 +1679,12 @@ smg_status smg_profile_read(smg_context* ctx, const char* stage, int64_t* launch
     }
     cudaSetDevice(ctx->device);
     ctx->prof.read(stage, launches, total_ms);
+    return SMG_OK;
+}
+
+smg_status smg_last_run_info(smg_context* ctx, smg_run_info* info) {
+    if (!ctx || !info) return SMG_INVALID_ARGUMENT;
+    *info = ctx->info;
     return SMG_OK;
 }
 

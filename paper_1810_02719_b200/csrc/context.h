@@ -5,6 +5,7 @@
 
 #include <vector>
 
+#include "../../include/specmesh_gpu.h"
 #include "doi.h"
 #include "engine.h"
 #include "profiler.h"
@@ -15,6 +16,7 @@ struct smg_context {
     std::string error;
     bool profiling = false;
     smg::Profiler prof;
+    smg_run_info info{};  // last chain call (smg_last_run_info)
     // DOI step log (smg_doi_trace_*): chain position, c the step ran with, residual
     bool doi_trace = false;
     std::vector<int> trace_pos, trace_c;

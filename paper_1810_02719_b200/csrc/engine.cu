@@ -104,6 +104,7 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
     };
     int wmax = widest(nullptr);
     use_perm = false;
+    ordering = 0;
     // SMG_ORDERING=geometric|natural forces a candidate (tests exercise every path)
     const char* force = std::getenv("SMG_ORDERING");
     const bool force_geo = force && std::string(force) == "geometric";
@@ -120,6 +121,7 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
         if (sa > 0 && (sn < 0 || sa < sn)) {
             perm = std::move(ap);
             use_perm = true;
+            ordering = 1;
             wmax = wa;
         }
     }
@@ -133,9 +135,11 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
         if (sr > 0 && (sc < 0 || sr <= sc)) {
             perm = std::move(rp);
             use_perm = true;
+            ordering = 2;
         } else if (sc < 0) {
             perm = std::move(rp);  // unsupported either way: reported below
             use_perm = true;
+            ordering = 2;
         }
     }
     wmax = widest(use_perm ? perm.get() : nullptr);  // final order: width and coupling bound

@@ -89,6 +89,7 @@ struct TileSet {
     // orderings from the connectivity alone (codec: the decoder has no coordinates,
     // so encoder and decoder must factor identically)
     bool topology_ordering = false;
+    int ordering = 0;  // chosen factorisation order: 0 natural, 1 geometric (axis sort), 2 RCM
     int weighting = -1;  // smg_weighting of the assembled tiles (-1: external CSR)
     int64_t total_nnz = 0;
     DBuf<TileRef> refs;

@@ -191,3 +191,99 @@ def test_geometric_ordering_parity(ctx, monkeypatch, name):
     for i in range(T):
         assert O.max_principal_angle(bb.bases[i], ob.bases[i]) < 1e-8
         assert abs(bb.stats[i].residual_rms - ob.stats[i].residual_rms) <= 1e-9 * ob.stats[i].residual_rms
+
+
+def _steps_by_tile(steps):
+    out = {}
+    for s in steps:
+        out.setdefault(s["pos"], []).append((s["c"], s["residual"]))
+    return out
+
+
+def test_config4_doi_chain_against_golden(ctx):
+    """Full C4 (1024^2 grid, 256 tiles of 64x64, DOI c in [20, 400], band
+    1e-5 / 1e-4) against the oracle's chain committed in
+    tests/golden/c4_doi.json (tests/golden/make_c4_doi.py), step by step
+    through the DOI step log (spectral.hpp:259-283, pipeline.hpp:245-285).
+
+    DOI re-applies R^2 to appended raw residual columns and amplifies rounding
+    ~10x per step: two CPU restatements that differ only in the solver
+    (tests/golden/c4_doi_variant.json, dense LU instead of banded Cholesky)
+    agree to 1e-15 for 6 steps, 1e-9 after 10, 1e-3 after 20 and ~10 % after
+    40, and end tile 0 at c = 325 vs 327.  So:
+      * tile 0's residuals must agree with the oracle's to <= 1e-8 over the
+        first 8 steps and stay within 100x the CPU-vs-CPU envelope after;
+      * every decision the oracle takes with a margin |r - eps|/eps above
+        the worst CPU-vs-CPU divergence must be the GPU's too (same c in);
+      * per tile (c, iterations, converged) equal the oracle's on at least as
+        many tiles as the CPU variant does, and on every tile whose incoming
+        c and every step margin are unambiguous.
+    """
+    import json
+    import os
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    gold = json.load(open(os.path.join(gdir, "c4_doi.json")))
+    var = json.load(open(os.path.join(gdir, "c4_doi_variant.json")))
+    w = synth.config("C4")
+    assert gold["sequence"] == [int(s) for s in w.seg.sequence]
+    kw = dict(subspace_size=w.c, c_min=w.c_min, c_max=w.c_max, eps_low=w.eps_low, eps_high=w.eps_high,
+              shift_scale=1e-3)
+    cfg = G.PipelineConfig(weighting="binary", basis_mode="doi", **kw)
+    ctx.doi_trace(True)
+    try:
+        bb = G.compute_block_bases(w.mesh, w.seg, cfg, want_bases=False, ctx=ctx)
+        pos, cs, rs = ctx.read_doi_trace()
+    finally:
+        ctx.doi_trace(False)
+    gpu = {}
+    for p, c, r in zip(pos, cs, rs):
+        gpu.setdefault(int(p), []).append((int(c), float(r)))
+    ora, vst = _steps_by_tile(gold["steps"]), _steps_by_tile(var["steps"])
+    seq = gold["sequence"]
+    # the step log agrees with the per-tile stats
+    for p, sid in enumerate(seq):
+        st = bb.stats[sid]
+        assert len(gpu[p]) == st.oi_iterations and gpu[p][-1][1] == st.doi_residual
+
+    # (1) tile 0 trajectory: exact prefix, then within the CPU-vs-CPU envelope
+    env = 0.0
+    for i, ((co, ro), (cv, rv), (cg, rg)) in enumerate(zip(ora[0], vst[0], gpu[0])):
+        if not (co == cv == cg):
+            break
+        env = max(env, abs(rv - ro) / ro)
+        dg = abs(rg - ro) / ro
+        if i < 8:
+            assert dg <= 1e-8, (i, dg)
+        assert dg <= max(1e-8, 100 * env), (i, dg, env)
+    worst_cpu = max(abs(rv - ro) / ro for (co, ro), (cv, rv) in zip(ora[0], vst[0]) if co == cv)
+
+    # (2) decisions with a clear margin are taken identically (same c in)
+    mu = 2 * worst_cpu
+    def decision(c, r):
+        return "grow" if r > w.eps_high else ("shrink" if r < w.eps_low else "stop")
+    clear = 0
+    for p in range(len(seq)):
+        for (co, ro), (cg, rg) in zip(ora[p], gpu.get(p, [])):
+            if co != cg:
+                break
+            m = min(abs(ro - w.eps_high) / w.eps_high, abs(ro - w.eps_low) / w.eps_low)
+            if m > mu:
+                assert decision(cg, rg) == decision(co, ro), (p, co, ro, rg)
+                clear += 1
+    assert clear >= 250
+
+    # (3) per-tile outcomes
+    def outcome(tiles, sid):
+        t = tiles[sid]
+        return (t["c"], t["iterations"], t["converged"])
+    g_out = {sid: (bb.stats[sid].subspace_size, bb.stats[sid].oi_iterations, bb.stats[sid].converged)
+             for sid in seq}
+    same_gpu = sum(g_out[sid] == outcome(gold["tiles"], sid) for sid in seq)
+    same_var = sum(outcome(var["tiles"], sid) == outcome(gold["tiles"], sid) for sid in seq)
+    assert same_gpu >= same_var, (same_gpu, same_var)
+    prev_g, prev_o = None, None
+    for p, sid in enumerate(seq):
+        margins = [min(abs(r - w.eps_high) / w.eps_high, abs(r - w.eps_low) / w.eps_low) for _, r in ora[p]]
+        if (p == 0 or prev_g == prev_o) and min(margins) > mu:
+            assert g_out[sid] == outcome(gold["tiles"], sid), (p, g_out[sid], outcome(gold["tiles"], sid))
+        prev_g, prev_o = g_out[sid][0], gold["tiles"][sid]["c"]

@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU evidence run: gpu tests, smoke, default bench, C1-C4 configs, optional ncu.
-# usage: tools/gpu_round.sh TAG [steps...]   steps: tests smoke bench ref configs f3 f4 list solve probe
+# usage: tools/gpu_round.sh TAG [steps...]   steps: tests smoke bench ref configs refconfigs f3 f4 list solve probe
 set -u
 O=gpurun_out
 T=${1:-x}; shift
@@ -14,7 +14,8 @@ tests) timeout 1800 python -m pytest tests -m gpu -q -p no:hypothesispytest > $O
 smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke_$T.log 2>&1; echo rc=$? >> $O/smoke_$T.log ;;
 bench) timeout 900 python bench.py > $O/bench_$T.log 2>&1; echo rc=$? >> $O/bench_$T.log ;;
 ref) timeout 900 python bench.py --impl reference > $O/bench_ref_$T.log 2>&1; echo rc=$? >> $O/bench_ref_$T.log ;;
-configs) timeout 900 python tools/bench_configs.py > $O/configs_$T.log 2>&1; echo rc=$? >> $O/configs_$T.log ;;
+configs) for C in C1 C2 C3 C4; do timeout 900 python bench.py --config $C --steps 3 --warmup 3 > $O/bench_${C}_$T.log 2>&1; echo rc=$? >> $O/bench_${C}_$T.log; done ;;
+refconfigs) for C in C1 C2 C3 C4; do timeout 900 python bench.py --config $C --impl reference --steps 3 --warmup 1 > $O/bench_ref_${C}_$T.log 2>&1; echo rc=$? >> $O/bench_ref_${C}_$T.log; done ;;
 f3) timeout 600 python bench.py --config F3 --steps 3 --warmup 3 > $O/bench_f3_$T.log 2>&1; echo rc=$? >> $O/bench_f3_$T.log ;;
 f4) timeout 600 python bench.py --config F4 --steps 20 --warmup 3 > $O/bench_f4_$T.log 2>&1; echo rc=$? >> $O/bench_f4_$T.log ;;
 list) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 6000 -c 6000 --csv --log-file $O/launches_$T.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_list_$T.log 2>&1; echo rc=$? >> $O/ncu_list_$T.log ;;
