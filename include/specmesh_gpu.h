@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SMG_ABI_VERSION 1
+#define SMG_ABI_VERSION 2
 
 /* 2 = InvalidArgument, 3 = Error, 4 = ParseError (core.hpp:18-34) */
 typedef enum { SMG_OK = 0, SMG_INVALID_ARGUMENT = 2, SMG_ERROR = 3, SMG_PARSE_ERROR = 4 } smg_status;
@@ -86,6 +86,10 @@ typedef struct {
     uint64_t seed;              /* (1) */
     int32_t dense_limit;        /* (4096) */
     double shift_scale;         /* delta = shift_scale * trace(L)/n_d (1e-8) */
+    /* segmentation (segment_mesh, pipeline.hpp:131-138): used when a chain call
+     * gets no Segmentation (seg == NULL), as the reference always segments */
+    int32_t part_count;         /* k (8) */
+    double growth;              /* overlap factor, n_d = floor(growth * max part) (1.15) */
 } smg_pipeline_config;
 
 /* Results of a chain: BlockBases.stats (pipeline.hpp:70-92) plus the optional
@@ -113,6 +117,13 @@ typedef struct {
      * [0] laplacian [1] factorize [2] basis (first submesh) [3] basis_total
      * [4] project (gft+igft+stitch) [5] total */
     double timings[6];
+    /* the segmentation the call used (optional; filled when the call segmented
+     * the mesh itself, seg == NULL): SubmeshOrder sequence [submesh_count],
+     * sorted member lists (submesh_count x block_size, row = submesh id) */
+    int32_t* sequence_out;
+    int32_t* members_out;
+    int64_t members_capacity;
+    int32_t block_size;       /* n_d (always written) */
 } smg_chain_output;
 
 int smg_abi_version(void);
@@ -139,6 +150,9 @@ smg_status smg_compute_block_bases_fixed_sizes(smg_context* ctx, const smg_mesh*
 /* compute_block_bases (pipeline.hpp:198-287) for basis_mode OI or DOI, over an
  * EXTERNAL segmentation (the reference segments internally at :201; the
  * configs supply their own tiles). */
+/* seg == NULL: the mesh is segmented on the GPU first (segment_mesh with
+ * cfg->part_count, cfg->growth, cfg->seed -- the reference's own flow,
+ * pipeline.hpp:198-201); out arrays then hold cfg->part_count submeshes. */
 smg_status smg_compute_block_bases(smg_context* ctx, const smg_mesh* mesh,
                                    const smg_segmentation* seg,
                                    const smg_pipeline_config* cfg, smg_chain_output* out);
@@ -257,6 +271,30 @@ smg_status smg_fine_denoise(smg_context* ctx, int64_t vertex_count, const double
                             const double* z, int64_t face_count, const int32_t* faces,
                             const smg_bilateral_params* params, double* out, double* normals_out,
                             int32_t on_device);
+
+/* ------------------------------------------------------------ segmentation (F1)
+ * The step before the path, on the GPU and bit-exact with the reference's tie
+ * rules.  Host or device mesh (mesh->on_device); outputs are host or device
+ * pointers (any, copied with cudaMemcpyDefault).  InvalidArgument texts are
+ * the reference's ("part count k must satisfy 1 <= k <= n/4", "partition
+ * failed: k is incompatible with the mesh connectivity (...)", "overlap growth
+ * must be >= 1.0", "partition has an empty part", ...). */
+
+/* partition_mesh (partition.hpp:84-159): assignment[n] = part id. */
+smg_status smg_partition_mesh(smg_context* ctx, const smg_mesh* mesh, int32_t part_count, uint64_t seed,
+                              int32_t* assignment);
+/* expand_overlaps (partition.hpp:205-253): part_count sorted member lists of
+ * n_d = floor(growth * max part size) vertices (row = part id); *block_size = n_d. */
+smg_status smg_expand_overlaps(smg_context* ctx, const smg_mesh* mesh, const int32_t* assignment,
+                               int32_t part_count, double growth, int32_t* members,
+                               int64_t members_capacity, int32_t* block_size);
+/* order_submeshes (partition.hpp:258-307): host member lists (offsets). */
+smg_status smg_order_submeshes(smg_context* ctx, int32_t submesh_count, const int32_t* member_offsets,
+                               const int32_t* members, uint64_t seed, int32_t* sequence);
+/* segment_mesh (pipeline.hpp:131-138) = the three above; assignment optional. */
+smg_status smg_segment_mesh(smg_context* ctx, const smg_mesh* mesh, int32_t part_count, double growth,
+                            uint64_t seed, int32_t* assignment, int32_t* members,
+                            int64_t members_capacity, int32_t* block_size, int32_t* sequence);
 
 /* ------------------------------------------------------------ L3 primitives
  * Host pointers, column-major.  They run the same kernels as the chain. */

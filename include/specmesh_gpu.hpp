@@ -215,6 +215,35 @@ inline BlockBases compute_block_bases(Context& ctx, const Mesh& mesh, const smg_
     return out.result(k, n_d);
 }
 
+// segment_mesh (pipeline.hpp:131-138) on the GPU: sorted member lists of
+// n_d vertices per submesh id + the SubmeshOrder sequence (assignment optional)
+inline Segmentation segment_mesh(Context& ctx, const Mesh& mesh, int part_count, double growth, uint64_t seed,
+                                 std::vector<int32_t>* assignment = nullptr) {
+    detail::Views v;
+    detail::make_views(mesh, Segmentation{{std::vector<int32_t>(1, 0)}, {0}}, v);
+    int32_t nd = 0;
+    std::vector<int32_t> seq(std::max(part_count, 1));
+    // first call sizes the member buffer (InvalidArgument "members capacity too small" with n_d set)
+    const smg_status st0 = smg_segment_mesh(ctx.get(), &v.mesh, part_count, growth, seed, nullptr, nullptr, 0, &nd,
+                                            seq.data());
+    if (nd <= 0) check(ctx.get(), st0);
+    std::vector<int32_t> mem((size_t)part_count * nd);
+    if (assignment) assignment->resize((size_t)mesh.vertex_count());
+    check(ctx.get(), smg_segment_mesh(ctx.get(), &v.mesh, part_count, growth, seed,
+                                      assignment ? assignment->data() : nullptr, mem.data(), (int64_t)mem.size(), &nd,
+                                      seq.data()));
+    Segmentation s;
+    for (int p = 0; p < part_count; ++p) s.submeshes.emplace_back(mem.begin() + (size_t)p * nd, mem.begin() + (size_t)(p + 1) * nd);
+    s.sequence = std::move(seq);
+    return s;
+}
+
+// compute_block_bases(mesh, edges, cfg) (pipeline.hpp:198-201): segments
+// internally like the reference (cfg.part_count, cfg.growth, cfg.seed)
+inline BlockBases compute_block_bases(Context& ctx, const Mesh& mesh, const smg_pipeline_config& cfg) {
+    return compute_block_bases(ctx, mesh, cfg, segment_mesh(ctx, mesh, cfg.part_count, cfg.growth, cfg.seed));
+}
+
 }  // namespace specmesh_gpu
 
 // ------------------------------------------------------------------ reference-typed layer
@@ -246,6 +275,8 @@ inline smg_pipeline_config to_c(const specmesh::PipelineConfig& cfg) {
     c.seed = cfg.seed;
     c.dense_limit = cfg.dense_limit;
     c.shift_scale = cfg.shift_scale;
+    c.part_count = cfg.part_count;
+    c.growth = cfg.growth;
     return c;
 }
 
@@ -286,6 +317,27 @@ inline specmesh::BlockBases compute_block_bases_fixed_sizes(const specmesh::Mesh
         r.stats[id] = specmesh::BlockStats{st.subspace_size, st.residual_rms, st.doi_residual, st.converged,
                                            st.oi_iterations};
     }
+    return r;
+}
+
+// drop-in for specmesh::segment_mesh (pipeline.hpp:131-138), on the GPU
+inline specmesh::Segmentation segment_mesh(const specmesh::Mesh& mesh, const specmesh::EdgeSet& edges,
+                                           const specmesh::PipelineConfig& cfg) {
+    Mesh m;
+    m.vertices.assign(mesh.vertices.data(), mesh.vertices.data() + mesh.vertices.size());
+    m.adj_offsets.assign(1, 0);
+    for (const auto& nb : edges.neighbors) {
+        m.adj_cols.insert(m.adj_cols.end(), nb.begin(), nb.end());
+        m.adj_offsets.push_back((int32_t)m.adj_cols.size());
+    }
+    std::vector<int32_t> assignment;
+    Segmentation s = specmesh_gpu::segment_mesh(thread_context(), m, cfg.part_count, cfg.growth, cfg.seed, &assignment);
+    specmesh::Segmentation r;
+    r.partition.part_count = cfg.part_count;
+    r.partition.assignment = Eigen::Map<const Eigen::VectorXi>(assignment.data(), (Eigen::Index)assignment.size());
+    for (auto& mem : s.submeshes)
+        r.submeshes.push_back(specmesh::detail::build_submesh(mesh, edges, std::vector<int>(mem.begin(), mem.end())));
+    r.order.sequence.assign(s.sequence.begin(), s.sequence.end());
     return r;
 }
 

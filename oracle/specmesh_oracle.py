@@ -29,6 +29,11 @@ What it restates (reference = /root/reference/proj/include/specmesh, cited file:
     Segmentation (the reference segments internally, :201)
   * project_blocks / coarse_reconstruct_points   pipeline.hpp:290-305
   * reconstruct_weighted      partition.hpp:311-355
+  * hop_distances / partition_mesh   partition.hpp:58-75, :84-159  (farthest-point
+    seeds, greedy smallest-part growth, exact tie rules)
+  * overlap_target_size / expand_overlaps   partition.hpp:162-165, :205-253
+  * order_submeshes           partition.hpp:258-307
+  * segment_mesh              pipeline.hpp:131-138
 
 Third-party dependency: the reference's arithmetic comes from Eigen (version
 unpinned; absent from this image, so the reference cannot be compiled here or on
@@ -56,7 +61,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
-from scipy.sparse.csgraph import reverse_cuthill_mckee
+from scipy.sparse.csgraph import dijkstra, reverse_cuthill_mckee
 
 
 class Error(RuntimeError):
@@ -1218,3 +1223,192 @@ def fine_denoise(vertices: np.ndarray, faces: np.ndarray, params: BilateralParam
     ring = face_ring_adjacency(faces, vertices.shape[0], params.ring_depth)
     filtered = bilateral_normals(cen, nrm, areas, degenerate, ring, params)
     return update_vertices(vertices, faces, filtered, params.vertex_iterations), filtered
+
+
+# --------------------------------------------------------------------------
+# segmentation (partition.hpp:58-307, pipeline.hpp:131-138)
+
+_INT_MAX = 2 ** 31 - 1
+
+
+def hop_distances(adj_offsets, adj_cols, sources) -> np.ndarray:
+    """partition.hpp:58-75: multi-source BFS hop distances, unreachable =
+    INT_MAX (scipy's unweighted multi-source Dijkstra = BFS, min over sources)."""
+    n = len(adj_offsets) - 1
+    g = sp.csr_matrix((np.ones(len(adj_cols)), np.asarray(adj_cols), np.asarray(adj_offsets)), shape=(n, n))
+    d = dijkstra(g, unweighted=True, indices=list(sources), min_only=True)
+    out = np.full(n, _INT_MAX, dtype=np.int64)
+    fin = np.isfinite(d)
+    out[fin] = d[fin].astype(np.int64)
+    return out
+
+
+@dataclasses.dataclass
+class Partition:
+    """partition.hpp:20-29"""
+
+    assignment: np.ndarray  # per-vertex part id
+    part_count: int
+
+    def part_sizes(self) -> List[int]:
+        return list(np.bincount(self.assignment, minlength=self.part_count))
+
+
+def partition_mesh(adj_offsets, adj_cols, k: int, seed: int) -> Partition:
+    """partition.hpp:84-159: farthest-point seeds (first = mt19937_64(seed)()
+    mod n; then the lowest-id vertex at the largest hop distance from all
+    seeds, unreachable first), then greedy region growing: always the
+    smallest part (lowest id on ties) with a nonempty frontier and size below
+    cap = int(ceil(n/k) * 1.1) (any frontier if all are capped) takes the
+    first unassigned neighbour of its frontier's front vertex."""
+    offs = np.asarray(adj_offsets, dtype=np.int64)
+    cols = np.asarray(adj_cols, dtype=np.int64)
+    n = len(offs) - 1
+    require(k >= 1 and k <= n // 4, "part count k must satisfy 1 <= k <= n/4")
+    rng = MT19937_64(seed)
+    seeds = [int(rng() % n)]
+    while len(seeds) < k:
+        dist = hop_distances(offs, cols, seeds)
+        seeds.append(int(np.argmax(dist)))  # first index of the maximum
+    cap = int(math.ceil(n / k) * 1.1)
+    assignment = [-1] * n
+    frontier = [[] for _ in range(k)]  # deque as list + head index
+    head = [0] * k
+    sizes = [0] * k
+    assigned = 0
+    for p in range(k):
+        assignment[seeds[p]] = p
+        sizes[p] = 1
+        assigned += 1
+        frontier[p].append(seeds[p])
+    offs_l, cols_l = offs.tolist(), cols.tolist()
+
+    def pick(respect_cap):
+        best = -1
+        for p in range(k):
+            if head[p] >= len(frontier[p]):
+                continue
+            if respect_cap and sizes[p] >= cap:
+                continue
+            if best == -1 or sizes[p] < sizes[best]:
+                best = p
+        return best
+
+    while assigned < n:
+        p = pick(True)
+        if p == -1:
+            p = pick(False)
+        if p == -1:
+            raise InvalidArgument("partition failed: k is incompatible with the mesh connectivity "
+                                  "(a component ended up without a seed)")
+        fr = frontier[p]
+        grew = False
+        while head[p] < len(fr) and not grew:
+            v = fr[head[p]]  # front; popped only when it has no unassigned neighbour left
+            for j in range(offs_l[v], offs_l[v + 1]):
+                w = cols_l[j]
+                if assignment[w] != -1:
+                    continue
+                assignment[w] = p
+                sizes[p] += 1
+                assigned += 1
+                fr.append(w)
+                grew = True
+                break
+            if not grew:
+                head[p] += 1
+    return Partition(np.asarray(assignment, dtype=np.int32), k)
+
+
+def overlap_target_size(max_raw_part_size: int, growth: float) -> int:
+    """partition.hpp:162-165"""
+    require(growth >= 1.0, "overlap growth must be >= 1.0")
+    return int(math.floor(growth * max_raw_part_size))
+
+
+def expand_overlaps(adj_offsets, adj_cols, partition: Partition, growth: float) -> List[np.ndarray]:
+    """partition.hpp:205-253: every part grows by BFS rings to exactly
+    n_d = floor(growth * max part size) vertices; the last ring is trimmed by
+    ascending id; an exhausted component is padded with the smallest unused
+    ids.  Returns the sorted member lists (build_submesh sorts, :170)."""
+    offs = np.asarray(adj_offsets, dtype=np.int64)
+    cols = np.asarray(adj_cols, dtype=np.int64)
+    n = len(offs) - 1
+    sizes = partition.part_sizes()
+    for p in range(partition.part_count):
+        require(sizes[p] > 0, "partition has an empty part")
+    target = overlap_target_size(max(sizes), growth)
+    require(target <= n, "target submesh size exceeds the vertex count")
+    out = []
+    for p in range(partition.part_count):
+        member = np.zeros(n, dtype=bool)
+        members = np.nonzero(partition.assignment == p)[0]
+        member[members] = True
+        count = members.size
+        parts = [members]
+        ring = members
+        while count < target:
+            nb = np.concatenate([cols[offs[v]:offs[v + 1]] for v in ring]) if ring.size else np.zeros(0, np.int64)
+            nxt = np.unique(nb[~member[nb]])  # sorted, deduplicated
+            if nxt.size == 0:
+                break
+            member[nxt] = True  # "seen" marks the whole ring, even the trimmed part
+            room = target - count
+            take = nxt[:room]
+            parts.append(take)
+            count += take.size
+            ring = take
+        if count < target:
+            pad = np.nonzero(~member)[0][:target - count]
+            parts.append(pad)
+        out.append(np.sort(np.concatenate(parts)).astype(np.int32))
+    return out
+
+
+def order_submeshes(members: Sequence[np.ndarray], seed: int) -> np.ndarray:
+    """partition.hpp:258-307: initial submesh mt19937_64(seed)() mod k, then
+    BFS over the shared-vertex adjacency graph, neighbours in ascending id,
+    restarting at the smallest unvisited id."""
+    k = len(members)
+    require(k > 0, "cannot order an empty submesh list")
+    owners: Dict[int, List[int]] = {}
+    for s_, m in enumerate(members):
+        for g in np.asarray(m).tolist():
+            owners.setdefault(g, []).append(s_)
+    adj = [set() for _ in range(k)]
+    for lst in owners.values():
+        for a in range(len(lst)):
+            for b in range(a + 1, len(lst)):
+                adj[lst[a]].add(lst[b])
+                adj[lst[b]].add(lst[a])
+    adjl = [sorted(a) for a in adj]
+    initial = int(MT19937_64(seed)() % k)
+    seq, visited, queue = [], [False] * k, []
+    qh = 0
+
+    def visit(s_):
+        visited[s_] = True
+        seq.append(s_)
+        queue.append(s_)
+
+    visit(initial)
+    nxt = 0
+    while len(seq) < k:
+        if qh >= len(queue):
+            while visited[nxt]:
+                nxt += 1
+            visit(nxt)
+            continue
+        s_ = queue[qh]
+        qh += 1
+        for t in adjl[s_]:
+            if not visited[t]:
+                visit(t)
+    return np.asarray(seq, dtype=np.int32)
+
+
+def segment_mesh(adj_offsets, adj_cols, part_count: int, growth: float, seed: int):
+    """pipeline.hpp:131-138 -> (Partition, sorted member lists, sequence)."""
+    part = partition_mesh(adj_offsets, adj_cols, part_count, seed)
+    members = expand_overlaps(adj_offsets, adj_cols, part, growth)
+    return part, members, order_submeshes(members, seed)

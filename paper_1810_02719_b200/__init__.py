@@ -143,6 +143,8 @@ class PipelineConfig:
     seed: int = 1
     dense_limit: int = 4096
     shift_scale: float = 1e-8
+    part_count: int = 8      # segment_mesh k (used when no Segmentation is given)
+    growth: float = 1.15     # overlap factor
 
     def to_c(self) -> _abi.smg_pipeline_config:
         if self.weighting not in _abi.WEIGHTING:
@@ -152,7 +154,8 @@ class PipelineConfig:
         return _abi.smg_pipeline_config(
             _abi.WEIGHTING[self.weighting], _abi.BASIS_MODE[self.basis_mode], self.subspace_size, self.eps_low,
             self.eps_high, self.c_min, self.c_max, self.power, self.iterations, self.initial_iterations,
-            self.doi_iterations, self.seed & ((1 << 64) - 1), self.dense_limit, self.shift_scale)
+            self.doi_iterations, self.seed & ((1 << 64) - 1), self.dense_limit, self.shift_scale, self.part_count,
+            self.growth)
 
 
 # ------------------------------------------------------------------ L3 primitives
@@ -447,9 +450,29 @@ def compute_block_bases_fixed_sizes(mesh, seg, cfg: PipelineConfig, sizes_in_ord
 
 def compute_block_bases(mesh, seg, cfg: PipelineConfig, want_bases: bool = False, want_coeffs: bool = True,
                         want_recon: bool = True, ctx: Optional[Context] = None) -> BlockBases:
-    """compute_block_bases (pipeline.hpp:198-287), OI or DOI, over an external
-    segmentation (the reference segments internally at pipeline.hpp:201)."""
+    """compute_block_bases (pipeline.hpp:198-287), OI or DOI.  ``seg=None`` is
+    the reference's own flow: the mesh is segmented on the GPU first
+    (segment_mesh with cfg.part_count / growth / seed, pipeline.hpp:201); the
+    result's ``sequence`` / ``block_size`` are the segmentation's (call
+    segment_mesh for the member lists).  Bases need an explicit segmentation."""
     ctx = ctx or default_context()
+    if seg is None:
+        if want_bases:
+            raise InvalidArgument("want_bases needs an explicit segmentation (segment_mesh)")
+        keep = []
+        mv = _mesh_view(mesh, keep)
+        k = int(cfg.part_count)
+        cap = cfg.subspace_size
+        if cfg.basis_mode == "doi":
+            cap = cfg.c_max if cfg.c_max > 0 else max(64, 2 * cfg.subspace_size)
+        out = _Out(k, 0, mesh.n, max(cap, 1), False, want_coeffs, want_recon)
+        oc = out.c()
+        seq = np.zeros(k, np.int32)
+        oc.sequence_out = seq.ctypes.data
+        cc = cfg.to_c()
+        ctx.check(ctx.lib.smg_compute_block_bases(ctx.handle, C.byref(mv), None, C.byref(cc), C.byref(oc)))
+        out.n_d = int(oc.block_size)
+        return out.result(seq)
     keep: list = []
     mv, sv = _mesh_view(mesh, keep), _seg_view(seg, keep)
     n_d = seg.block_size
@@ -463,6 +486,68 @@ def compute_block_bases(mesh, seg, cfg: PipelineConfig, want_bases: bool = False
     cc = cfg.to_c()
     ctx.check(ctx.lib.smg_compute_block_bases(ctx.handle, C.byref(mv), C.byref(sv), C.byref(cc), C.byref(oc)))
     return out.result(seg.sequence)
+
+
+# ------------------------------------------------------------------ segmentation (F1)
+
+def partition_mesh(mesh, k: int, seed: int = 1, ctx: Optional[Context] = None) -> np.ndarray:
+    """partition_mesh (partition.hpp:84-159) on the GPU: per-vertex part id."""
+    ctx = ctx or default_context()
+    keep: list = []
+    mv = _mesh_view(mesh, keep)
+    a = np.empty(mesh.n, np.int32)
+    ctx.check(ctx.lib.smg_partition_mesh(ctx.handle, C.byref(mv), int(k), seed & ((1 << 64) - 1), _ptr(a)))
+    return a
+
+
+def expand_overlaps(mesh, assignment, k: int, growth: float, ctx: Optional[Context] = None) -> List[np.ndarray]:
+    """expand_overlaps (partition.hpp:205-253) on the GPU: k sorted member lists of n_d."""
+    ctx = ctx or default_context()
+    keep: list = []
+    mv = _mesh_view(mesh, keep)
+    a = _i32(assignment)
+    nd = C.c_int32()
+    st = ctx.lib.smg_expand_overlaps(ctx.handle, C.byref(mv), _ptr(a), int(k), float(growth), None, 0, C.byref(nd))
+    if nd.value <= 0:
+        ctx.check(st)
+    mem = np.empty(int(k) * nd.value, np.int32)
+    ctx.check(ctx.lib.smg_expand_overlaps(ctx.handle, C.byref(mv), _ptr(a), int(k), float(growth), _ptr(mem),
+                                          mem.size, C.byref(nd)))
+    return [mem[i * nd.value:(i + 1) * nd.value].copy() for i in range(int(k))]
+
+
+def order_submeshes(members: Sequence[np.ndarray], seed: int = 1, ctx: Optional[Context] = None) -> np.ndarray:
+    """order_submeshes (partition.hpp:258-307) on the GPU."""
+    ctx = ctx or default_context()
+    offs = np.zeros(len(members) + 1, np.int32)
+    offs[1:] = np.cumsum([len(m) for m in members])
+    flat = _i32(np.concatenate([np.asarray(m) for m in members])) if len(members) else np.zeros(0, np.int32)
+    seq = np.empty(len(members), np.int32)
+    ctx.check(ctx.lib.smg_order_submeshes(ctx.handle, len(members), _ptr(offs), _ptr(flat), seed & ((1 << 64) - 1),
+                                          _ptr(seq)))
+    return seq
+
+
+def segment_mesh(mesh, part_count: int = 8, growth: float = 1.15, seed: int = 1, ctx: Optional[Context] = None,
+                 return_assignment: bool = False):
+    """segment_mesh (pipeline.hpp:131-138) on the GPU -> synth.Segmentation
+    (sorted member lists by submesh id + the SubmeshOrder sequence)."""
+    from .synth import Segmentation
+    ctx = ctx or default_context()
+    keep: list = []
+    mv = _mesh_view(mesh, keep)
+    nd = C.c_int32()
+    seq = np.empty(int(part_count), np.int32)
+    a = np.empty(mesh.n, np.int32)
+    st = ctx.lib.smg_segment_mesh(ctx.handle, C.byref(mv), int(part_count), float(growth), seed & ((1 << 64) - 1),
+                                  None, None, 0, C.byref(nd), _ptr(seq))
+    if nd.value <= 0:
+        ctx.check(st)
+    mem = np.empty(int(part_count) * nd.value, np.int32)
+    ctx.check(ctx.lib.smg_segment_mesh(ctx.handle, C.byref(mv), int(part_count), float(growth),
+                                       seed & ((1 << 64) - 1), _ptr(a), _ptr(mem), mem.size, C.byref(nd), _ptr(seq)))
+    segm = Segmentation([mem[i * nd.value:(i + 1) * nd.value].copy() for i in range(int(part_count))], seq)
+    return (segm, a) if return_assignment else segm
 
 
 def run_chains(meshes, segs, cfg: PipelineConfig, sizes_in_order: Sequence[int], want_bases: bool = False,

@@ -38,7 +38,7 @@ class smg_pipeline_config(C.Structure):
                 ("eps_low", C.c_double), ("eps_high", C.c_double), ("c_min", C.c_int32), ("c_max", C.c_int32),
                 ("power", C.c_int32), ("iterations", C.c_int32), ("initial_iterations", C.c_int32),
                 ("doi_iterations", C.c_int32), ("seed", C.c_uint64), ("dense_limit", C.c_int32),
-                ("shift_scale", C.c_double)]
+                ("shift_scale", C.c_double), ("part_count", C.c_int32), ("growth", C.c_double)]
 
 
 class smg_chain_output(C.Structure):
@@ -46,7 +46,9 @@ class smg_chain_output(C.Structure):
                 ("converged", C.c_void_p), ("oi_iterations", C.c_void_p), ("reconstruction", C.c_void_p),
                 ("coefficients", C.c_void_p), ("coefficients_capacity", C.c_int64),
                 ("coefficient_offsets", C.c_void_p), ("bases", C.c_void_p), ("bases_capacity", C.c_int64),
-                ("basis_offsets", C.c_void_p), ("on_device", C.c_int32), ("timings", C.c_double * 6)]
+                ("basis_offsets", C.c_void_p), ("on_device", C.c_int32), ("timings", C.c_double * 6),
+                ("sequence_out", C.c_void_p), ("members_out", C.c_void_p), ("members_capacity", C.c_int64),
+                ("block_size", C.c_int32)]
 
 
 class smg_bases(C.Structure):
@@ -82,7 +84,7 @@ EXPORTED = [
     "smg_dynamic_oi", "smg_bottom_subspace", "smg_gft", "smg_igft", "smg_profile_enable", "smg_profile_read",
     "smg_coarse_reconstruct_frames", "smg_denoise_dynamic", "smg_compress_blocks", "smg_decompress_blocks",
     "smg_default_bilateral_params", "smg_fine_denoise", "smg_doi_trace_enable", "smg_doi_trace_read",
-    "smg_last_run_info",
+    "smg_last_run_info", "smg_partition_mesh", "smg_expand_overlaps", "smg_order_submeshes", "smg_segment_mesh",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -128,6 +130,12 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_profile_read": ([vp, C.c_char_p, c_int64_p, c_double_p], C.c_int),
         "smg_doi_trace_enable": ([vp, C.c_int32], C.c_int),
         "smg_last_run_info": ([vp, C.POINTER(smg_run_info)], C.c_int),
+        "smg_partition_mesh": ([vp, C.POINTER(smg_mesh), C.c_int32, C.c_uint64, vp], C.c_int),
+        "smg_expand_overlaps": ([vp, C.POINTER(smg_mesh), vp, C.c_int32, C.c_double, vp, C.c_int64, c_int32_p],
+                                C.c_int),
+        "smg_order_submeshes": ([vp, C.c_int32, vp, vp, C.c_uint64, vp], C.c_int),
+        "smg_segment_mesh": ([vp, C.POINTER(smg_mesh), C.c_int32, C.c_double, C.c_uint64, vp, vp, C.c_int64,
+                              c_int32_p, vp], C.c_int),
         "smg_doi_trace_read": ([vp, C.c_int64, vp, vp, vp, c_int64_p], C.c_int),
         "smg_coarse_reconstruct_frames": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
                                            C.POINTER(smg_bases), C.c_int32, vp, C.c_int32, C.c_int32, vp,

@@ -15,6 +15,7 @@
 #include "engine.h"
 #include "doi.h"
 #include "firstbasis.h"
+#include "segment.h"
 
 using namespace smg;
 
@@ -296,6 +297,7 @@ public:
             stage_mesh(&meshes[b], meshes_[b], st_, msh);
             stage_seg(&segs[b], segs_[b], st_, ssh);
             outs_[b].out = &outs[b];
+            outs[b].block_size = segs_[b].n_d;
         }
         K_ = segs_[0].k;
         n_ = segs_[0].n_d;
@@ -620,6 +622,8 @@ private:
             tile_of_[b].upload(t, st_);
         }
     }
+
+    int block_size() const { return n_; }
 
     void record_info(int groups) {
         ctx_->info.block_width = ts_.W;
@@ -1187,6 +1191,8 @@ void smg_default_config(smg_pipeline_config* c) {
     c->seed = 1;
     c->dense_limit = 4096;
     c->shift_scale = 1e-8;
+    c->part_count = 8;
+    c->growth = 1.15;
 }
 
 smg_status smg_compute_block_bases_fixed_sizes(smg_context* ctx, const smg_mesh* mesh, const smg_segmentation* seg,
@@ -1205,6 +1211,42 @@ smg_status smg_compute_block_bases(smg_context* ctx, const smg_mesh* mesh, const
     return guard(ctx, [&] {
         require(out != nullptr, "output is null");
         Cfg c = read_cfg(cfg);
+        // no Segmentation: segment_mesh on the GPU first (pipeline.hpp:198-201)
+        DeviceSegmentation dseg;
+        DBuf<int32_t> dseq;
+        smg_segmentation own{};
+        if (!seg) {
+            require(mesh != nullptr, "mesh view is null");
+            GraphDev g;
+            g.n = (int)mesh->vertex_count;
+            DBuf<int32_t> go, gc;
+            if (mesh->on_device) {
+                g.offs = mesh->adj_offsets;
+                g.cols = mesh->adj_cols;
+            } else {
+                go.upload(mesh->adj_offsets, (size_t)g.n + 1, ctx->stream);
+                gc.upload(mesh->adj_cols, (size_t)mesh->adj_offsets[g.n], ctx->stream);
+                g.offs = go.get();
+                g.cols = gc.get();
+            }
+            segment_mesh_dev(g, cfg->part_count, cfg->growth, cfg->seed, dseg, ctx->stream);
+            dseq.upload(dseg.sequence_h, ctx->stream);
+            own.submesh_count = dseg.k;
+            own.member_offsets = dseg.offsets.get();
+            own.members = dseg.members.get();
+            own.sequence_length = dseg.k;
+            own.sequence = dseq.get();
+            own.on_device = 1;
+            seg = &own;
+            const int64_t need = (int64_t)dseg.k * dseg.n_d;
+            if (out->sequence_out) std::copy(dseg.sequence_h.begin(), dseg.sequence_h.end(), out->sequence_out);
+            if (out->members_out) {
+                require(out->members_capacity >= need, "members capacity too small: need part_count * n_d = " +
+                                                           std::to_string(need));
+                SMG_CUDA(cudaMemcpyAsync(out->members_out, dseg.members.get(), sizeof(int32_t) * need,
+                                         cudaMemcpyDefault, ctx->stream));
+            }
+        }
         ChainRunner r(ctx, 1, mesh, seg, c, out);
         if (c.basis_mode == SMG_BASIS_OI) {
             std::vector<int32_t> sizes(seg->submesh_count, c.subspace_size);
