@@ -66,12 +66,13 @@ def test_library_loads_and_exports_all_symbols():
     for name in header_symbols():
         assert hasattr(lib, name), name
     lib = _abi.load()
-    assert lib.smg_abi_version() == 1
+    assert lib.smg_abi_version() == 2
     # host-only entry points (no device work)
     assert lib.smg_default_shift(5890.0, 1024, 1e-3) == max(1e-3 * (5890.0 / 1024), 1e-300)
     cfg = _abi.smg_pipeline_config()
     lib.smg_default_config(ctypes.byref(cfg))
     assert (cfg.power, cfg.iterations, cfg.dense_limit, cfg.shift_scale, cfg.weighting) == (2, 2, 4096, 1e-8, 1)
+    assert (cfg.part_count, cfg.growth) == (8, 1.15)  # pipeline.hpp:42-43
 
 
 def test_no_gpu_create_fails_loudly():
