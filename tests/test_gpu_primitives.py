@@ -123,6 +123,26 @@ def test_orthonormalize_rank_deficiency_error_parity(ctx, col):
     assert str(eg.value) == str(eo.value) == f"orthonormalize: block is rank deficient at column {col}"
 
 
+def test_rank_test_resolution_divergence(ctx):
+    """Known deviation: two unit columns at an angle of 1e-7.
+    Householder QR gives |r_11| = sin(1e-7) ~ 1e-7 >= 1e-13 ||V||_F, so the
+    reference passes; the column-scaled Cholesky pivot is 1 - cos^2 ~ 1e-14,
+    below the Gram's resolution (1e-12), and the GPU reports rank deficiency
+    at column 1.  Larger angles (1e-5) pass on both."""
+    rng = np.random.default_rng(3)
+    e, f = np.linalg.qr(rng.standard_normal((64, 2)))[0].T
+    for theta, gpu_fails in ((1e-7, True), (1e-5, False)):
+        b = np.stack([e, np.cos(theta) * e + np.sin(theta) * f], axis=1)
+        qo = O.orthonormalize(b)  # the reference's test passes
+        if gpu_fails:
+            with pytest.raises(G.SpecmeshError, match="rank deficient at column 1"):
+                G.orthonormalize(b, ctx=ctx)
+        else:
+            q = G.orthonormalize(b, ctx=ctx)
+            assert np.abs(q.T @ q - np.eye(2)).max() < 1e-9
+            assert O.max_principal_angle(q, qo) < 1e-6
+
+
 @pytest.mark.parametrize("c", [33, 300, 512])
 def test_orthonormalize_wide_blocks(ctx, c):
     """Multi-panel CholeskyQR2 up to the 512-column limit, graded column norms."""
