@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     const int CL = (int)cl_size(), rank = (int)cl_rank();
     const int b = blockIdx.x / CL;
     if (p.status[b] != kOk) return;  // sticky first error of this chain
+    if (p.skip && p.skip[b]) return;  // adaptive pass 2: the pass-1 factor is orthonormal already
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const int P = (c + 31) / 32, cp = P * 32;
     const double* G = p.G + (int64_t)b * p.strideG;
@@ -572,7 +573,58 @@ __global__ void rank_partial_kernel(RankCheckParams p) {
     if (threadIdx.x == 0) p.counter[b] = 0;
 }
 
+// max over the upper triangle of |G - I| (one CTA per chain; independent
+// loads, 8 in flight per thread) -> skip flag
+__global__ void orth_check_kernel(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int64_t dimStride,
+                                  int c_cap, double tol, int* skip) {
+    __shared__ double red[32];
+    const int b = blockIdx.x;
+    const int c = dimC ? dimC[(int64_t)b * dimStride] : c_cap;
+    const double* g = G + (int64_t)b * strideG;
+    const int64_t total = (int64_t)c * c;
+    double e = 0.0;
+    for (int64_t base = threadIdx.x; base < total; base += (int64_t)blockDim.x * 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t idx = base + (int64_t)u * blockDim.x;
+            const int i = (int)(idx / c), k = (int)(idx % c);
+            v[u] = (idx < total && k >= i) ? fabs(g[(int64_t)i * ldg + k] - (i == k ? 1.0 : 0.0)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) e = (v[u] <= e) ? e : (v[u] == v[u] ? v[u] : INFINITY);  // NaN -> no skip
+    }
+    e = warp_max(e);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+        skip[b] = (m <= tol) ? 1 : 0;
+    }
+}
+
+__global__ void copy_unskipped_kernel(const double* src, double* dst, int64_t elems, int64_t stride, const int* skip) {
+    const int b = blockIdx.y;
+    if (skip[b]) return;
+    const double2* s = reinterpret_cast<const double2*>(src + (int64_t)b * stride);
+    double2* d = reinterpret_cast<double2*>(dst + (int64_t)b * stride);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < elems / 2; i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+
 }  // namespace
+
+void orth_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int64_t dimStride, int c_cap,
+                int batch, double tol, int* skip, cudaStream_t st) {
+    ::smg::count_launch(), orth_check_kernel<<<batch, 256, 0, st>>>(G, ldg, strideG, dimC, dimStride, c_cap, tol, skip);
+}
+
+void copy_unskipped(const double* src, double* dst, int64_t elems, int64_t stride, int batch, const int* skip,
+                    cudaStream_t st) {
+    const int blocks = (int)std::min<int64_t>(64, (elems / 2 + 255) / 256);
+    ::smg::count_launch(), copy_unskipped_kernel<<<dim3(std::max(blocks, 1), batch), 256, 0, st>>>(src, dst, elems, stride, skip);
+}
 
 void rank_check(const RankCheckParams& p, cudaStream_t st) {
     const int chunks = (p.n + RC_ROWS - 1) / RC_ROWS;

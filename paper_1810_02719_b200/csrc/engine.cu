@@ -234,6 +234,8 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     stats.alloc((size_t)B * 4, st);
     status.alloc(B, st);
     status.zero();
+    skip.alloc(B, st);
+    skip.zero();
     errpos.alloc(B, st);
     errpos.zero();
     detail.alloc(B, st);
@@ -343,8 +345,10 @@ bool use_trsm(int c, int batch) {
     return !off && batch <= maxb && trsm_supported(c);
 }
 
-void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st) {
+void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st,
+          const int* skip = nullptr) {
     GemmParams g;
+    g.skip = skip;
     g.M = n;
     g.N = c;
     g.K = c;
@@ -367,8 +371,9 @@ void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, i
 }
 
 void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_scale, int pos, cudaStream_t st,
-          bool near_identity = false, bool skip_inverse = false) {
+          bool near_identity = false, bool skip_inverse = false, const int* skip = nullptr) {
     CholParams p;
+    p.skip = skip;
     p.batch = ws.B;
     p.c_cap = c;
     p.G = ws.G.get();
@@ -399,10 +404,11 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
 }  // namespace
 
 void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
-                bool rank_test, int pos, int passes) {
+                bool rank_test, int pos, int passes, double skip_tol) {
     ProfScope prof("orthonormalize", cx.st);
     const int n = ws.npad;
-    if (rank_test && in == out) {
+    const bool adaptive = skip_tol > 0.0 && passes == 2;
+    if ((rank_test || adaptive) && in == out) {
         // keep the input for the accurate rank test (T is free between solves)
         SMG_CUDA(cudaMemcpyAsync(ws.T.get(), in, sizeof(double) * ws.mstride() * ws.B, cudaMemcpyDeviceToDevice,
                                  cx.st));
@@ -420,10 +426,24 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
         SMG_CUDA(cudaGetLastError());
         return;
     }
-    pass1(ws.R.get());
-    gram(ws, ws.R.get(), c, dimC, n, cx.st);
-    chol(ws, c, dimC, false, true, pos, cx.st, true);
-    trmm(ws, ws.R.get(), out, c, dimC, n, cx.st);
+    if (adaptive) {
+        // Q1 straight into out; pass 2 only for chains whose Q1 is not yet
+        // orthonormal to skip_tol (their Q = Q1 B2 goes through R and back)
+        pass1(out);
+        gram(ws, out, c, dimC, n, cx.st);
+        {
+            ProfScope pc("chol", cx.st);
+            orth_check(ws.G.get(), ws.ld, (int64_t)ws.ld * ws.ld, dimC, 1, c, ws.B, skip_tol, ws.skip.get(), cx.st);
+        }
+        chol(ws, c, dimC, false, true, pos, cx.st, true, false, ws.skip.get());
+        trmm(ws, out, ws.R.get(), c, dimC, n, cx.st, ws.skip.get());
+        copy_unskipped(ws.R.get(), out, ws.mstride(), ws.mstride(), ws.B, ws.skip.get(), cx.st);
+    } else {
+        pass1(ws.R.get());
+        gram(ws, ws.R.get(), c, dimC, n, cx.st);
+        chol(ws, c, dimC, false, true, pos, cx.st, true);
+        trmm(ws, ws.R.get(), out, c, dimC, n, cx.st);
+    }
     if (rank_test) {
         RankCheckParams r;
         r.n = ws.n;

@@ -133,7 +133,7 @@ struct Workspace {
     int splits = 1;
     DBuf<double> U, V, T, R, G, Gws, Bm, work, rdiag, vnorm, rpart, coeff, sign, e, ppart, ppart2, stats;
     DBuf<int> counters;
-    DBuf<int> status, errpos, scratch_status;
+    DBuf<int> status, errpos, scratch_status, skip;
     DBuf<int64_t> detail;
     DBuf<double> H, Hst, Vj, theta, theta_s, Wm, ritz_part, ritz;
     void init(int B, int n, int npad, int ccap, cudaStream_t st);
@@ -150,8 +150,11 @@ struct StepCtx {
 void solve_batch(const StepCtx& cx, Workspace& ws, const FactorSet& fs, int tile0, int tstride, const double* in,
                  double* out, int c, const int* dimC, int z, bool once);
 // CholeskyQR2: out = orth(in); sticky per-chain status, error position `pos`.
+// skip_tol > 0: adaptive -- a chain whose pass-1 factor Q1 is orthonormal to
+// skip_tol (max |Q1^T Q1 - I|, from the pass-2 Gram) keeps Q1 (no second
+// Cholesky, no second triangular product).
 void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
-                bool rank_test, int pos, int passes = 2);
+                bool rank_test, int pos, int passes = 2, double skip_tol = 0.0);
 void project_batch(const StepCtx& cx, Workspace& ws, const double* Q, int c, const int* dimC, const double* X,
                    int64_t strideX, double* xhat, int64_t strideXhat);
 

@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(NT, 4) gemm_kernel(GemmParams p, int n_base, i
     const int splits = p.splits > 0 ? p.splits : 1;
     const int b = blockIdx.z / splits;
     const int s = blockIdx.z % splits;
+    if (p.skip && p.skip[b]) return;
     const int M = p.dimM ? p.dimM[(int64_t)b * p.dimStride] : p.M;
     const int N = min(p.dimN ? p.dimN[(int64_t)b * p.dimStride] : p.N, n_end);  // this launch's columns
     const int K = p.dimK ? p.dimK[(int64_t)b * p.dimStride] : p.K;
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(PipeShape<MW>::THREADS, PipeShape<MW>::MINB)
     const int splits = p.splits > 0 ? p.splits : 1;
     const int b = blockIdx.z / splits;
     const int s = blockIdx.z % splits;
+    if (p.skip && p.skip[b]) return;
     const int M = p.dimM ? p.dimM[(int64_t)b * p.dimStride] : p.M;
     const int N = min(p.dimN ? p.dimN[(int64_t)b * p.dimStride] : p.N, n_end);
     const int K = p.dimK ? p.dimK[(int64_t)b * p.dimStride] : p.K;
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(PipeShape<MW>::THREADS, PipeShape<MW>::MINB)
 
 __global__ void gemm_reduce_kernel(GemmParams p) {
     const int b = blockIdx.y;
+    if (p.skip && p.skip[b]) return;
     const int M = p.dimM ? p.dimM[(int64_t)b * p.dimStride] : p.M;
     const int N = p.dimN ? p.dimN[(int64_t)b * p.dimStride] : p.N;
     const int64_t total = (int64_t)M * N;

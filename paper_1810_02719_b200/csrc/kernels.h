@@ -34,6 +34,7 @@ struct GemmParams {
     int64_t dimStride = 0;
     int upperB = 0;     // B upper triangular (square): k < n0 + 64
     int syrkUpper = 0;  // only tiles with tile_m <= tile_n
+    const int* skip = nullptr;  // optional per batch entry: nonzero -> no work (adaptive CholeskyQR2)
 };
 void gemm(const GemmParams& p, bool transA, bool transB, cudaStream_t st);
 
@@ -126,8 +127,16 @@ struct CholParams {
     // skip the block back-substitution for R~^-1 (off-diagonal blocks of B); the
     // caller forms Q with trsm_right_upper instead
     int skip_inverse = 0;
+    const int* skip = nullptr;  // optional per chain: nonzero -> nothing to do (pass 2 not needed)
 };
 void chol_factor(const CholParams& p, cudaStream_t st);
+// Adaptive CholeskyQR2: skip[b] = 1 when the pass-1 factor is already
+// orthonormal to tol, max_{i<=k<c} |G_ik - delta_ik| <= tol (G = Q1^T Q1, upper)
+void orth_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int64_t dimStride, int c_cap,
+                int batch, double tol, int* skip, cudaStream_t st);
+// dst_b = src_b for the batch entries with skip[b] == 0 (n x ld row-major blocks)
+void copy_unskipped(const double* src, double* dst, int64_t elems, int64_t stride, int batch, const int* skip,
+                    cudaStream_t st);
 int chol_smem_bytes(int c_cap);
 // Q = V D^-1 R~^-1 by a row-parallel right triangular solve (trsm.cu), from the
 // Cholesky's R~ (upper blocks in R) and diagonal-block inverses (diag of Binv).
