@@ -581,18 +581,21 @@ __global__ void orth_check_kernel(const double* G, int64_t ldg, int64_t strideG,
     const int b = blockIdx.x;
     const int c = dimC ? dimC[(int64_t)b * dimStride] : c_cap;
     const double* g = G + (int64_t)b * strideG;
-    const int64_t total = (int64_t)c * c;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double e = 0.0;
-    for (int64_t base = threadIdx.x; base < total; base += (int64_t)blockDim.x * 8) {
-        double v[8];
+    // a warp per row (upper triangle), 8 independent loads in flight per lane
+    for (int i = warp; i < c; i += nw) {
+        const double* row = g + (int64_t)i * ldg;
+        for (int k0 = i + lane; k0 < c; k0 += 256) {
+            double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int64_t idx = base + (int64_t)u * blockDim.x;
-            const int i = (int)(idx / c), k = (int)(idx % c);
-            v[u] = (idx < total && k >= i) ? fabs(g[(int64_t)i * ldg + k] - (i == k ? 1.0 : 0.0)) : 0.0;
+            for (int u = 0; u < 8; ++u) {
+                const int k = k0 + 32 * u;
+                v[u] = k < c ? fabs(__ldcg(row + k) - (i == k ? 1.0 : 0.0)) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) e = (v[u] <= e) ? e : (v[u] == v[u] ? v[u] : INFINITY);  // NaN -> no skip
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) e = (v[u] <= e) ? e : (v[u] == v[u] ? v[u] : INFINITY);  // NaN -> no skip
     }
     e = warp_max(e);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
@@ -639,12 +642,15 @@ int chol_smem_bytes(int c_cap) {
 }
 
 void chol_factor(const CholParams& p, cudaStream_t st) {
+    if (cholx_factor(p, st)) return;
     const int bytes = chol_smem_bytes(p.c_cap);
     ensure_smem((const void*)chol_kernel, bytes);
     // a few chains with c > 224: a cluster of 4 CTAs per chain splits the panel
     // rows and trailing updates (single-chain configs are bound by this kernel)
     const int P = (p.c_cap + 31) / 32;
-    const bool cluster = p.batch <= 4 && P >= 8 && !std::getenv("SMG_CHOL_NOCLUSTER");
+    static const int minp = std::getenv("SMG_CHOL_CLUSTER_MINP") ? std::atoi(std::getenv("SMG_CHOL_CLUSTER_MINP")) : 8;
+    static const int maxb = std::getenv("SMG_CHOL_CLUSTER_MAXB") ? std::atoi(std::getenv("SMG_CHOL_CLUSTER_MAXB")) : 4;
+    const bool cluster = p.batch <= maxb && P >= minp && !std::getenv("SMG_CHOL_NOCLUSTER");
     if (!cluster) {
         ::smg::count_launch(), chol_kernel<<<p.batch, CNT, bytes, st>>>(p);
         return;

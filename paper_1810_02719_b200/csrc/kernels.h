@@ -130,6 +130,8 @@ struct CholParams {
     const int* skip = nullptr;  // optional per chain: nonzero -> nothing to do (pass 2 not needed)
 };
 void chol_factor(const CholParams& p, cudaStream_t st);
+// the shared-memory (cluster) Cholesky (cholx.cu); false when it does not apply
+bool cholx_factor(const CholParams& p, cudaStream_t st);
 // Adaptive CholeskyQR2: skip[b] = 1 when the pass-1 factor is already
 // orthonormal to tol, max_{i<=k<c} |G_ik - delta_ik| <= tol (G = Q1^T Q1, upper)
 void orth_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int64_t dimStride, int c_cap,
