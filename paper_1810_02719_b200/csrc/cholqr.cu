@@ -180,17 +180,32 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
     const double thresh = 1e-13 * scale;
     __syncthreads();
     if (p.near_identity) {
-        double e = 0.0;
+        double e = 0.0, er = 0.0;
         for (int i = warp; i < c; i += CW)
             for (int k = i + lane; k < c; k += 32) {
-                const double x = fabs(fma(G[(int64_t)i * p.ldg + k] * rds[i], rds[k], (i == k) ? -1.0 : 0.0));
+                const double gik = G[(int64_t)i * p.ldg + k];
+                const double x = fabs(fma(gik * rds[i], rds[k], (i == k) ? -1.0 : 0.0));
+                const double xr = fabs(gik - ((i == k) ? 1.0 : 0.0));
                 e = (x <= e) ? e : (x == x ? x : INFINITY);  // NaN -> full path
+                er = (xr <= er) ? er : (xr == xr ? xr : INFINITY);
             }
         for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+        for (int o = 16; o > 0; o >>= 1) er = fmax(er, __shfl_xor_sync(0xffffffffu, er, o));
+        __syncthreads();  // red[] is reused
         if (lane == 0) red[warp] = e;
         __syncthreads();
         e = red[0];
         for (int w = 1; w < CW; ++w) e = fmax(e, red[w]);
+        __syncthreads();
+        if (lane == 0) red[warp] = er;
+        __syncthreads();
+        er = red[0];
+        for (int w = 1; w < CW; ++w) er = fmax(er, red[w]);
+        if (p.skip_out) {
+            const bool sk = er <= p.skip_tol;
+            if (tid == 0) p.skip_out[b] = sk ? 1 : 0;
+            if (sk) return;
+        }
         if (e <= 1e-9) {
             for (int i = warp; i < cp; i += CW)
                 for (int k = lane; k < cp; k += 32) {
@@ -607,6 +622,55 @@ __global__ void orth_check_kernel(const double* G, int64_t ldg, int64_t strideG,
     }
 }
 
+// row block of 32 rows per CTA, warp per row: max |G_ik / (d_i d_k) - delta_ik|, k >= i
+__global__ void near_check_kernel(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap,
+                                  unsigned long long* nmax) {
+    const int b = blockIdx.y;
+    const int c = dimC ? dimC[b] : c_cap;
+    const double* g = G + (int64_t)b * strideG;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double e = 0.0;
+    for (int i = blockIdx.x * 32 + warp; i < min(c, blockIdx.x * 32 + 32); i += nw) {
+        const double ri = 1.0 / sqrt(__ldcg(g + (int64_t)i * ldg + i));
+        for (int k = i + lane; k < c; k += 32) {
+            const double rk = 1.0 / sqrt(__ldcg(g + (int64_t)k * ldg + k));
+            const double x = fabs(__ldcg(g + (int64_t)i * ldg + k) * ri * rk - (i == k ? 1.0 : 0.0));
+            e = (x <= e) ? e : (x == x ? x : INFINITY);
+        }
+    }
+    e = warp_max(e);
+    if (lane == 0 && e > 0.0) atomicMax(nmax + b, (unsigned long long)__double_as_longlong(e));
+}
+
+__global__ void near_fill_kernel(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap,
+                                 const unsigned long long* nmax, const int* skip_in, int* skip_out, double* Bo,
+                                 int64_t ldb, int64_t strideB, double* dscale, int64_t strideD) {
+    const int b = blockIdx.y;
+    const bool skipped = skip_in && skip_in[b];
+    const double m = __longlong_as_double((long long)nmax[b]);
+    const bool near = !skipped && m <= 1e-9;
+    if (blockIdx.x == 0 && threadIdx.x == 0) skip_out[b] = (skipped || near) ? 1 : 0;
+    if (!near) return;
+    const int c = dimC ? dimC[b] : c_cap;
+    const int cp = (c_cap + 31) / 32 * 32;
+    const double* g = G + (int64_t)b * strideG;
+    double* B = Bo + (int64_t)b * strideB;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = blockIdx.x * 32 + warp; i < min(cp, blockIdx.x * 32 + 32); i += nw) {
+        const double di = i < c ? sqrt(__ldcg(g + (int64_t)i * ldg + i)) : 1.0;
+        const double ri = di > 0.0 ? 1.0 / di : 0.0;
+        if (lane == 0) dscale[(int64_t)b * strideD + i] = di;
+        for (int k = lane; k < cp; k += 32) {
+            double v = (k == i) ? 1.0 : 0.0;
+            if (k > i && k < c) {
+                const double rk = 1.0 / sqrt(__ldcg(g + (int64_t)k * ldg + k));
+                v = -__ldcg(g + (int64_t)i * ldg + k) * ri * rk;
+            }
+            B[(int64_t)i * ldb + k] = v * ri;
+        }
+    }
+}
+
 __global__ void copy_unskipped_kernel(const double* src, double* dst, int64_t elems, int64_t stride, const int* skip) {
     const int b = blockIdx.y;
     if (skip[b]) return;
@@ -621,6 +685,20 @@ __global__ void copy_unskipped_kernel(const double* src, double* dst, int64_t el
 void orth_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int64_t dimStride, int c_cap,
                 int batch, double tol, int* skip, cudaStream_t st) {
     ::smg::count_launch(), orth_check_kernel<<<batch, 256, 0, st>>>(G, ldg, strideG, dimC, dimStride, c_cap, tol, skip);
+}
+
+void near_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap, int batch,
+                unsigned long long* nmax, cudaStream_t st) {
+    const int P = (c_cap + 31) / 32;
+    ::smg::count_launch(), near_check_kernel<<<dim3(P, batch), 256, 0, st>>>(G, ldg, strideG, dimC, c_cap, nmax);
+}
+
+void near_fill(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap, int batch,
+               const unsigned long long* nmax, const int* skip_in, int* skip_out, double* Binv, int64_t ldb,
+               int64_t strideB, double* dscale, int64_t strideD, cudaStream_t st) {
+    const int P = (c_cap + 31) / 32;
+    ::smg::count_launch(), near_fill_kernel<<<dim3(P, batch), 256, 0, st>>>(G, ldg, strideG, dimC, c_cap, nmax, skip_in,
+                                                                            skip_out, Binv, ldb, strideB, dscale, strideD);
 }
 
 void copy_unskipped(const double* src, double* dst, int64_t elems, int64_t stride, int batch, const int* skip,

@@ -248,17 +248,17 @@ __global__ void __launch_bounds__(XNT, 1) cholx_kernel(CholParams p) {
                 // the division as a product with 1/R[i][i] (rinvb)
                 double* rinvb = xloc;  // free until the panel-row phase
                 rinvb[lane] = rinv;
+                // R is in D (written above): broadcast reads, no per-row barrier; the sum
+                // runs from the oldest x (l = 31) to the newest (l = i + 1), so each
+                // row's chain waits on the previous row only for its last term
+                __syncwarp();
                 double x[32];
 #pragma unroll
                 for (int i = 31; i >= 0; --i) {
-                    // row i of R (final) broadcast: lanes l >= i hold R[i][l] = a[i]
-                    __syncwarp();
-                    rowb[lane] = a[i];
-                    __syncwarp();
                     double s0 = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
-                    for (int l = i + 1; l < 32; ++l)
-                        if (l <= lane) s0 = fma(-rowb[l], x[l], s0);
+                    for (int l = 31; l > i; --l)
+                        if (l <= lane) s0 = fma(-D[sw(i, l)], x[l], s0);
                     x[i] = (i <= lane) ? s0 * rinvb[i] : 0.0;
                 }
 #pragma unroll
@@ -446,7 +446,8 @@ void launch_cholx(const CholParams& p, int P, cudaStream_t st) {
 // CTAs for few chains (latency), 0 when c is out of range
 int cholx_cluster(int c_cap, int batch) {
     const int P = (c_cap + 31) / 32;
-    if (P < 1 || P > kXMaxP) return 0;
+    // up to 2 panels the old single-CTA kernel is as fast (c = 60: 89 vs 92 us per position)
+    if (P < 3 || P > kXMaxP) return 0;
     static const int force = std::getenv("SMG_CHOLX_CL") ? std::atoi(std::getenv("SMG_CHOLX_CL")) : 0;
     const int limit = 227 * 1024;
     // single chains: the widest cluster (latency); small batches: pairs (a wide

@@ -1,3 +1,5 @@
+#include <cstdlib>
+
 #include "doi.h"
 
 namespace smg {
@@ -5,6 +7,40 @@ namespace smg {
 DoiLoop::~DoiLoop() {
     if (exec_) cudaGraphExecDestroy(exec_);
     if (graph_) cudaGraphDestroy(graph_);
+}
+
+void DoiLoop::issue(cudaStream_t cs, cudaGraphConditionalHandle h, int use_handle) {
+    const TileSet& ts = *ts_;
+    Workspace& ws = *ws_;
+    StepCtx cx{cs, &ts};
+    DoiState* state = state_.get();
+    const int* dimC = &state->c;
+    SolveParams p;
+    p.n = ts.n;
+    p.Kb = ts.Kb;
+    p.z = prm_.power;
+    p.c_cap = ws.ccap;
+    p.batch = 1;
+    p.Ffwd = Ff_.get();
+    p.Fbwd = Fb_.get();
+    p.strideF = strideF_;
+    p.perm = ts.use_perm ? P_.get() : nullptr;
+    p.in = ws.U.get();
+    p.ldin = ws.ld;
+    p.strideIn = ws.mstride();
+    p.tmp = ws.T.get();
+    p.ldt = ws.ld;
+    p.strideT = ws.mstride();
+    p.out = ws.V.get();
+    p.ldout = ws.ld;
+    p.strideOut = ws.mstride();
+    p.dimC = dimC;
+    p.dimStride = 1;
+    solve_block_tridiag(p, ts.W, cs);
+    orth_batch(cx, ws, ws.V.get(), ws.U.get(), ws.ccap, dimC, true, -1);
+    project_batch(cx, ws, ws.U.get(), ws.ccap, dimC, X_.get(), 0, nullptr, 0);
+    doi_decide(state, 1, ws.stats.get(), 4, h, use_handle, ws.status.get(), cs, trace_c_.get(), trace_r_.get());
+    doi_append(state, ws.U.get(), ws.ld, ws.mstride(), ws.e.get(), ws.npad, ts.n, 1, cs);
 }
 
 void DoiLoop::build(const TileSet& ts, Workspace& ws, const DoiParams& prm, int64_t strideF, cudaStream_t st) {
@@ -34,38 +70,11 @@ void DoiLoop::build(const TileSet& ts, Workspace& ws, const DoiParams& prm, int6
     SMG_CUDA(cudaGraphAddNode(&node, graph_, nullptr, 0, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
 
+    nograph_ = std::getenv("SMG_DOI_NOGRAPH") != nullptr;
     cudaStream_t cs;
     SMG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     SMG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    StepCtx cx{cs, &ts};
-    DoiState* state = state_.get();
-    const int* dimC = &state->c;
-    SolveParams p;
-    p.n = ts.n;
-    p.Kb = ts.Kb;
-    p.z = prm.power;
-    p.c_cap = ws.ccap;
-    p.batch = 1;
-    p.Ffwd = Ff_.get();
-    p.Fbwd = Fb_.get();
-    p.strideF = strideF;
-    p.perm = ts.use_perm ? P_.get() : nullptr;
-    p.in = ws.U.get();
-    p.ldin = ws.ld;
-    p.strideIn = ws.mstride();
-    p.tmp = ws.T.get();
-    p.ldt = ws.ld;
-    p.strideT = ws.mstride();
-    p.out = ws.V.get();
-    p.ldout = ws.ld;
-    p.strideOut = ws.mstride();
-    p.dimC = dimC;
-    p.dimStride = 1;
-    solve_block_tridiag(p, ts.W, cs);
-    orth_batch(cx, ws, ws.V.get(), ws.U.get(), ws.ccap, dimC, true, -1);
-    project_batch(cx, ws, ws.U.get(), ws.ccap, dimC, X_.get(), 0, nullptr, 0);
-    doi_decide(state, 1, ws.stats.get(), 4, h, 1, ws.status.get(), cs, trace_c_.get(), trace_r_.get());
-    doi_append(state, ws.U.get(), ws.ld, ws.mstride(), ws.e.get(), ws.npad, ts.n, 1, cs);
+    issue(cs, h, 1);
     cudaGraph_t captured;
     SMG_CUDA(cudaStreamEndCapture(cs, &captured));
     SMG_CUDA(cudaStreamDestroy(cs));
@@ -90,7 +99,15 @@ DoiState DoiLoop::run(const double* Ff, const double* Fb, const int32_t* perm, c
     s.eps_high = prm_.eps_high;
     s.scale = bbox == 0.0 ? 1.0 : bbox;  // spectral.hpp:253-254
     SMG_CUDA(cudaMemcpyAsync(state_.get(), &s, sizeof(s), cudaMemcpyHostToDevice, st_));
-    if (prm_.t_max > 0) SMG_CUDA(cudaGraphLaunch(exec_, st_));
+    if (prm_.t_max > 0 && !nograph_) SMG_CUDA(cudaGraphLaunch(exec_, st_));
+    if (prm_.t_max > 0 && nograph_) {
+        DoiState h{};
+        do {
+            issue(st_, cudaGraphConditionalHandle{}, 0);
+            SMG_CUDA(cudaMemcpyAsync(&h, state_.get(), sizeof(h), cudaMemcpyDeviceToHost, st_));
+            SMG_CUDA(cudaStreamSynchronize(st_));
+        } while (h.active);
+    }
     DoiState r{};
     SMG_CUDA(cudaMemcpyAsync(&r, state_.get(), sizeof(r), cudaMemcpyDeviceToHost, st_));
     SMG_CUDA(cudaStreamSynchronize(st_));

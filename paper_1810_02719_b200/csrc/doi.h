@@ -33,6 +33,9 @@ public:
     void read_trace(int steps, std::vector<int>& c, std::vector<double>& r) const;
 
 private:
+    // one DOI iteration (solve -> CholeskyQR2 -> residual -> decide -> append)
+    void issue(cudaStream_t cs, cudaGraphConditionalHandle h, int use_handle);
+    bool nograph_ = false;  // SMG_DOI_NOGRAPH=1: host-driven loop (profilers see every kernel)
     const TileSet* ts_ = nullptr;
     Workspace* ws_ = nullptr;
     DoiParams prm_;

@@ -236,6 +236,9 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     status.zero();
     skip.alloc(B, st);
     skip.zero();
+    skip2.alloc(B, st);
+    skip2.zero();
+    nmax.alloc(B, st);
     errpos.alloc(B, st);
     errpos.zero();
     detail.alloc(B, st);
@@ -371,9 +374,12 @@ void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, i
 }
 
 void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_scale, int pos, cudaStream_t st,
-          bool near_identity = false, bool skip_inverse = false, const int* skip = nullptr) {
+          bool near_identity = false, bool skip_inverse = false, const int* skip = nullptr, int* skip_out = nullptr,
+          double skip_tol = 0.0) {
     CholParams p;
     p.skip = skip;
+    p.skip_out = skip_out;
+    p.skip_tol = skip_tol;
     p.batch = ws.B;
     p.c_cap = c;
     p.G = ws.G.get();
@@ -403,6 +409,24 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
 }
 }  // namespace
 
+// second CholeskyQR pass: near-identity chains (max |G~ - I| <= 1e-9, the usual
+// case) get B to first order on all SMs; only the others run the full Cholesky
+void chol_pass2(Workspace& ws, int c, const int* dimC, int pos, cudaStream_t st, const int* skip_in) {
+    if (c <= 256) {
+        // small c: the single-CTA near-identity scan inside the Cholesky kernel is
+        // cheaper than three launches
+        chol(ws, c, dimC, false, true, pos, st, true, false, skip_in);
+        return;
+    }
+    ProfScope prof("chol", st);
+    const int64_t sG = (int64_t)ws.ld * ws.ld;
+    SMG_CUDA(cudaMemsetAsync(ws.nmax.get(), 0, sizeof(unsigned long long) * ws.B, st));
+    near_check(ws.G.get(), ws.ld, sG, dimC, c, ws.B, ws.nmax.get(), st);
+    near_fill(ws.G.get(), ws.ld, sG, dimC, c, ws.B, ws.nmax.get(), skip_in, ws.skip2.get(), ws.Bm.get(), ws.ld, sG,
+              ws.rdiag.get(), ws.ld, st);
+    chol(ws, c, dimC, false, true, pos, st, false, false, ws.skip2.get());
+}
+
 void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
                 bool rank_test, int pos, int passes, double skip_tol) {
     ProfScope prof("orthonormalize", cx.st);
@@ -431,17 +455,22 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
         // orthonormal to skip_tol (their Q = Q1 B2 goes through R and back)
         pass1(out);
         gram(ws, out, c, dimC, n, cx.st);
-        {
-            ProfScope pc("chol", cx.st);
-            orth_check(ws.G.get(), ws.ld, (int64_t)ws.ld * ws.ld, dimC, 1, c, ws.B, skip_tol, ws.skip.get(), cx.st);
+        if (c <= 256) {
+            // the single-CTA pass-2 scan decides the skip too (one launch)
+            chol(ws, c, dimC, false, true, pos, cx.st, true, false, nullptr, ws.skip.get(), skip_tol);
+        } else {
+            {
+                ProfScope pc("chol", cx.st);
+                orth_check(ws.G.get(), ws.ld, (int64_t)ws.ld * ws.ld, dimC, 1, c, ws.B, skip_tol, ws.skip.get(), cx.st);
+            }
+            chol_pass2(ws, c, dimC, pos, cx.st, ws.skip.get());
         }
-        chol(ws, c, dimC, false, true, pos, cx.st, true, false, ws.skip.get());
         trmm(ws, out, ws.R.get(), c, dimC, n, cx.st, ws.skip.get());
         copy_unskipped(ws.R.get(), out, ws.mstride(), ws.mstride(), ws.B, ws.skip.get(), cx.st);
     } else {
         pass1(ws.R.get());
         gram(ws, ws.R.get(), c, dimC, n, cx.st);
-        chol(ws, c, dimC, false, true, pos, cx.st, true);
+        chol_pass2(ws, c, dimC, pos, cx.st, nullptr);
         trmm(ws, ws.R.get(), out, c, dimC, n, cx.st);
     }
     if (rank_test) {

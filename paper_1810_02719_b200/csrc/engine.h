@@ -133,7 +133,8 @@ struct Workspace {
     int splits = 1;
     DBuf<double> U, V, T, R, G, Gws, Bm, work, rdiag, vnorm, rpart, coeff, sign, e, ppart, ppart2, stats;
     DBuf<int> counters;
-    DBuf<int> status, errpos, scratch_status, skip;
+    DBuf<int> status, errpos, scratch_status, skip, skip2;
+    DBuf<unsigned long long> nmax;
     DBuf<int64_t> detail;
     DBuf<double> H, Hst, Vj, theta, theta_s, Wm, ritz_part, ritz;
     void init(int B, int n, int npad, int ccap, cudaStream_t st);

@@ -128,6 +128,11 @@ struct CholParams {
     // caller forms Q with trsm_right_upper instead
     int skip_inverse = 0;
     const int* skip = nullptr;  // optional per chain: nonzero -> nothing to do (pass 2 not needed)
+    // adaptive CholeskyQR2 decided inside the near-identity scan (pass 2, single
+    // CTA path): skip_out[b] = max |G - I| <= skip_tol (unscaled; the pass-1
+    // factor is then kept and nothing else is written)
+    int* skip_out = nullptr;
+    double skip_tol = 0.0;
 };
 void chol_factor(const CholParams& p, cudaStream_t st);
 // the shared-memory (cluster) Cholesky (cholx.cu); false when it does not apply
@@ -136,6 +141,17 @@ bool cholx_factor(const CholParams& p, cudaStream_t st);
 // orthonormal to tol, max_{i<=k<c} |G_ik - delta_ik| <= tol (G = Q1^T Q1, upper)
 void orth_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int64_t dimStride, int c_cap,
                 int batch, double tol, int* skip, cudaStream_t st);
+// Second CholeskyQR pass, near-identity case on all SMs: nmax[b] = max over the
+// upper triangle of |G~ - I| (G~ = D^-1 G D^-1, D = sqrt(diag G); NaN -> inf;
+// nmax zeroed by the caller), then for chains not skipped (skip_in) with
+// nmax <= 1e-9: B = D^-1 (I - triu(G~ - I, 1)) (the factor to first order,
+// error <= c * 1e-18) and d = D; skip_out[b] = skip_in[b] || near (the full
+// Cholesky then runs only for the rest)
+void near_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap, int batch,
+                unsigned long long* nmax, cudaStream_t st);
+void near_fill(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap, int batch,
+               const unsigned long long* nmax, const int* skip_in, int* skip_out, double* Binv, int64_t ldb,
+               int64_t strideB, double* dscale, int64_t strideD, cudaStream_t st);
 // dst_b = src_b for the batch entries with skip[b] == 0 (n x ld row-major blocks)
 void copy_unskipped(const double* src, double* dst, int64_t elems, int64_t stride, int batch, const int* skip,
                     cudaStream_t st);
