@@ -16,6 +16,8 @@
 // in a fixed order (32 columns x 8 contiguous chunk ranges per CTA); pass 3
 // (thread = column part x 4 rows) rebuilds X^ and e and the chain's last CTA
 // sums the residual partials in block order.  Deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -277,10 +279,158 @@ __global__ void __launch_bounds__(PNT) recon_kernel(ProjParams p) {
     p.counter[2 * b + 1] = 0;
 }
 
+// Reconstruction, warp per RW rows: lane l reads the double2 of columns
+// 64k + 2l of each row (a warp instruction = 512 contiguous bytes of one row),
+// RW rows x 2 column chunks = 2 RW independent 16-byte loads in flight per lane
+// (the older thread-per-column-part kernel had 4 and sat at ~28 % of HBM);
+// the RW x 4 lane partials are summed by a halving butterfly (each step sends
+// half of the values to the partner lane): V values over 32 lanes in V - 1 + ...
+// shuffles, a fixed tree (deterministic); afterwards lane l holds value k(l).
+
+// halving step: keep the half selected by `up`, add the partner's copy of it
+template <int V>
+SMG_DEV void halve(double (&v)[32], int s, bool up) {
+#pragma unroll
+    for (int j = 0; j < V / 2; ++j) {
+        const double send = up ? v[j] : v[j + V / 2];
+        const double keep = up ? v[j + V / 2] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+}
+
+template <int RW, int NCH>
+__global__ void __launch_bounds__(PNT) recon_warp_kernel(ProjParams p) {
+    static_assert(RW * 4 <= 32, "one lane per (row, output)");
+    __shared__ double red[2][PNT / 32];
+    extern __shared__ __align__(16) double scoef[];  // c_cap x 4: Px Py Pz Ps
+    const int b = blockIdx.y;
+    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    const double* Q = p.Q + (int64_t)b * p.strideQ;
+    const double* X = p.X + (int64_t)b * p.strideX;
+    {
+        const double2* src = reinterpret_cast<const double2*>(p.coeff + (int64_t)b * p.strideCoef);
+        double2* dst = reinterpret_cast<double2*>(scoef);
+        const int cpad = (p.c_cap + 64 * NCH - 1) / (64 * NCH) * (64 * NCH);
+        for (int e = threadIdx.x; e < 2 * cpad; e += PNT) dst[e] = (e >> 1) < c ? src[e] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double4* cf = reinterpret_cast<const double4*>(scoef);
+    // this CTA's rows: a contiguous range of the chain, in row groups of RW per warp
+    const int per = ((p.n + gridDim.x - 1) / gridDim.x + RW * (PNT / 32) - 1) / (RW * (PNT / 32)) * (RW * (PNT / 32));
+    const int rbeg = blockIdx.x * per, rend = min(p.n, rbeg + per);
+    double res2 = 0.0, e2 = 0.0;
+    for (int row0 = rbeg + warp * RW; row0 < rend; row0 += RW * (PNT / 32)) {
+        double acc[RW][4];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
+        for (int base = 0; base < c; base += 64 * NCH) {
+            double2 q[NCH][RW];
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+                const int col = base + 64 * h + 2 * lane;
+#pragma unroll
+                for (int r = 0; r < RW; ++r) {
+                    const int row = row0 + r;
+                    q[h][r] = (col < c && row < rend)
+                                  ? __ldg(reinterpret_cast<const double2*>(Q + (int64_t)row * p.ldq + col))
+                                  : make_double2(0.0, 0.0);
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+                const int col = base + 64 * h + 2 * lane;
+                const double4 c0 = cf[col], c1 = cf[col + 1];  // zero beyond c (odd c: the padding column too)
+#pragma unroll
+                for (int r = 0; r < RW; ++r) {
+                    acc[r][0] = fma(q[h][r].x, c0.x, acc[r][0]);
+                    acc[r][1] = fma(q[h][r].x, c0.y, acc[r][1]);
+                    acc[r][2] = fma(q[h][r].x, c0.z, acc[r][2]);
+                    acc[r][3] = fma(q[h][r].x, c0.w, acc[r][3]);
+                    acc[r][0] = fma(q[h][r].y, c1.x, acc[r][0]);
+                    acc[r][1] = fma(q[h][r].y, c1.y, acc[r][1]);
+                    acc[r][2] = fma(q[h][r].y, c1.z, acc[r][2]);
+                    acc[r][3] = fma(q[h][r].y, c1.w, acc[r][3]);
+                }
+            }
+        }
+        constexpr int V = RW * 4;
+        double v[32];
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+            for (int a = 0; a < 4; ++a) v[r * 4 + a] = acc[r][a];
+        // halving steps over lane bits 4, 3, ..: afterwards lane l holds value
+        // k = bits (4, 3, ..) of l; the remaining lane bits are plain butterflies
+        int k = 0;
+        {
+            int vv = V;
+#pragma unroll
+            for (int s = 16; s >= 1; s >>= 1) {
+                if (vv > 1) {
+                    const bool up = (lane & s) != 0;
+                    if (vv == 32) halve<32>(v, s, up);
+                    else if (vv == 16) halve<16>(v, s, up);
+                    else if (vv == 8) halve<8>(v, s, up);
+                    else if (vv == 4) halve<4>(v, s, up);
+                    else halve<2>(v, s, up);
+                    vv >>= 1;
+                    k = 2 * k + (up ? 1 : 0);
+                } else {
+                    v[0] += __shfl_xor_sync(0xffffffffu, v[0], s);
+                }
+            }
+        }
+        const bool owner = (V == 32) || ((lane & (32 / V - 1)) == 0);  // one lane per value
+        if (owner) {
+            const double val = v[0];
+            const int r = k >> 2, a = k & 3, i = row0 + r;
+            if (i < rend) {
+                const double* xi = X + 3 * (int64_t)i;
+                if (a < 3) {
+                    if (p.xhat) p.xhat[(int64_t)b * p.strideXhat + 3 * i + a] = val;
+                    const double d = xi[a] - val;
+                    res2 += d * d;
+                } else {
+                    const double e = ((xi[0] + xi[1]) + xi[2]) - val;
+                    if (p.e_out) p.e_out[(int64_t)b * p.strideE + i] = e;
+                    e2 += e * e;
+                }
+            }
+        }
+    }
+    res2 = warp_sum(res2);
+    e2 = warp_sum(e2);
+    if (lane == 0) {
+        red[0][warp] = res2;
+        red[1][warp] = e2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, e = 0.0;
+        for (int w = 0; w < PNT / 32; ++w) {
+            a += red[0][w];
+            e += red[1][w];
+        }
+        double* o = p.partial2 + ((int64_t)b * gridDim.x + blockIdx.x) * 2;
+        o[0] = a;
+        o[1] = e;
+    }
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&p.counter[2 * b + 1], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    stats_block(p, b, gridDim.x);
+    p.counter[2 * b + 1] = 0;
+}
+
 }  // namespace
 
 int proj_chunks(int n) { return (n + RPC - 1) / RPC; }
-int proj_recon_blocks(int n, int /*rows_per_warp*/) { return (n + PNT / 8 - 1) / (PNT / 8); }  // upper bound
+int proj_recon_blocks(int n, int /*rows_per_warp*/) { return (n + 15) / 16; }  // upper bound (8 warps x 2 rows)
 
 void project(const ProjParams& p0, cudaStream_t st) {
     ProjParams p = p0;
@@ -288,6 +438,21 @@ void project(const ProjParams& p0, cudaStream_t st) {
     p.nchunks = proj_chunks(p.n);
     ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), QNT, 0, st>>>(p);
     ::smg::count_launch(), chunk_reduce_kernel<<<dim3((p.c_cap + RCOL - 1) / RCOL, p.batch), RCOL * RPART, 0, st>>>(p);
+    if (!std::getenv("SMG_RECON_OLD")) {
+        // one row group per warp (measured: 46 us per C5 launch against 63 us for
+        // the thread-per-column-part kernel; a persistent sweep over row ranges
+        // was slower, 58 us); RW rows x 2 column chunks in flight per lane
+        const int wsmem = (p.c_cap + 127) / 128 * 128 * 4 * (int)sizeof(double);
+        const int maxb = proj_recon_blocks(p.n, 0);
+        if (p.batch >= 8) {
+            const int cpc = std::min(maxb, (p.n + 4 * (PNT / 32) - 1) / (4 * (PNT / 32)));
+            ::smg::count_launch(), recon_warp_kernel<4, 2><<<dim3(cpc, p.batch), PNT, wsmem, st>>>(p);
+        } else {
+            const int cpc = std::min(maxb, (p.n + 2 * (PNT / 32) - 1) / (2 * (PNT / 32)));
+            ::smg::count_launch(), recon_warp_kernel<2, 2><<<dim3(cpc, p.batch), PNT, wsmem, st>>>(p);
+        }
+        return;
+    }
     const int smem = ((p.c_cap + 1) / 2 + 7) / 8 * 32 * (int)sizeof(double2);
     const int nb4 = (p.n + 4 * (PNT / 8) - 1) / (4 * (PNT / 8));
     if ((int64_t)nb4 * p.batch >= 2 * 148) {
