@@ -23,7 +23,7 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $(LIB))
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static -lcuda
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static -lcuda -ldl
 
 oracle: oracle/_ref/rng_ref
 

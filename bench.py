@@ -288,6 +288,12 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     ctx = G.Context(local_rank)
+    comm = None
+    if dist is not None and cfg["meshes"] > 1:
+        # the library's NCCL communicator (smg_comm_create): the per-mesh gather
+        # runs in the C++ host, the process group only broadcasts the unique id
+        comm = shard.LibComm(ctx, world, rank, broadcast=shard.torch_broadcast)
+    args._comm = comm
     out = measure_job(args, cfg, rank, world, local_rank, ctx, dist, weak=args.weak)
     if out is not None and world > 1 and cfg["meshes"] > 1 and not args.weak:
         # the second scaling mode on the same ranks: every GPU carries a full
@@ -297,6 +303,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             out["weak_scaling"] = w
     elif world > 1 and cfg["meshes"] > 1 and not args.weak:
         measure_job(args, cfg, rank, world, local_rank, ctx, dist, weak=True, brief=True)
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.destroy_process_group()
     ctx.close()
@@ -318,12 +326,19 @@ def measure_job(args, cfg, rank, world, local_rank, ctx, dist, weak=False, brief
     job = GpuJob(cfg, ids, local_rank, ctx)
     verts_per_unit = job.n
     gather = dist is not None and cfg["meshes"] > 1
+    comm = getattr(args, "_comm", None)
+    gathered = torch.empty((total_meshes, 3 * job.n), dtype=torch.float64, device=job.dev) if gather else None
 
     def step(on_device):
         job.run(on_device)
         if gather and on_device:
-            # per-mesh reconstructions to every rank (NCCL over NVLink)
-            shard.gather_meshes(job.d_recon, total_meshes)
+            # per-mesh reconstructions to every rank: smg_gather_meshes (NCCL
+            # all-gather over NVLink, ragged shards padded in the library)
+            if comm is not None:
+                comm.gather(job.d_recon, gathered, total_meshes, 3 * job.n)
+                torch.cuda.synchronize()
+            else:
+                shard.gather_meshes(job.d_recon, total_meshes)
 
     def barrier():
         torch.cuda.synchronize()

@@ -46,6 +46,7 @@ typedef enum { SMG_BASIS_OI = 0, SMG_BASIS_DOI = 1 } smg_basis_mode;
 
 typedef struct smg_context smg_context;
 typedef struct smg_operator smg_operator;
+typedef struct smg_comm smg_comm;
 
 /* Mesh (mesh.hpp:18-37) + EdgeSet (mesh.hpp:40-50, neighbour lists sorted ascending). */
 typedef struct {
@@ -271,6 +272,24 @@ smg_status smg_fine_denoise(smg_context* ctx, int64_t vertex_count, const double
                             const double* z, int64_t face_count, const int32_t* faces,
                             const smg_bilateral_params* params, double* out, double* normals_out,
                             int32_t on_device);
+
+/* ------------------------------------------------------------ multi-GPU
+ * Independent chains shard over ranks, one process per GPU, no exchange during
+ * compute; per-mesh results are all-gathered (NCCL over NVLink / NVSwitch).
+ * NCCL is loaded at run time (libnccl.so.2; SMG_NCCL_LIB overrides). */
+
+/* the contiguous balanced slice of `total` chains owned by `rank` (the first
+ * total % world ranks get one extra) */
+smg_status smg_shard_range(int32_t total, int32_t world, int32_t rank, int32_t* first, int32_t* count);
+/* rank 0: a 128-byte NCCL unique id for the caller to broadcast */
+smg_status smg_comm_unique_id(smg_context* ctx, uint8_t* id);
+smg_status smg_comm_create(smg_context* ctx, const uint8_t* id, int32_t world, int32_t rank, smg_comm** out);
+void smg_comm_destroy(smg_comm* comm);
+/* all-gather of per-mesh rows in global mesh order: `local` = this rank's
+ * shard (smg_shard_range rows of row_doubles, device), `out` = total rows
+ * (device), on the context stream; ragged shards are padded internally */
+smg_status smg_gather_meshes(smg_context* ctx, smg_comm* comm, int32_t total, int64_t row_doubles,
+                             const double* local, double* out);
 
 /* ------------------------------------------------------------ segmentation (F1)
  * The step before the path, on the GPU and bit-exact with the reference's tie

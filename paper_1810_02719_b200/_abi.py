@@ -85,6 +85,7 @@ EXPORTED = [
     "smg_coarse_reconstruct_frames", "smg_denoise_dynamic", "smg_compress_blocks", "smg_decompress_blocks",
     "smg_default_bilateral_params", "smg_fine_denoise", "smg_doi_trace_enable", "smg_doi_trace_read",
     "smg_last_run_info", "smg_partition_mesh", "smg_expand_overlaps", "smg_order_submeshes", "smg_segment_mesh",
+    "smg_shard_range", "smg_comm_unique_id", "smg_comm_create", "smg_comm_destroy", "smg_gather_meshes",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -131,6 +132,11 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_doi_trace_enable": ([vp, C.c_int32], C.c_int),
         "smg_last_run_info": ([vp, C.POINTER(smg_run_info)], C.c_int),
         "smg_partition_mesh": ([vp, C.POINTER(smg_mesh), C.c_int32, C.c_uint64, vp], C.c_int),
+        "smg_shard_range": ([C.c_int32, C.c_int32, C.c_int32, c_int32_p, c_int32_p], C.c_int),
+        "smg_comm_unique_id": ([vp, vp], C.c_int),
+        "smg_comm_create": ([vp, vp, C.c_int32, C.c_int32, C.POINTER(vp)], C.c_int),
+        "smg_comm_destroy": ([vp], None),
+        "smg_gather_meshes": ([vp, vp, C.c_int32, C.c_int64, vp, vp], C.c_int),
         "smg_expand_overlaps": ([vp, C.POINTER(smg_mesh), vp, C.c_int32, C.c_double, vp, C.c_int64, c_int32_p],
                                 C.c_int),
         "smg_order_submeshes": ([vp, C.c_int32, vp, vp, C.c_uint64, vp], C.c_int),

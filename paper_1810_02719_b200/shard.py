@@ -70,4 +70,54 @@ def owner_of(mesh_id: int, total: int, world: int) -> int:
     raise AssertionError("unreachable")
 
 
-__all__: Sequence[str] = ("shard_meshes", "shard_counts", "gather_meshes", "owner_of")
+class LibComm:
+    """The library's own NCCL communicator (smg_comm_create): rank 0 makes the
+    unique id (smg_comm_unique_id), the caller's process group broadcasts it,
+    and smg_gather_meshes all-gathers per-mesh rows on the context stream --
+    the C++ host path a reference-side caller (C++ / MPI) would use directly."""
+
+    def __init__(self, ctx, world: int, rank: int, broadcast=None):
+        import ctypes as C
+        import numpy as np
+        self.ctx, self.world, self.rank = ctx, world, rank
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            ctx.check(ctx.lib.smg_comm_unique_id(ctx.handle, uid.ctypes.data))
+        if world > 1:
+            if broadcast is None:
+                raise ValueError("world > 1 needs a broadcast of the unique id")
+            uid = broadcast(uid)
+        self.handle = C.c_void_p()
+        ctx.check(ctx.lib.smg_comm_create(ctx.handle, uid.ctypes.data, world, rank, C.byref(self.handle)))
+
+    def gather(self, local, out, total: int, row_doubles: int) -> None:
+        """device pointers (ints) or objects with data_ptr()"""
+        lp = local.data_ptr() if hasattr(local, "data_ptr") else local
+        op = out.data_ptr() if hasattr(out, "data_ptr") else out
+        self.ctx.check(self.ctx.lib.smg_gather_meshes(self.ctx.handle, self.handle, int(total), int(row_doubles),
+                                                      lp, op))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.ctx.lib.smg_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def torch_broadcast(uid):
+    """broadcast a uint8 numpy array from rank 0 over the default process group"""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.from_numpy(uid.copy()).to(dev)
+    dist.broadcast(t, 0)
+    return np.ascontiguousarray(t.cpu().numpy())
+
+
+__all__: Sequence[str] = ("shard_meshes", "shard_counts", "gather_meshes", "owner_of", "LibComm", "torch_broadcast")

@@ -86,3 +86,20 @@ def test_gather_matches_single_process(total):
     for r in range(2):
         assert got[r].shape == expect.shape
         np.testing.assert_array_equal(got[r], expect)
+
+
+def test_library_shard_range_matches():
+    """smg_shard_range (the C++ host's sharding, include/specmesh_gpu.h) gives the
+    same slices as shard.shard_meshes -- host-only, no GPU needed."""
+    import ctypes as C
+    from paper_1810_02719_b200 import _abi
+    if not os.path.exists(_abi.LIB_PATH):
+        pytest.skip("libspecmesh_b200.so not built")
+    lib = _abi.load()
+    f, c = C.c_int32(), C.c_int32()
+    for total in range(0, 70):
+        for world in range(1, 9):
+            for r in range(world):
+                assert lib.smg_shard_range(total, world, r, C.byref(f), C.byref(c)) == 0
+                assert list(range(f.value, f.value + c.value)) == shard.shard_meshes(total, world, r)
+    assert lib.smg_shard_range(4, 2, 2, C.byref(f), C.byref(c)) == 2
