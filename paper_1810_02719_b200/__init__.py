@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
+import math
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -537,15 +538,22 @@ def segment_mesh(mesh, part_count: int = 8, growth: float = 1.15, seed: int = 1,
     keep: list = []
     mv = _mesh_view(mesh, keep)
     nd = C.c_int32()
-    seq = np.empty(int(part_count), np.int32)
+    k = int(part_count)
+    seq = np.empty(k, np.int32)
     a = np.empty(mesh.n, np.int32)
-    st = ctx.lib.smg_segment_mesh(ctx.handle, C.byref(mv), int(part_count), float(growth), seed & ((1 << 64) - 1),
-                                  None, None, 0, C.byref(nd), _ptr(seq))
-    if nd.value <= 0:
-        ctx.check(st)
-    mem = np.empty(int(part_count) * nd.value, np.int32)
-    ctx.check(ctx.lib.smg_segment_mesh(ctx.handle, C.byref(mv), int(part_count), float(growth),
-                                       seed & ((1 << 64) - 1), _ptr(a), _ptr(mem), mem.size, C.byref(nd), _ptr(seq)))
+    # parts stay near cap = int(ceil(n/k) * 1.1) (beyond it only once every part is capped):
+    # size the member buffer for that (a second call only in the rare case)
+    cap = int(math.ceil(mesh.n / max(k, 1)) * 1.1) if k >= 1 else 1
+    guess = max(1, min(mesh.n, int(math.floor(float(growth) * 2 * cap)) + 1))
+    mem = np.empty(max(k, 1) * guess, np.int32)
+    st = ctx.lib.smg_segment_mesh(ctx.handle, C.byref(mv), k, float(growth), seed & ((1 << 64) - 1), _ptr(a),
+                                  _ptr(mem), mem.size, C.byref(nd), _ptr(seq))
+    if st != _abi.SMG_OK:
+        if nd.value <= 0 or k * nd.value <= mem.size:
+            ctx.check(st)
+        mem = np.empty(k * nd.value, np.int32)
+        ctx.check(ctx.lib.smg_segment_mesh(ctx.handle, C.byref(mv), k, float(growth), seed & ((1 << 64) - 1),
+                                           _ptr(a), _ptr(mem), mem.size, C.byref(nd), _ptr(seq)))
     segm = Segmentation([mem[i * nd.value:(i + 1) * nd.value].copy() for i in range(int(part_count))], seq)
     return (segm, a) if return_assignment else segm
 

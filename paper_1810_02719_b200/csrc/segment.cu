@@ -183,6 +183,235 @@ __global__ void grow_kernel(const int32_t* __restrict__ offs, const int32_t* __r
     }
 }
 
+// The same loop, round-parallel and exact.  While no part fails or reaches
+// the cap, the serial loop picks the parts of the current minimum size in
+// ascending id, each growing by one (after p grows to s+1, every remaining
+// size-s part still precedes it): a "round".  All parts of a round propose
+// their next vertex at once against the assignment at the round's start
+// (front vertices without an unassigned neighbour are popped -- that stays
+// true); then the proposals are taken in id order.  A proposal is exactly the
+// serial choice unless an earlier part of the round took the same vertex
+// (claim[w] = lowest proposer, atomicMin): from the first such collision on,
+// the parts are replayed one by one by warp 0 (the rescan sees the earlier
+// parts' assignments), which is the serial loop itself.  Rounds of one or two
+// parts run serially outright.
+constexpr int kGrowWarps = 32;
+
+__global__ void __launch_bounds__(kGrowWarps * 32) grow_rounds_kernel(const int32_t* __restrict__ offs,
+                                                                      const int32_t* __restrict__ cols, int n, int k,
+                                                                      int cap, const int32_t* seeds, int32_t* assign,
+                                                                      int32_t* next, int32_t* cursor, int32_t* claim,
+                                                                      int* status) {
+    extern __shared__ int sm[];
+    int* head = sm;
+    int* tail = sm + k;
+    int* size = sm + 2 * k;
+    int* R = sm + 3 * k;      // this round's parts, ascending id
+    int* prop = sm + 4 * k;   // proposed vertex (-1: frontier exhausted)
+    int* pcur = sm + 5 * k;   // cursor value after the proposal
+    int* pv = sm + 6 * k;     // front vertex the proposal came from
+    __shared__ int nR, smin_cap, smin_any, assigned_s, first_conflict, err;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int p = tid; p < k; p += blockDim.x) {
+        const int s = seeds[p];
+        head[p] = tail[p] = s;
+        size[p] = 1;
+        assign[s] = p;
+        next[s] = -1;
+    }
+    if (tid == 0) {
+        assigned_s = k;
+        err = 0;
+    }
+    __syncthreads();
+    // one-warp replay of a pick of part p (the serial loop's body); returns grew
+    auto serial_pick = [&](int p) -> bool {
+        bool grew = false;
+        while (!grew) {
+            const int v = head[p];
+            if (v < 0) break;
+            const int o0 = offs[v], o1 = offs[v + 1];
+            int base = o0 + __ldcg(cursor + v);
+            while (base < o1) {
+                const int j = base + lane;
+                int w = -1;
+                bool fr = false;
+                if (j < o1) {
+                    w = cols[j];
+                    fr = __ldcg(assign + w) < 0;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, fr);
+                if (m) {
+                    const int f = __ffs(m) - 1;
+                    w = __shfl_sync(0xffffffffu, w, f);
+                    if (lane == 0) {
+                        assign[w] = p;
+                        next[w] = -1;
+                        next[tail[p]] = w;
+                        tail[p] = w;
+                        size[p] += 1;
+                        cursor[v] = base + f + 1 - o0;
+                    }
+                    grew = true;
+                    break;
+                }
+                base += 32;
+            }
+            if (!grew && lane == 0) {
+                cursor[v] = o1 - o0;
+                const int nx = __ldcg(next + v);
+                head[p] = nx;
+                if (nx < 0) tail[p] = -1;
+            }
+            __syncwarp();
+        }
+        return grew;
+    };
+    while (true) {
+        // ---- the round: parts of the minimum size among those with a frontier
+        // below cap (or, once every such part is capped, among all with one)
+        if (tid == 0) {
+            smin_cap = INT_MAX;
+            smin_any = INT_MAX;
+            nR = 0;
+            first_conflict = INT_MAX;
+        }
+        __syncthreads();
+        if (assigned_s >= n) break;
+        for (int p = tid; p < k; p += blockDim.x)
+            if (head[p] >= 0) {
+                atomicMin(&smin_any, size[p]);
+                if (size[p] < cap) atomicMin(&smin_cap, size[p]);
+            }
+        __syncthreads();
+        const bool capmode = smin_cap != INT_MAX;
+        const int smin = capmode ? smin_cap : smin_any;
+        if (smin == INT_MAX) {
+            if (tid == 0) *status = 1;
+            return;
+        }
+        // compaction in id order (warp-level ballots, warps in order)
+        if (warp == 0) {
+            int cnt = 0;
+            for (int p0 = 0; p0 < k; p0 += 32) {
+                const int p = p0 + lane;
+                const bool in = p < k && head[p] >= 0 && size[p] == smin && (!capmode || size[p] < cap);
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                if (in) R[cnt + __popc(m & ((1u << lane) - 1))] = p;
+                cnt += __popc(m);
+            }
+            if (lane == 0) nR = cnt;
+        }
+        __syncthreads();
+        const int nr = nR;
+        if (nr <= 2) {
+            if (warp == 0) {
+                int grown = 0;
+                for (int i = 0; i < nr; ++i) grown += serial_pick(R[i]) ? 1 : 0;
+                if (lane == 0) assigned_s += grown;
+            }
+            __syncthreads();
+            continue;
+        }
+        // ---- proposals, one warp per part (scans read the round-start assignment)
+        for (int i = warp; i < nr; i += kGrowWarps) {
+            const int p = R[i];
+            int w = -1, cur = 0, vv = -1;
+            while (true) {
+                const int v = head[p];
+                if (v < 0) break;
+                const int o0 = offs[v], o1 = offs[v + 1];
+                int base = o0 + __ldcg(cursor + v);
+                bool found = false;
+                while (base < o1) {
+                    const int j = base + lane;
+                    int x = -1;
+                    bool fr = false;
+                    if (j < o1) {
+                        x = cols[j];
+                        fr = __ldcg(assign + x) < 0;
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, fr);
+                    if (m) {
+                        const int f = __ffs(m) - 1;
+                        w = __shfl_sync(0xffffffffu, x, f);
+                        cur = base + f + 1 - o0;
+                        vv = v;
+                        found = true;
+                        break;
+                    }
+                    base += 32;
+                }
+                if (found) break;
+                if (lane == 0) {  // exhausted at the round start: exhausted for good
+                    cursor[v] = o1 - o0;
+                    const int nx = __ldcg(next + v);
+                    head[p] = nx;
+                    if (nx < 0) tail[p] = -1;
+                }
+                __syncwarp();
+            }
+            if (lane == 0) {
+                prop[i] = w;
+                pcur[i] = cur;
+                pv[i] = vv;
+                if (w >= 0) atomicMin(claim + w, i);
+            }
+        }
+        __syncthreads();
+        // ---- first collision in id order
+        for (int i = tid; i < nr; i += blockDim.x)
+            if (prop[i] >= 0 && __ldcg(claim + prop[i]) != i) atomicMin(&first_conflict, i);
+        __syncthreads();
+        const int cfl = first_conflict;
+        // the collision-free prefix commits in parallel
+        int grown = 0;
+        for (int i = tid; i < min(nr, cfl); i += blockDim.x) {
+            const int p = R[i], w = prop[i];
+            if (w < 0) continue;
+            assign[w] = p;
+            next[w] = -1;
+            next[tail[p]] = w;
+            tail[p] = w;
+            size[p] += 1;
+            cursor[pv[i]] = pcur[i];
+            ++grown;
+        }
+        grown = __reduce_add_sync(0xffffffffu, grown);
+        if (lane == 0 && grown) atomicAdd(&assigned_s, grown);
+        __syncthreads();
+        // from the collision on: the serial loop (a proposal still stands when
+        // no earlier part claimed its vertex and it is still free)
+        if (cfl < nr && warp == 0) {
+            int g2 = 0;
+            for (int i = cfl; i < nr; ++i) {
+                const int p = R[i], w = prop[i];
+                if (w < 0) continue;  // frontier exhausted: this pick fails
+                const bool ok = (__ldcg(claim + w) == i) && (__ldcg(assign + w) < 0);
+                if (ok) {
+                    if (lane == 0) {
+                        assign[w] = p;
+                        next[w] = -1;
+                        next[tail[p]] = w;
+                        tail[p] = w;
+                        size[p] += 1;
+                        cursor[pv[i]] = pcur[i];
+                    }
+                    __syncwarp();
+                    ++g2;
+                } else {
+                    g2 += serial_pick(p) ? 1 : 0;
+                }
+            }
+            if (lane == 0) assigned_s += g2;
+        }
+        __syncthreads();
+        for (int i = tid; i < nr; i += blockDim.x)
+            if (prop[i] >= 0) claim[prop[i]] = INT_MAX;
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------ expand_overlaps
 
 constexpr int kExpThreads = 512;
@@ -464,10 +693,20 @@ void partition_mesh_dev(const GraphDev& g, int k, uint64_t seed, int32_t* assign
     status.zero();
     SMG_CUDA(cudaMemsetAsync(assignment, 0xFF, sizeof(int32_t) * n, st));  // -1
     const int cap = (int)(std::ceil((double)n / k) * 1.1);
-    const int smem = 3 * k * (int)sizeof(int);
-    ensure_smem((const void*)grow_kernel, smem);
-    ::smg::count_launch(), grow_kernel<<<1, 32, smem, st>>>(g.offs, g.cols, n, k, cap, seeds.get(), assignment,
-                                                            next.get(), cursor.get(), status.get());
+    if (std::getenv("SMG_GROW_SERIAL") || 7 * k * (int)sizeof(int) > 200 * 1024) {
+        const int smem = 3 * k * (int)sizeof(int);
+        ensure_smem((const void*)grow_kernel, smem);
+        ::smg::count_launch(), grow_kernel<<<1, 32, smem, st>>>(g.offs, g.cols, n, k, cap, seeds.get(), assignment,
+                                                                next.get(), cursor.get(), status.get());
+    } else {
+        DBuf<int32_t> claim;
+        claim.alloc(n, st);
+        SMG_CUDA(cudaMemsetAsync(claim.get(), 0x7F, sizeof(int32_t) * n, st));  // 0x7F7F7F7F > any round index
+        const int smem = 7 * k * (int)sizeof(int);
+        ensure_smem((const void*)grow_rounds_kernel, smem);
+        ::smg::count_launch(), grow_rounds_kernel<<<1, kGrowWarps * 32, smem, st>>>(
+            g.offs, g.cols, n, k, cap, seeds.get(), assignment, next.get(), cursor.get(), claim.get(), status.get());
+    }
     SMG_CUDA(cudaGetLastError());
     int h = 0;
     SMG_CUDA(cudaMemcpyAsync(&h, status.get(), sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -73,7 +73,7 @@ def test_segment_mesh_bit_exact(ctx, name, k):
     for gm, om in zip(seg.members, members):
         assert np.array_equal(gm, om)
     assert np.array_equal(seg.sequence, seq)
-    print(f"{name} k={k}: n_d={seg.block_size}, GPU segment_mesh {t_gpu * 1e3:.1f} ms (two calls)")
+    print(f"{name} k={k}: n_d={seg.block_size}, GPU segment_mesh {t_gpu * 1e3:.1f} ms")
 
 
 def test_compute_block_bases_segments_itself(ctx):
