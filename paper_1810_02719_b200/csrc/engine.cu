@@ -112,7 +112,7 @@ void TileSet::finish_build(double shift_scale, const std::vector<double>* explic
     // A narrower W halves the solve's flops and shrinks its per-step slabs, but
     // doubles its sequential steps: worth it when many tiles keep the GPU
     // throughput-bound, not for a few latency-bound chains whose natural order works.
-    if (coords && !topology_ordering && !force_nat && (supported_width(wmax) < 0 || ntiles >= 2048 || force_geo)) {
+    if (coords && !topology_ordering && !force_nat && (supported_width(wmax) < 0 || ntiles >= 1024 || force_geo)) {
         DBuf<int32_t> ap;
         ap.alloc((size_t)ntiles * n, st);
         axis_order(coords, (int64_t)n * 3, ntiles, n, ap.get(), st);
