@@ -32,7 +32,7 @@ oracle/_ref/rng_ref: oracle/rng_ref.cpp
 	g++ -O2 -std=c++17 -o $@ $<
 
 # standalone kernel timing tools (not part of the library)
-tools: build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_f3r4 build/solve_bench_nomma_ns5 build/chol_bench
+tools: build/cholx_bench build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_f3r4 build/solve_bench_nomma_ns5 build/chol_bench
 
 build/solve_bench: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
@@ -74,3 +74,7 @@ clean:
 	rm -rf build $(LIB) oracle/_ref
 
 .PHONY: all clean oracle tools
+
+build/cholx_bench: tools/cholx_bench.cu $(SRC_DIR)/cholx.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_CHOLX_TIMING -o $@ $<

@@ -246,3 +246,31 @@ def test_chain_cold_start_first_basis(ctx, dense_limit):
     # the cold start is not the dense eigenbasis: 12 R^2 steps from a random block
     dense = O.bottom_subspace(O.dense_eigendecomposition(O.build_laplacian(subs[0], mesh.vertices, O.BINARY)), 24)
     assert O.max_principal_angle(ob.bases[0], dense) > 1e-6
+
+
+def test_run_info_and_doi_host_loop(ctx, monkeypatch):
+    """smg_last_run_info reports the factorisation the library chose; the
+    host-driven DOI loop (SMG_DOI_NOGRAPH, for profilers) takes the same
+    decisions as the CUDA-graph WHILE loop, step for step."""
+    mesh = synth.small_grid(128, 64, 32, 32, seed=4, flip=8)
+    seg = synth.grid_tiles(128, 64, 32, 32)
+    cfg = G.PipelineConfig(weighting="binary", subspace_size=40, iterations=1, shift_scale=1e-3)
+    G.compute_block_bases_fixed_sizes(mesh, seg, cfg, [40] * seg.count, ctx=ctx)
+    info = ctx.last_run_info()
+    assert info["chains"] == 1 and info["positions"] == seg.count and info["block_width"] in (32, 33, 48, 64)
+    assert info["ordering"] in ("natural", "geometric", "rcm")
+    dcfg = G.PipelineConfig(weighting="binary", basis_mode="doi", subspace_size=10, c_min=5, c_max=120,
+                            eps_low=3e-4, eps_high=3e-3, shift_scale=1e-3)
+    ctx.doi_trace(True)
+    a = G.compute_block_bases(mesh, seg, dcfg, ctx=ctx)
+    ta = ctx.read_doi_trace()
+    ctx.doi_trace(True)
+    monkeypatch.setenv("SMG_DOI_NOGRAPH", "1")
+    b = G.compute_block_bases(mesh, seg, dcfg, ctx=ctx)
+    tb = ctx.read_doi_trace()
+    ctx.doi_trace(False)
+    assert [s.subspace_size for s in a.stats] == [s.subspace_size for s in b.stats]
+    assert [s.oi_iterations for s in a.stats] == [s.oi_iterations for s in b.stats]
+    assert np.array_equal(ta[0], tb[0]) and np.array_equal(ta[1], tb[1])
+    assert np.allclose(ta[2], tb[2], rtol=1e-12, atol=0)
+    assert np.array_equal(a.reconstruction, b.reconstruction)
