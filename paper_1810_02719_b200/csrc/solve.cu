@@ -46,7 +46,12 @@ struct SolveSmem {
     static constexpr int F_ELEMS = 2 * W * FS;
     static constexpr int R_ELEMS = W * XS;
     static constexpr int FB = F_ELEMS * 8, RB = R_ELEMS * 8, YB = 2 * RB;
-    static constexpr int HALF = 113 * 1024, FULL = 226 * 1024;
+    // W = 32, CS = 16 (large batches): a budget for three CTAs per SM (two rhs
+    // slots instead of six).  The solve is bound by per-CTA step latency, so a
+    // third resident CTA raises the SM's throughput: C5 418 -> 377 us per
+    // launch against 32-column slices at two CTAs per SM (which were faster
+    // than 16-column slices at two per SM).
+    static constexpr int HALF = (W == 32 && CS == 16) ? 75 * 1024 : 113 * 1024, FULL = 226 * 1024;
     static constexpr bool TWO = 2 * FB + 3 * RB + YB <= HALF;
     static constexpr int BUDGET = TWO ? HALF : FULL;
 #ifdef SMG_SOLVE_NSF_FORCE  // timing probe: slab ring depth override
@@ -470,7 +475,7 @@ void solve_block_tridiag(const SolveParams& p, int W, cudaStream_t st) {
     switch (W) {
         case 16: launch<16, 8>(p, st); break;
         case 32:
-            if (wide) launch<32, 32>(p, st);
+            if (wide && std::getenv("SMG_SOLVE_CS") && std::atoi(std::getenv("SMG_SOLVE_CS")) >= 32) launch<32, 32>(p, st);
             else if (mid) launch<32, 16>(p, st);
             else launch<32, 8>(p, st);
             break;
