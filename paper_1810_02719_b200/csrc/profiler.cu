@@ -41,6 +41,7 @@ Profiler*& active_profiler() {
 }
 
 void Profiler::clear() {
+    std::lock_guard<std::mutex> lock(mu_);
     for (cudaEvent_t e : pool_) cudaEventDestroy(e);
     pool_.clear();
     spans_.clear();
@@ -58,15 +59,18 @@ int Profiler::begin(cudaStream_t st) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
     if (cs != cudaStreamCaptureStatusNone) return -1;  // not inside graph capture
+    std::lock_guard<std::mutex> lock(mu_);
     return new_event(st);
 }
 
 void Profiler::end(const char* stage, int token, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(mu_);
     const int b = new_event(st);
     if (b >= 0) spans_[stage].push_back({token, b});
 }
 
 bool Profiler::read(const std::string& stage, int64_t* launches, double* total_ms) {
+    std::lock_guard<std::mutex> lock(mu_);
     auto it = spans_.find(stage);
     if (it == spans_.end()) {
         *launches = 0;

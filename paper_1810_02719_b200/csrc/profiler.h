@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -25,6 +26,7 @@ public:
 private:
     std::vector<cudaEvent_t> pool_;
     std::map<std::string, std::vector<std::pair<int, int>>> spans_;
+    std::mutex mu_;  // chain groups issue from their own host threads
     int new_event(cudaStream_t st);
 };
 
