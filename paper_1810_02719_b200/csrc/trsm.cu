@@ -28,7 +28,9 @@ template <int MI, bool CHUNK>
 struct TrsmCfg {
     static constexpr int TRB = 32 * MI;
     __host__ __device__ static int qs(int cp) { return cp + 4; }
-    static int bytes(int cp) { return (TRB * qs(cp) + (CHUNK ? KC : cp) * PS36 + 32 * PS36 + TRB * PS36) * 8; }
+    // CHUNK: two KC-row buffers (the next chunk streams in by cp.async while the
+    // current one is multiplied)
+    static int bytes(int cp) { return (TRB * qs(cp) + (CHUNK ? 2 * KC : cp) * PS36 + 32 * PS36 + TRB * PS36) * 8; }
 };
 using TrsmFull = TrsmCfg<2, false>;
 using TrsmStream = TrsmCfg<1, true>;
@@ -44,8 +46,8 @@ __global__ void __launch_bounds__(TNT) trsm_kernel(TrsmParams p) {
     const int P = (c + 31) / 32, cp = (p.c_cap + 31) / 32 * 32;
     const int QS = TC::qs(cp);
     double* Qs = sm;                         // TRB x QS: finished panels of this row block
-    double* Rc = Qs + TRB * QS;              // (cp | KC) x 36: column panel p of R~ (rows < p0)
-    double* Xp = Rc + (CHUNK ? KC : cp) * PS36;  // 32 x 36: X_pp
+    double* Rc = Qs + TRB * QS;              // (cp | 2 x KC) x 36: column panel p of R~ (rows < p0)
+    double* Xp = Rc + (CHUNK ? 2 * KC : cp) * PS36;  // 32 x 36: X_pp
     double* Tp = Xp + 32 * PS36;      // TRB x 36: T
     const int r0 = blockIdx.x * TRB;
     const double* V = p.V + (int64_t)b * p.strideV;
@@ -82,15 +84,32 @@ __global__ void __launch_bounds__(TNT) trsm_kernel(TrsmParams p) {
                 }
         __syncthreads();
         // T -= Q[:, <p] R~[<p, p]
-        for (int k0 = 0; k0 < p0; k0 += (CHUNK ? KC : p0)) {
+        // CHUNK: the R~ column streams through two KC-row buffers, chunk i+1
+        // copied by cp.async while chunk i is multiplied
+        const int nch = CHUNK ? (p0 + KC - 1) / KC : (p0 > 0 ? 1 : 0);
+        auto stage = [&](int ci) {
+            double* buf = Rc + (ci & 1) * KC * PS36;
+            const int k0 = ci * KC, rows = min(KC, p0 - k0);
+            for (int e = tid; e < rows * 16; e += TNT) {  // 16 pieces of 16 bytes per 32-double row
+                const int r = e >> 4, q = e & 15;
+                cp_async16(buf + r * PS36 + 2 * q, A + (int64_t)(k0 + r) * p.ldr + p0 + 2 * q);
+            }
+            cp_async_commit();
+        };
+        if (CHUNK && nch > 0) stage(0);
+        for (int ci = 0; ci < nch; ++ci) {
+            const int k0 = CHUNK ? ci * KC : 0;
             const int k1 = CHUNK ? min(p0, k0 + KC) : p0;
+            const double* rc = Rc;
             if (CHUNK) {
-                if (k0 > 0) __syncthreads();  // the previous chunk is consumed
-                for (int e = tid; e < (k1 - k0) * 32; e += TNT) {
-                    const int r = e >> 5, k = e & 31;
-                    Rc[r * PS36 + k] = A[(int64_t)(k0 + r) * p.ldr + p0 + k];
+                if (ci + 1 < nch) {
+                    stage(ci + 1);
+                    cp_async_wait<1>();
+                } else {
+                    cp_async_wait<0>();
                 }
-                __syncthreads();
+                __syncthreads();  // chunk ci visible to every warp
+                rc = Rc + (ci & 1) * KC * PS36;
             }
             for (int kk = k0; kk < k1; kk += 4) {
                 const int kr = CHUNK ? kk - k0 : kk;
@@ -98,12 +117,13 @@ __global__ void __launch_bounds__(TNT) trsm_kernel(TrsmParams p) {
 #pragma unroll
                 for (int i = 0; i < MI; ++i) a[i] = Qs[(8 * MI * wm + 8 * i + g) * QS + kk + t];
 #pragma unroll
-                for (int j = 0; j < 2; ++j) bb[j] = -Rc[(kr + t) * PS36 + 16 * wn + 8 * j + g];
+                for (int j = 0; j < 2; ++j) bb[j] = -rc[(kr + t) * PS36 + 16 * wn + 8 * j + g];
 #pragma unroll
                 for (int i = 0; i < MI; ++i)
 #pragma unroll
                     for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
             }
+            if (CHUNK) __syncthreads();  // buffer ci & 1 is re-staged at iteration ci + 1
         }
 #pragma unroll
         for (int i = 0; i < MI; ++i)
