@@ -541,8 +541,18 @@ SMG_DEV void rank_test_block(const RankCheckParams& p, int b, int nchunks) {
     __syncthreads();
     const double thresh = 1e-13 * p.vnorm[b];
     for (int k = threadIdx.x; k < c; k += blockDim.x) {
+        // chunk order (deterministic); 16 loads issued ahead of their adds
         double r = 0.0;
-        for (int ch = 0; ch < nchunks; ++ch) r += p.partial[((int64_t)b * nchunks + ch) * p.c_cap + k];
+        const double* src = p.partial + (int64_t)b * nchunks * p.c_cap + k;
+        int ch = 0;
+        for (; ch + 16 <= nchunks; ch += 16) {
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = __ldcg(src + (int64_t)(ch + u) * p.c_cap);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) r += v[u];
+        }
+        for (; ch < nchunks; ++ch) r += __ldcg(src + (int64_t)ch * p.c_cap);
         if (!(fabs(r) >= thresh)) atomicMin(&first, k);
     }
     __syncthreads();
