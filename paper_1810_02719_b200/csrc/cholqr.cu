@@ -632,19 +632,26 @@ __global__ void orth_check_kernel(const double* G, int64_t ldg, int64_t strideG,
     }
 }
 
-// row block of 32 rows per CTA, warp per row: max |G_ik / (d_i d_k) - delta_ik|, k >= i
+// NEAR_ROWS rows per CTA (warp per row), the diagonal's reciprocal square
+// roots staged once per CTA: max |G_ik / (d_i d_k) - delta_ik|, k >= i
+constexpr int NEAR_ROWS = 8;
+constexpr int NEAR_MAXC = 512;
 __global__ void near_check_kernel(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap,
                                   unsigned long long* nmax) {
+    __shared__ double rd[NEAR_MAXC];
     const int b = blockIdx.y;
     const int c = dimC ? dimC[b] : c_cap;
     const double* g = G + (int64_t)b * strideG;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x * NEAR_ROWS >= c) return;
+    for (int k = threadIdx.x; k < c; k += blockDim.x) rd[k] = 1.0 / sqrt(__ldcg(g + (int64_t)k * ldg + k));
+    __syncthreads();
     double e = 0.0;
-    for (int i = blockIdx.x * 32 + warp; i < min(c, blockIdx.x * 32 + 32); i += nw) {
-        const double ri = 1.0 / sqrt(__ldcg(g + (int64_t)i * ldg + i));
+    const int i = blockIdx.x * NEAR_ROWS + warp;
+    if (i < c) {
+        const double ri = rd[i];
         for (int k = i + lane; k < c; k += 32) {
-            const double rk = 1.0 / sqrt(__ldcg(g + (int64_t)k * ldg + k));
-            const double x = fabs(__ldcg(g + (int64_t)i * ldg + k) * ri * rk - (i == k ? 1.0 : 0.0));
+            const double x = fabs(__ldcg(g + (int64_t)i * ldg + k) * ri * rd[k] - (i == k ? 1.0 : 0.0));
             e = (x <= e) ? e : (x == x ? x : INFINITY);
         }
     }
@@ -665,17 +672,19 @@ __global__ void near_fill_kernel(const double* G, int64_t ldg, int64_t strideG, 
     const int cp = (c_cap + 31) / 32 * 32;
     const double* g = G + (int64_t)b * strideG;
     double* B = Bo + (int64_t)b * strideB;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int i = blockIdx.x * 32 + warp; i < min(cp, blockIdx.x * 32 + 32); i += nw) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x * NEAR_ROWS >= cp) return;
+    __shared__ double rd[NEAR_MAXC];
+    for (int k = threadIdx.x; k < c; k += blockDim.x) rd[k] = 1.0 / sqrt(__ldcg(g + (int64_t)k * ldg + k));
+    __syncthreads();
+    const int i = blockIdx.x * NEAR_ROWS + warp;
+    if (i < cp) {
         const double di = i < c ? sqrt(__ldcg(g + (int64_t)i * ldg + i)) : 1.0;
         const double ri = di > 0.0 ? 1.0 / di : 0.0;
         if (lane == 0) dscale[(int64_t)b * strideD + i] = di;
         for (int k = lane; k < cp; k += 32) {
             double v = (k == i) ? 1.0 : 0.0;
-            if (k > i && k < c) {
-                const double rk = 1.0 / sqrt(__ldcg(g + (int64_t)k * ldg + k));
-                v = -__ldcg(g + (int64_t)i * ldg + k) * ri * rk;
-            }
+            if (k > i && k < c) v = -__ldcg(g + (int64_t)i * ldg + k) * ri * rd[k];
             B[(int64_t)i * ldb + k] = v * ri;
         }
     }
@@ -699,16 +708,16 @@ void orth_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, 
 
 void near_check(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap, int batch,
                 unsigned long long* nmax, cudaStream_t st) {
-    const int P = (c_cap + 31) / 32;
-    ::smg::count_launch(), near_check_kernel<<<dim3(P, batch), 256, 0, st>>>(G, ldg, strideG, dimC, c_cap, nmax);
+    const int nb = (c_cap + NEAR_ROWS - 1) / NEAR_ROWS;
+    ::smg::count_launch(), near_check_kernel<<<dim3(nb, batch), 32 * NEAR_ROWS, 0, st>>>(G, ldg, strideG, dimC, c_cap, nmax);
 }
 
 void near_fill(const double* G, int64_t ldg, int64_t strideG, const int* dimC, int c_cap, int batch,
                const unsigned long long* nmax, const int* skip_in, int* skip_out, double* Binv, int64_t ldb,
                int64_t strideB, double* dscale, int64_t strideD, cudaStream_t st) {
-    const int P = (c_cap + 31) / 32;
-    ::smg::count_launch(), near_fill_kernel<<<dim3(P, batch), 256, 0, st>>>(G, ldg, strideG, dimC, c_cap, nmax, skip_in,
-                                                                            skip_out, Binv, ldb, strideB, dscale, strideD);
+    const int nb = ((c_cap + 31) / 32 * 32 + NEAR_ROWS - 1) / NEAR_ROWS;
+    ::smg::count_launch(), near_fill_kernel<<<dim3(nb, batch), 32 * NEAR_ROWS, 0, st>>>(
+        G, ldg, strideG, dimC, c_cap, nmax, skip_in, skip_out, Binv, ldb, strideB, dscale, strideD);
 }
 
 void copy_unskipped(const double* src, double* dst, int64_t elems, int64_t stride, int batch, const int* skip,
