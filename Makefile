@@ -32,7 +32,7 @@ oracle/_ref/rng_ref: oracle/rng_ref.cpp
 	g++ -O2 -std=c++17 -o $@ $<
 
 # standalone kernel timing tools (not part of the library)
-tools: build/cholx_bench build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_f3r4 build/solve_bench_nomma_ns5 build/chol_bench
+tools: build/cholx_bench build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_halfslab build/solve_bench_notri build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_f3r4 build/solve_bench_nomma_ns5
 
 build/solve_bench: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
@@ -44,7 +44,15 @@ build/solve_bench_norhs: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 
 build/solve_bench_noslab: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
-	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_SLAB -o $@ $<
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_SLAB_DIV=1000 -o $@ $<
+
+build/solve_bench_notri: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_NO_TRI -o $@ $<
+
+build/solve_bench_halfslab: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_SOLVE_SLAB_DIV=2 -o $@ $<
 
 build/solve_bench_f3r4: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build

@@ -453,7 +453,9 @@ public:
                         solve_batch(gx, g.ws, fcur, tile0, 1, g.ws.U.get(), g.ws.V.get(), c, nullptr, cfg_.power,
                                     false);
                         wait_proj();
-                        orth_batch(gx, g.ws, g.ws.V.get(), g.ws.U.get(), c, nullptr, true, pos, 2, orth_skip_tol());
+                        const bool last_it = it + 1 == cfg_.iterations;
+                        orth_batch(gx, g.ws, g.ws.V.get(), g.ws.U.get(), c, nullptr, true, pos, 2, orth_skip_tol(),
+                                   last_it ? ts_.X.get() + (int64_t)tile0 * n_ * 3 : nullptr, (int64_t)n_ * 3);
                     }
                     SMG_CUDA(cudaEventRecord(g.ev_orth, g.st));
                     SMG_CUDA(cudaStreamWaitEvent(g.pst, g.ev_orth, 0));

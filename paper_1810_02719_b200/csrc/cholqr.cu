@@ -270,13 +270,15 @@ __global__ void __launch_bounds__(CNT) chol_kernel(CholParams p) {
         // failing column of the block (the pivots do not depend on the test)
         if (warp == 0) {
             const int gj = p0 + lane;
-            bool badc = false;
+            bool badc = false, unsure = false;
             if (gj < c) {
                 const double pj = pivs[lane];
                 const bool bp = !(pj > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(pj) || !(ds[gj] > 0.0);
                 const double rkk = bp ? 0.0 : sqrt(pj) * ds[gj];
                 badc = bp || (p.rank_test && rkk < thresh);
+                unsure = p.rank_test && !bp && (pj < kRankCertPiv || rkk < kRankCertRel * scale);
             }
+            if (p.rank_need && __any_sync(0xffffffffu, unsure) && lane == 0) atomicOr(p.rank_need + b, 1);
             const unsigned m = __ballot_sync(0xffffffffu, badc);
             if (lane == 0 && m) {
                 record(p.rank_test ? kRankDeficient : kNotFinite, p0 + __ffs(m) - 1);
@@ -568,6 +570,7 @@ constexpr int RC_ROWS = 32;
 __global__ void rank_partial_kernel(RankCheckParams p) {
     const int b = blockIdx.y, chunk = blockIdx.x;
     if (p.status[b] != kOk) return;
+    if (p.need && !p.need[b]) return;  // every column certified by the pass-1 pivots
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
     const int r0 = chunk * RC_ROWS, r1 = min(p.n, r0 + RC_ROWS);
     const double* Q = p.Q + (int64_t)b * p.stride;

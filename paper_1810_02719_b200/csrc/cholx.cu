@@ -220,12 +220,14 @@ __global__ void __launch_bounds__(XNT, 1) cholx_kernel(CholParams p) {
             }
             // rank test on the pivots (first failing column of the block)
             const int gj = pb * 32 + lane;
-            bool badc = false;
+            bool badc = false, unsure = false;
             if (gj < c) {
                 const bool bp = !(piv > (p.rank_test ? 1e-12 : 0.0)) || !isfinite(piv) || !(ds[gj] > 0.0);
                 const double rkk = bp ? 0.0 : sqrt(piv) * ds[gj];
                 badc = bp || (p.rank_test && rkk < thresh);
+                unsure = p.rank_test && !bp && (piv < kRankCertPiv || rkk < kRankCertRel * scale);
             }
+            if (p.rank_need && __any_sync(0xffffffffu, unsure) && lane == 0) atomicOr(p.rank_need + b, 1);
             const unsigned m = __ballot_sync(0xffffffffu, badc);
             if (m) {
                 if (lane == 0) {

@@ -77,6 +77,13 @@ SMG_DEV double block_sum(double v, double* scratch /* >= 32 doubles */) {
     return r;
 }
 
+// Rank test certification margins (pass-1 Cholesky of the column-scaled Gram,
+// unit diagonal): a scaled pivot >= 1e-8 is known to relative 1e-6 (absolute
+// pivot error ~ c * eps), and r_kk >= 1e-9 ||V||_F is 1e4 above the reference
+// threshold 1e-13 ||V||_F (spectral.hpp:126-128), so |q_k^T v_k| passes for sure.
+constexpr double kRankCertPiv = 1e-8;
+constexpr double kRankCertRel = 1e-9;
+
 // Status codes written by kernels into device status words.
 enum DeviceStatus : int {
     kOk = 0,

@@ -241,6 +241,8 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     nmax.alloc(B, st);
     errpos.alloc(B, st);
     errpos.zero();
+    rneed.alloc(B, st);
+    rneed.zero();
     detail.alloc(B, st);
     detail.zero();
 }
@@ -349,8 +351,16 @@ bool use_trsm(int c, int batch) {
 }
 
 void trmm(Workspace& ws, const double* V, double* out, int c, const int* dimC, int n, cudaStream_t st,
-          const int* skip = nullptr) {
+          const int* skip = nullptr, const double* projX = nullptr, int64_t strideX = 0) {
     GemmParams g;
+    if (projX) {
+        g.projX = projX;
+        g.strideProjX = strideX;
+        g.projPart = ws.ppart.get();
+        g.projN = ws.n;
+        g.projChunks = proj_chunks(ws.n);
+        g.projCcap = c;
+    }
     g.skip = skip;
     g.M = n;
     g.N = c;
@@ -402,6 +412,7 @@ void chol(Workspace& ws, int c, const int* dimC, bool rank_test, bool column_sca
     p.rank_test = rank_test ? 1 : 0;
     p.column_scale = column_scale ? 1 : 0;
     p.vnorm = rank_test ? ws.vnorm.get() : nullptr;
+    p.rank_need = rank_test ? ws.rneed.get() : nullptr;
     p.near_identity = near_identity ? 1 : 0;
     p.skip_inverse = skip_inverse ? 1 : 0;
     ProfScope prof("chol", st);
@@ -428,8 +439,9 @@ void chol_pass2(Workspace& ws, int c, const int* dimC, int pos, cudaStream_t st,
 }
 
 void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
-                bool rank_test, int pos, int passes, double skip_tol) {
+                bool rank_test, int pos, int passes, double skip_tol, const double* projX, int64_t strideX) {
     ProfScope prof("orthonormalize", cx.st);
+    ws.proj_ready = false;
     const int n = ws.npad;
     const bool adaptive = skip_tol > 0.0 && passes == 2;
     if ((rank_test || adaptive) && in == out) {
@@ -439,6 +451,7 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
         in = ws.T.get();
     }
     gram(ws, in, c, dimC, n, cx.st);
+    if (rank_test) SMG_CUDA(cudaMemsetAsync(ws.rneed.get(), 0, sizeof(int) * ws.B, cx.st));
     const bool ts = use_trsm(c, ws.B);
     chol(ws, c, dimC, rank_test, true, pos, cx.st, false, ts);
     auto pass1 = [&](double* dst) {
@@ -453,7 +466,11 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
     if (adaptive) {
         // Q1 straight into out; pass 2 only for chains whose Q1 is not yet
         // orthonormal to skip_tol (their Q = Q1 B2 goes through R and back)
-        pass1(out);
+        // the triangular products also emit the projection's partial records
+        // (project_batch then skips its read of the basis)
+        const bool fuse = projX != nullptr && !ts && dimC == nullptr && std::getenv("SMG_PROJ_FUSE") != nullptr;
+        if (fuse) trmm(ws, in, out, c, dimC, n, cx.st, nullptr, projX, strideX);
+        else pass1(out);
         gram(ws, out, c, dimC, n, cx.st);
         if (c <= 256) {
             // the single-CTA pass-2 scan decides the skip too (one launch)
@@ -465,7 +482,8 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
             }
             chol_pass2(ws, c, dimC, pos, cx.st, ws.skip.get());
         }
-        trmm(ws, out, ws.R.get(), c, dimC, n, cx.st, ws.skip.get());
+        trmm(ws, out, ws.R.get(), c, dimC, n, cx.st, ws.skip.get(), fuse ? projX : nullptr, strideX);
+        ws.proj_ready = fuse;
         copy_unskipped(ws.R.get(), out, ws.mstride(), ws.mstride(), ws.B, ws.skip.get(), cx.st);
     } else {
         pass1(ws.R.get());
@@ -487,6 +505,7 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
         r.vnorm = ws.vnorm.get();
         r.partial = ws.rpart.get();
         r.counter = ws.counters.get();
+        r.need = ws.rneed.get();
         r.status = ws.status.get();
         r.status_detail = ws.detail.get();
         r.errpos = ws.errpos.get();
@@ -524,6 +543,8 @@ void project_batch(const StepCtx& cx, Workspace& ws, const double* Q, int c, con
     p.strideStats = 4;
     p.rows_per_warp = 2;
     p.counter = ws.counters.get() + ws.B;
+    p.partials_ready = ws.proj_ready ? 1 : 0;
+    ws.proj_ready = false;
     project(p, cx.st);
     SMG_CUDA(cudaGetLastError());
 }

@@ -133,10 +133,11 @@ struct Workspace {
     int splits = 1;
     DBuf<double> U, V, T, R, G, Gws, Bm, work, rdiag, vnorm, rpart, coeff, sign, e, ppart, ppart2, stats;
     DBuf<int> counters;
-    DBuf<int> status, errpos, scratch_status, skip, skip2;
+    DBuf<int> status, errpos, scratch_status, skip, skip2, rneed;
     DBuf<unsigned long long> nmax;
     DBuf<int64_t> detail;
     DBuf<double> H, Hst, Vj, theta, theta_s, Wm, ritz_part, ritz;
+    bool proj_ready = false;  // ppart holds the last orth_batch's projection partials (host-side flag)
     void init(int B, int n, int npad, int ccap, cudaStream_t st);
     int64_t mstride() const { return (int64_t)npad * ld; }
 };
@@ -153,9 +154,12 @@ void solve_batch(const StepCtx& cx, Workspace& ws, const FactorSet& fs, int tile
 // CholeskyQR2: out = orth(in); sticky per-chain status, error position `pos`.
 // skip_tol > 0: adaptive -- a chain whose pass-1 factor Q1 is orthonormal to
 // skip_tol (max |Q1^T Q1 - I|, from the pass-2 Gram) keeps Q1 (no second
-// Cholesky, no second triangular product).
+// Cholesky, no second triangular product).  projX (adaptive path): the
+// triangular products also write the projection's partial records for these
+// coordinates, and the next project_batch on this workspace skips its pass 1.
 void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out, int c, const int* dimC,
-                bool rank_test, int pos, int passes = 2, double skip_tol = 0.0);
+                bool rank_test, int pos, int passes = 2, double skip_tol = 0.0, const double* projX = nullptr,
+                int64_t strideX = 0);
 void project_batch(const StepCtx& cx, Workspace& ws, const double* Q, int c, const int* dimC, const double* X,
                    int64_t strideX, double* xhat, int64_t strideXhat);
 

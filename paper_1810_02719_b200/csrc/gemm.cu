@@ -128,6 +128,68 @@ SMG_DEV void slab_mma(const double* __restrict__ as, const double* __restrict__ 
         }
 }
 
+// Projection partials of one warp tile (32 rows r0.. = one 32-row chunk of
+// project.cu's partial pass, 8NJ columns c0..): lane (g, t) holds rows r0 + 8i + g,
+// columns c0 + 8j + 2t + q.  Per column, the lane's 4 rows are combined in row
+// order and the 8 lanes of a column group by a fixed xor tree (deterministic);
+// the argmax keeps the larger |q|, the smaller row on ties (first index wins,
+// spectral.hpp:72-85).
+template <int NJ>
+SMG_DEV void proj_epilogue(const GemmParams& p, const double (&acc)[4][NJ][2], int b, int r0, int c0, int N, int g,
+                           int t) {
+    if (r0 >= p.projN) return;  // warp-uniform: rows past n are padding (no chunk)
+    const int c = min(N, p.projCcap);
+    const double* X = p.projX + (int64_t)b * p.strideProjX;
+    double* part = p.projPart + ((int64_t)b * p.projChunks + (r0 >> 5)) * (int64_t)p.projCcap * 8;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            double best = -1.0, bval = 0.0, px = 0.0, py = 0.0, pz = 0.0, ps = 0.0;
+            int brow = 1 << 30;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int row = r0 + 8 * i + g;
+                if (row >= p.projN) continue;
+                // coordinates re-read per column (L1 hits): keeps the epilogue's
+                // live registers at the accumulators
+                const double x = __ldg(X + 3 * (int64_t)row), y = __ldg(X + 3 * (int64_t)row + 1),
+                             z = __ldg(X + 3 * (int64_t)row + 2);
+                const double v = acc[i][j][q], m = fabs(v);
+                if (m > best) {
+                    best = m;
+                    bval = v;
+                    brow = row;
+                }
+                px = fma(v, x, px);
+                py = fma(v, y, py);
+                pz = fma(v, z, pz);
+                ps = fma(v, (x + y) + z, ps);
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const double ov = __shfl_xor_sync(0xffffffffu, bval, o);
+                const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+                if (ob > best || (ob == best && orow < brow)) {
+                    best = ob;
+                    bval = ov;
+                    brow = orow;
+                }
+                px += __shfl_xor_sync(0xffffffffu, px, o);
+                py += __shfl_xor_sync(0xffffffffu, py, o);
+                pz += __shfl_xor_sync(0xffffffffu, pz, o);
+                ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            }
+            const int col = c0 + 8 * j + 2 * t + q;
+            if (g == 0 && col < c) {
+                double4* o4 = reinterpret_cast<double4*>(part + (int64_t)col * 8);
+                o4[0] = make_double4(best, bval, px, py);
+                o4[1] = make_double4(pz, ps, 0.0, 0.0);
+            }
+        }
+}
+
 template <bool TA, bool TB, int NJ>
 __global__ void __launch_bounds__(NT, 4) gemm_kernel(GemmParams p, int n_base, int n_end) {
     constexpr int BN = 16 * NJ;
@@ -238,6 +300,7 @@ __global__ void __launch_bounds__(NT, 4) gemm_kernel(GemmParams p, int n_base, i
             }
         }
     }
+    if (p.projPart && splits == 1) proj_epilogue<NJ>(p, acc, b, m0 + wm, n0 + wn, N, g, t);
 }
 
 
@@ -315,7 +378,7 @@ struct PipeShape {
     static constexpr int BMv = 32 * MW, NDW = 2 * MW, THREADS = 32 * NDW + 32, MINB = 4;
 };
 
-template <bool TA, bool TB, int NJ, int MW = 2>
+template <bool TA, bool TB, int NJ, int MW = 2, bool PROJ = false>
 __global__ void __launch_bounds__(PipeShape<MW>::THREADS, PipeShape<MW>::MINB)
     gemm_pipe_kernel(GemmParams p, int n_base, int n_end) {
     constexpr int BN = 16 * NJ;
@@ -433,6 +496,7 @@ __global__ void __launch_bounds__(PipeShape<MW>::THREADS, PipeShape<MW>::MINB)
             }
         }
     }
+    if constexpr (PROJ) proj_epilogue<NJ>(p, acc, b, m0 + wm, n0 + wn, N, g, t);
 }
 
 __global__ void gemm_reduce_kernel(GemmParams p) {
@@ -470,20 +534,33 @@ void launch_tiles(const GemmParams& p, int n_base, int width, cudaStream_t st) {
     if (aligned) {
         // a launch that cannot fill the GPU runs 32-row tiles (twice the CTAs)
         const bool small = (int64_t)gm * gn * p.batch * p.splits < 148 && !std::getenv("SMG_GEMM_NOSMALL");
+        // projection partials in the epilogue: plain V * B products only
+        constexpr bool CAN_PROJ = !TA && !TB;
+        const bool proj = CAN_PROJ && p.projPart != nullptr && p.splits == 1;
         if (small) {
             using SA = Slab<32, TA, BKP>;
             using SB = Slab<BN, !TB, BKP>;
             const int bytes = PNS * (SA::ELEMS + SB::ELEMS) * 8;
-            ensure_smem((const void*)gemm_pipe_kernel<TA, TB, NJ, 1>, bytes);
             dim3 g2(gn, (p.M + 31) / 32, p.batch * p.splits);
-            gemm_pipe_kernel<TA, TB, NJ, 1><<<g2, PipeShape<1>::THREADS, bytes, st>>>(p, n_base, n_base + width);
+            if (proj) {
+                ensure_smem((const void*)gemm_pipe_kernel<TA, TB, NJ, 1, CAN_PROJ>, bytes);
+                gemm_pipe_kernel<TA, TB, NJ, 1, CAN_PROJ><<<g2, PipeShape<1>::THREADS, bytes, st>>>(p, n_base, n_base + width);
+            } else {
+                ensure_smem((const void*)gemm_pipe_kernel<TA, TB, NJ, 1>, bytes);
+                gemm_pipe_kernel<TA, TB, NJ, 1><<<g2, PipeShape<1>::THREADS, bytes, st>>>(p, n_base, n_base + width);
+            }
             return;
         }
         using SA = Slab<BM, TA, BKP>;
         using SB = Slab<BN, !TB, BKP>;
         const int bytes = PNS * (SA::ELEMS + SB::ELEMS) * 8;
-        ensure_smem((const void*)gemm_pipe_kernel<TA, TB, NJ>, bytes);
-        gemm_pipe_kernel<TA, TB, NJ><<<grid, NT_P, bytes, st>>>(p, n_base, n_base + width);
+        if (proj) {
+            ensure_smem((const void*)gemm_pipe_kernel<TA, TB, NJ, 2, CAN_PROJ>, bytes);
+            gemm_pipe_kernel<TA, TB, NJ, 2, CAN_PROJ><<<grid, NT_P, bytes, st>>>(p, n_base, n_base + width);
+        } else {
+            ensure_smem((const void*)gemm_pipe_kernel<TA, TB, NJ>, bytes);
+            gemm_pipe_kernel<TA, TB, NJ><<<grid, NT_P, bytes, st>>>(p, n_base, n_base + width);
+        }
         return;
     }
     gemm_kernel<TA, TB, NJ><<<grid, NT, 0, st>>>(p, n_base, n_base + width);

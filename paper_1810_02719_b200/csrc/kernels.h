@@ -35,6 +35,15 @@ struct GemmParams {
     int upperB = 0;     // B upper triangular (square): k < n0 + 64
     int syrkUpper = 0;  // only tiles with tile_m <= tile_n
     const int* skip = nullptr;  // optional per batch entry: nonzero -> no work (adaptive CholeskyQR2)
+    // optional projection partials in the epilogue of a plain (unsplit) product
+    // C = A B whose rows are basis rows (the CholeskyQR triangular product): per
+    // 32-row chunk and column the record of project.cu's partial pass -- best
+    // |q| (first row wins ties), its q, and q^T [x y z (x+y)+z] over the chunk
+    // -- so the projection need not re-read the basis
+    const double* projX = nullptr;  // n x 3 local coordinates per batch entry
+    int64_t strideProjX = 0;
+    double* projPart = nullptr;     // batch * projChunks * projCcap * 8
+    int projN = 0, projChunks = 0, projCcap = 0;
 };
 void gemm(const GemmParams& p, bool transA, bool transB, cudaStream_t st);
 
@@ -119,6 +128,11 @@ struct CholParams {
     int pos = 0;
     double* vnorm = nullptr;         // ||V||_F per batch entry (rank-test scale)
     int rank_test = 1;
+    // rank test: set to 1 (atomicOr, zeroed by the caller) when some pivot is not
+    // far enough above the reference threshold for the Cholesky to certify it
+    // (scaled pivot < 1e-8 or r_kk < 1e-9 ||V||_F): only then does the exact
+    // |q_k^T v_k| test (rank_check) have anything to decide
+    int* rank_need = nullptr;
     int column_scale = 1;
     // second CholeskyQR pass: when max|G~ - I| <= 1e-9 the factor is taken to
     // first order, R~ = I + triu(G~ - I, 1) (error O(|E|^2) <= c * 1e-18), and
@@ -193,6 +207,7 @@ struct RankCheckParams {
     int* errpos = nullptr;
     int pos = 0;
     int* counter = nullptr;  // per batch, zero: the last chunk CTA of a chain runs the test
+    const int* need = nullptr;  // optional per batch: 0 -> the pass-1 pivots certified every column
 };
 void rank_check(const RankCheckParams& p, cudaStream_t st);
 
@@ -208,6 +223,7 @@ struct ProjParams {
     double* partial = nullptr;   // batch * nchunks * c_cap * 8
     double* partial2 = nullptr;  // batch * recon_blocks * 2
     int nchunks = 0, rows_per_chunk = 64, rows_per_warp = 2;
+    int partials_ready = 0;  // the partial records were written by the CholeskyQR product (gemm projPart)
     double* coeff = nullptr;  // c_cap x 4 per batch: Px Py Pz Ps (unsigned)
     int64_t strideCoef = 0;
     double* sign = nullptr;  // per batch, stride strideSign

@@ -439,6 +439,137 @@ __global__ void __launch_bounds__(PNT) recon_warp_kernel(ProjParams p) {
     p.counter[2 * b + 1] = 0;
 }
 
+// Reconstruction on the DMMA pipe: [X^ | Ps] (n x 4) = Q (n x c) * C (c x 4),
+// one m16n8k8 per 16 rows x 8 columns of Q (B = the coefficients, outputs 4-7
+// zero).  The A fragments are read straight from global memory -- lane (g, t)
+// loads Q[g][k+t], Q[g+8][k+t], Q[g][k+t+4], Q[g+8][k+t+4], so every warp load
+// touches 16 rows x 32 contiguous bytes (whole sectors) -- KU k-steps of loads
+// are issued before their products (4 * KU * RT 8-byte loads in flight per
+// lane), and the coefficients come from shared memory (16 consecutive doubles
+// per fragment, conflict-free).  No shuffles: the accumulator of lane (g, t < 2)
+// is exactly (x^, y^) or (z^, s^) of rows g and g + 8.
+constexpr int MNT = 256;  // 8 warps
+template <int RT>
+__global__ void __launch_bounds__(MNT, RT == 1 ? 4 : 3) recon_mma_kernel(ProjParams p) {
+    constexpr int KU = RT == 1 ? 4 : 2;  // 16 loads in flight per lane either way
+    __shared__ double red[2][MNT / 32];
+    // B fragments pre-paired: scoef[(kb * 4 + t) * 8 + g] = (C[8kb+t][g], C[8kb+t+4][g])
+    // (outputs g = Px Py Pz Ps, zero for g >= 4 and past c): one 16-byte load per
+    // lane and k-step, a warp reads 512 contiguous bytes
+    extern __shared__ __align__(16) double2 scoef2[];
+    const int b = blockIdx.y;
+    const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
+    const int kpad = (c + 8 * KU - 1) / (8 * KU) * (8 * KU);
+    {
+        const double* src = p.coeff + (int64_t)b * p.strideCoef;
+        for (int e = threadIdx.x; e < 4 * kpad; e += MNT) {
+            const int gg = e & 7, tt = (e >> 3) & 3, kb = e >> 5;
+            const int k0 = 8 * kb + tt, k1 = k0 + 4;
+            scoef2[e] = make_double2(gg < 4 && k0 < c ? src[4 * k0 + gg] : 0.0, gg < 4 && k1 < c ? src[4 * k1 + gg] : 0.0);
+        }
+    }
+    __syncthreads();
+    const double* Q = p.Q + (int64_t)b * p.strideQ;
+    const double* X = p.X + (int64_t)b * p.strideX;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int row0 = (blockIdx.x * (MNT / 32) + warp) * 16 * RT;
+    double acc[RT][4];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.0;
+    // row pointers of the lane's rows (clamped; masked values are zero)
+    const double* qr[RT][2];
+    bool rv[RT][2];
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = row0 + 16 * r + 8 * h + g;
+            rv[r][h] = i < p.n;
+            qr[r][h] = Q + (int64_t)(rv[r][h] ? i : 0) * p.ldq + t;
+        }
+    for (int k0 = 0; k0 < c; k0 += 8 * KU) {
+        double a[KU][RT][4];
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+            const int k = k0 + 8 * u;
+            const bool c0 = k + t < c, c1 = k + t + 4 < c;
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                a[u][r][0] = (rv[r][0] && c0) ? __ldg(qr[r][0] + k) : 0.0;
+                a[u][r][1] = (rv[r][1] && c0) ? __ldg(qr[r][1] + k) : 0.0;
+                a[u][r][2] = (rv[r][0] && c1) ? __ldg(qr[r][0] + k + 4) : 0.0;
+                a[u][r][3] = (rv[r][1] && c1) ? __ldg(qr[r][1] + k + 4) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+            const int k = k0 + 8 * u;
+            const double2 bb = scoef2[((k >> 3) * 4 + t) * 8 + g];
+#pragma unroll
+            for (int r = 0; r < RT; ++r)
+                dmma1688(acc[r][0], acc[r][1], acc[r][2], acc[r][3], a[u][r][0], a[u][r][1], a[u][r][2], a[u][r][3],
+                         bb.x, bb.y);
+        }
+    }
+    // lane (g, 0): (x^, y^), lane (g, 1): (z^, s^) of rows g (acc 0, 1) and g + 8 (acc 2, 3)
+    double res2 = 0.0, e2 = 0.0;
+    if (t < 2) {
+#pragma unroll
+        for (int r = 0; r < RT; ++r)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = row0 + 16 * r + 8 * h + g;
+                if (i >= p.n) continue;
+                const double v0 = acc[r][2 * h], v1 = acc[r][2 * h + 1];
+                const double* xi = X + 3 * (int64_t)i;
+                double* xh = p.xhat ? p.xhat + (int64_t)b * p.strideXhat + 3 * (int64_t)i : nullptr;
+                if (t == 0) {
+                    const double dx = xi[0] - v0, dy = xi[1] - v1;
+                    res2 += dx * dx + dy * dy;
+                    if (xh) {
+                        xh[0] = v0;
+                        xh[1] = v1;
+                    }
+                } else {
+                    const double x = xi[0], y = xi[1], z = xi[2];
+                    const double dz = z - v0;
+                    res2 += dz * dz;
+                    const double e = ((x + y) + z) - v1;
+                    e2 += e * e;
+                    if (xh) xh[2] = v0;
+                    if (p.e_out) p.e_out[(int64_t)b * p.strideE + i] = e;
+                }
+            }
+    }
+    res2 = warp_sum(res2);
+    e2 = warp_sum(e2);
+    if (lane == 0) {
+        red[0][warp] = res2;
+        red[1][warp] = e2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sa = 0.0, se = 0.0;
+        for (int w = 0; w < MNT / 32; ++w) {
+            sa += red[0][w];
+            se += red[1][w];
+        }
+        double* o = p.partial2 + ((int64_t)b * gridDim.x + blockIdx.x) * 2;
+        o[0] = sa;
+        o[1] = se;
+    }
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&p.counter[2 * b + 1], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    stats_block(p, b, gridDim.x);
+    p.counter[2 * b + 1] = 0;
+}
+
 }  // namespace
 
 int proj_chunks(int n) { return (n + RPC - 1) / RPC; }
@@ -448,8 +579,23 @@ void project(const ProjParams& p0, cudaStream_t st) {
     ProjParams p = p0;
     p.rows_per_chunk = RPC;
     p.nchunks = proj_chunks(p.n);
-    ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), QNT, 0, st>>>(p);
+    if (!p.partials_ready) ::smg::count_launch(), partial_kernel<<<dim3(p.nchunks, p.batch), QNT, 0, st>>>(p);
     ::smg::count_launch(), chunk_reduce_kernel<<<dim3((p.c_cap + RCOL - 1) / RCOL, p.batch), RCOL * RPART, 0, st>>>(p);
+    if (!std::getenv("SMG_RECON_OLD") && !std::getenv("SMG_RECON_WARP")) {
+        // DMMA reconstruction: 32 rows per warp when the batch fills the GPU, 16 otherwise
+        const int kpad = (p.c_cap + 31) / 32 * 32;
+        const int msmem = kpad * 4 * (int)sizeof(double2);
+        ensure_smem((const void*)recon_mma_kernel<2>, msmem);
+        ensure_smem((const void*)recon_mma_kernel<1>, msmem);
+        if ((int64_t)p.batch * ((p.n + 255) / 256) >= 2 * 148) {
+            const int nb = (p.n + 255) / 256;
+            ::smg::count_launch(), recon_mma_kernel<2><<<dim3(nb, p.batch), MNT, msmem, st>>>(p);
+        } else {
+            const int nb = (p.n + 127) / 128;
+            ::smg::count_launch(), recon_mma_kernel<1><<<dim3(nb, p.batch), MNT, msmem, st>>>(p);
+        }
+        return;
+    }
     if (!std::getenv("SMG_RECON_OLD")) {
         // one row group per warp (measured: 46 us per C5 launch against 63 us for
         // the thread-per-column-part kernel; a persistent sweep over row ranges

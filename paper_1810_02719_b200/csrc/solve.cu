@@ -308,9 +308,14 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 const int gs = cu.gs, sl = gs % NSF;
                 if (gs >= NSF) mbar_wait(&consF[sl], ((gs - NSF) / NSF) & 1);
                 const double* F = ((cu.sweep & 1) ? Fbwd : Ffwd) + (int64_t)cu.k() * slab;
-                mbar_arrive_expect_tx(&fullF[sl], (uint32_t)(2 * W * FS * 8));
+#ifdef SMG_SOLVE_SLAB_DIV  // timing probe: move only 1/DIV of the slab bytes
+                constexpr uint32_t kSlabBytes = (2 * W * FS * 8 / SMG_SOLVE_SLAB_DIV + 15) / 16 * 16;
+#else
+                constexpr uint32_t kSlabBytes = 2 * W * FS * 8;
+#endif
+                mbar_arrive_expect_tx(&fullF[sl], kSlabBytes);
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                bulk_g2s(Fs(sl), F, 2 * W * FS * 8, &fullF[sl]);
+                bulk_g2s(Fs(sl), F, kSlabBytes, &fullF[sl]);
             }
         }
     } else if (warp > kSolveWarps) {
@@ -370,7 +375,11 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
         auto first = [&](int gs, int sweep) {
             mbar_wait(&fullR[gs % NSR], (gs / NSR) & 1);
             mbar_wait(&fullF[gs % NSF], (gs / NSF) & 1);
-#ifndef SMG_SOLVE_NO_MMA
+#if defined(SMG_SOLVE_NO_TRI)  // timing probe: coupling half only (one dense product per step)
+            (void)sweep;
+            for (int i = 0; i < TL::MT; ++i)
+                for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Rs(gs % NSR)[tid & 63];
+#elif !defined(SMG_SOLVE_NO_MMA)
             if ((sweep & 1) == 0) mma_step<W, CS, true>(Fs(gs % NSF), Rs(gs % NSR), nullptr, acc, warp, g, t, 1);
             else mma_step<W, CS, false>(Fs(gs % NSF), Rs(gs % NSR), nullptr, acc, warp, g, t, 1);
 #else
