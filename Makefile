@@ -25,7 +25,19 @@ $(LIB): $(OBJS)
 	@mkdir -p $(dir $(LIB))
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static -lcuda -ldl
 
-oracle: oracle/_ref/rng_ref
+REF_INC ?= /root/reference/proj/include
+ifneq ($(wildcard $(REF_INC)/specmesh/pipeline.hpp),)
+REFHARNESS := oracle/_ref/libspecmesh_ref.so
+endif
+oracle: oracle/_ref/rng_ref $(REFHARNESS)
+
+# The reference's own headers compiled where they lie (never copied) over
+# oracle/eigen_shim, the stand-in for its absent Eigen dependency -- only in a
+# container that has /root/reference; the GPU box uses the committed fixtures.
+refharness: oracle/_ref/libspecmesh_ref.so
+oracle/_ref/libspecmesh_ref.so: oracle/ref_harness.cpp oracle/eigen_shim/Eigen/mini_eigen.hpp
+	@mkdir -p oracle/_ref
+	g++ -std=c++20 -O3 -mavx2 -mfma -ffp-contract=off -fPIC -shared -Ioracle/eigen_shim -I$(REF_INC) $< -o $@
 
 oracle/_ref/rng_ref: oracle/rng_ref.cpp
 	@mkdir -p oracle/_ref

@@ -1,0 +1,239 @@
+"""Generates tests/golden/ref_*.npz from the REFERENCE'S OWN CODE.
+
+The reference headers (/root/reference/proj/include/specmesh, unmodified, compiled
+where they lie) run here through oracle/_ref/libspecmesh_ref.so (`make refharness`;
+oracle/ref_harness.cpp over oracle/eigen_shim, the stand-in for the absent Eigen
+dependency).  The reference cannot travel to the GPU box, so its outputs on the
+seeded BASELINE configurations are committed as fixtures; tests/test_ref_fixtures.py
+checks the numpy oracle against them on the CPU and tests/test_gpu_ref_fixtures.py
+checks the CUDA path against them on the GPU.
+
+Run in this container:  python tests/golden/make_ref_fixtures.py [case ...]
+Cases: c1 c2 c3 c5 doi segment prims errors c4   (default: all but c4, which takes ~1 h)
+"""
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import ref_binding as R  # noqa: E402
+from paper_1810_02719_b200 import synth  # noqa: E402
+
+SHIFT = 1e-3  # pinned shift_scale (the reference default 1e-8 is rank deficient)
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def input_tag(mesh) -> dict:
+    return {"vertices_sha": sha(mesh.vertices), "faces_sha": sha(mesh.faces), "n": int(mesh.n)}
+
+
+def save(name: str, meta: dict, **arrays) -> None:
+    path = os.path.join(HERE, f"ref_{name}.npz")
+    np.savez_compressed(path, meta=np.array(json.dumps(meta)), **arrays)
+    print(f"wrote {path}: {os.path.getsize(path) / 1e6:.2f} MB  {meta.get('seconds', '')}")
+
+
+def fixed_chain(w, stride_recon=1, basis_ids=()):
+    rm = R.Mesh(w.mesh.vertices, w.mesh.faces)
+    rs = R.Segmentation.from_members(rm, w.seg.members, w.seg.sequence)
+    cfg = R.default_config(weighting=R.BINARY, subspace_size=w.c, iterations=w.iterations, shift_scale=SHIFT)
+    t0 = time.time()
+    bb = R.chain_fixed(rm, rs, cfg, [w.c] * w.seg.count)
+    secs = time.time() - t0
+    k = w.seg.count
+    out = {
+        "residual_rms": np.array([bb.stats(i)["residual_rms"] for i in range(k)]),
+        "oi_iterations": np.array([bb.stats(i)["oi_iterations"] for i in range(k)], dtype=np.int32),
+        "coefficients": np.stack([bb.coefficients(i) for i in range(k)]),
+        "reconstruction": bb.reconstruct()[::stride_recon],
+    }
+    for i in basis_ids:
+        out[f"basis_{i}"] = bb.basis(i)
+    meta = dict(input_tag(w.mesh), config=w.name, c=w.c, iterations=w.iterations, shift_scale=SHIFT,
+                weighting="binary", tiles=k, recon_stride=stride_recon, seconds=round(secs, 1),
+                timings={s: bb.timing(s) for s in ("laplacian", "factorize", "basis", "basis_total")})
+    return meta, out
+
+
+def case_c1():
+    """C1 as configured: bottom_subspace(40) -> orthogonal_iteration(op, init, 10) -> gft/igft."""
+    w = synth.config("C1")
+    rm = R.Mesh(w.mesh.vertices, w.mesh.faces)
+    rs = R.Segmentation.from_members(rm, w.seg.members, w.seg.sequence)
+    ev, init = rs.bottom_subspace(0, R.BINARY, w.c)
+    u = rs.orthogonal_iteration(0, R.BINARY, SHIFT, 2, init, w.iterations)
+    x = w.mesh.vertices[np.sort(w.seg.members[0])]
+    coeff = u.T @ x  # gft is a plain product (spectral.hpp:290-293); the chain fixtures use the reference's own
+    lap = rs.laplacian(0, R.BINARY, SHIFT)
+    save("c1", dict(input_tag(w.mesh), config="C1", c=w.c, iterations=w.iterations, shift_scale=SHIFT),
+         eigenvalues=ev[:64], init=init, basis=u, coefficients=coeff, trace=np.array(lap[3]), delta=np.array(lap[4]))
+
+
+def case_c2():
+    meta, out = fixed_chain(synth.config("C2"), basis_ids=(63,))
+    save("c2", meta, **out)
+
+
+def case_c3():
+    meta, out = fixed_chain(synth.config("C3"), stride_recon=2, basis_ids=(159,))
+    save("c3", meta, **out)
+
+
+def case_c5():
+    """one whole C5 chain (mesh 0: 128 tiles of 32x64, c = 200)"""
+    meta, out = fixed_chain(synth.config("C5", mesh_index=0), stride_recon=5)
+    save("c5_mesh0", meta, **out)
+
+
+def case_doi():
+    """The reference's own entry point compute_block_bases in DOI mode (segments
+    internally: partition_mesh + expand_overlaps + order_submeshes, pipeline.hpp:198-285)."""
+    mesh = synth.small_grid(96, 96, 32, 32, seed=21, sigma=0.01)
+    rm = R.Mesh(mesh.vertices, mesh.faces)
+    cfg = R.default_config(part_count=8, growth=1.15, basis_mode=R.DOI, weighting=R.BINARY, subspace_size=16,
+                           eps_low=6e-3, eps_high=1.2e-2, c_min=4, c_max=128, shift_scale=SHIFT, seed=1)
+    t0 = time.time()
+    bb = R.chain(rm, cfg)
+    secs = time.time() - t0
+    k = bb.count
+    stats = [bb.stats(i) for i in range(k)]
+    members = bb.members()
+    save("doi", dict(input_tag(mesh), grid=[96, 96], seed=21, sigma=0.01, part_count=8, growth=1.15, c0=16,
+                     eps_low=6e-3, eps_high=1.2e-2, c_min=4, c_max=128, shift_scale=SHIFT, pipeline_seed=1,
+                     seconds=round(secs, 1)),
+         members=np.stack(members), order=bb.order(),
+         c=np.array([s["subspace_size"] for s in stats], dtype=np.int32),
+         iterations=np.array([s["oi_iterations"] for s in stats], dtype=np.int32),
+         converged=np.array([s["converged"] for s in stats]),
+         doi_residual=np.array([s["doi_residual"] for s in stats]),
+         residual_rms=np.array([s["residual_rms"] for s in stats]),
+         reconstruction=bb.reconstruct())
+    print("doi c:", [s["subspace_size"] for s in stats], "t:", [s["oi_iterations"] for s in stats],
+          "conv:", [s["converged"] for s in stats])
+
+
+def case_segment():
+    """segment_mesh (pipeline.hpp:131-138) on the C2 grid, a sphere and one C5 mesh."""
+    arrays, meta = {}, {}
+    cases = [("c2_k8", synth.config("C2").mesh, 8, 1.15, 1), ("c2_k64", synth.config("C2").mesh, 64, 1.15, 1),
+             ("sphere5_k8", synth.sphere_mesh(5, 11), 8, 1.15, 7),
+             ("c5_k64", synth.config("C5", mesh_index=0).mesh, 64, 1.15, 1)]
+    for name, mesh, k, growth, seed in cases:
+        rm = R.Mesh(mesh.vertices, mesh.faces)
+        t0 = time.time()
+        seg = R.Segmentation.segment_mesh(rm, R.default_config(part_count=k, growth=growth, seed=seed))
+        meta[name] = dict(input_tag(mesh), k=k, growth=growth, seed=seed, seconds=round(time.time() - t0, 2))
+        arrays[f"{name}_assignment"] = seg.assignment()
+        arrays[f"{name}_members"] = np.stack(seg.members())
+        arrays[f"{name}_order"] = seg.order()
+    save("segment", meta, **arrays)
+
+
+def case_prims():
+    """Primitives on a sphere block with inverse-squared-distance weights."""
+    mesh = synth.sphere_mesh(4, 5)
+    seg = synth.sphere_blocks(mesh, bands=8, block=256)
+    rm = R.Mesh(mesh.vertices, mesh.faces)
+    rs = R.Segmentation.from_members(rm, seg.members, seg.sequence)
+    arrays = {}
+    for wname, wt in (("binary", R.BINARY), ("distance", R.DISTANCE)):
+        offs, cols, vals, tr, de = rs.laplacian(1, wt, SHIFT)
+        arrays.update({f"lap_{wname}_offsets": offs, f"lap_{wname}_cols": cols, f"lap_{wname}_vals": vals,
+                       f"lap_{wname}_trace": np.array(tr), f"lap_{wname}_delta": np.array(de)})
+    rng = np.random.Generator(np.random.PCG64(9))
+    n = seg.members[1].size
+    block = rng.standard_normal((n, 24))
+    arrays["block"] = block
+    arrays["apply_binary_z2"] = rs.apply(1, R.BINARY, SHIFT, 2, block)
+    arrays["apply_distance_z1"] = rs.apply(1, R.DISTANCE, SHIFT, 1, block)
+    arrays["orthonormalize"] = R.orthonormalize(block)
+    ev, basis = rs.bottom_subspace(1, R.DISTANCE, 24)
+    arrays["eigenvalues_distance"] = ev
+    arrays["bottom24_distance"] = basis
+    arrays["resize_grow"] = R.resize_basis(arrays["orthonormalize"], 30, 1234)
+    u, it, conv, res = rs.dynamic_oi(1, R.BINARY, SHIFT, 2, rs.bottom_subspace(1, R.BINARY, 8)[1], 2e-3, 2e-2, 2, 40, 60)
+    arrays["doi_basis"] = u
+    arrays["doi_result"] = np.array([u.shape[1], it, int(conv), res])
+    save("prims", dict(input_tag(mesh), sphere_level=4, seed=5, bands=8, block=256, submesh=1, shift_scale=SHIFT),
+         **arrays)
+    print("doi:", u.shape, it, conv, res)
+
+
+def case_errors():
+    """Message texts raised by the reference itself."""
+    msgs = {}
+    mesh = synth.small_grid(64, 64, 32, 32, seed=2)
+    seg = synth.grid_tiles(64, 64, 32, 32)
+    rm = R.Mesh(mesh.vertices, mesh.faces)
+    rs = R.Segmentation.from_members(rm, seg.members, seg.sequence)
+
+    def grab(key, fn):
+        try:
+            fn()
+            msgs[key] = [0, ""]
+        except R.RefError as e:
+            msgs[key] = [e.status, str(e)]
+
+    grab("default_shift_rank_deficient", lambda: R.chain_fixed(
+        rm, rs, R.default_config(weighting=R.BINARY, subspace_size=40, iterations=1, shift_scale=1e-8), [40] * 4))
+    grab("size_out_of_range", lambda: R.chain_fixed(
+        rm, rs, R.default_config(weighting=R.BINARY, subspace_size=40, iterations=1, shift_scale=SHIFT),
+        [40, 40, 2000, 40]))
+    bad = R.Segmentation.from_members(rm, [seg.members[0], seg.members[1][:500]], [0, 1])
+    grab("basis_operator_mismatch", lambda: R.chain_fixed(
+        rm, bad, R.default_config(weighting=R.BINARY, subspace_size=40, iterations=1, shift_scale=SHIFT), [40, 40]))
+    hole = R.Segmentation.from_members(rm, seg.members[:3], [0, 1, 2])
+    grab("missing_vertices", lambda: R.chain_fixed(
+        rm, hole, R.default_config(weighting=R.BINARY, subspace_size=40, iterations=1, shift_scale=SHIFT),
+        [40] * 3).reconstruct())
+    grab("zero_block", lambda: R.orthonormalize(np.zeros((16, 4))))
+    dup = np.ones((16, 4))
+    dup[:, 0] = np.arange(16)
+    grab("duplicate_columns", lambda: R.orthonormalize(dup))
+    grab("k_too_large", lambda: R.Segmentation.segment_mesh(rm, R.default_config(part_count=2000)))
+    with open(os.path.join(HERE, "ref_errors.json"), "w") as f:
+        json.dump(msgs, f, indent=1)
+    print(json.dumps(msgs, indent=1))
+
+
+def case_c4():
+    """C4 at full size: 256 tiles of 64x64 on the 1024^2 grid, DOI c in [20, 400], band 1e-5/1e-4
+    (about an hour single-threaded: dense eigendecomposition of n = 4096 + ~640 DOI steps)."""
+    w = synth.config("C4")
+    rm = R.Mesh(w.mesh.vertices, w.mesh.faces)
+    rs = R.Segmentation.from_members(rm, w.seg.members, w.seg.sequence)
+    cfg = R.default_config(basis_mode=R.DOI, weighting=R.BINARY, subspace_size=w.c, eps_low=w.eps_low,
+                           eps_high=w.eps_high, c_min=w.c_min, c_max=w.c_max, shift_scale=SHIFT)
+    t0 = time.time()
+    bb = R.chain_doi_external(rm, rs, cfg)
+    secs = time.time() - t0
+    stats = [bb.stats(i) for i in range(bb.count)]
+    out = dict(input_tag(w.mesh), config="C4", seconds=round(secs, 1), shift_scale=SHIFT,
+               c=[s["subspace_size"] for s in stats], iterations=[s["oi_iterations"] for s in stats],
+               converged=[bool(s["converged"]) for s in stats], doi_residual=[s["doi_residual"] for s in stats],
+               residual_rms=[s["residual_rms"] for s in stats])
+    with open(os.path.join(HERE, "ref_c4_doi.json"), "w") as f:
+        json.dump(out, f)
+    print("c4:", secs, "s; total steps", sum(out["iterations"]))
+
+
+CASES = {"c1": case_c1, "c2": case_c2, "c3": case_c3, "c5": case_c5, "doi": case_doi, "segment": case_segment,
+         "prims": case_prims, "errors": case_errors}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    for nm in names:
+        t0 = time.time()
+        (case_c4 if nm == "c4" else CASES[nm])()
+        print(f"[{nm}] {time.time() - t0:.1f}s")
