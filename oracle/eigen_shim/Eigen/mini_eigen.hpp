@@ -189,6 +189,54 @@ public:
 
     JacobiSVD<Mat> jacobiSvd() const;
 
+    // coefficient-wise view (denoise.hpp:221-222, :267)
+    struct BoolArray {
+        std::vector<char> v;
+        bool all() const {
+            return std::all_of(v.begin(), v.end(), [](char c) { return c != 0; });
+        }
+    };
+    struct ArrayView {
+        const Mat& m;
+        Mat sqrt() const {
+            Mat out(m.r_, m.c_);
+            for (Index i = 0; i < m.size(); ++i) out[i] = std::sqrt(m[i]);
+            return out;
+        }
+        Mat rsqrt() const {
+            Mat out(m.r_, m.c_);
+            for (Index i = 0; i < m.size(); ++i) out[i] = T(1) / std::sqrt(m[i]);
+            return out;
+        }
+        friend BoolArray operator==(const ArrayView& a, const ArrayView& b) {
+            same_shape(a.m, b.m);
+            BoolArray out;
+            out.v.resize(static_cast<std::size_t>(a.m.size()));
+            for (Index i = 0; i < a.m.size(); ++i) out.v[static_cast<std::size_t>(i)] = a.m[i] == b.m[i];
+            return out;
+        }
+    };
+    ArrayView array() const { return ArrayView{*this}; }
+
+    // a vector as a (dense, eager) diagonal matrix; inverse() of such a matrix is only
+    // used on diagonals (denoise.hpp:225)
+    Mat asDiagonal() const {
+        const Index n = size();
+        Mat out(n, n);
+        for (Index i = 0; i < n; ++i) out(i, i) = (*this)[i];
+        return out;
+    }
+    Mat inverse() const {
+        if (r_ != c_) shim_detail::fail("inverse of a non-square matrix");
+        Mat out(r_, c_);
+        for (Index j = 0; j < c_; ++j)
+            for (Index i = 0; i < r_; ++i) {
+                if (i != j && (*this)(i, j) != T()) shim_detail::fail("inverse(): only diagonal matrices");
+                if (i == j) out(i, i) = T(1) / (*this)(i, i);
+            }
+        return out;
+    }
+
     // ---- arithmetic (hidden friends: found for Mat, its subclasses and BlockRef<Mat>)
     static void same_shape(const Mat& a, const Mat& b) {
         if (a.r_ != b.r_ || a.c_ != b.c_) shim_detail::fail("shape mismatch");

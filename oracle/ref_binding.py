@@ -295,3 +295,39 @@ def max_principal_angle(a: np.ndarray, b: np.ndarray) -> float:
     out = C.c_double()
     _check(lib().ref_max_principal_angle(a.shape[0], a.shape[1], _p(a), _p(b), C.byref(out)))
     return out.value
+
+
+def compress(mesh: Mesh, cfg: Config, quant_bits: int) -> bytes:
+    """serialize_encoded_mesh(compress_mesh(mesh, {cfg, quant_bits})) (compress.hpp:152-219, :378-420)."""
+    n = C.c_longlong()
+    _check(lib().ref_compress(mesh.h, C.byref(cfg), quant_bits, None, C.c_longlong(0), C.byref(n)))
+    buf = np.zeros(n.value, dtype=np.uint8)
+    _check(lib().ref_compress(mesh.h, C.byref(cfg), quant_bits, _p(buf), C.c_longlong(n.value), C.byref(n)))
+    return buf.tobytes()
+
+
+def decompress(data: bytes, n: int) -> np.ndarray:
+    """decompress_mesh(parse_encoded_mesh(data)).vertices (compress.hpp:210-262, :422-474)."""
+    buf = np.frombuffer(data, dtype=np.uint8).copy()
+    out = np.zeros((n, 3))
+    _check(lib().ref_decompress(_p(buf), C.c_longlong(buf.size), _p(out), n))
+    return out
+
+
+def fine_denoise(mesh: Mesh, nf: int, sigma_spatial=0.0, sigma_range=0.35, normal_iterations=5, vertex_iterations=10,
+                 ring_depth=1):
+    """fine_denoise (denoise.hpp:175-180) -> (vertices n x 3, filtered normals nf x 3)."""
+    out = np.zeros((mesh.n, 3))
+    nrm = np.zeros((nf, 3))
+    _check(lib().ref_fine_denoise(mesh.h, C.c_double(sigma_spatial), C.c_double(sigma_range), normal_iterations,
+                                  vertex_iterations, ring_depth, _p(out), _p(nrm)))
+    return out, nrm
+
+
+def denoise_dynamic(mesh: Mesh, frames: Sequence[np.ndarray], cfg: Config, weighted: bool = True):
+    """denoise_dynamic (denoise.hpp:258-291); ``mesh`` is frame 0 (connectivity shared)."""
+    x = np.ascontiguousarray(np.stack(frames), dtype=np.float64)
+    out = np.zeros_like(x)
+    nb = C.c_int()
+    _check(lib().ref_denoise_dynamic(mesh.h, x.shape[0], _p(x), C.byref(cfg), int(weighted), _p(out), C.byref(nb)))
+    return out, nb.value

@@ -5,6 +5,8 @@
 // Built by `make refharness` into oracle/_ref/libspecmesh_ref.so (git-ignored);
 // used by tests/golden/make_ref_fixtures.py to generate the committed golden
 // vectors and, when present, by the CPU tests to check the numpy oracle directly.
+#include "specmesh/compress.hpp"
+#include "specmesh/denoise.hpp"
 #include "specmesh/pipeline.hpp"
 
 #include <cstdio>
@@ -400,5 +402,74 @@ int ref_bases_reconstruct(void* b, void* mesh, int weighted, double* out) {
     });
 }
 double ref_bases_timing(void* b, const char* stage) { return static_cast<RefBases*>(b)->bb.timings.get(stage); }
+
+
+// ---- F2: the spectral codec (compress.hpp:152-219, :378-474): SPECMSH1 bytes
+int ref_compress(void* mesh, const ref_config* cfg, int quant_bits, unsigned char* out, long long cap,
+                 long long* out_len) {
+    return guarded([&] {
+        CompressionConfig cc;
+        cc.pipeline = to_cfg(cfg);
+        cc.quant_bits = quant_bits;
+        const std::vector<std::uint8_t> bytes =
+            serialize_encoded_mesh(compress_mesh(static_cast<RefMesh*>(mesh)->mesh, cc));
+        *out_len = static_cast<long long>(bytes.size());
+        if (static_cast<long long>(bytes.size()) <= cap) std::copy(bytes.begin(), bytes.end(), out);
+    });
+}
+// decompress_mesh(parse_encoded_mesh(bytes)) -> vertices row-major n x 3
+int ref_decompress(const unsigned char* bytes, long long len, double* out, int n_expected) {
+    return guarded([&] {
+        const Mesh m = decompress_mesh(parse_encoded_mesh(std::vector<std::uint8_t>(bytes, bytes + len)));
+        require(m.vertex_count() == n_expected, "vertex count mismatch");
+        for (Eigen::Index i = 0; i < m.vertices.rows(); ++i)
+            for (int a = 0; a < 3; ++a) out[3 * i + a] = m.vertices(i, a);
+    });
+}
+
+// ---- F4: fine_denoise (denoise.hpp:175-180); out row-major n x 3, normals nf x 3
+int ref_fine_denoise(void* mesh, double sigma_spatial, double sigma_range, int normal_iterations,
+                     int vertex_iterations, int ring_depth, double* out, double* out_normals) {
+    return guarded([&] {
+        const Mesh& m = static_cast<RefMesh*>(mesh)->mesh;
+        BilateralParams p;
+        p.sigma_spatial = sigma_spatial;
+        p.sigma_range = sigma_range;
+        p.normal_iterations = normal_iterations;
+        p.vertex_iterations = vertex_iterations;
+        p.ring_depth = ring_depth;
+        p.validate();
+        const Mesh r = fine_denoise(m, p);
+        for (Eigen::Index i = 0; i < r.vertices.rows(); ++i)
+            for (int a = 0; a < 3; ++a) out[3 * i + a] = r.vertices(i, a);
+        if (out_normals) {
+            const Points nrm = bilateral_normals(face_geometry(m), face_ring_adjacency(m, p.ring_depth), p);
+            for (Eigen::Index f = 0; f < nrm.rows(); ++f)
+                for (int a = 0; a < 3; ++a) out_normals[3 * f + a] = nrm(f, a);
+        }
+    });
+}
+
+// ---- F3: denoise_dynamic (denoise.hpp:258-291); frames row-major F x n x 3 sharing the mesh's faces
+int ref_denoise_dynamic(void* mesh, int frames, const double* xyz, const ref_config* cfg, int weighted, double* out,
+                        int* blocks_computed) {
+    return guarded([&] {
+        const Mesh& first = static_cast<RefMesh*>(mesh)->mesh;
+        const int n = static_cast<int>(first.vertex_count());
+        std::vector<Mesh> seq(static_cast<std::size_t>(frames));
+        for (int f = 0; f < frames; ++f) {
+            seq[f].faces = first.faces;
+            seq[f].vertices.resize(n, 3);
+            for (int i = 0; i < n; ++i)
+                for (int a = 0; a < 3; ++a) seq[f].vertices(i, a) = xyz[(static_cast<std::size_t>(f) * n + i) * 3 + a];
+        }
+        const DynamicDenoiseResult r =
+            denoise_dynamic(seq, to_cfg(cfg), weighted ? AverageMode::Weighted : AverageMode::Simple);
+        for (int f = 0; f < frames; ++f)
+            for (int i = 0; i < n; ++i)
+                for (int a = 0; a < 3; ++a) out[(static_cast<std::size_t>(f) * n + i) * 3 + a] = r.frames[f].vertices(i, a);
+        *blocks_computed = r.basis_blocks_computed;
+    });
+}
 
 }  // extern "C"

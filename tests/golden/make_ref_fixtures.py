@@ -9,7 +9,7 @@ checks the numpy oracle against them on the CPU and tests/test_gpu_ref_fixtures.
 checks the CUDA path against them on the GPU.
 
 Run in this container:  python tests/golden/make_ref_fixtures.py [case ...]
-Cases: c1 c2 c3 c5 doi segment prims errors c4   (default: all but c4, which takes ~1 h)
+Cases: c1 c2 c3 c5 doi segment prims errors codec fine frames c4   (default: all but c4, which takes ~1 h)
 """
 import hashlib
 import json
@@ -207,6 +207,66 @@ def case_errors():
     print(json.dumps(msgs, indent=1))
 
 
+def widened_grid():
+    return synth.small_grid(96, 96, 32, 32, seed=31, sigma=0.01, flip=4)
+
+
+def case_codec():
+    """F2: compress_mesh -> SPECMSH1 bytes -> decompress_mesh (compress.hpp).  (A DOI-mode case on
+    this mesh is a rounding tie: the oracle ends block 0 at c = 68, the reference at 71 -- DESIGN.md §5.4.)"""
+    mesh = widened_grid()
+    rm = R.Mesh(mesh.vertices, mesh.faces)
+    arrays = {}
+    oi = R.default_config(part_count=8, growth=1.15, basis_mode=R.OI, subspace_size=32, iterations=1,
+                          shift_scale=SHIFT, seed=1)
+    for name, cfg, q in (("oi_q12", oi, 12), ("oi_q5", oi, 5)):
+        data = R.compress(rm, cfg, q)
+        arrays[f"{name}_bytes"] = np.frombuffer(data, dtype=np.uint8)
+        arrays[f"{name}_decoded"] = R.decompress(data, mesh.n)
+    save("codec", dict(input_tag(mesh), grid=[96, 96], seed=31, sigma=0.01, flip=4, part_count=8, growth=1.15,
+                       shift_scale=SHIFT), **arrays)
+
+
+def fine_inputs():
+    m = synth.small_grid(40, 30, 40, 30, seed=5, flip=5)
+    v = m.vertices.copy()
+    v[:, 2] = 0.2 * v[:, 2] + 0.05 * np.random.default_rng(5).standard_normal(v.shape[0])
+    return v, m.faces
+
+
+def case_fine():
+    """F4: fine_denoise (denoise.hpp:175-180)."""
+    v, f = fine_inputs()
+    rm = R.Mesh(v, f)
+    arrays = {}
+    for name, kw in (("default", {}), ("ring2", {"ring_depth": 2, "normal_iterations": 3}),
+                     ("sigma", {"sigma_spatial": 1.5, "sigma_range": 0.2, "vertex_iterations": 4})):
+        out, nrm = R.fine_denoise(rm, f.shape[0], **kw)
+        arrays[f"{name}_vertices"] = out
+        arrays[f"{name}_normals"] = nrm
+    sp = synth.sphere_mesh(3, seed=7)
+    out, nrm = R.fine_denoise(R.Mesh(sp.vertices, sp.faces), sp.faces.shape[0])
+    arrays["sphere_vertices"] = out
+    arrays["sphere_normals"] = nrm
+    save("fine", {"vertices_sha": sha(v), "faces_sha": sha(f), "n": int(v.shape[0])}, **arrays)
+
+
+def case_frames():
+    """F3: denoise_dynamic (denoise.hpp:258-291), both averaging modes."""
+    topo = synth.small_grid(64, 64, 32, 32, seed=11, flip=3)
+    verts = synth.grid_sequence(64, 64, 5, 11, 0.01)
+    rm = R.Mesh(verts[0], topo.faces)
+    cfg = R.default_config(part_count=8, growth=1.15, basis_mode=R.OI, weighting=R.BINARY, subspace_size=40,
+                           iterations=1, shift_scale=SHIFT, seed=1)
+    arrays = {}
+    for name, wt in (("weighted", True), ("simple", False)):
+        out, nb = R.denoise_dynamic(rm, verts, cfg, wt)
+        arrays[name] = out
+        arrays[f"{name}_blocks"] = np.array(nb)
+    save("frames", {"vertices_sha": sha(verts[0]), "faces_sha": sha(topo.faces), "n": int(topo.n), "frames": 5,
+                    "part_count": 8, "growth": 1.15, "c": 40, "shift_scale": SHIFT}, **arrays)
+
+
 def case_c4():
     """C4 at full size: 256 tiles of 64x64 on the 1024^2 grid, DOI c in [20, 400], band 1e-5/1e-4
     (about an hour single-threaded: dense eigendecomposition of n = 4096 + ~640 DOI steps)."""
@@ -229,7 +289,8 @@ def case_c4():
 
 
 CASES = {"c1": case_c1, "c2": case_c2, "c3": case_c3, "c5": case_c5, "doi": case_doi, "segment": case_segment,
-         "prims": case_prims, "errors": case_errors}
+         "prims": case_prims, "errors": case_errors, "codec": case_codec, "fine": case_fine,
+         "frames": case_frames}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
