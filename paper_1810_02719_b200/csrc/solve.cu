@@ -45,7 +45,10 @@ struct SolveSmem {
     static constexpr int XS = CS + 4;  // padded row of the right-hand-side slab
     static constexpr int F_ELEMS = 2 * W * FS;
     static constexpr int R_ELEMS = W * XS;
-    static constexpr int FB = F_ELEMS * 8, RB = R_ELEMS * 8, YB = 2 * RB;
+    // column-private mode (CS = 64): warp w owns all row tiles of columns 8w..8w+7, so the
+    // carry y_{k-1} never crosses warps -- one carry buffer, no CTA-level barrier per step
+    static constexpr bool PRIV = (CS == 64);
+    static constexpr int FB = F_ELEMS * 8, RB = R_ELEMS * 8, YB = PRIV ? RB : 2 * RB;
     // W = 32, CS = 16 (large batches): a budget for three CTAs per SM (two rhs
     // slots instead of six).  The solve is bound by per-CTA step latency, so a
     // third resident CTA raises the SM's throughput: C5 418 -> 377 us per
@@ -82,11 +85,13 @@ SMG_DEV void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
 template <int W, int CS>
 struct SolveTiling {
     static constexpr int MT_ALL = W / 8, NT_ALL = CS / 8;
+    static constexpr bool PRIV = SolveSmem<W, CS>::PRIV;
     // 8 warps (two per SM sub-partition hide the DMMA issue latency); prefer a
     // 4 x 2 warp grid, a full m-column of warps when there is one n-tile
     static constexpr int NW = kSolveWarps;
-    static constexpr int WM = (NT_ALL == 1) ? (MT_ALL < NW ? MT_ALL : NW)
-                                            : ((MT_ALL % 4 == 0) ? 4 : ((MT_ALL % 2 == 0) ? 2 : 1));
+    static constexpr int WM = PRIV ? 1
+                                   : (NT_ALL == 1) ? (MT_ALL < NW ? MT_ALL : NW)
+                                                   : ((MT_ALL % 4 == 0) ? 4 : ((MT_ALL % 2 == 0) ? 2 : 1));
     static constexpr int WN_RAW = NW / WM;
     static constexpr int WN = (NT_ALL % WN_RAW == 0) ? WN_RAW
                                                      : ((NT_ALL % 4 == 0 && WN_RAW >= 4) ? 4 : ((NT_ALL % 2 == 0 && WN_RAW >= 2) ? 2 : 1));
@@ -96,7 +101,8 @@ struct SolveTiling {
     // triangular block, so contiguous row tiles would give the bottom warps up
     // to 4x the DMMAs of the top ones; pairing tile r with MT_ALL-1-r balances
     // every warp (and so every SM sub-partition).
-    static constexpr bool PAIRED = (MT == 2 && MT_ALL == 2 * WM);
+    static constexpr bool PAIRED = !PRIV && (MT == 2 && MT_ALL == 2 * WM);
+    static_assert(!PRIV || (NT == 1 && MT == MT_ALL && WN == NW), "column-private tiling: one n-tile per warp");
     SMG_DEV static int tile(int wm, int i) { return PAIRED ? (i == 0 ? wm : MT_ALL - 1 - wm) : wm * MT + i; }
 };
 
@@ -119,7 +125,23 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     // first half: triangular block (Linv_k lower for FWD, Linv_k^T Sigma upper for BWD)
-    if constexpr (TL::PAIRED) {
+    if constexpr (TL::PRIV) {
+        // all row tiles of one n-tile: in the 8-wide k block kb only the row tiles
+        // i >= kb (FWD) / i <= kb (BWD) are nonzero -- compile-time, fully unrolled
+#pragma unroll
+        for (int kb = 0; kb < MT; ++kb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int kk = 8 * kb + 4 * h;
+                const double b = xs[(kk + t) * XS + 8 * wn + g];
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+                    if (FWD ? (i >= kb) : (i <= kb)) {
+                        const double a = fs[(kk + t) * FS + 8 * i + g];
+                        dmma884(acc[i][0][0], acc[i][0][1], a, b);
+                    }
+            }
+    } else if constexpr (TL::PAIRED) {
         // row tiles lo = wm and hi = MT_ALL-1-wm; the k ranges where a tile's
         // block is nonzero are loop bounds, not predicates (a predicated-off
         // DMMA still occupies the pipe): FWD tile r needs kk < 8r+8, BWD kk >= 8r
@@ -252,7 +274,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
     extern __shared__ __align__(16) double smem[];
     auto Fs = [&](int i) { return smem + i * S::F_ELEMS; };
     auto Rs = [&](int i) { return smem + NSF * S::F_ELEMS + i * S::R_ELEMS; };
-    auto Ys = [&](int i) { return smem + NSF * S::F_ELEMS + NSR * S::R_ELEMS + i * S::R_ELEMS; };
+    auto Ys = [&](int i) { return smem + NSF * S::F_ELEMS + NSR * S::R_ELEMS + (S::PRIV ? 0 : i) * S::R_ELEMS; };
 
     const int b = blockIdx.y;
     const int c = p.dimC ? p.dimC[(int64_t)b * p.dimStride] : p.c_cap;
@@ -335,6 +357,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
         };
         Cursor nx{0, 0, 0, Kb};
         src_rows(nx, pn);
+        const int cmax = min(p.ldin, p.ldt);  // a slice wider than the remaining columns stops at the row end
         for (Cursor cu{0, 0, 0, Kb}; cu.gs < total; cu.next()) {
             const int gs = cu.gs, sweep = cu.sweep, step = cu.step, k = cu.k(), sl = gs % NSR;
             int rows[PER];
@@ -355,7 +378,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 const int e = rt + i * NT_RHS;
                 if (e >= W * CCH) break;
                 const int r = e / CCH, ch = e % CCH;
-                if (r < nvalid) {
+                if (r < nvalid && col0 + 2 * ch < cmax) {
                     const double* src = (sweep == 0) ? in + (int64_t)rows[i] * p.ldin + col0
                                                      : tmp + (int64_t)rows[i] * p.ldt + col0;
                     cp_async16(xs + r * XS + 2 * ch, src + 2 * ch);
@@ -371,10 +394,13 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
         asm volatile("cp.async.wait_all;\n" ::: "memory");
     } else {
         double acc[TL::MT][TL::NT][2];
+        // column-private mode: a warp whose 8 columns lie past c only keeps the rings moving
+        const bool live = !S::PRIV || col0 + 8 * warp < c;
         // the independent half of step gs (waits for the step's slab and rhs block)
         auto first = [&](int gs, int sweep) {
             mbar_wait(&fullR[gs % NSR], (gs / NSR) & 1);
             mbar_wait(&fullF[gs % NSF], (gs / NSF) & 1);
+            if (!live) return;
 #if defined(SMG_SOLVE_NO_TRI)  // timing probe: coupling half only (one dense product per step)
             (void)sweep;
             for (int i = 0; i < TL::MT; ++i)
@@ -409,7 +435,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
             const double* yprev = Ys((gs + 1) & 1);
             // the carry of a sweep's first step is zero
 #ifndef SMG_SOLVE_NO_MMA
-            if (step != 0) {
+            if (step != 0 && live) {
                 if ((sweep & 1) == 0) mma_step<W, CS, true>(Fs(sf), nullptr, yprev, acc, warp, g, t, 2);
                 else mma_step<W, CS, false>(Fs(sf), nullptr, yprev, acc, warp, g, t, 2);
             }
@@ -424,7 +450,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 mbar_arrive_local(&consF[sf]);
                 if (step + 1 != Kb) mbar_arrive_local(&consR[sr]);
             }
-            if (warp < TL::ACTIVE) {
+            if (warp < TL::ACTIVE && live) {
                 const int wm = warp % TL::WM, wn = warp / TL::WM;
 #pragma unroll
                 for (int i = 0; i < TL::MT; ++i)
@@ -453,7 +479,9 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 if (lane == 0) mbar_arrive_local(&consR[sr]);
             }
             if (nx.gs < total) first(nx.gs, nx.sweep);  // off the critical path: before the barrier
-            mma_bar();  // ycur complete before the next step reads it; yprev free for reuse
+            // ycur complete before the next step reads it; yprev free for reuse
+            if constexpr (S::PRIV) __syncwarp();  // the carry columns are the warp's own
+            else mma_bar();
         }
     }
 }
@@ -484,7 +512,8 @@ void solve_block_tridiag(const SolveParams& p, int W, cudaStream_t st) {
     switch (W) {
         case 16: launch<16, 8>(p, st); break;
         case 32:
-            if (wide && std::getenv("SMG_SOLVE_CS") && std::atoi(std::getenv("SMG_SOLVE_CS")) >= 32) launch<32, 32>(p, st);
+            if (std::getenv("SMG_SOLVE_CS") && std::atoi(std::getenv("SMG_SOLVE_CS")) >= 64) launch<32, 64>(p, st);
+            else if (wide && std::getenv("SMG_SOLVE_CS") && std::atoi(std::getenv("SMG_SOLVE_CS")) >= 32) launch<32, 32>(p, st);
             else if (mid) launch<32, 16>(p, st);
             else launch<32, 8>(p, st);
             break;
