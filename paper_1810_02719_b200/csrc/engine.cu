@@ -234,6 +234,8 @@ void Workspace::init(int B_, int n_, int npad_, int ccap_, cudaStream_t st) {
     stats.alloc((size_t)B * 4, st);
     status.alloc(B, st);
     status.zero();
+    probe_part.alloc((size_t)B * orth_probe_chunks(n) * ld * 8, st);
+    probe_est.alloc(B, st);
     skip.alloc(B, st);
     skip.zero();
     skip2.alloc(B, st);
@@ -279,8 +281,10 @@ void solve_batch(const StepCtx& cx, Workspace& ws, const FactorSet& fs, int tile
 }
 
 namespace {
-void gram(Workspace& ws, const double* V, int c, const int* dimC, int n, cudaStream_t st) {
+void gram(Workspace& ws, const double* V, int c, const int* dimC, int n, cudaStream_t st,
+          const int* skip = nullptr) {
     GemmParams g;
+    g.skip = skip;
     g.M = c;
     g.N = c;
     g.K = n;
@@ -471,11 +475,25 @@ void orth_batch(const StepCtx& cx, Workspace& ws, const double* in, double* out,
         const bool fuse = projX != nullptr && !ts && dimC == nullptr && std::getenv("SMG_PROJ_FUSE") != nullptr;
         if (fuse) trmm(ws, in, out, c, dimC, n, cx.st, nullptr, projX, strideX);
         else pass1(out);
-        gram(ws, out, c, dimC, n, cx.st);
-        if (c <= 256) {
+        // Is Q1 orthonormal already?  Default: a one-pass randomized probe of |Q1^T Q1 - I|_F
+        // (probe.cu) against skip_tol * sqrt(c); the chains that fail (and only they) form the
+        // second Gram and factor it.  SMG_ORTH_PROBE=0: the exact max-entry test on the full
+        // second Gram of every chain, as before.
+        static const bool probe = !(std::getenv("SMG_ORTH_PROBE") && std::atoi(std::getenv("SMG_ORTH_PROBE")) == 0);
+        if (probe) {
+            {
+                ProfScope pc("chol", cx.st);
+                orth_probe(out, ws.ld, ws.mstride(), ws.n, dimC, c, ws.B, skip_tol * std::sqrt((double)c),
+                           ws.probe_part.get(), ws.skip.get(), ws.probe_est.get(), cx.st);
+            }
+            gram(ws, out, c, dimC, n, cx.st, ws.skip.get());
+            chol_pass2(ws, c, dimC, pos, cx.st, ws.skip.get());
+        } else if (c <= 256) {
+            gram(ws, out, c, dimC, n, cx.st);
             // the single-CTA pass-2 scan decides the skip too (one launch)
             chol(ws, c, dimC, false, true, pos, cx.st, true, false, nullptr, ws.skip.get(), skip_tol);
         } else {
+            gram(ws, out, c, dimC, n, cx.st);
             {
                 ProfScope pc("chol", cx.st);
                 orth_check(ws.G.get(), ws.ld, (int64_t)ws.ld * ws.ld, dimC, 1, c, ws.B, skip_tol, ws.skip.get(), cx.st);

@@ -132,6 +132,7 @@ struct Workspace {
     int B = 0, n = 0, npad = 0, ld = 0, ccap = 0;
     int splits = 1;
     DBuf<double> U, V, T, R, G, Gws, Bm, work, rdiag, vnorm, rpart, coeff, sign, e, ppart, ppart2, stats;
+    DBuf<double> probe_part, probe_est;  // orthonormality probe of the adaptive CholeskyQR2 (probe.cu)
     DBuf<int> counters;
     DBuf<int> status, errpos, scratch_status, skip, skip2, rneed;
     DBuf<unsigned long long> nmax;

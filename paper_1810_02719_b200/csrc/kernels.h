@@ -167,6 +167,11 @@ void near_fill(const double* G, int64_t ldg, int64_t strideG, const int* dimC, i
                const unsigned long long* nmax, const int* skip_in, int* skip_out, double* Binv, int64_t ldb,
                int64_t strideB, double* dscale, int64_t strideD, cudaStream_t st);
 // dst_b = src_b for the batch entries with skip[b] == 0 (n x ld row-major blocks)
+// Orthonormality probe (probe.cu): skip[b] = (estimated |Q^T Q - I|_F <= tol) from 8 fixed
+// +-1 probe vectors in one pass over Q; part holds batch * orth_probe_chunks(n) * c_cap * 8.
+int orth_probe_chunks(int n);
+void orth_probe(const double* Q, int64_t ldq, int64_t strideQ, int n, const int* dimC, int c_cap, int batch, double tol,
+                double* part, int* skip, double* est_out, cudaStream_t st);
 void copy_unskipped(const double* src, double* dst, int64_t elems, int64_t stride, int batch, const int* skip,
                     cudaStream_t st);
 int chol_smem_bytes(int c_cap);

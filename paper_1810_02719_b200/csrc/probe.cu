@@ -1,0 +1,180 @@
+// Orthonormality probe for the adaptive CholeskyQR2 (K6/K7): decides per chain whether
+// the pass-1 factor Q1 is already orthonormal WITHOUT forming the second Gram.
+//
+// With P = 8 fixed +-1 probe vectors X (c x 8, a hash of the column index),
+//   Z = Q1^T (Q1 X) - X = (Q1^T Q1 - I) X,      E[ |Z|_F^2 / P ] = |Q1^T Q1 - I|_F^2
+// (Hutchinson; E[x x^T] = I).  One pass over Q1 (n x c, read once: 8 n c bytes per chain
+// instead of the Gram's n c^2 flops): a CTA takes 128 rows, stages 32 at a time in shared
+// memory (rows padded to 4 mod 16 doubles: conflict-free DMMA fragments), forms y = Q_rows X
+// (32 x 8) and accumulates z += Q_rows^T y (c x 8) on the FP64 tensor pipe (m8n8k4; the probe
+// signs are generated in registers); the per-CTA partials are summed in chunk order by one
+// CTA per chain, which sets skip[b] = (sqrt(|Z|_F^2 / P) <= tol).  Fixed order throughout.
+// Chains that fail take the exact path (second Gram, near-identity or full second Cholesky).
+// Replaces nothing in the reference: HouseholderQR (spectral.hpp:125-129) needs no second
+// pass; this is the check that lets CholeskyQR2 stop after one.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace smg {
+
+namespace {
+
+constexpr int PROBES = 8, SUB = 32, ROWS_PER_CTA = 128, PNT_ = 256, PWARPS = PNT_ / 32;
+constexpr int MAX_MT = 8;  // column tiles (of 8) per warp: c <= 8 * 8 * 8 = 512
+
+SMG_DEV unsigned probe_bits(int k) {
+    unsigned h = (unsigned)k * 0x9E3779B9u + 0x7F4A7C15u;
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h & 0xFFu;
+}
+
+__host__ __device__ inline int probe_lds(int c) { return ((c + 15) / 16) * 16 + 4; }  // staged row stride, 4 mod 16
+
+__global__ void __launch_bounds__(PNT_) orth_probe_partial_kernel(const double* __restrict__ Q, int64_t ldq,
+                                                                  int64_t strideQ, int n, const int* dimC, int c_cap,
+                                                                  double* __restrict__ part, int chunks) {
+    extern __shared__ __align__(16) double psm[];
+    const int b = blockIdx.y, chunk = blockIdx.x;
+    const int c = dimC ? dimC[b] : c_cap;
+    const int lds = probe_lds(c_cap);
+    const int c8 = (c + 7) & ~7;          // columns staged (zero past c): whole 8-wide tiles
+    double* S = psm;                      // SUB x lds
+    double* ysm = psm + SUB * lds;        // SUB x PROBES (+ the second k-half's partial)
+    double* yhalf = ysm + SUB * PROBES;
+    const double* q = Q + (int64_t)b * strideQ;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int r0 = chunk * ROWS_PER_CTA;
+    const int ntile = c8 / 8;
+    double z[MAX_MT][2];
+#pragma unroll
+    for (int i = 0; i < MAX_MT; ++i) z[i][0] = z[i][1] = 0.0;
+    for (int sub = 0; sub < ROWS_PER_CTA / SUB; ++sub) {
+        const int rs = r0 + sub * SUB;
+        if (rs >= n) break;
+        // stage SUB rows x c8 columns (zeros past n and past c)
+        for (int e = tid; e < SUB * (c8 / 2); e += PNT_) {
+            const int r = e / (c8 / 2), kk = 2 * (e % (c8 / 2));
+            double2 v = make_double2(0.0, 0.0);
+            if (rs + r < n && kk < c) v = __ldcg(reinterpret_cast<const double2*>(q + (int64_t)(rs + r) * ldq + kk));
+            if (kk + 1 >= c) v.y = 0.0;
+            *reinterpret_cast<double2*>(S + r * lds + kk) = v;
+        }
+        __syncthreads();
+        // y = S X: row tile (warp & 3), the k range split in two halves (warp >> 2)
+        {
+            const int mt = warp & 3, half = warp >> 2;
+            const int ksteps = c8 / 4, kmid = (ksteps + 1) / 2;
+            const int kb = half ? kmid : 0, ke = half ? ksteps : kmid;
+            double y0[2] = {0.0, 0.0}, y1[2] = {0.0, 0.0};
+            const double* srow = S + (8 * mt + g) * lds + t;
+            int ks = kb;
+            for (; ks + 1 < ke; ks += 2) {
+                const double a0 = srow[4 * ks], a1 = srow[4 * ks + 4];
+                const double b0 = ((probe_bits(4 * ks + t) >> g) & 1u) ? 1.0 : -1.0;
+                const double b1 = ((probe_bits(4 * ks + 4 + t) >> g) & 1u) ? 1.0 : -1.0;
+                dmma884(y0[0], y0[1], a0, b0);
+                dmma884(y1[0], y1[1], a1, b1);
+            }
+            if (ks < ke) {
+                const double a0 = srow[4 * ks];
+                const double b0 = ((probe_bits(4 * ks + t) >> g) & 1u) ? 1.0 : -1.0;
+                dmma884(y0[0], y0[1], a0, b0);
+            }
+            y0[0] += y1[0];
+            y0[1] += y1[1];
+            double* dst = (half ? yhalf : ysm) + (8 * mt + g) * PROBES + 2 * t;
+            *reinterpret_cast<double2*>(dst) = make_double2(y0[0], y0[1]);
+        }
+        __syncthreads();
+        if (tid < SUB * PROBES) ysm[tid] += yhalf[tid];
+        __syncthreads();
+        // z += S^T y: column tiles warp, warp + 8, ...; k = the SUB rows
+        {
+            double bf[SUB / 4];
+#pragma unroll
+            for (int k4 = 0; k4 < SUB / 4; ++k4) bf[k4] = ysm[(4 * k4 + t) * PROBES + g];
+#pragma unroll
+            for (int i = 0; i < MAX_MT; ++i) {
+                const int mt = warp + PWARPS * i;
+                if (mt < ntile) {
+#pragma unroll
+                    for (int k4 = 0; k4 < SUB / 4; ++k4)
+                        dmma884(z[i][0], z[i][1], S[(4 * k4 + t) * lds + 8 * mt + g], bf[k4]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double* out = part + ((int64_t)b * chunks + chunk) * (int64_t)c_cap * PROBES;
+#pragma unroll
+    for (int i = 0; i < MAX_MT; ++i) {
+        const int k = 8 * (warp + PWARPS * i) + g;
+        if (k < c) *reinterpret_cast<double2*>(out + (int64_t)k * PROBES + 2 * t) = make_double2(z[i][0], z[i][1]);
+    }
+}
+
+// Z = sum over chunks (in order) - X; est = sqrt(|Z|_F^2 / P).  A thread per (column, probe
+// pair): the chunk loads are independent, the adds ordered.
+__global__ void __launch_bounds__(PNT_) orth_probe_finish_kernel(const double* __restrict__ part, int chunks, int n,
+                                                                 const int* dimC, int c_cap, double tol, int* skip,
+                                                                 double* est_out) {
+    __shared__ double red[PNT_];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const int c = dimC ? dimC[b] : c_cap;
+    const int live = min(chunks, (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
+    double ss = 0.0;
+    for (int item = tid; item < c * (PROBES / 2); item += PNT_) {
+        const int k = item / (PROBES / 2), pp = 2 * (item % (PROBES / 2));
+        const double* src = part + ((int64_t)b * chunks * c_cap + k) * PROBES + pp;
+        double2 zs = make_double2(0.0, 0.0);
+        for (int ch0 = 0; ch0 < live; ch0 += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                v[u] = ch0 + u < live ? __ldcg(reinterpret_cast<const double2*>(src + (int64_t)(ch0 + u) * c_cap * PROBES))
+                                      : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                zs.x += v[u].x;
+                zs.y += v[u].y;
+            }
+        }
+        const unsigned bits = probe_bits(k);
+        zs.x -= ((bits >> pp) & 1u) ? 1.0 : -1.0;
+        zs.y -= ((bits >> (pp + 1)) & 1u) ? 1.0 : -1.0;
+        ss += zs.x * zs.x + zs.y * zs.y;
+    }
+    red[tid] = ss;
+    __syncthreads();
+    for (int o = PNT_ / 2; o > 0; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const double est = sqrt(red[0] / PROBES);
+        skip[b] = (est <= tol) ? 1 : 0;  // NaN -> no skip
+        if (est_out) est_out[b] = est;
+    }
+}
+
+}  // namespace
+
+int orth_probe_chunks(int n) { return (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA; }
+
+void orth_probe(const double* Q, int64_t ldq, int64_t strideQ, int n, const int* dimC, int c_cap, int batch, double tol,
+                double* part, int* skip, double* est_out, cudaStream_t st) {
+    const int chunks = orth_probe_chunks(n);
+    const int bytes = (SUB * probe_lds(c_cap) + 2 * SUB * PROBES) * (int)sizeof(double);
+    ensure_smem((const void*)orth_probe_partial_kernel, bytes);
+    ::smg::count_launch(), orth_probe_partial_kernel<<<dim3(chunks, batch), PNT_, bytes, st>>>(Q, ldq, strideQ, n, dimC,
+                                                                                               c_cap, part, chunks);
+    ::smg::count_launch(), orth_probe_finish_kernel<<<batch, PNT_, 0, st>>>(part, chunks, n, dimC, c_cap, tol, skip,
+                                                                            est_out);
+}
+
+}  // namespace smg

@@ -48,6 +48,11 @@ struct SolveSmem {
     // column-private mode (CS = 64): warp w owns all row tiles of columns 8w..8w+7, so the
     // carry y_{k-1} never crosses warps -- one carry buffer, no CTA-level barrier per step
     static constexpr bool PRIV = (CS == 64);
+    // consumer (DMMA) warps: the cooperative tiling uses all 8; column-private warps own 16
+    // columns each (4 x 2 tiles of 8 x 8: eight independent accumulator chains saturate the
+    // warp's sub-partition, tools/dmma_lat.cu) -- one warp per SM sub-partition
+    static constexpr int NCW = PRIV ? CS / 16 : kSolveWarps;
+    static constexpr int THREADS = (NCW + kProdWarps) * 32;
     static constexpr int FB = F_ELEMS * 8, RB = R_ELEMS * 8, YB = PRIV ? RB : 2 * RB;
     // W = 32, CS = 16 (large batches): a budget for three CTAs per SM (two rhs
     // slots instead of six).  The solve is bound by per-CTA step latency, so a
@@ -88,7 +93,7 @@ struct SolveTiling {
     static constexpr bool PRIV = SolveSmem<W, CS>::PRIV;
     // 8 warps (two per SM sub-partition hide the DMMA issue latency); prefer a
     // 4 x 2 warp grid, a full m-column of warps when there is one n-tile
-    static constexpr int NW = kSolveWarps;
+    static constexpr int NW = SolveSmem<W, CS>::NCW;
     static constexpr int WM = PRIV ? 1
                                    : (NT_ALL == 1) ? (MT_ALL < NW ? MT_ALL : NW)
                                                    : ((MT_ALL % 4 == 0) ? 4 : ((MT_ALL % 2 == 0) ? 2 : 1));
@@ -102,7 +107,7 @@ struct SolveTiling {
     // to 4x the DMMAs of the top ones; pairing tile r with MT_ALL-1-r balances
     // every warp (and so every SM sub-partition).
     static constexpr bool PAIRED = !PRIV && (MT == 2 && MT_ALL == 2 * WM);
-    static_assert(!PRIV || (NT == 1 && MT == MT_ALL && WN == NW), "column-private tiling: one n-tile per warp");
+    static_assert(!PRIV || (NT == 2 && MT == MT_ALL && WN == NW), "column-private tiling: 16 columns per warp");
     SMG_DEV static int tile(int wm, int i) { return PAIRED ? (i == 0 ? wm : MT_ALL - 1 - wm) : wm * MT + i; }
 };
 
@@ -133,12 +138,15 @@ SMG_DEV void mma_step(const double* __restrict__ fs, const double* __restrict__ 
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int kk = 8 * kb + 4 * h;
-                const double b = xs[(kk + t) * XS + 8 * wn + g];
+                double b[NT];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) b[j] = xs[(kk + t) * XS + 8 * (wn * NT + j) + g];
 #pragma unroll
                 for (int i = 0; i < MT; ++i)
                     if (FWD ? (i >= kb) : (i <= kb)) {
                         const double a = fs[(kk + t) * FS + 8 * i + g];
-                        dmma884(acc[i][0][0], acc[i][0][1], a, b);
+#pragma unroll
+                        for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a, b[j]);
                     }
             }
     } else if constexpr (TL::PAIRED) {
@@ -258,7 +266,8 @@ SMG_DEV void mbar_arrive_local(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 // named barrier over the DMMA warps only (the producers run ahead on mbarriers)
-SMG_DEV void mma_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT_MMA) : "memory"); }
+template <int THREADS_MMA>
+SMG_DEV void mma_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(THREADS_MMA) : "memory"); }
 
 // Warp-specialised: the DMMA warps run the steps (named barrier among
 // themselves for the carry rows); one producer warp streams the factor slabs
@@ -266,8 +275,9 @@ SMG_DEV void mma_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT_MMA) : "memor
 // ring, deeper).  Producers never meet the DMMA warps at a CTA barrier.  Ring
 // slot s of step gs is gs % N, the phase parity of that step (gs / N) & 1.
 template <int W, int CS>
-__global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
+__global__ void __launch_bounds__((SolveSmem<W, CS>::THREADS)) solve_kernel(SolveParams p) {
     using S = SolveSmem<W, CS>;
+    constexpr int kSolveWarps = S::NCW, NT_MMA = S::NCW * 32;  // shadow the file-scope defaults
     using TL = SolveTiling<W, CS>;
     constexpr int FS = S::FS, XS = S::XS;
     constexpr int NSF = S::NSF, NSR = S::NSR;
@@ -394,10 +404,10 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
         asm volatile("cp.async.wait_all;\n" ::: "memory");
     } else {
         double acc[TL::MT][TL::NT][2];
-        // column-private mode: a warp whose 8 columns lie past c only keeps the rings moving
-        const bool live = !S::PRIV || col0 + 8 * warp < c;
+        // column-private mode: a warp whose 16 columns lie past c only keeps the rings moving
+        const bool live = !S::PRIV || col0 + 16 * warp < c;
         // the independent half of step gs (waits for the step's slab and rhs block)
-        auto first = [&](int gs, int sweep) {
+        auto first = [&](double (&acc)[TL::MT][TL::NT][2], int gs, int sweep) {
             mbar_wait(&fullR[gs % NSR], (gs / NSR) & 1);
             mbar_wait(&fullF[gs % NSF], (gs / NSF) & 1);
             if (!live) return;
@@ -413,7 +423,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 for (int j = 0; j < TL::NT; ++j) acc[i][j][0] = acc[i][j][1] = Rs(gs % NSR)[tid];
 #endif
         };
-        first(0, 0);
+        first(acc, 0, 0);
         Cursor nx{0, 0, 0, Kb};
         for (Cursor cu{0, 0, 0, Kb}; cu.gs < total; cu.next()) {
             const int gs = cu.gs, sweep = cu.sweep, step = cu.step, k = cu.k();
@@ -478,10 +488,10 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams p) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive_local(&consR[sr]);
             }
-            if (nx.gs < total) first(nx.gs, nx.sweep);  // off the critical path: before the barrier
+            if (nx.gs < total) first(acc, nx.gs, nx.sweep);  // off the critical path: before the barrier
             // ycur complete before the next step reads it; yprev free for reuse
-            if constexpr (S::PRIV) __syncwarp();  // the carry columns are the warp's own
-            else mma_bar();
+            if constexpr (S::PRIV) __syncwarp();  // the carry columns are the warp's own: no CTA barrier
+            else mma_bar<NT_MMA>();
         }
     }
 }
@@ -492,7 +502,7 @@ void launch(const SolveParams& p, cudaStream_t st) {
     const int slices = (p.c_cap + CS - 1) / CS;
     ensure_smem((const void*)solve_kernel<W, CS>, bytes);
     dim3 grid(slices, p.batch);
-    ::smg::count_launch(), solve_kernel<W, CS><<<grid, NT, bytes, st>>>(p);
+    ::smg::count_launch(), solve_kernel<W, CS><<<grid, SolveSmem<W, CS>::THREADS, bytes, st>>>(p);
 }
 
 }  // namespace
