@@ -37,7 +37,14 @@ void DoiLoop::issue(cudaStream_t cs, cudaGraphConditionalHandle h, int use_handl
     p.dimC = dimC;
     p.dimStride = 1;
     solve_block_tridiag(p, ts.W, cs);
-    orth_batch(cx, ws, ws.V.get(), ws.U.get(), ws.ccap, dimC, true, -1);
+    // Two full CholeskyQR passes per DOI step by default.  SMG_DOI_ADAPTIVE=1 lets the probe skip
+    // the second pass (C4 485 -> 455 ms), but a DOI trajectory amplifies any change of rounding
+    // by ~1/r per growth step: on the reference-generated fixture ref_doi.npz
+    // the first block's last decision has a 2.4 % margin and flips (c = 51 instead of 50).
+    static const double skip_tol = (std::getenv("SMG_DOI_ADAPTIVE") && std::atoi(std::getenv("SMG_DOI_ADAPTIVE")) == 1)
+                                       ? (std::getenv("SMG_ORTH_SKIP_TOL") ? std::atof(std::getenv("SMG_ORTH_SKIP_TOL")) : 1e-13)
+                                       : 0.0;
+    orth_batch(cx, ws, ws.V.get(), ws.U.get(), ws.ccap, dimC, true, -1, 2, skip_tol);
     project_batch(cx, ws, ws.U.get(), ws.ccap, dimC, X_.get(), 0, nullptr, 0);
     doi_decide(state, 1, ws.stats.get(), 4, h, use_handle, ws.status.get(), cs, trace_c_.get(), trace_r_.get());
     doi_append(state, ws.U.get(), ws.ld, ws.mstride(), ws.e.get(), ws.npad, ts.n, 1, cs);
