@@ -408,6 +408,10 @@ __global__ void __launch_bounds__(PipeShape<MW>::THREADS, PipeShape<MW>::MINB)
     extern __shared__ __align__(16) double gsm[];
     double* As = gsm;
     double* Bs = gsm + PNS * SA::ELEMS;
+    // diagonal tile of a Gram (V^T V, both operands the same k-major columns): the B slab
+    // would duplicate the A slab -- load once, read twice (half the L2 traffic of that tile)
+    const bool same_slab = TA && !TB && BM == BN && p.syrkUpper && p.A == p.B && p.lda == p.ldb &&
+                           p.strideA == p.strideB && m0 == n0 && M == N;
     __shared__ __align__(8) uint64_t full[PNS], consumed[PNS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(PipeShape<MW>::THREADS, PipeShape<MW>::MINB)
             }
             // op(A)(m, k) lives at A[k*lda + m] (TA, k-major) or A[m*lda + k]
             issue_slab<BM, TA>(As + st * SA::ELEMS, A, p.lda, k0, m0, kStop, M, lane);
-            issue_slab<BN, !TB>(Bs + st * SB::ELEMS, B, p.ldb, k0, n0, kStop, N, lane);
+            if (!same_slab) issue_slab<BN, !TB>(Bs + st * SB::ELEMS, B, p.ldb, k0, n0, kStop, N, lane);
             asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(g_smem_u32(&full[st])) : "memory");
             __syncwarp();
             if (lane == 0) g_mbar_arrive(&full[st]);
@@ -464,8 +468,8 @@ __global__ void __launch_bounds__(PipeShape<MW>::THREADS, PipeShape<MW>::MINB)
         const int st = ks % PNS, k0 = kBeg + ks * BKP;
         g_mbar_wait(&full[st], fph[st]);
         fph[st] ^= 1u;
-        slab_mma<SA, SB, NJ>(As + st * SA::ELEMS, Bs + st * SB::ELEMS, acc, fmask, kFull, k0, kdiag, p.upperB, wm, wn,
-                             g, t);
+        slab_mma<SA, SB, NJ>(As + st * SA::ELEMS, same_slab ? As + st * SA::ELEMS : Bs + st * SB::ELEMS, acc, fmask,
+                             kFull, k0, kdiag, p.upperB, wm, wn, g, t);
         __syncwarp();
         if (lane == 0) g_mbar_arrive(&consumed[st]);
     }

@@ -42,29 +42,52 @@ __global__ void __launch_bounds__(PNT_) orth_probe_partial_kernel(const double* 
     const int c = dimC ? dimC[b] : c_cap;
     const int lds = probe_lds(c_cap);
     const int c8 = (c + 7) & ~7;          // columns staged (zero past c): whole 8-wide tiles
-    double* S = psm;                      // SUB x lds
-    double* ysm = psm + SUB * lds;        // SUB x PROBES (+ the second k-half's partial)
+    double* Sbuf[2] = {psm, psm + SUB * lds};   // two SUB x lds stages (cp.async double buffer)
+    double* ysm = psm + 2 * SUB * lds;    // SUB x PROBES (+ the second k-half's partial)
     double* yhalf = ysm + SUB * PROBES;
     const double* q = Q + (int64_t)b * strideQ;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int r0 = chunk * ROWS_PER_CTA;
     const int ntile = c8 / 8;
+    const int nsub = min(ROWS_PER_CTA / SUB, (n - r0 + SUB - 1) / SUB);
     double z[MAX_MT][2];
 #pragma unroll
     for (int i = 0; i < MAX_MT; ++i) z[i][0] = z[i][1] = 0.0;
-    for (int sub = 0; sub < ROWS_PER_CTA / SUB; ++sub) {
-        const int rs = r0 + sub * SUB;
-        if (rs >= n) break;
-        // stage SUB rows x c8 columns (zeros past n and past c)
-        for (int e = tid; e < SUB * (c8 / 2); e += PNT_) {
-            const int r = e / (c8 / 2), kk = 2 * (e % (c8 / 2));
-            double2 v = make_double2(0.0, 0.0);
-            if (rs + r < n && kk < c) v = __ldcg(reinterpret_cast<const double2*>(q + (int64_t)(rs + r) * ldq + kk));
-            if (kk + 1 >= c) v.y = 0.0;
-            *reinterpret_cast<double2*>(S + r * lds + kk) = v;
+    // the padding (columns c..c8, rows past n) is zeroed once; the copies never touch it
+    for (int e = tid; e < 2 * SUB * lds; e += PNT_) psm[e] = 0.0;
+    __syncthreads();
+    // stage sub-chunk `sub` into buffer sub & 1: whole double2 chunks + the odd last column
+    auto stage = [&](int sub) {
+        double* S = Sbuf[sub & 1];
+        const int rs = r0 + sub * SUB, pairs = c / 2;
+        for (int e = tid; e < SUB * pairs; e += PNT_) {
+            const int r = e / pairs, kk = 2 * (e % pairs);
+            if (rs + r < n) cp_async16(S + r * lds + kk, q + (int64_t)(rs + r) * ldq + kk);
+        }
+        if ((c & 1) && tid < SUB && rs + tid < n) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(S + tid * lds + c - 1));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(q + (int64_t)(rs + tid) * ldq + c - 1));
+        }
+        cp_async_commit();
+    };
+    if (nsub > 0) stage(0);
+    for (int sub = 0; sub < nsub; ++sub) {
+        if (sub + 1 < nsub) {
+            // a partial last sub-chunk reuses a buffer that held full rows: clear the rows past n
+            // (the buffer's previous reader finished at the barrier that ended sub - 1)
+            const int nextrows = n - (r0 + (sub + 1) * SUB);
+            if (nextrows < SUB) {
+                double* Sn = Sbuf[(sub + 1) & 1];
+                for (int e = tid; e < (SUB - nextrows) * lds; e += PNT_) Sn[nextrows * lds + e] = 0.0;
+            }
+            stage(sub + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
+        const double* S = Sbuf[sub & 1];
         // y = S X: row tile (warp & 3), the k range split in two halves (warp >> 2)
         {
             const int mt = warp & 3, half = warp >> 2;
@@ -120,15 +143,16 @@ __global__ void __launch_bounds__(PNT_) orth_probe_partial_kernel(const double* 
 
 // Z = sum over chunks (in order) - X; est = sqrt(|Z|_F^2 / P).  A thread per (column, probe
 // pair): the chunk loads are independent, the adds ordered.
-__global__ void __launch_bounds__(PNT_) orth_probe_finish_kernel(const double* __restrict__ part, int chunks, int n,
+constexpr int FNT_ = 1024;  // one item per thread at c = 200: two rounds of 8 independent loads
+__global__ void __launch_bounds__(FNT_) orth_probe_finish_kernel(const double* __restrict__ part, int chunks, int n,
                                                                  const int* dimC, int c_cap, double tol, int* skip,
                                                                  double* est_out) {
-    __shared__ double red[PNT_];
+    __shared__ double red[FNT_];
     const int b = blockIdx.x, tid = threadIdx.x;
     const int c = dimC ? dimC[b] : c_cap;
     const int live = min(chunks, (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA);
     double ss = 0.0;
-    for (int item = tid; item < c * (PROBES / 2); item += PNT_) {
+    for (int item = tid; item < c * (PROBES / 2); item += FNT_) {
         const int k = item / (PROBES / 2), pp = 2 * (item % (PROBES / 2));
         const double* src = part + ((int64_t)b * chunks * c_cap + k) * PROBES + pp;
         double2 zs = make_double2(0.0, 0.0);
@@ -151,7 +175,7 @@ __global__ void __launch_bounds__(PNT_) orth_probe_finish_kernel(const double* _
     }
     red[tid] = ss;
     __syncthreads();
-    for (int o = PNT_ / 2; o > 0; o >>= 1) {
+    for (int o = FNT_ / 2; o > 0; o >>= 1) {
         if (tid < o) red[tid] += red[tid + o];
         __syncthreads();
     }
@@ -169,11 +193,11 @@ int orth_probe_chunks(int n) { return (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA; }
 void orth_probe(const double* Q, int64_t ldq, int64_t strideQ, int n, const int* dimC, int c_cap, int batch, double tol,
                 double* part, int* skip, double* est_out, cudaStream_t st) {
     const int chunks = orth_probe_chunks(n);
-    const int bytes = (SUB * probe_lds(c_cap) + 2 * SUB * PROBES) * (int)sizeof(double);
+    const int bytes = (2 * SUB * probe_lds(c_cap) + 2 * SUB * PROBES) * (int)sizeof(double);
     ensure_smem((const void*)orth_probe_partial_kernel, bytes);
     ::smg::count_launch(), orth_probe_partial_kernel<<<dim3(chunks, batch), PNT_, bytes, st>>>(Q, ldq, strideQ, n, dimC,
                                                                                                c_cap, part, chunks);
-    ::smg::count_launch(), orth_probe_finish_kernel<<<batch, PNT_, 0, st>>>(part, chunks, n, dimC, c_cap, tol, skip,
+    ::smg::count_launch(), orth_probe_finish_kernel<<<batch, FNT_, 0, st>>>(part, chunks, n, dimC, c_cap, tol, skip,
                                                                             est_out);
 }
 
