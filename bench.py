@@ -432,14 +432,14 @@ def measure_job(args, cfg, rank, world, local_rank, ctx, dist, weak=False, brief
     achieved = alg / (solve["ms"] * 1e-3) / 1e12 if solve["ms"] > 0 else None
     traffic = None
     try:  # dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "solve_traffic_r01.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "solve_traffic_r02.json")) as f:
             traffic = json.load(f)["dram_bytes_per_launch"] if args.config == "C5" else None
     except (OSError, KeyError, ValueError):
         pass
     roofline = {"kernel": kernel, "bound": "tensor",
                 "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
-                "traffic_source": "profiles/solve_traffic_r01.json (bytes per launch of 32 chains)",
+                "traffic_source": "profiles/solve_traffic_r02.json (bytes per launch of 32 chains)",
                 "peak_source": "measured FP64 DMMA peak, profiles/fp64_peak_r01.txt (MEASURED_PEAKS.json has no FP64 entry)",
                 "flops_per_launch": alg / max(spl, 1e-9), "avg_launch_ms": solve["ms"] / max(spl, 1e-9),
                 "b_algorithmic": b_half, "block_width_used": W_used, "ordering": info["ordering"],
