@@ -404,6 +404,14 @@ smg_status smg_doi_trace_enable(smg_context* ctx, int32_t on);
 smg_status smg_doi_trace_read(smg_context* ctx, int64_t capacity, int32_t* position,
                               int32_t* subspace_size, double* residual, int64_t* count);
 
+/* The one-pass orthonormality probe of the adaptive CholeskyQR2 (probe.cu): an estimate of
+ * ||Q^T Q - I||_F from 8 fixed +-1 vectors, for a column-major rows x cols block.  In the fixed-c
+ * chain a pass-1 factor whose estimate is <= 1e-13 sqrt(c) skips the second pass; this entry
+ * exposes the estimator so tests can hold it against the exact norm.  No reference counterpart
+ * (HouseholderQR, spectral.hpp:125-129, needs no second pass). */
+smg_status smg_orthonormality_estimate(smg_context* ctx, int32_t rows, int32_t cols, const double* q,
+                                       double* estimate);
+
 #ifdef __cplusplus
 }
 #endif

@@ -270,6 +270,15 @@ def orthonormalize(block, ctx: Optional[Context] = None) -> np.ndarray:
     return np.ascontiguousarray(q)
 
 
+def orthonormality_estimate(block, ctx: Optional[Context] = None) -> float:
+    """The adaptive CholeskyQR2's one-pass estimate of ||Q^T Q - I||_F (probe.cu; diagnostics)."""
+    ctx = ctx or default_context()
+    b = _colmajor(np.asarray(block, dtype=np.float64))
+    est = C.c_double()
+    ctx.check(ctx.lib.smg_orthonormality_estimate(ctx.handle, b.shape[0], b.shape[1], _ptr(b), C.byref(est)))
+    return est.value
+
+
 def orthogonal_iteration(op: ShiftedInverseOperator, init, t_max: int) -> np.ndarray:
     """orthogonal_iteration (spectral.hpp:204-211)."""
     init = np.asarray(init, dtype=np.float64)

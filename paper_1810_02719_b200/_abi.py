@@ -86,6 +86,7 @@ EXPORTED = [
     "smg_default_bilateral_params", "smg_fine_denoise", "smg_doi_trace_enable", "smg_doi_trace_read",
     "smg_last_run_info", "smg_partition_mesh", "smg_expand_overlaps", "smg_order_submeshes", "smg_segment_mesh",
     "smg_shard_range", "smg_comm_unique_id", "smg_comm_create", "smg_comm_destroy", "smg_gather_meshes",
+    "smg_orthonormality_estimate",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -143,6 +144,7 @@ def load(path: Optional[str] = None) -> C.CDLL:
         "smg_segment_mesh": ([vp, C.POINTER(smg_mesh), C.c_int32, C.c_double, C.c_uint64, vp, vp, C.c_int64,
                               c_int32_p, vp], C.c_int),
         "smg_doi_trace_read": ([vp, C.c_int64, vp, vp, vp, c_int64_p], C.c_int),
+        "smg_orthonormality_estimate": ([vp, C.c_int32, C.c_int32, vp, c_double_p], C.c_int),
         "smg_coarse_reconstruct_frames": ([vp, C.POINTER(smg_mesh), C.POINTER(smg_segmentation),
                                            C.POINTER(smg_bases), C.c_int32, vp, C.c_int32, C.c_int32, vp,
                                            C.c_int32], C.c_int),

@@ -204,6 +204,24 @@ smg_status smg_orthonormalize(smg_context* ctx, int32_t rows, int32_t cols, cons
     });
 }
 
+smg_status smg_orthonormality_estimate(smg_context* ctx, int32_t rows, int32_t cols, const double* q,
+                                       double* estimate) {
+    return guard(ctx, [&] {
+        require(cols >= 1 && rows >= cols, "block must be tall (rows >= cols >= 1)");
+        require(cols <= 512, "block width exceeds the GPU limit of 512");
+        require(estimate != nullptr, "estimate is null");
+        const cudaStream_t st = ctx->stream;
+        Workspace ws;
+        ws.init(1, rows, round_up(rows, 64), cols, st);
+        put_block(q, rows, cols, ws.V.get(), ws.ld, st);
+        orth_probe(ws.V.get(), ws.ld, ws.mstride(), rows, nullptr, cols, 1, 0.0, ws.probe_part.get(), ws.skip.get(),
+                   ws.probe_est.get(), st);
+        SMG_CUDA(cudaGetLastError());
+        SMG_CUDA(cudaMemcpyAsync(estimate, ws.probe_est.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+        SMG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 smg_status smg_orthogonal_iteration(smg_context* ctx, const smg_operator* op, int32_t c, const double* init,
                                     int32_t t_max, double* out) {
     return guard(ctx, [&] {

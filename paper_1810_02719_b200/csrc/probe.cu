@@ -19,7 +19,8 @@ namespace smg {
 
 namespace {
 
-constexpr int PROBES = 8, SUB = 32, ROWS_PER_CTA = 128, PNT_ = 256, PWARPS = PNT_ / 32;
+constexpr int PROBES = 8, ROWS_PER_CTA = 128, PNT_ = 256, PWARPS = PNT_ / 32;
+// SUB rows are staged at a time: 32, or 16 when two 32-row stages of a wide block (c > 432) would not fit
 constexpr int MAX_MT = 8;  // column tiles (of 8) per warp: c <= 8 * 8 * 8 = 512
 
 SMG_DEV unsigned probe_bits(int k) {
@@ -34,6 +35,7 @@ SMG_DEV unsigned probe_bits(int k) {
 
 __host__ __device__ inline int probe_lds(int c) { return ((c + 15) / 16) * 16 + 4; }  // staged row stride, 4 mod 16
 
+template <int SUB>
 __global__ void __launch_bounds__(PNT_) orth_probe_partial_kernel(const double* __restrict__ Q, int64_t ldq,
                                                                   int64_t strideQ, int n, const int* dimC, int c_cap,
                                                                   double* __restrict__ part, int chunks) {
@@ -43,8 +45,8 @@ __global__ void __launch_bounds__(PNT_) orth_probe_partial_kernel(const double* 
     const int lds = probe_lds(c_cap);
     const int c8 = (c + 7) & ~7;          // columns staged (zero past c): whole 8-wide tiles
     double* Sbuf[2] = {psm, psm + SUB * lds};   // two SUB x lds stages (cp.async double buffer)
-    double* ysm = psm + 2 * SUB * lds;    // SUB x PROBES (+ the second k-half's partial)
-    double* yhalf = ysm + SUB * PROBES;
+    constexpr int MTILES = SUB / 8, KPARTS = PWARPS / MTILES;  // y = S X: row tiles x k-range parts over the warps
+    double* ysm = psm + 2 * SUB * lds;    // KPARTS partial (SUB x PROBES) blocks; block 0 receives the sum
     const double* q = Q + (int64_t)b * strideQ;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -88,11 +90,11 @@ __global__ void __launch_bounds__(PNT_) orth_probe_partial_kernel(const double* 
         }
         __syncthreads();
         const double* S = Sbuf[sub & 1];
-        // y = S X: row tile (warp & 3), the k range split in two halves (warp >> 2)
+        // y = S X: row tile warp % MTILES, the k range split in KPARTS parts
         {
-            const int mt = warp & 3, half = warp >> 2;
-            const int ksteps = c8 / 4, kmid = (ksteps + 1) / 2;
-            const int kb = half ? kmid : 0, ke = half ? ksteps : kmid;
+            const int mt = warp % MTILES, part = warp / MTILES;
+            const int ksteps = c8 / 4, per = (ksteps + KPARTS - 1) / KPARTS;
+            const int kb = min(ksteps, part * per), ke = min(ksteps, kb + per);
             double y0[2] = {0.0, 0.0}, y1[2] = {0.0, 0.0};
             const double* srow = S + (8 * mt + g) * lds + t;
             int ks = kb;
@@ -110,11 +112,16 @@ __global__ void __launch_bounds__(PNT_) orth_probe_partial_kernel(const double* 
             }
             y0[0] += y1[0];
             y0[1] += y1[1];
-            double* dst = (half ? yhalf : ysm) + (8 * mt + g) * PROBES + 2 * t;
+            double* dst = ysm + part * (SUB * PROBES) + (8 * mt + g) * PROBES + 2 * t;
             *reinterpret_cast<double2*>(dst) = make_double2(y0[0], y0[1]);
         }
         __syncthreads();
-        if (tid < SUB * PROBES) ysm[tid] += yhalf[tid];
+        if (tid < SUB * PROBES) {
+            double v = ysm[tid];
+#pragma unroll
+            for (int part = 1; part < KPARTS; ++part) v += ysm[part * (SUB * PROBES) + tid];
+            ysm[tid] = v;
+        }
         __syncthreads();
         // z += S^T y: column tiles warp, warp + 8, ...; k = the SUB rows
         {
@@ -193,10 +200,18 @@ int orth_probe_chunks(int n) { return (n + ROWS_PER_CTA - 1) / ROWS_PER_CTA; }
 void orth_probe(const double* Q, int64_t ldq, int64_t strideQ, int n, const int* dimC, int c_cap, int batch, double tol,
                 double* part, int* skip, double* est_out, cudaStream_t st) {
     const int chunks = orth_probe_chunks(n);
-    const int bytes = (2 * SUB * probe_lds(c_cap) + 2 * SUB * PROBES) * (int)sizeof(double);
-    ensure_smem((const void*)orth_probe_partial_kernel, bytes);
-    ::smg::count_launch(), orth_probe_partial_kernel<<<dim3(chunks, batch), PNT_, bytes, st>>>(Q, ldq, strideQ, n, dimC,
-                                                                                               c_cap, part, chunks);
+    const int lds = probe_lds(c_cap);
+    const int bytes32 = (2 * 32 * lds + PWARPS * 8 * PROBES) * (int)sizeof(double);
+    const int bytes16 = (2 * 16 * lds + PWARPS * 8 * PROBES) * (int)sizeof(double);
+    if (bytes32 <= 220 * 1024) {
+        ensure_smem((const void*)orth_probe_partial_kernel<32>, bytes32);
+        ::smg::count_launch(), orth_probe_partial_kernel<32><<<dim3(chunks, batch), PNT_, bytes32, st>>>(
+            Q, ldq, strideQ, n, dimC, c_cap, part, chunks);
+    } else {
+        ensure_smem((const void*)orth_probe_partial_kernel<16>, bytes16);
+        ::smg::count_launch(), orth_probe_partial_kernel<16><<<dim3(chunks, batch), PNT_, bytes16, st>>>(
+            Q, ldq, strideQ, n, dimC, c_cap, part, chunks);
+    }
     ::smg::count_launch(), orth_probe_finish_kernel<<<batch, FNT_, 0, st>>>(part, chunks, n, dimC, c_cap, tol, skip,
                                                                             est_out);
 }

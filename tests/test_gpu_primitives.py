@@ -305,3 +305,33 @@ def test_first_basis_fallback_paths(ctx, grid, monkeypatch, env):
     ug, ev = G.bottom_subspace(g, c, return_eigenvalues=True)
     assert O.max_principal_angle(ug, u[:, :c]) < 1e-9
     assert np.abs(ev - w[:c]).max() < 1e-10
+
+
+@pytest.mark.parametrize("rows,cols", [(2048, 200), (1026, 60), (4096, 399), (700, 512), (64, 7)])
+def test_orthonormality_probe_tracks_the_exact_norm(ctx, rows, cols):
+    """The adaptive CholeskyQR2 decides its pass-2 skip from a one-pass randomized estimate of
+    ||Q^T Q - I||_F (probe.cu, 8 fixed +-1 vectors).  Against the exact norm: an orthonormal
+    block sits at rounding level; a block with a known departure E (dense, or concentrated in
+    one entry -- the estimator's worst case) is estimated within the Hutchinson spread; odd
+    widths, the width limit and row counts that are not multiples of the 32-row stage."""
+    rng = np.random.Generator(np.random.PCG64(rows * 1000 + cols))
+    q, _ = np.linalg.qr(rng.standard_normal((rows, cols)))
+    assert G.orthonormality_estimate(q, ctx=ctx) < 1e-13
+    # dense symmetric departure: Q (I + S) with ||S||_F = 1e-9  ->  Q^T Q - I ~ 2 S
+    s = rng.standard_normal((cols, cols))
+    s = (s + s.T) / 2
+    s *= 1e-9 / np.linalg.norm(s)
+    p = q @ (np.eye(cols) + s)
+    exact = np.linalg.norm(p.T @ p - np.eye(cols))
+    est = G.orthonormality_estimate(p, ctx=ctx)
+    assert 0.6 * exact <= est <= 1.6 * exact, (est, exact)
+    # rank-one departure (one column scaled): every probe sees it with weight 1
+    p = q.copy()
+    p[:, cols // 2] *= 1 + 1e-8
+    exact = np.linalg.norm(p.T @ p - np.eye(cols))
+    est = G.orthonormality_estimate(p, ctx=ctx)
+    assert 0.9 * exact <= est <= 1.1 * exact, (est, exact)
+    # two nearly parallel columns: far above any skip threshold
+    p = q.copy()
+    p[:, 0] = p[:, 1]
+    assert G.orthonormality_estimate(p, ctx=ctx) > 0.5
