@@ -688,8 +688,8 @@ def cpu_baseline(args, cfg, total_units):
     return {"value": verts / t, "unit": "vertices/s", "cores": P, "kind": "port",
             "steady_state_value": verts / (t - tfb) if t > tfb else None,
             "sample": f"{P} whole chains ({cfg['desc']}) in parallel, 1 per core, BLAS 1 thread; numpy/LAPACK "
-                      f"restatement oracle/specmesh_oracle.py (the C++/Eigen reference cannot be built: Eigen absent, "
-                      f"profiles/eigen_probe_r02.txt); banded Cholesky at the bandwidth-minimising order (RCM, "
+                      f"restatement oracle/specmesh_oracle.py (pinned to the reference's own code run over an Eigen stand-in, "
+                      f"tests/golden/ref_*; that build is slower than LAPACK, so the port is the baseline); banded Cholesky at the bandwidth-minimising order (RCM, "
                       f"b=33 like the GPU); timed track+project+reconstruct per chain, no extrapolation; "
                       f"step {t:.1f}s, first basis {tfb:.1f}s per chain"}
 
@@ -730,7 +730,7 @@ def reference_arm(args, cfg):
             "data": "synthetic (seeded sinusoid height-field grids + N(0,sigma^2) noise)",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "meshes_per_step": P,
                        "job_meshes": total_units},
-            "impl": "reference", "arm": "oracle port (numpy/LAPACK restatement of the reference; Eigen absent)",
+            "impl": "reference", "arm": "oracle port (numpy/LAPACK restatement of the reference, pinned to the reference's own code over an Eigen stand-in; Eigen itself is absent)",
             "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
