@@ -21,7 +21,15 @@ namespace smg {
 
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT_DEFAULT = 256;
+// threads per CTA: the W = 32 factor is barrier-latency bound (a barrier per column), so it runs
+// 128-thread CTAs (cheaper barriers; 93 registers, five CTAs per SM: C5 309.2 -> 306.8 ms; forcing
+// eight per SM at 63 registers was slower, 314 ms) unless SMG_FACTOR_NT256 is defined
+#ifdef SMG_FACTOR_NT256
+template <int W> struct FThreads { static constexpr int value = NT_DEFAULT; };
+#else
+template <int W> struct FThreads { static constexpr int value = W == 32 ? 128 : NT_DEFAULT; };
+#endif
 
 // Shared memory: three W x W matrices (S, P and L, where L holds Linv_{k-1}
 // until -P Linv_{k-1} is written and then receives Linv_k), the coupling lists
@@ -43,7 +51,7 @@ template <int W>
 struct FTile {
     // 8x8 tiles per warp: W=16 1x1 (4 warps), 32 1x2 (8), 48 2x3 (6), 64 2x4 (8)
     static constexpr int MT = (W == 48 || W == 64) ? 2 : 1;
-    static constexpr int NTT = W == 16 ? 1 : (W == 32 ? 2 : (W == 48 ? 3 : 4));
+    static constexpr int NTT = W == 16 ? 1 : (W == 32 ? (FThreads<32>::value == 128 ? 4 : 2) : (W == 48 ? 3 : 4));
     static constexpr int WMG = (W / 8) / MT;  // warps along m
     static constexpr int WNG = (W / 8) / NTT; // warps along n
     static constexpr int ACTIVE = WMG * WNG;
@@ -72,7 +80,8 @@ SMG_DEV void fblock_mma(double (&acc)[FTile<W>::MT][FTile<W>::NTT][2], FA a, FB 
 }
 
 template <int W>
-__global__ void __launch_bounds__(NT) factor_kernel(FactorParams p) {
+__global__ void __launch_bounds__((FThreads<W>::value)) factor_kernel(FactorParams p) {
+    constexpr int NT = FThreads<W>::value;
     constexpr int LD = FactorSmem<W>::LD;
     constexpr int MAT = FactorSmem<W>::MAT;
     extern __shared__ __align__(16) double sm[];
@@ -323,7 +332,7 @@ template <int W>
 void launch(const FactorParams& p, cudaStream_t st) {
     const int bytes = FactorSmem<W>::bytes(p.n, p.cpl, p.perm != nullptr);
     cudaFuncSetAttribute(factor_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    ::smg::count_launch(), factor_kernel<W><<<p.ntiles, NT, bytes, st>>>(p);
+    ::smg::count_launch(), factor_kernel<W><<<p.ntiles, FThreads<W>::value, bytes, st>>>(p);
 }
 
 }  // namespace
