@@ -36,19 +36,27 @@ What it restates (reference = /root/reference/proj/include/specmesh, cited file:
   * segment_mesh              pipeline.hpp:131-138
 
 Third-party dependency: the reference's arithmetic comes from Eigen (version
-unpinned; absent from this image, so the reference cannot be compiled here or on
-the GPU box -- SURVEY.md §8(c)).  Its published algorithms are restated with
+unpinned; absent from this image and the GPU box -- SURVEY.md §8(c)).  Its
+published algorithms are restated with
 LAPACK through scipy: SimplicialLDLT (AMD order, no pivoting) -> banded Cholesky
 (LAPACK dpbtrf/dpbtrs) in natural or RCM order, with a no-pivot banded LDL^T for
 indefinite matrices (what Eigen's LDL^T tolerates); HouseholderQR ->
 LAPACK dgeqrf/dorgqr; SelfAdjointEigenSolver -> LAPACK dsyevd.  They differ from
 Eigen only in rounding.
 
-Parity pin: the reference ships no tests, fixtures or golden vectors.  This
-oracle is pinned to the SPEC.md known-answer examples in
-tests/test_oracle_known_answers.py, and its RNG to libstdc++'s own
-std::mt19937_64 / std::normal_distribution (oracle/rng_ref.cpp).  Against the
-reference's code itself parity is UNPINNED (Eigen absent).
+Parity pin: the reference ships no tests, fixtures or golden vectors, but its own
+unmodified headers run in this container over oracle/eigen_shim (a stand-in for the
+Eigen API subset they use; oracle/ref_harness.cpp, `make refharness`).  Their outputs
+on the seeded configurations are committed as tests/golden/ref_* (made by
+tests/golden/make_ref_fixtures.py) and tests/test_ref_fixtures.py holds this oracle to
+them: edges, partitions, member lists, orders, CSR patterns and values (1/d^2
+included), traces, shifts, DOI decisions and exception texts identical; subspace
+angles <= 1e-8, reconstructions <= 1e-9, coefficients <= 1e-8 on C1, C2, C3, a whole
+C5 chain and the widened rows.  That pins every line of the reference's own code;
+what stays unpinned is only the rounding of Eigen's inner kernels (the shim restates
+them too -- see its header).  Also pinned: the SPEC.md known-answer examples
+(tests/test_oracle_known_answers.py) and the RNG, bit-exact against
+libstdc++'s std::mt19937_64 / std::normal_distribution (oracle/rng_ref.cpp).
 """
 from __future__ import annotations
 
