@@ -44,7 +44,7 @@ oracle/_ref/rng_ref: oracle/rng_ref.cpp
 	g++ -O2 -std=c++17 -o $@ $<
 
 # standalone kernel timing tools (not part of the library)
-tools: build/cholx_bench build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_halfslab build/solve_bench_notri build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_f3r4 build/solve_bench_nomma_ns5
+tools: build/dmma_lat build/cholx_bench build/solve_bench build/solve_bench_norhs build/solve_bench_noslab build/solve_bench_halfslab build/solve_bench_notri build/solve_bench_nomma build/solve_bench_nomma_norhs build/solve_bench_nomma_noslab build/solve_bench_f3r4 build/solve_bench_nomma_ns5
 
 build/solve_bench: tools/solve_bench.cu $(SRC_DIR)/solve.cu $(HDRS)
 	@mkdir -p build
@@ -98,3 +98,7 @@ clean:
 build/cholx_bench: tools/cholx_bench.cu $(SRC_DIR)/cholx.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) -std=c++17 $(ARCH) -O3 -lineinfo -DSMG_CHOLX_TIMING -o $@ $<
+
+build/dmma_lat: tools/dmma_lat.cu
+	@mkdir -p build
+	$(NVCC) -std=c++17 $(ARCH) -O3 -o $@ $<
