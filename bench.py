@@ -685,13 +685,52 @@ def cpu_baseline(args, cfg, total_units):
         t, verts, tfb = arm.step()
     finally:
         arm.close()
-    return {"value": verts / t, "unit": "vertices/s", "cores": P, "kind": "port",
+    out = {"value": verts / t, "unit": "vertices/s", "cores": P, "kind": "port",
             "steady_state_value": verts / (t - tfb) if t > tfb else None,
             "sample": f"{P} whole chains ({cfg['desc']}) in parallel, 1 per core, BLAS 1 thread; numpy/LAPACK "
                       f"restatement oracle/specmesh_oracle.py (pinned to the reference's own code run over an Eigen stand-in, "
                       f"tests/golden/ref_*; that build is slower than LAPACK, so the port is the baseline); banded Cholesky at the bandwidth-minimising order (RCM, "
                       f"b=33 like the GPU); timed track+project+reconstruct per chain, no extrapolation; "
                       f"step {t:.1f}s, first basis {tfb:.1f}s per chain"}
+    ref = reference_code_sample(args)
+    if ref:
+        out["reference_code"] = ref
+    return out
+
+
+def reference_code_sample(args, tiles=32):
+    """The reference's OWN chain code (its headers over oracle/eigen_shim, built where
+    /root/reference exists and shipped as oracle/_ref/libspecmesh_ref.so) on a bounded sample:
+    the first `tiles` tiles of one C5 chain on one core, tracking only (the first-submesh
+    eigendecomposition excluded).  A cross-check of the port's baseline, not the baseline: the
+    stand-in's unblocked QR / LDL^T are slower than LAPACK (and than real Eigen)."""
+    if args.config != "C5":
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import numpy as np
+        import ref_binding as R
+        if not R.available():
+            return None
+        from paper_1810_02719_b200 import synth
+        w = synth.config("C5", mesh_index=0)
+        rm = R.Mesh(w.mesh.vertices, w.mesh.faces)
+        # dense_limit below n_d: the first tile starts from the reference's cold random basis with one
+        # OI step (pipeline.hpp:118-119) instead of the n_d^3 dense eigendecomposition, so the sample
+        # times tracking steps only (their cost does not depend on the basis values)
+        cfg = R.default_config(weighting=R.BINARY, subspace_size=w.c, iterations=w.iterations, shift_scale=1e-3,
+                               dense_limit=16, initial_iterations=1)
+        rs = R.Segmentation.from_members(rm, w.seg.members[:tiles], np.arange(tiles, dtype=np.int32))
+        t0 = time.perf_counter()
+        R.chain_fixed(rm, rs, cfg, [w.c] * tiles)
+        per_tile = (time.perf_counter() - t0) / tiles
+        n_d = int(w.seg.members[0].size)
+        return {"value": n_d / per_tile, "unit": "vertices/s", "cores": 1, "seconds_per_tile": per_tile,
+                "sample": f"compute_block_bases_fixed_sizes (pipeline.hpp:144-194) of the reference itself over "
+                          f"oracle/eigen_shim on {tiles} tiles of C5 mesh 0 (cold-start first tile, no dense "
+                          f"eigendecomposition), one core, tracking steps only"}
+    except Exception as exc:  # the cross-check never fails the bench
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
 
 
 def reference_arm(args, cfg):
