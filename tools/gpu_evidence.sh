@@ -16,5 +16,5 @@ timeout 600 python bench.py --config F3 --steps 3 --warmup 3 > $O/bench_F3_$T.lo
 timeout 600 python bench.py --config F4 --steps 20 --warmup 3 > $O/bench_F4_$T.log 2>&1; echo rc=$? >> $O/bench_F4_$T.log
 for m in 8 16 32; do timeout 600 python bench.py --meshes $m --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_m${m}_$T.log 2>&1; done
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 5400 -c 5400 --csv --log-file $O/launches_$T.csv $CMD > $O/ncu_list_$T.log 2>&1; echo rc=$? >> $O/ncu_list_$T.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 6100 -c 6100 --csv --log-file $O/launches_$T.csv $CMD > $O/ncu_list_$T.log 2>&1; echo rc=$? >> $O/ncu_list_$T.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"solve_kernel|recon_mma|partial_kernel|orth_probe|gemm_pipe_kernel|cholx" -s 300 -c 14 -o $O/prof_main_$T $CMD > $O/ncu_full_$T.log 2>&1; echo rc=$? >> $O/ncu_full_$T.log

@@ -18,7 +18,7 @@ configs) for C in C1 C2 C3 C4; do timeout 900 python bench.py --config $C --step
 refconfigs) for C in C1 C2 C3 C4; do timeout 900 python bench.py --config $C --impl reference --steps 3 --warmup 1 > $O/bench_ref_${C}_$T.log 2>&1; echo rc=$? >> $O/bench_ref_${C}_$T.log; done ;;
 f3) timeout 600 python bench.py --config F3 --steps 3 --warmup 3 > $O/bench_f3_$T.log 2>&1; echo rc=$? >> $O/bench_f3_$T.log ;;
 f4) timeout 600 python bench.py --config F4 --steps 20 --warmup 3 > $O/bench_f4_$T.log 2>&1; echo rc=$? >> $O/bench_f4_$T.log ;;
-list) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 6000 -c 6000 --csv --log-file $O/launches_$T.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_list_$T.log 2>&1; echo rc=$? >> $O/ncu_list_$T.log ;;
+list) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 6100 -c 6100 --csv --log-file $O/launches_$T.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_list_$T.log 2>&1; echo rc=$? >> $O/ncu_list_$T.log ;;
 solve) timeout 900 ncu --set full --clock-control none --import-source on -k regex:solve -s 40 -c 2 -o $O/prof_solve_$T python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_full_$T.log 2>&1; echo rc=$? >> $O/ncu_full_$T.log ;;
 esac
 done
