@@ -51,7 +51,14 @@ struct SolveSmem {
     // consumer (DMMA) warps: the cooperative tiling uses all 8; column-private warps own 16
     // columns each (4 x 2 tiles of 8 x 8: eight independent accumulator chains saturate the
     // warp's sub-partition, tools/dmma_lat.cu) -- one warp per SM sub-partition
-    static constexpr int NCW = PRIV ? CS / 16 : kSolveWarps;
+    // 16-column slices at W = 32 (large batches, three CTAs per SM): FOUR DMMA warps, each one row
+    // tile x both column tiles (3 operand loads per 2 DMMAs instead of 4, half the per-column scalar
+    // work): 359 -> 317 us per 32-chain launch, C5 307 -> 299 ms per step; two warps (2 x 2 tiles
+    // each) fall back to 360 us -- too few warps per scheduler
+#ifndef SMG_SOLVE_NCW16
+#define SMG_SOLVE_NCW16 4
+#endif
+    static constexpr int NCW = PRIV ? CS / 16 : ((W == 32 && CS == 16) ? SMG_SOLVE_NCW16 : kSolveWarps);
     static constexpr int THREADS = (NCW + kProdWarps) * 32;
     static constexpr int FB = F_ELEMS * 8, RB = R_ELEMS * 8, YB = PRIV ? RB : 2 * RB;
     // W = 32, CS = 16 (large batches): a budget for three CTAs per SM (two rhs
@@ -96,7 +103,8 @@ struct SolveTiling {
     static constexpr int NW = SolveSmem<W, CS>::NCW;
     static constexpr int WM = PRIV ? 1
                                    : (NT_ALL == 1) ? (MT_ALL < NW ? MT_ALL : NW)
-                                                   : ((MT_ALL % 4 == 0) ? 4 : ((MT_ALL % 2 == 0) ? 2 : 1));
+                                                   : ((MT_ALL % 4 == 0 && NW >= 4) ? 4
+                                                                                   : ((MT_ALL % 2 == 0 && NW >= 2) ? 2 : 1));
     static constexpr int WN_RAW = NW / WM;
     static constexpr int WN = (NT_ALL % WN_RAW == 0) ? WN_RAW
                                                      : ((NT_ALL % 4 == 0 && WN_RAW >= 4) ? 4 : ((NT_ALL % 2 == 0 && WN_RAW >= 2) ? 2 : 1));
