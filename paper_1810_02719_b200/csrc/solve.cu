@@ -58,7 +58,12 @@ struct SolveSmem {
 #ifndef SMG_SOLVE_NCW16
 #define SMG_SOLVE_NCW16 4
 #endif
-    static constexpr int NCW = PRIV ? CS / 16 : ((W == 32 && CS == 16) ? SMG_SOLVE_NCW16 : kSolveWarps);
+#ifndef SMG_SOLVE_NCW32
+#define SMG_SOLVE_NCW32 8
+#endif
+    static constexpr int NCW = PRIV ? CS / 16
+                                    : ((W == 32 && CS == 16) ? SMG_SOLVE_NCW16
+                                                             : ((W == 32 && CS == 32) ? SMG_SOLVE_NCW32 : kSolveWarps));
     static constexpr int THREADS = (NCW + kProdWarps) * 32;
     static constexpr int FB = F_ELEMS * 8, RB = R_ELEMS * 8, YB = PRIV ? RB : 2 * RB;
     // W = 32, CS = 16 (large batches): a budget for three CTAs per SM (two rhs
