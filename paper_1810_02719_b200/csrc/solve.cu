@@ -54,16 +54,11 @@ struct SolveSmem {
     // 16-column slices at W = 32 (large batches, three CTAs per SM): FOUR DMMA warps, each one row
     // tile x both column tiles (3 operand loads per 2 DMMAs instead of 4, half the per-column scalar
     // work): 359 -> 317 us per 32-chain launch, C5 307 -> 299 ms per step; two warps (2 x 2 tiles
-    // each) fall back to 360 us -- too few warps per scheduler
+    // each) fall back to 360 us -- too few warps per scheduler; 32-column slices with four 1 x 4 warps: 401 us
 #ifndef SMG_SOLVE_NCW16
 #define SMG_SOLVE_NCW16 4
 #endif
-#ifndef SMG_SOLVE_NCW32
-#define SMG_SOLVE_NCW32 8
-#endif
-    static constexpr int NCW = PRIV ? CS / 16
-                                    : ((W == 32 && CS == 16) ? SMG_SOLVE_NCW16
-                                                             : ((W == 32 && CS == 32) ? SMG_SOLVE_NCW32 : kSolveWarps));
+    static constexpr int NCW = PRIV ? CS / 16 : ((W == 32 && CS == 16) ? SMG_SOLVE_NCW16 : kSolveWarps);
     static constexpr int THREADS = (NCW + kProdWarps) * 32;
     static constexpr int FB = F_ELEMS * 8, RB = R_ELEMS * 8, YB = PRIV ? RB : 2 * RB;
     // W = 32, CS = 16 (large batches): a budget for three CTAs per SM (two rhs
